@@ -1,0 +1,176 @@
+// Shared pieces of the jagged HSTU attention kernels: segment decoding, the
+// on-device work-list builder (no host sync: lists are built from the
+// device-resident offsets and ordered longest-first), kernel parameter block.
+#pragma once
+#include "bias.cuh"
+
+namespace jh {
+
+constexpr int kBM = 128;  // q rows per tile
+constexpr int kBN = 128;  // kv rows per tile
+
+struct SegArgs {
+  const int64_t* q_offsets;
+  const int64_t* q_pos0;
+  const int64_t* kv_start;
+  const int64_t* kv_len;
+  int64_t num_segments;
+};
+
+struct Seg {
+  int64_t q_row0, lq, qp0, kv_row0, kv_len;
+};
+
+JH_DEV Seg load_seg(const SegArgs& a, int64_t s) {
+  Seg g;
+  g.q_row0 = a.q_offsets[s];
+  g.lq = a.q_offsets[s + 1] - g.q_row0;
+  g.qp0 = a.q_pos0 ? a.q_pos0[s] : 0;
+  g.kv_row0 = a.kv_start ? a.kv_start[s] : g.q_row0;
+  g.kv_len = a.kv_len ? a.kv_len[s] : g.lq;
+  return g;
+}
+
+// kv positions a q tile (rows t*128 ..) can see: [0, kv_lim)
+JH_DEV int64_t fwd_kv_lim(const Seg& g, int t) {
+  int64_t nq = g.lq - (int64_t)t * kBM;
+  nq = nq < kBM ? nq : kBM;
+  int64_t e = g.qp0 + (int64_t)t * kBM + nq;
+  return e < g.kv_len ? e : g.kv_len;
+}
+// kv positions any q row of the segment can see
+JH_DEV int64_t seg_kv_vis(const Seg& g) {
+  int64_t e = g.qp0 + g.lq;
+  return e < g.kv_len ? e : g.kv_len;
+}
+
+struct WorkHeader {
+  int32_t n_fwd, n_bwd;
+  int32_t pad[14];
+};
+
+// Workspace: [WorkHeader][fwd items int2 x max_f][bwd items int2 x max_b][dq_accum fp32]
+struct WorkLists {
+  WorkHeader* hdr;
+  int2* fwd;
+  int2* bwd;
+  float* dq_accum;
+};
+
+constexpr int kLevels = 4096;
+
+// One block of 1024 threads.  fwd items (s, q_tile) ordered by #kv tiles
+// descending; bwd items (s, kv_tile) ordered by #q tiles descending.
+static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, WorkLists wl) {
+  __shared__ int hist_f[kLevels], hist_b[kLevels];
+  __shared__ int warp_sum[32];
+  for (int i = threadIdx.x; i < kLevels; i += blockDim.x) hist_f[i] = hist_b[i] = 0;
+  __syncthreads();
+  for (int64_t s = threadIdx.x; s < sa.num_segments; s += blockDim.x) {
+    Seg g = load_seg(sa, s);
+    int nt = (int)((g.lq + kBM - 1) / kBM);
+    for (int t = 0; t < nt; ++t) {
+      int w = (int)((fwd_kv_lim(g, t) + kBN - 1) / kBN);
+      atomicAdd(&hist_f[min(w, kLevels - 1)], 1);
+    }
+    int64_t vis = seg_kv_vis(g);
+    int nj = (int)((vis + kBN - 1) / kBN);
+    int64_t qend = g.qp0 + g.lq;
+    for (int j = 0; j < nj; ++j) {
+      // q rows with position >= j*128
+      int64_t first = (int64_t)j * kBN - g.qp0;
+      first = first < 0 ? 0 : first;
+      int w = (int)((g.lq - first + kBM - 1) / kBM);
+      (void)qend;
+      atomicAdd(&hist_b[min(w, kLevels - 1)], 1);
+    }
+  }
+  __syncthreads();
+  // descending exclusive scan: start[w] = sum_{w' > w} hist[w'] (in place)
+  for (int pass = 0; pass < 2; ++pass) {
+    int* h = pass ? hist_b : hist_f;
+    constexpr int per = kLevels / 1024;
+    int vals[per];
+    int local = 0;
+    // thread i owns levels reversed: idx = kLevels-1 - (i*per + k)
+    for (int k = 0; k < per; ++k) {
+      vals[k] = h[kLevels - 1 - (threadIdx.x * per + k)];
+      local += vals[k];
+    }
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int incl = local;
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_sum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int x = warp_sum[lane];
+      int xi = x;
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, xi, o);
+        if (lane >= o) xi += y;
+      }
+      warp_sum[lane] = xi - x;  // exclusive
+    }
+    __syncthreads();
+    int run = warp_sum[wid] + incl - local;
+    for (int k = 0; k < per; ++k) {
+      h[kLevels - 1 - (threadIdx.x * per + k)] = run;
+      run += vals[k];
+    }
+    if (threadIdx.x == blockDim.x - 1) {
+      if (pass)
+        wl.hdr->n_bwd = run;
+      else
+        wl.hdr->n_fwd = run;
+    }
+    __syncthreads();
+  }
+  for (int64_t s = threadIdx.x; s < sa.num_segments; s += blockDim.x) {
+    Seg g = load_seg(sa, s);
+    int nt = (int)((g.lq + kBM - 1) / kBM);
+    for (int t = 0; t < nt; ++t) {
+      int w = (int)((fwd_kv_lim(g, t) + kBN - 1) / kBN);
+      int idx = atomicAdd(&hist_f[min(w, kLevels - 1)], 1);
+      wl.fwd[idx] = make_int2((int)s, t);
+    }
+    int64_t vis = seg_kv_vis(g);
+    int nj = (int)((vis + kBN - 1) / kBN);
+    for (int j = 0; j < nj; ++j) {
+      int64_t first = (int64_t)j * kBN - g.qp0;
+      first = first < 0 ? 0 : first;
+      int w = (int)((g.lq - first + kBM - 1) / kBM);
+      int idx = atomicAdd(&hist_b[min(w, kLevels - 1)], 1);
+      wl.bwd[idx] = make_int2((int)s, j);
+    }
+  }
+}
+
+// Parameters shared by the fwd / bwd attention kernels.
+struct AttnParams {
+  SegArgs seg;
+  const int64_t* ts_q;
+  const int64_t* ts_k;
+  const float* ts_weights;
+  const float* pos_weights;
+  int32_t num_pos;
+  int32_t num_heads;
+  int64_t q_rows, kv_rows;
+  // fwd
+  __nv_bfloat16* out;
+  int64_t ld_o;
+  // bwd
+  __nv_bfloat16* dk;
+  __nv_bfloat16* dv;
+  int64_t ld_dk, ld_dv;
+  float* dk_accum;
+  float* dv_accum;
+  double* d_ts_weights;
+  double* d_pos_weights;
+  WorkLists wl;
+  DevBiasTable bias;
+};
+
+}  // namespace jh

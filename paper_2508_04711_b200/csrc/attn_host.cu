@@ -1,0 +1,192 @@
+// Host launch code for the attention kernels (jh_attn_fwd / jh_attn_bwd):
+// argument validation, tensor maps, work-list build, kernel launches.
+#include <algorithm>
+#include <cstring>
+
+#include "abi_internal.h"
+#include "attn_common.cuh"
+#include "tmap.h"
+
+namespace jh {
+
+template <int D>
+int launch_fwd(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const AttnParams&, int, cudaStream_t);
+template <int D>
+int launch_bwd(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const AttnParams&,
+               const jh_attn_args&, int, cudaStream_t);
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+struct WsLayout {
+  size_t items_f, items_b, dq, total;
+};
+
+static WsLayout ws_layout(int64_t q_rows, int64_t kv_total, int64_t nseg, int32_t H, int32_t D) {
+  WsLayout w;
+  int64_t max_f = q_rows / kBM + nseg + 1;
+  int64_t max_b = kv_total / kBN + nseg + 1;
+  w.items_f = sizeof(WorkHeader);
+  w.items_b = w.items_f + ((size_t)max_f * 8 + 255) / 256 * 256;
+  w.dq = w.items_b + ((size_t)max_b * 8 + 255) / 256 * 256;
+  w.total = w.dq + (size_t)std::max<int64_t>(q_rows, 0) * H * D * 4;
+  return w;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static int validate(const jh_attn_args* a, bool bwd) {
+  if (!a) return set_error(JH_ERR_INVALID, "args is NULL");
+  if (a->head_dim != 64 && a->head_dim != 128)
+    return set_error(JH_ERR_UNSUPPORTED, "head_dim %d unsupported (64 or 128)", a->head_dim);
+  if (a->num_heads < 1) return set_error(JH_ERR_INVALID, "num_heads must be >= 1");
+  if (a->num_segments < 0 || a->q_rows < 0 || a->kv_rows < 0) return set_error(JH_ERR_INVALID, "negative size");
+  if (a->num_segments >= (int64_t(1) << 31)) return set_error(JH_ERR_UNSUPPORTED, "too many segments");
+  if (a->q_rows >= (int64_t(1) << 31) || a->kv_rows >= (int64_t(1) << 31))
+    return set_error(JH_ERR_UNSUPPORTED, "more than 2^31 rows");
+  if (a->num_buckets < 1 || a->num_buckets > 256)
+    return set_error(JH_ERR_INVALID, "num_buckets must be in [1, 256]");
+  if (!a->ts_weights) return set_error(JH_ERR_INVALID, "ts_weights is NULL");
+  if (a->num_pos < 0 || a->num_pos > 1024) return set_error(JH_ERR_UNSUPPORTED, "num_pos must be in [0, 1024]");
+  if (a->num_pos > 0 && !a->pos_weights) return set_error(JH_ERR_INVALID, "pos_weights is NULL");
+  if (!a->q_offsets) return set_error(JH_ERR_INVALID, "q_offsets is NULL");
+  const int64_t HD = (int64_t)a->num_heads * a->head_dim;
+  if (a->q_rows > 0 || a->kv_rows > 0) {
+    if (!a->q || !a->k || !a->v || !a->ts_q || !a->ts_k) return set_error(JH_ERR_INVALID, "NULL input tensor");
+    if (a->ld_q < HD || a->ld_k < HD || a->ld_v < HD) return set_error(JH_ERR_INVALID, "row stride < H*d");
+    if ((a->ld_q * 2) % 16 || (a->ld_k * 2) % 16 || (a->ld_v * 2) % 16)
+      return set_error(JH_ERR_INVALID, "row strides must be multiples of 16 bytes");
+    if (!aligned16(a->q) || !aligned16(a->k) || !aligned16(a->v))
+      return set_error(JH_ERR_INVALID, "q/k/v must be 16-byte aligned");
+  }
+  if (!bwd) {
+    if (a->q_rows > 0 && (!a->out || a->ld_o < HD || (a->ld_o * 2) % 16 || !aligned16(a->out)))
+      return set_error(JH_ERR_INVALID, "bad out tensor");
+  } else {
+    if (!a->d_ts_weights) return set_error(JH_ERR_INVALID, "d_ts_weights is NULL");
+    if (a->num_pos > 0 && !a->d_pos_weights) return set_error(JH_ERR_INVALID, "d_pos_weights is NULL");
+    if (a->q_rows > 0 && (!a->dout || !a->dq || a->ld_do < HD || a->ld_dq < HD || (a->ld_do * 2) % 16 ||
+                          !aligned16(a->dout)))
+      return set_error(JH_ERR_INVALID, "bad dout/dq tensor");
+    if (a->kv_rows > 0) {
+      if (!a->dk_accum && (!a->dk || a->ld_dk < HD)) return set_error(JH_ERR_INVALID, "bad dk tensor");
+      if (!a->dv_accum && (!a->dv || a->ld_dv < HD)) return set_error(JH_ERR_INVALID, "bad dv tensor");
+    }
+  }
+  WsLayout w = ws_layout(a->q_rows, a->q_rows, a->num_segments, a->num_heads, a->head_dim);
+  if (!a->workspace || a->workspace_bytes < (bwd ? w.total : w.dq))
+    return set_error(JH_ERR_INVALID, "workspace too small (need >= %zu bytes)", bwd ? w.total : w.dq);
+  return JH_OK;
+}
+
+static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, CUtensorMap* tq, CUtensorMap* tk,
+                   CUtensorMap* tv, CUtensorMap* tdo, cudaStream_t s) {
+  const BiasTable* bt = bias_table_cached(a->num_buckets);
+  if (!bt) return set_error(JH_ERR_INVALID, "num_buckets must be >= 1");
+  memset(p, 0, sizeof(*p));
+  p->seg = SegArgs{a->q_offsets, a->q_pos0, a->kv_start, a->kv_len, a->num_segments};
+  p->ts_q = a->ts_q;
+  p->ts_k = a->ts_k;
+  p->ts_weights = a->ts_weights;
+  p->pos_weights = a->pos_weights;
+  p->num_pos = a->num_pos;
+  p->num_heads = a->num_heads;
+  p->q_rows = a->q_rows;
+  p->kv_rows = a->kv_rows;
+  p->out = (__nv_bfloat16*)a->out;
+  p->ld_o = a->ld_o;
+  p->dk = (__nv_bfloat16*)a->dk;
+  p->dv = (__nv_bfloat16*)a->dv;
+  p->ld_dk = a->ld_dk;
+  p->ld_dv = a->ld_dv;
+  p->dk_accum = a->dk_accum;
+  p->dv_accum = a->dv_accum;
+  p->d_ts_weights = a->d_ts_weights;
+  p->d_pos_weights = a->d_pos_weights;
+  for (int i = 0; i < 64; ++i) {
+    p->bias.thr[i] = bt->thr[i];
+    p->bias.base[i] = bt->base[i];
+  }
+  p->bias.cap = bt->cap;
+  p->bias.nb = a->num_buckets;
+  // workspace carve-up (bound computed with the caller's kv total unknown:
+  // the bwd list is placed after a q_rows-sized fwd list, see ws_layout)
+  WsLayout w = ws_layout(a->q_rows, std::max<int64_t>(a->q_rows, 0), a->num_segments, a->num_heads, a->head_dim);
+  uint8_t* ws = (uint8_t*)a->workspace;
+  p->wl.hdr = (WorkHeader*)ws;
+  p->wl.fwd = (int2*)(ws + w.items_f);
+  p->wl.bwd = (int2*)(ws + w.items_b);
+  // dq accumulator at the end of the caller's workspace (its size is q_rows*H*d*4)
+  size_t dq_bytes = (size_t)a->q_rows * a->num_heads * a->head_dim * 4;
+  p->wl.dq_accum = bwd ? (float*)(ws + ((a->workspace_bytes - dq_bytes) & ~size_t(255))) : nullptr;
+  if (bwd && (uint8_t*)p->wl.dq_accum < ws + w.items_b + 8)
+    return set_error(JH_ERR_INVALID, "workspace too small");
+  const uint64_t HD = (uint64_t)a->num_heads * a->head_dim;
+  if (make_tmap_bf16_2d(tq, a->q, a->q_rows, HD, a->ld_q, 128) ||
+      make_tmap_bf16_2d(tk, a->k, a->kv_rows, HD, a->ld_k, 128) ||
+      make_tmap_bf16_2d(tv, a->v, a->kv_rows, HD, a->ld_v, 128))
+    return set_error(JH_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  if (bwd && make_tmap_bf16_2d(tdo, a->dout, a->q_rows, HD, a->ld_do, 128))
+    return set_error(JH_ERR_CUDA, "cuTensorMapEncodeTiled failed (dout)");
+  build_work_kernel<<<1, 1024, 0, s>>>(p->seg, p->wl);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(JH_ERR_CUDA, "build_work: %s", cudaGetErrorString(e));
+  return JH_OK;
+}
+
+}  // namespace jh
+
+using namespace jh;
+
+extern "C" {
+
+size_t jh_attn_workspace_bytes(int64_t q_rows, int64_t kv_len_total, int64_t num_segments, int32_t num_heads,
+                               int32_t head_dim) {
+  // the layout is q_rows-bounded for the fwd list; the bwd list bound uses
+  // max(kv_len_total, q_rows); dq accumulator last
+  int64_t kvt = std::max(kv_len_total, q_rows);
+  WsLayout a = ws_layout(q_rows, q_rows, num_segments, num_heads, head_dim);
+  WsLayout b = ws_layout(q_rows, kvt, num_segments, num_heads, head_dim);
+  return std::max(a.total, b.total) + 256;
+}
+
+int jh_attn_fwd(const jh_attn_args* a, void* stream) {
+  int rc = validate(a, false);
+  if (rc) return rc;
+  if (a->q_rows == 0 || a->num_segments == 0) return JH_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  AttnParams p;
+  CUtensorMap tq, tk, tv, tdo;
+  rc = prepare(a, false, &p, &tq, &tk, &tv, &tdo, s);
+  if (rc) return rc;
+  int grid = sm_count();
+  int lr = a->head_dim == 64 ? launch_fwd<64>(tq, tk, tv, p, grid, s) : launch_fwd<128>(tq, tk, tv, p, grid, s);
+  if (lr) return set_error(JH_ERR_CUDA, "hstu_fwd launch: %s", cudaGetErrorString(cudaGetLastError()));
+  return JH_OK;
+}
+
+int jh_attn_bwd(const jh_attn_args* a, void* stream) {
+  int rc = validate(a, true);
+  if (rc) return rc;
+  if (a->q_rows == 0 || a->num_segments == 0) return JH_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  AttnParams p;
+  CUtensorMap tq, tk, tv, tdo;
+  rc = prepare(a, true, &p, &tq, &tk, &tv, &tdo, s);
+  if (rc) return rc;
+  int grid = sm_count();
+  int lr = a->head_dim == 64 ? launch_bwd<64>(tq, tk, tv, tdo, p, *a, grid, s)
+                             : launch_bwd<128>(tq, tk, tv, tdo, p, *a, grid, s);
+  if (lr) return set_error(JH_ERR_CUDA, "hstu_bwd launch: %s", cudaGetErrorString(cudaGetLastError()));
+  return JH_OK;
+}
+
+}  // extern "C"

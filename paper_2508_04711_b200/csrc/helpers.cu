@@ -1,0 +1,255 @@
+// Bandwidth-bound helpers (HBM roofline): bucketize, compute_bias, the
+// ts_weights scatter-add gradient, row gather/scatter (reorder / CP pack),
+// jagged <-> padded conversion.  All vectorised 16 B (or 8 B) per lane.
+#include <algorithm>
+
+#include "abi_internal.h"
+#include "bias.cuh"
+
+namespace jh {
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+static int launch_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(JH_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return JH_OK;
+}
+
+static bool fill_dev_table(int nb, DevBiasTable* t) {
+  const BiasTable* h = bias_table_cached(nb);
+  if (!h) return false;
+  for (int i = 0; i < 64; ++i) {
+    t->thr[i] = h->thr[i];
+    t->base[i] = h->base[i];
+  }
+  t->cap = h->cap;
+  t->nb = nb;
+  return true;
+}
+
+// ---------------------------------------------------------------- bucketize
+__global__ void bucketize_kernel(const int64_t* __restrict__ d, int64_t n, const __grid_constant__ DevBiasTable t,
+                                 int32_t* __restrict__ out) {
+  __shared__ int64_t thr[64];
+  __shared__ int32_t base[64];
+  if (threadIdx.x < 64) {
+    thr[threadIdx.x] = t.thr[threadIdx.x];
+    base[threadIdx.x] = t.base[threadIdx.x];
+  }
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = bucket_of(d[i], thr, base, t.cap);
+}
+
+// ------------------------------------------------------------ compute_bias
+// out[i, j] = w[bucket(tq[i] - tk[j])]; 4 outputs per thread, row-wise.
+__global__ void compute_bias_kernel(const int64_t* __restrict__ tq, int64_t nq, const int64_t* __restrict__ tk,
+                                    int64_t nk, const float* __restrict__ w, const __grid_constant__ DevBiasTable t,
+                                    float* __restrict__ out) {
+  __shared__ int64_t thr[64];
+  __shared__ int32_t base[64];
+  __shared__ float ws[256];
+  if (threadIdx.x < 64) {
+    thr[threadIdx.x] = t.thr[threadIdx.x];
+    base[threadIdx.x] = t.base[threadIdx.x];
+  }
+  for (int i = threadIdx.x; i < t.nb && i < 256; i += blockDim.x) ws[i] = w[i];
+  __syncthreads();
+  const int64_t groups_per_row = (nk + 3) / 4;
+  const int64_t total = nq * groups_per_row;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = g / groups_per_row, j0 = (g - i * groups_per_row) * 4;
+    int64_t q = tq[i];
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int64_t j = j0 + u;
+      v[u] = j < nk ? ws[bucket_of(q - tk[j], thr, base, t.cap)] : 0.f;
+    }
+    float* o = out + i * nk + j0;
+    if ((nk & 3) == 0) {
+      *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+      for (int u = 0; u < 4 && j0 + u < nk; ++u) o[u] = v[u];
+    }
+  }
+}
+
+// ------------------------------------------------------------ dbias scatter
+// d_w[b] += sum dbias[i, j] over bucket(tq[i]-tk[j]) == b.  Per-thread fp32
+// partial for the saturated (last) bucket, fp64 smem bins for the rest.
+__global__ void dbias_scatter_kernel(const int64_t* __restrict__ tq, int64_t nq, const int64_t* __restrict__ tk,
+                                     int64_t nk, const float* __restrict__ db, const __grid_constant__ DevBiasTable t,
+                                     double* __restrict__ d_w) {
+  __shared__ int64_t thr[64];
+  __shared__ int32_t base[64];
+  __shared__ double bins[256];
+  if (threadIdx.x < 64) {
+    thr[threadIdx.x] = t.thr[threadIdx.x];
+    base[threadIdx.x] = t.base[threadIdx.x];
+  }
+  for (int i = threadIdx.x; i < t.nb; i += blockDim.x) bins[i] = 0.0;
+  __syncthreads();
+  const int last = t.nb - 1;
+  float sat = 0.f;
+  const int64_t total = nq * nk;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = g / nk, j = g - i * nk;
+    int b = bucket_of(tq[i] - tk[j], thr, base, t.cap);
+    float x = db[g];
+    if (b == last)
+      sat += x;
+    else
+      atomicAdd(&bins[b], (double)x);
+  }
+  // warp-reduce the saturated partial
+  for (int o = 16; o; o >>= 1) sat += __shfl_xor_sync(0xffffffffu, sat, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&bins[last], (double)sat);
+  __syncthreads();
+  for (int i = threadIdx.x; i < t.nb; i += blockDim.x)
+    if (bins[i] != 0.0) atomicAdd(&d_w[i], bins[i]);
+}
+
+// --------------------------------------------------------- row movement
+template <typename V>
+__global__ void gather_rows_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                   const int64_t* __restrict__ perm, int64_t rows, int64_t row_bytes, int scatter) {
+  const int64_t vec_per_row = row_bytes / sizeof(V);
+  const int64_t total = rows * vec_per_row;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = g / vec_per_row, c = g - r * vec_per_row;
+    int64_t p = perm[r];
+    const V* s = reinterpret_cast<const V*>(src + (scatter ? r : p) * row_bytes) + c;
+    V* d = reinterpret_cast<V*>(dst + (scatter ? p : r) * row_bytes) + c;
+    *d = __ldg(s);
+  }
+}
+
+// padded[b, pos, :] <-> values[offsets[b] + pos, :]
+template <typename V>
+__global__ void pad_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                           const int64_t* __restrict__ offsets, int64_t num_seqs, int64_t max_len, int64_t row_bytes,
+                           int to_padded) {
+  const int64_t vec_per_row = row_bytes / sizeof(V);
+  const int64_t total = num_seqs * max_len * vec_per_row;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    int64_t pr = g / vec_per_row, c = g - pr * vec_per_row;
+    int64_t b = pr / max_len, pos = pr - b * max_len;
+    int64_t lo = offsets[b], L = offsets[b + 1] - lo;
+    if (to_padded) {
+      V v;
+      if (pos < L)
+        v = __ldg(reinterpret_cast<const V*>(src + (lo + pos) * row_bytes) + c);
+      else
+        memset(&v, 0, sizeof(V));
+      reinterpret_cast<V*>(dst + pr * row_bytes)[c] = v;
+    } else if (pos < L) {
+      reinterpret_cast<V*>(dst + (lo + pos) * row_bytes)[c] = __ldg(reinterpret_cast<const V*>(src + pr * row_bytes) + c);
+    }
+  }
+}
+
+static int grid_for(int64_t work, int threads) {
+  int64_t g = (work + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms() * 8;
+  return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
+}  // namespace jh
+
+using namespace jh;
+
+extern "C" {
+
+int jh_bucketize(const int64_t* deltas, int64_t n, int num_buckets, int32_t* out, void* stream) {
+  if (n < 0) return set_error(JH_ERR_INVALID, "n must be >= 0");
+  DevBiasTable t;
+  if (!fill_dev_table(num_buckets, &t)) return set_error(JH_ERR_INVALID, "num_buckets must be >= 1");
+  if (n == 0) return JH_OK;
+  bucketize_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(deltas, n, t, out);
+  return launch_check("bucketize");
+}
+
+int jh_compute_bias(const int64_t* ts_q, int64_t nq, const int64_t* ts_k, int64_t nk, const float* ts_weights,
+                    int num_buckets, float* out, void* stream) {
+  if (nq < 0 || nk < 0) return set_error(JH_ERR_INVALID, "sizes must be >= 0");
+  if (num_buckets > 256) return set_error(JH_ERR_UNSUPPORTED, "num_buckets > 256");
+  DevBiasTable t;
+  if (!fill_dev_table(num_buckets, &t)) return set_error(JH_ERR_INVALID, "num_buckets must be >= 1");
+  if (nq == 0 || nk == 0) return JH_OK;
+  int64_t work = nq * ((nk + 3) / 4);
+  compute_bias_kernel<<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(ts_q, nq, ts_k, nk, ts_weights, t, out);
+  return launch_check("compute_bias");
+}
+
+int jh_dbias_scatter(const int64_t* ts_q, int64_t nq, const int64_t* ts_k, int64_t nk, const float* dbias,
+                     int num_buckets, double* d_w, void* stream) {
+  if (nq < 0 || nk < 0) return set_error(JH_ERR_INVALID, "sizes must be >= 0");
+  if (num_buckets > 256) return set_error(JH_ERR_UNSUPPORTED, "num_buckets > 256");
+  DevBiasTable t;
+  if (!fill_dev_table(num_buckets, &t)) return set_error(JH_ERR_INVALID, "num_buckets must be >= 1");
+  if (nq == 0 || nk == 0) return JH_OK;
+  dbias_scatter_kernel<<<grid_for(nq * nk, 256), 256, 0, (cudaStream_t)stream>>>(ts_q, nq, ts_k, nk, dbias, t, d_w);
+  return launch_check("dbias_scatter");
+}
+
+static int rows_common(const void* src, void* dst, const int64_t* perm, int64_t rows, int64_t row_bytes,
+                       void* stream, int scatter) {
+  if (rows < 0 || row_bytes <= 0 || row_bytes % 8)
+    return set_error(JH_ERR_INVALID, "rows must be >= 0 and row_bytes a positive multiple of 8");
+  if (rows == 0) return JH_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  bool v16 = (row_bytes % 16 == 0) && ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0);
+  if (v16)
+    gather_rows_kernel<int4><<<grid_for(rows * row_bytes / 16, 256), 256, 0, s>>>(
+        (const uint8_t*)src, (uint8_t*)dst, perm, rows, row_bytes, scatter);
+  else
+    gather_rows_kernel<int2><<<grid_for(rows * row_bytes / 8, 256), 256, 0, s>>>(
+        (const uint8_t*)src, (uint8_t*)dst, perm, rows, row_bytes, scatter);
+  return launch_check(scatter ? "scatter_rows" : "gather_rows");
+}
+
+int jh_gather_rows(const void* src, void* dst, const int64_t* perm, int64_t rows, int64_t row_bytes, void* stream) {
+  return rows_common(src, dst, perm, rows, row_bytes, stream, 0);
+}
+int jh_scatter_rows(const void* src, void* dst, const int64_t* perm, int64_t rows, int64_t row_bytes, void* stream) {
+  return rows_common(src, dst, perm, rows, row_bytes, stream, 1);
+}
+
+static int pad_common(const void* src, void* dst, const int64_t* offsets, int64_t num_seqs, int64_t max_len,
+                      int64_t row_bytes, void* stream, int to_padded) {
+  if (num_seqs < 0 || max_len < 0 || row_bytes <= 0 || row_bytes % 8)
+    return set_error(JH_ERR_INVALID, "invalid jagged/padded shape");
+  int64_t work = num_seqs * max_len;
+  if (work == 0) return JH_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  bool v16 = (row_bytes % 16 == 0) && ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0);
+  if (v16)
+    pad_kernel<int4><<<grid_for(work * row_bytes / 16, 256), 256, 0, s>>>(
+        (const uint8_t*)src, (uint8_t*)dst, offsets, num_seqs, max_len, row_bytes, to_padded);
+  else
+    pad_kernel<int2><<<grid_for(work * row_bytes / 8, 256), 256, 0, s>>>(
+        (const uint8_t*)src, (uint8_t*)dst, offsets, num_seqs, max_len, row_bytes, to_padded);
+  return launch_check(to_padded ? "jagged_to_padded" : "padded_to_jagged");
+}
+
+int jh_jagged_to_padded(const void* values, const int64_t* offsets, int64_t num_seqs, int64_t max_len,
+                        int64_t row_bytes, void* padded, void* stream) {
+  return pad_common(values, padded, offsets, num_seqs, max_len, row_bytes, stream, 1);
+}
+int jh_padded_to_jagged(const void* padded, const int64_t* offsets, int64_t num_seqs, int64_t max_len,
+                        int64_t row_bytes, void* values, void* stream) {
+  return pad_common(padded, values, offsets, num_seqs, max_len, row_bytes, stream, 0);
+}
+
+}  // extern "C"

@@ -1,0 +1,257 @@
+"""Torch-facing launchers for the C ABI (libjh_hstu.so).
+
+Every function here takes CUDA tensors, validates dtype/device/shape, allocates
+outputs and scratch with the torch caching allocator, and launches on the
+current torch stream through ``_lib``.  No CPU path exists: a non-CUDA tensor
+or a missing library raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import JhAttnArgs, check
+
+_LAUNCHES = {"count": 0}
+
+
+def launch_count() -> int:
+    """Number of jh_* GPU entry points invoked (bench gpu_launches accounting)."""
+    return _LAUNCHES["count"]
+
+
+def _bump(n: int = 1) -> None:
+    _LAUNCHES["count"] += n
+
+
+def _stream(t: torch.Tensor) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _require_cuda(name: str, t: torch.Tensor, dtype=None):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+def _rowmajor(name: str, t: torch.Tensor):
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError(f"{name} must be 2-D with unit column stride")
+
+
+# ----------------------------------------------------------------------- bias
+
+_TABLE_CACHE: dict[int, tuple[np.ndarray, np.ndarray, int]] = {}
+
+
+def bias_table(num_buckets: int):
+    """(thr[64], base[64], cap): the bit-exact octave table (host)."""
+    if num_buckets not in _TABLE_CACHE:
+        thr = (ctypes.c_int64 * 64)()
+        base = (ctypes.c_int32 * 64)()
+        cap = ctypes.c_int64()
+        check(_lib.lib().jh_bias_table_build(int(num_buckets), thr, base, ctypes.byref(cap)), "bias_table")
+        _TABLE_CACHE[num_buckets] = (np.array(thr[:], dtype=np.int64), np.array(base[:], dtype=np.int32), cap.value)
+    return _TABLE_CACHE[num_buckets]
+
+
+def bucketize(deltas: torch.Tensor, num_buckets: int) -> torch.Tensor:
+    _require_cuda("deltas", deltas, torch.int64)
+    d = deltas.contiguous()
+    out = torch.empty(d.shape, dtype=torch.int32, device=d.device)
+    check(_lib.lib().jh_bucketize(_ptr(d), d.numel(), int(num_buckets), _ptr(out), _stream(d)), "bucketize")
+    _bump()
+    return out
+
+
+def compute_bias(ts_q: torch.Tensor, ts_k: torch.Tensor, ts_weights: torch.Tensor, num_buckets: int) -> torch.Tensor:
+    _require_cuda("ts_q", ts_q, torch.int64)
+    _require_cuda("ts_k", ts_k, torch.int64)
+    w = ts_weights.to(device=ts_q.device, dtype=torch.float32).contiguous()
+    tq, tk = ts_q.contiguous(), ts_k.contiguous()
+    out = torch.empty((tq.numel(), tk.numel()), dtype=torch.float32, device=tq.device)
+    check(_lib.lib().jh_compute_bias(_ptr(tq), tq.numel(), _ptr(tk), tk.numel(), _ptr(w), int(num_buckets),
+                                     _ptr(out), _stream(tq)), "compute_bias")
+    _bump()
+    return out
+
+
+def dbias_scatter(ts_q, ts_k, dbias: torch.Tensor, num_buckets: int, d_w: torch.Tensor | None = None):
+    _require_cuda("dbias", dbias, torch.float32)
+    tq, tk, db = ts_q.contiguous(), ts_k.contiguous(), dbias.contiguous()
+    if d_w is None:
+        d_w = torch.zeros(num_buckets, dtype=torch.float64, device=db.device)
+    check(_lib.lib().jh_dbias_scatter(_ptr(tq), tq.numel(), _ptr(tk), tk.numel(), _ptr(db), int(num_buckets),
+                                      _ptr(d_w), _stream(db)), "dbias_scatter")
+    _bump()
+    return d_w
+
+
+# ------------------------------------------------------------------ row moves
+
+def gather_rows(src: torch.Tensor, perm: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """out[i] = src[perm[i]] (jagged.py:244 ``jt.values[perm]``)."""
+    _require_cuda("src", src)
+    _require_cuda("perm", perm, torch.int64)
+    s = src.contiguous()
+    rows = perm.numel()
+    row_bytes = s[0].numel() * s.element_size() if s.shape[0] else (s.numel() and 0)
+    if out is None:
+        out = torch.empty((rows,) + tuple(s.shape[1:]), dtype=s.dtype, device=s.device)
+    if rows:
+        row_bytes = s.stride(0) * s.element_size()
+        check(_lib.lib().jh_gather_rows(_ptr(s), _ptr(out), _ptr(perm), rows, row_bytes, _stream(s)), "gather_rows")
+        _bump()
+    return out
+
+
+def scatter_rows(src: torch.Tensor, perm: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """out[perm[i]] = src[i] (jagged.py:256-257 ``restored[perm] = values``)."""
+    _require_cuda("src", src)
+    _require_cuda("perm", perm, torch.int64)
+    s = src.contiguous()
+    rows = perm.numel()
+    if out is None:
+        out = torch.empty_like(s)
+    if rows:
+        row_bytes = s.stride(0) * s.element_size()
+        check(_lib.lib().jh_scatter_rows(_ptr(s), _ptr(out), _ptr(perm), rows, row_bytes, _stream(s)), "scatter_rows")
+        _bump()
+    return out
+
+
+def jagged_to_padded(values: torch.Tensor, offsets: torch.Tensor, max_len: int) -> torch.Tensor:
+    _require_cuda("values", values)
+    _require_cuda("offsets", offsets, torch.int64)
+    v = values.contiguous()
+    B = offsets.numel() - 1
+    out = torch.empty((B, max_len) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)
+    row_bytes = (v[0].numel() if v.dim() > 1 else 1) * v.element_size()
+    check(_lib.lib().jh_jagged_to_padded(_ptr(v), _ptr(offsets), B, int(max_len), row_bytes, _ptr(out), _stream(v)),
+          "jagged_to_padded")
+    _bump()
+    return out
+
+
+def padded_to_jagged(padded: torch.Tensor, offsets: torch.Tensor, total: int) -> torch.Tensor:
+    _require_cuda("padded", padded)
+    _require_cuda("offsets", offsets, torch.int64)
+    p = padded.contiguous()
+    B, max_len = p.shape[0], p.shape[1]
+    out = torch.empty((total,) + tuple(p.shape[2:]), dtype=p.dtype, device=p.device)
+    row_bytes = int(np.prod(p.shape[2:])) * p.element_size()
+    check(_lib.lib().jh_padded_to_jagged(_ptr(p), _ptr(offsets), B, max_len, row_bytes, _ptr(out), _stream(p)),
+          "padded_to_jagged")
+    _bump()
+    return out
+
+
+# ------------------------------------------------------------------ attention
+
+def _attn_args(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets, pos_weights,
+               q_pos0=None, kv_start=None, kv_len=None):
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        _require_cuda(name, t, torch.bfloat16)
+        _rowmajor(name, t)
+    for name, t in (("ts_q", ts_q), ("ts_k", ts_k), ("q_offsets", q_offsets)):
+        _require_cuda(name, t, torch.int64)
+    D = q.shape[1]
+    if D % num_heads:
+        raise ValueError(f"embed_dim {D} not divisible by num_heads {num_heads}")
+    if k.shape[1] != D or v.shape[1] != D:
+        raise ValueError("q, k, v must share embed_dim")
+    a = JhAttnArgs()
+    a.q, a.k, a.v = q.data_ptr(), k.data_ptr(), v.data_ptr()
+    a.ld_q, a.ld_k, a.ld_v = q.stride(0), k.stride(0), v.stride(0)
+    a.ts_q, a.ts_k = ts_q.data_ptr(), ts_k.data_ptr()
+    a.q_offsets = q_offsets.data_ptr()
+    a.q_pos0 = None if q_pos0 is None else q_pos0.data_ptr()
+    a.kv_start = None if kv_start is None else kv_start.data_ptr()
+    a.kv_len = None if kv_len is None else kv_len.data_ptr()
+    a.num_segments = q_offsets.numel() - 1
+    a.q_rows = q.shape[0]
+    a.kv_rows = k.shape[0]
+    a.num_heads = num_heads
+    a.head_dim = D // num_heads
+    a.ts_weights = ts_weights.data_ptr()
+    a.num_buckets = int(num_buckets)
+    if pos_weights is not None:
+        a.pos_weights = pos_weights.data_ptr()
+        a.num_pos = pos_weights.numel()
+    return a
+
+
+def _workspace(q_rows, kv_total, nseg, H, d, device):
+    nbytes = _lib.lib().jh_attn_workspace_bytes(q_rows, kv_total, nseg, H, d)
+    return torch.empty(nbytes, dtype=torch.uint8, device=device), nbytes
+
+
+def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=16, pos_weights=None,
+             q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, out=None):
+    """Fused jagged HSTU forward (jh_attn_fwd).  bf16 in/out, fp32 weights."""
+    w = ts_weights.to(device=q.device, dtype=torch.float32).contiguous()
+    pw = None if pos_weights is None else pos_weights.to(device=q.device, dtype=torch.float32).contiguous()
+    a = _attn_args(q, k, v, ts_q, ts_k, q_offsets, num_heads, w, num_buckets, pw, q_pos0, kv_start, kv_len)
+    if out is None:
+        out = torch.empty_like(q)
+    a.out, a.ld_o = out.data_ptr(), out.stride(0)
+    ws, nbytes = _workspace(q.shape[0], q.shape[0] if kv_len_total is None else kv_len_total, a.num_segments,
+                            num_heads, a.head_dim, q.device)
+    a.workspace, a.workspace_bytes = ws.data_ptr(), nbytes
+    check(_lib.lib().jh_attn_fwd(ctypes.byref(a), _stream(q)), "hstu_attention forward")
+    _bump(2)  # work-list build + fused forward
+    return out
+
+
+def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_buckets=16, pos_weights=None,
+             q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, accumulate_dkv=False):
+    """Fused jagged HSTU backward (jh_attn_bwd).
+
+    Returns (dq bf16, dk, dv, d_ts_weights f64, d_pos f64 or None); dk/dv are
+    bf16, or fp32 accumulators when ``accumulate_dkv`` (CP partials)."""
+    w = ts_weights.to(device=q.device, dtype=torch.float32).contiguous()
+    pw = None if pos_weights is None else pos_weights.to(device=q.device, dtype=torch.float32).contiguous()
+    a = _attn_args(q, k, v, ts_q, ts_k, q_offsets, num_heads, w, num_buckets, pw, q_pos0, kv_start, kv_len)
+    _require_cuda("dout", dout, torch.bfloat16)
+    _rowmajor("dout", dout)
+    dq = torch.empty_like(q)
+    a.dout, a.ld_do = dout.data_ptr(), dout.stride(0)
+    a.dq, a.ld_dq = dq.data_ptr(), dq.stride(0)
+    if accumulate_dkv:
+        dk = torch.zeros(k.shape, dtype=torch.float32, device=k.device)
+        dv = torch.zeros(v.shape, dtype=torch.float32, device=v.device)
+        a.dk_accum, a.dv_accum = dk.data_ptr(), dv.data_ptr()
+        a.ld_dk = a.ld_dv = k.shape[1]
+    else:
+        dk, dv = torch.empty_like(k), torch.empty_like(v)
+        a.dk, a.dv = dk.data_ptr(), dv.data_ptr()
+        a.ld_dk, a.ld_dv = dk.stride(0), dv.stride(0)
+    d_w = torch.zeros(num_buckets, dtype=torch.float64, device=q.device)
+    a.d_ts_weights = d_w.data_ptr()
+    d_pos = None
+    if pw is not None:
+        d_pos = torch.zeros(pw.numel(), dtype=torch.float64, device=q.device)
+        a.d_pos_weights = d_pos.data_ptr()
+    ws, nbytes = _workspace(q.shape[0], q.shape[0] if kv_len_total is None else kv_len_total, a.num_segments,
+                            num_heads, a.head_dim, q.device)
+    a.workspace, a.workspace_bytes = ws.data_ptr(), nbytes
+    check(_lib.lib().jh_attn_bwd(ctypes.byref(a), _stream(q)), "hstu_attention backward")
+    _bump(4)  # work-list build + dq memset + fused backward + dq convert
+    return dq, dk, dv, d_w, d_pos
+
+
+def debug_umma(a: torch.Tensor, b: torch.Tensor, a_mode: int, b_mode: int) -> torch.Tensor:
+    _require_cuda("a", a, torch.bfloat16)
+    d = torch.empty((128, 128), dtype=torch.float32, device=a.device)
+    check(_lib.lib().jh_debug_umma(_ptr(a.contiguous()), _ptr(b.contiguous()), _ptr(d), a_mode, b_mode, _stream(a)),
+          "debug_umma")
+    return d

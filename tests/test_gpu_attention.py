@@ -1,0 +1,68 @@
+"""GPU parity of the fused jagged HSTU attention against the CPU oracle.
+
+Tolerance (bf16 inputs, fp32 accumulation, bf16 P and outputs): the
+reference's own row-normalized error metric (harness.py:189-206,
+||got-want||_inf,row / max(1, ||want||_inf,row)) <= 2e-2 for out/dq/dk/dv,
+and max|d_w - ref| / max|ref| <= 1e-3 for d_ts_weights.  The oracle is fed
+the identical bf16-rounded inputs (f32 arithmetic).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from _cases import make_case, synthetic, to_cuda, row_rel
+from conftest import load_npz_cases
+
+pytestmark = pytest.mark.gpu
+
+ROW_TOL = 2e-2
+DW_TOL = 1e-3
+
+
+def _fwd(case, H, pos=None):
+    from paper_2508_04711_b200 import kernels
+    c = to_cuda(case)
+    out = kernels.attn_fwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], H, c["w"], case["nb"],
+                           pos_weights=None if pos is None else torch.from_numpy(pos).float().cuda())
+    torch.cuda.synchronize()
+    return out.float().cpu().numpy()
+
+
+@pytest.mark.parametrize("lens,H,d", [
+    ([1], 1, 128), ([5, 0, 17, 1, 32], 1, 64), ([128], 1, 128), ([129, 255, 256, 257], 2, 64),
+    ([300, 77, 1000], 4, 128), ([513, 1, 2, 3], 2, 128),
+])
+def test_fwd_matches_oracle(lens, H, d):
+    case = make_case(lens, H * d, seed=sum(lens) + H)
+    got = _fwd(case, H)
+    want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], case["offsets"], case["w"], 16, H)
+    _, rel = row_rel(got, want)
+    assert rel <= ROW_TOL, rel
+
+
+def test_fwd_unsorted_timestamps_and_small_gaps():
+    # exercises the per-element bucket path on every tile (no saturation)
+    case = make_case([400, 200], 128, seed=5, unsorted_ts=True)
+    got = _fwd(case, 1)
+    want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], case["offsets"], case["w"], 16, 1)
+    assert row_rel(got, want)[1] <= ROW_TOL
+
+
+@pytest.mark.parametrize("name", ["f32_c1_bf16", "f32_d64_bf16_long"])
+def test_fwd_matches_reference_golden(name):
+    c = load_npz_cases("attention_cases.npz")[name]
+    H, nb = (int(x) for x in c["meta"])
+    case = dict(q=c["q"], k=c["k"], v=c["v"], ts=c["ts"], offsets=c["offsets"], w=c["w"], nb=nb)
+    got = _fwd(case, H)
+    assert row_rel(got, c["o"])[1] <= ROW_TOL
+
+
+def test_fwd_synthetic_c2_subset():
+    b = synthetic(7, 0, 8, 1024, 4, 128)
+    case = dict(q=b["q"], k=b["k"], v=b["v"], ts=b["ts"], offsets=b["offsets"],
+                w=oracle.normal_init_ts_weights(16, 7 + 0x5EED), nb=16)
+    got = _fwd(case, 4)
+    want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], case["offsets"], case["w"], 16, 4)
+    assert row_rel(got, want)[1] <= ROW_TOL
