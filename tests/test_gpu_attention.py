@@ -66,3 +66,48 @@ def test_fwd_synthetic_c2_subset():
     got = _fwd(case, 4)
     want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], case["offsets"], case["w"], 16, 4)
     assert row_rel(got, want)[1] <= ROW_TOL
+
+
+def _bwd(case, H, pos=None):
+    from paper_2508_04711_b200 import kernels
+    c = to_cuda(case)
+    dq, dk, dv, dw, dpos = kernels.attn_bwd(
+        c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], c["g"], H, c["w"], case["nb"],
+        pos_weights=None if pos is None else torch.from_numpy(pos).float().cuda())
+    torch.cuda.synchronize()
+    f = lambda t: t.float().cpu().numpy()  # noqa: E731
+    return f(dq), f(dk), f(dv), dw.cpu().numpy(), None if dpos is None else dpos.cpu().numpy()
+
+
+def _check_bwd(case, H, got):
+    dq, dk, dv, dw, _ = got
+    wq, wk, wv, ww, _ = oracle.hstu_backward(case["q"], case["k"], case["v"], case["ts"], case["offsets"],
+                                              case["g"], case["w"], case["nb"], H)
+    for name, a, b in (("dq", dq, wq), ("dk", dk, wk), ("dv", dv, wv)):
+        assert row_rel(a, b)[1] <= ROW_TOL, (name, row_rel(a, b))
+    assert np.abs(dw - ww).max() / max(np.abs(ww).max(), 1e-30) <= DW_TOL, (dw, ww)
+
+
+@pytest.mark.parametrize("lens,H,d", [
+    ([1], 1, 128), ([5, 0, 17, 1, 32], 1, 64), ([128], 1, 128), ([129, 255, 256, 257], 2, 64),
+    ([300, 77, 1000], 4, 128), ([513, 1, 2, 3], 2, 128),
+])
+def test_bwd_matches_oracle(lens, H, d):
+    case = make_case(lens, H * d, seed=sum(lens) + 7 * H)
+    _check_bwd(case, H, _bwd(case, H))
+
+
+def test_bwd_unsorted_timestamps():
+    case = make_case([400, 200], 128, seed=5, unsorted_ts=True)
+    _check_bwd(case, 1, _bwd(case, 1))
+
+
+@pytest.mark.parametrize("name", ["f32_c1_bf16", "f32_d64_bf16_long"])
+def test_bwd_matches_reference_golden(name):
+    c = load_npz_cases("attention_cases.npz")[name]
+    H, nb = (int(x) for x in c["meta"])
+    case = dict(q=c["q"], k=c["k"], v=c["v"], g=c["g"], ts=c["ts"], offsets=c["offsets"], w=c["w"], nb=nb)
+    dq, dk, dv, dw, _ = _bwd(case, H)
+    for a, b in ((dq, c["dq"]), (dk, c["dk"]), (dv, c["dv"])):
+        assert row_rel(a, b)[1] <= ROW_TOL
+    assert np.abs(dw - c["dw"]).max() / np.abs(c["dw"]).max() <= DW_TOL
