@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark: jagged HSTU attention fwd+bwd tokens/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N = 1  -> config C2 (BASELINE.json configs[1]): B=32 sequences, lengths
+          uniform[1,1024], H=4 heads, d=128, bf16, reference generator seed 7.
+N > 1  -> jagged context parallelism over N ranks (one process per GPU,
+          torchrun, NCCL): each rank contributes B=32 sequences (per-rank batch
+          fixed -> weak scaling), sharded by the balanced 2*CP mini-chunk plan.
+
+A step is one forward + backward of the attention over the whole batch.
+``value`` = tokens of all ranks / device step time (inputs resident, L2
+flushed between timed steps); ``e2e`` = the same through the public API with
+host (pinned) inputs copied H2D and d_ts_weights read D2H inside the timed
+region.  ``--impl reference`` times the CPU reference (the oracle port of
+jaggedcp's numpy path) on host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HSTU jagged attn fwd+bwd tokens/sec"
+UNIT = "tokens/s"
+SEED = 7
+B, MAXLEN, H, D = 32, 1024, 4, 128
+NB = 16
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", p["bf16_tflops"])), float(
+            p["hbm_gbs"]), "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def _host_batch(rank: int):
+    from paper_2508_04711_b200.harness import ExperimentConfig, gen_synthetic_host
+    cfg = ExperimentConfig(cp_size=1, batch_size=B, min_len=1, max_len=MAXLEN, max_length=MAXLEN,
+                           embed_dim=H * D, seed=SEED)
+    return gen_synthetic_host(cfg, rank)
+
+
+def _ts_weights():
+    from paper_2508_04711_b200.attention import BiasConfig, BiasParams
+    return BiasParams.normal_init(BiasConfig(NB), SEED + 0x5EED).ts_weights
+
+
+def _flops(lengths) -> float:
+    s = float(sum(int(L) * (int(L) + 1) for L in lengths))
+    return 7.0 * D * H * s, 2.0 * D * H * s, 5.0 * D * H * s
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.2)
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), parts[2:6]))
+                except ValueError:
+                    pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, flags in rows for i, f in enumerate(flags) if f.lower() == "active"})
+        busy = [r[0] for r in rows]
+        return {"sm_mhz": float(np.median(busy)), "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# --------------------------------------------------------------------- GPU arm
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2508_04711_b200 import kernels
+    from paper_2508_04711_b200.attention import (AttentionInputs, BiasConfig, BiasParams,
+                                                 hstu_attention_backward, hstu_attention_reference)
+    from paper_2508_04711_b200.jagged import new_int_series, new_jagged
+
+    h = _host_batch(rank)
+    lens = np.diff(h["offsets"])
+    T = int(h["offsets"][-1])
+    rng = np.random.default_rng([SEED, 99, rank])
+    g_host = rng.standard_normal((T, H * D), dtype=np.float32)
+    w_host = _ts_weights()
+
+    q = torch.from_numpy(h["q"]).to(dev).bfloat16()
+    k = torch.from_numpy(h["k"]).to(dev).bfloat16()
+    v = torch.from_numpy(h["v"]).to(dev).bfloat16()
+    g = torch.from_numpy(g_host).to(dev).bfloat16()
+    ts = torch.from_numpy(h["ts"]).to(dev)
+    offs = torch.from_numpy(h["offsets"]).to(dev)
+    w = torch.from_numpy(w_host.astype(np.float32)).to(dev)
+
+    if world > 1:
+        from paper_2508_04711_b200.cp_layer import CPAttention
+        cp = CPAttention(dist.group.WORLD, H, NB)
+        step_fn = cp.bench_step(q, k, v, ts, h["offsets"], g, w)
+        all_lens = [None] * world
+        dist.all_gather_object(all_lens, [int(x) for x in lens])
+        tokens_total = sum(sum(x) for x in all_lens)
+        flat_lens = [x for r in all_lens for x in r]
+    else:
+        def step_fn(prof=None):
+            kernels.attn_fwd(q, k, v, ts, ts, offs, H, w, NB, prof=None if prof is None else prof[0])
+            return kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, NB, prof=None if prof is None else prof[1])
+        tokens_total = T
+        flat_lens = [int(x) for x in lens]
+
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step_fn()
+    barrier()
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    kev = [((torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)),
+            (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))) for _ in range(K)]
+    launches0 = kernels.launch_count()
+    with Clocks(local) as clk:
+        barrier()
+        for i in range(K):
+            flush.fill_(float(i))  # evict the step's inputs from L2 (512 MiB > 126 MB L2)
+            ev[i][0].record(stream)
+            step_fn(prof=kev[i] if world == 1 else None)
+            ev[i][1].record(stream)
+        barrier()
+    launches = kernels.launch_count() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / K
+    value = tokens_total / (ms_per_step / 1e3)
+
+    peak, peak_sus, hbm, peak_kind = _peaks()
+    F, Ff, Fb = _flops(flat_lens)
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (reference generator harness.py:123, seed 7; q/k/v/dO bf16)",
+        "config": {"workload": "C2: jagged HSTU attention fwd+bwd, B=32/rank, lengths uniform[1,1024], "
+                               "H=4, d=128, nb=16" + ("" if world == 1 else f", jagged CP={world} (balanced)"),
+                   "batch_per_rank": B, "max_seq_len": MAXLEN, "heads": H, "head_dim": D, "tokens": tokens_total,
+                   "parallelism": "single" if world == 1 else f"cp{world}",
+                   "l2": "flushed between timed steps (512 MiB write, outside the timed events)"},
+        "tflops": F / (ms_per_step / 1e3) / 1e12,
+        "tensor_frac_step": F / (ms_per_step / 1e3) / (world * peak * 1e12),
+        "gpu_launches": int(launches),
+    }
+    if world == 1:
+        fwd_ms = float(np.mean([a.elapsed_time(b) for (a, b), _ in kev]))
+        bwd_ms = float(np.mean([a.elapsed_time(b) for _, (a, b) in kev]))
+        ach_b = Fb / (bwd_ms / 1e3) / 1e12
+        ach_f = Ff / (fwd_ms / 1e3) / 1e12
+        result["roofline"] = {
+            "bound": "tensor", "kernel": "hstu_bwd_kernel<128>", "achieved": ach_b, "peak": peak,
+            "unit": "TFLOP/s", "frac": ach_b / peak, "traffic": _traffic("bwd"),
+            "peak_kind": f"{peak_kind} burst bf16 (MEASURED_PEAKS.json)",
+            "algorithmic_flops_per_launch": Fb, "ms_per_launch": bwd_ms,
+            "fwd": {"kernel": "hstu_fwd_kernel<128>", "achieved": ach_f, "frac": ach_f / peak,
+                    "algorithmic_flops_per_launch": Ff, "ms_per_launch": fwd_ms, "traffic": _traffic("fwd")},
+        }
+    result["clocks"] = clk.summary()
+
+    # ---------------- e2e through the public API with host buffers
+    import torch as _t
+    pin = lambda a: _t.from_numpy(a).pin_memory()  # noqa: E731
+    qh, kh, vh = (pin(h[x]).bfloat16().pin_memory() for x in ("q", "k", "v"))
+    gh = pin(g_host).bfloat16().pin_memory()
+    tsh, offh = pin(h["ts"]), h["offsets"]
+    params, bcfg = BiasParams(w_host), BiasConfig(NB)
+    h2d = sum(x.numel() * x.element_size() for x in (qh, kh, vh, gh, tsh)) + 5 * offh.nbytes + 2 * NB * 4
+    d2h = NB * 8
+
+    def e2e_step():
+        qj = new_jagged(qh.to(dev, non_blocking=True), offh, MAXLEN, copy=False)
+        kj = new_jagged(kh.to(dev, non_blocking=True), offh, MAXLEN, copy=False)
+        vj = new_jagged(vh.to(dev, non_blocking=True), offh, MAXLEN, copy=False)
+        tj = new_int_series(tsh.to(dev, non_blocking=True), offh)
+        inp = AttentionInputs(qj, kj, vj, tj, params, bcfg, num_heads=H)
+        hstu_attention_reference(inp)
+        gr = hstu_attention_backward(inp, new_jagged(gh.to(dev, non_blocking=True), offh, MAXLEN, copy=False))
+        return gr.d_ts_weights.cpu()
+
+    if world == 1:
+        for _ in range(max(args.warmup, 3)):
+            e2e_step()
+        torch.cuda.synchronize()
+        Ke = K
+        tot = 0.0
+        for i in range(Ke):
+            flush.fill_(float(i))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            e2e_step()
+            e1.record(stream)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        e2e_ms = tot / Ke
+        result["e2e"] = {"value": T / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                         "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
+                         "api": "paper_2508_04711_b200.attention.hstu_attention_reference + hstu_attention_backward"}
+    else:
+        result["e2e"] = None
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(h, g_host, w_host)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result))
+
+
+def _traffic(which: str):
+    """DRAM bytes per launch from the committed ncu --set full capture (or None)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(which)
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------- CPU legs
+
+def _cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        n = max((i.get("num_threads", 1) for i in info), default=1)
+        return int(n), [{k: i.get(k) for k in ("internal_api", "num_threads")} for i in info]
+    except Exception:
+        return os.cpu_count() or 1, []
+
+
+def _oracle_fwd_bwd(h, g, w, seq_ids):
+    import oracle
+    offs = h["offsets"]
+    rows = np.concatenate([np.arange(offs[b], offs[b + 1]) for b in seq_ids]) if len(seq_ids) else np.zeros(0, int)
+    sub_offs = np.concatenate([[0], np.cumsum([offs[b + 1] - offs[b] for b in seq_ids])]).astype(np.int64)
+    bf = lambda a: a[rows].astype(np.float32)  # noqa: E731
+    q, k, v, gg = bf(h["q"]), bf(h["k"]), bf(h["v"]), bf(g)
+    ts = h["ts"][rows]
+    t0 = time.perf_counter()
+    oracle.hstu_forward(q, k, v, ts, sub_offs, w, NB, H)
+    oracle.hstu_backward(q, k, v, ts, sub_offs, gg, w, NB, H)
+    return time.perf_counter() - t0, int(sub_offs[-1])
+
+
+def cpu_baseline(h, g, w):
+    """Oracle port (numpy restatement of jaggedcp attention.py) on the host's
+    cores: the full C2 batch, fwd+bwd, f32 (a reported baseline only)."""
+    cores, info = _cpu_threads()
+    secs, toks = _oracle_fwd_bwd(h, g, w, list(range(len(h["offsets"]) - 1)))
+    return {"value": toks / secs, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"full C2 batch ({toks} tokens, 32 sequences, 4 heads), fwd+bwd f32, one pass, "
+                      f"{secs:.2f} s", "host_cpus": os.cpu_count(), "blas": info}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (oracle port) on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    h = _host_batch(0)
+    T = int(h["offsets"][-1])
+    rng = np.random.default_rng([SEED, 99, 0])
+    g = rng.standard_normal((T, H * D), dtype=np.float32)
+    w = _ts_weights()
+    lens = np.diff(h["offsets"])
+    # bounded per-step sample: the 3 sequences closest to the median length (~0.6 s / step)
+    order = np.argsort(np.abs(lens - np.median(lens)))[:3]
+    sample = sorted(int(x) for x in order)
+    for _ in range(args.warmup):
+        _oracle_fwd_bwd(h, g, w, sample)
+    tot_s, tot_tok = 0.0, 0
+    for _ in range(args.steps):
+        s, t = _oracle_fwd_bwd(h, g, w, sample)
+        tot_s += s
+        tot_tok += t
+    value = tot_tok / tot_s
+    cores, info = _cpu_threads()
+    desc = f"3 of the 32 C2 sequences per step (lengths {[int(lens[i]) for i in sample]}), 4 heads, fwd+bwd f32"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference generator harness.py:123, seed 7)",
+        "config": {"workload": "C2: jagged HSTU attention fwd+bwd, B=32, lengths uniform[1,1024], H=4, d=128",
+                   "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -127,6 +127,10 @@ typedef struct jh_attn_args {
   /* scratch */
   void* workspace;
   size_t workspace_bytes;
+  /* optional profiling: cudaEvent_t pair recorded on `stream` immediately
+   * before / after the main fused kernel (NULL = off) */
+  void* prof_event_start;
+  void* prof_event_end;
 } jh_attn_args;
 
 /* kv_len_total = sum over segments of kv_len[s] (= q_rows when kv_len is NULL). */

@@ -1,0 +1,246 @@
+"""SPMD jagged context-parallel HSTU attention (one process per GPU).
+
+This is the multi-GPU form of the reference pipeline ``run_pipeline``
+(cp_engine.py:563-598: plan -> redistribute_alltoall -> ring_hstu_attention ->
+restore_outputs), plus the backward pass the reference leaves out
+(SPEC.md:390), over ``torch.distributed`` (NCCL on B200, gloo in CPU tests):
+
+1. plan (cp_engine.py:105-147, exact integers from the C ABI): per-rank
+   sequence lengths are all-gathered once per distinct batch shape and the
+   balanced 2*CP mini-chunk plan is cached;
+2. redistribution = one all-to-all (cp_engine.py:330-371): each rank packs its
+   own sequences' chunks destination-major with the row-gather kernel; the
+   received buffer is already in plan order (source-major == plan order);
+3. KV exchange = all-gather of the resident K, V, ts slabs (cp_engine.py:
+   384-453 rotates them in a ring; summing SiLU partials is order-free, so one
+   gather + one fused attention over the visible prefix gives the same
+   result); the gathered rows are re-ordered into sequence order and each
+   resident chunk attends to its causal prefix [0, chunk end);
+4. backward: dK/dV partials for the whole group batch are reduced to their
+   owners with reduce-scatter, d_ts_weights is all-reduced;
+5. restore = the inverse all-to-all (cp_engine.py:468-525).
+
+Gradient semantics for DDP composition: ts_weights gradients are SUMMED over
+the CP group here (every rank holds different tokens of the same batch);
+average over data-parallel replicas only.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .cp_engine import build_shard_plan
+
+
+@dataclass
+class CPPlan:
+    """Host-side routing for one rank under one batch shape."""
+
+    cp: int
+    rank: int
+    plan: object                 # ShardPlan (global)
+    send_perm: np.ndarray        # local rows, destination-major (seq, chunk order)
+    send_counts: list            # rows to each destination
+    recv_counts: list            # rows from each source (== my resident rows per source)
+    n_res: int                   # resident rows
+    max_res: int                 # max resident rows over ranks (gather padding)
+    res_counts: list             # resident rows of every rank
+    seq_perm: np.ndarray         # group rows (sequence order) -> index in the padded gathered buffer
+    q_offsets: np.ndarray        # resident segments (one per resident chunk)
+    q_pos0: np.ndarray
+    kv_start: np.ndarray
+    kv_len: np.ndarray
+    group_rows: int
+
+
+def build_cp_plan(lengths_per_rank, cp: int, rank: int, balance_mode: str = "balanced_minichunk") -> CPPlan:
+    plan = build_shard_plan(lengths_per_rank, cp, balance_mode)
+    goff = plan.group_offsets()
+    # local sequences of this rank: global ids [base, base + n_local)
+    seq_base = int(np.sum([len(x) for x in lengths_per_rank[:rank]]))
+    local_off = np.concatenate([[0], np.cumsum(lengths_per_rank[rank])]).astype(np.int64)
+    # (1) pack order for redistribution: destination-major, plan order within
+    send_rows, send_counts = [], []
+    for dst in range(cp):
+        n = 0
+        for e in plan.rank_entries[dst]:
+            if plan.seq_owner[e.seq_id] != rank:
+                continue
+            base = int(local_off[e.seq_id - seq_base])
+            send_rows.append(np.arange(base + e.start, base + e.end, dtype=np.int64))
+            n += e.count
+        send_counts.append(n)
+    send_perm = np.concatenate(send_rows) if send_rows else np.zeros(0, np.int64)
+    # (2) receive counts per source (my plan entries, grouped by the contributing rank)
+    recv_counts = [0] * cp
+    for e in plan.rank_entries[rank]:
+        recv_counts[plan.seq_owner[e.seq_id]] += e.count
+    res_counts = list(plan.rank_token_counts())
+    n_res, max_res = res_counts[rank], max(res_counts) if res_counts else 0
+    # (3) sequence-order view of the padded, rank-major gathered buffer
+    seq_perm = np.zeros(int(goff[-1]), dtype=np.int64)
+    for r in range(cp):
+        row = r * max_res
+        for e in plan.rank_entries[r]:
+            g0 = int(goff[e.seq_id])
+            seq_perm[g0 + e.start:g0 + e.end] = np.arange(row, row + e.count, dtype=np.int64)
+            row += e.count
+    # (4) one attention segment per resident chunk: causal prefix [0, end) of its sequence
+    qo, qp, ks, kl = [0], [], [], []
+    for e in plan.rank_entries[rank]:
+        if e.count == 0:
+            continue
+        qo.append(qo[-1] + e.count)
+        qp.append(e.start)
+        ks.append(int(goff[e.seq_id]))
+        kl.append(e.end)
+    return CPPlan(cp, rank, plan, send_perm, send_counts, recv_counts, n_res, max_res, res_counts, seq_perm,
+                  np.asarray(qo, np.int64), np.asarray(qp, np.int64), np.asarray(ks, np.int64),
+                  np.asarray(kl, np.int64), int(goff[-1]))
+
+
+class GpuBackend:
+    """Compute pieces on the B200 kernels (libjh_hstu.so)."""
+
+    def __init__(self):
+        from . import kernels
+        self.k = kernels
+
+    def gather(self, src, perm):
+        return self.k.gather_rows(src, perm)
+
+    def scatter(self, src, perm, out):
+        return self.k.scatter_rows(src, perm, out)
+
+    def fwd(self, q, k, v, ts_q, ts_k, segs, H, w, nb):
+        qo, qp, ks, kl, kvt = segs
+        return self.k.attn_fwd(q, k, v, ts_q, ts_k, qo, H, w, nb, q_pos0=qp, kv_start=ks, kv_len=kl,
+                               kv_len_total=kvt)
+
+    def bwd(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb):
+        qo, qp, ks, kl, kvt = segs
+        dq, dk, dv, dw, _ = self.k.attn_bwd(q, k, v, ts_q, ts_k, qo, g, H, w, nb, q_pos0=qp, kv_start=ks,
+                                            kv_len=kl, kv_len_total=kvt, accumulate_dkv=True)
+        return dq, dk, dv, dw
+
+
+class CPAttention:
+    """Context-parallel jagged HSTU attention over a process group."""
+
+    def __init__(self, group, num_heads: int, num_buckets: int = 16, balance_mode: str = "balanced_minichunk",
+                 backend=None):
+        self.group = group
+        self.cp = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.H = num_heads
+        self.nb = num_buckets
+        self.mode = balance_mode
+        self.be = backend if backend is not None else GpuBackend()
+        self._plans: dict = {}
+
+    # ---------------------------------------------------------------- plan
+    def plan_for(self, local_lengths, device) -> tuple[CPPlan, dict]:
+        key = tuple(int(x) for x in local_lengths)
+        if key not in self._plans:
+            allv = [None] * self.cp
+            dist.all_gather_object(allv, list(key), group=self.group)
+            if len(self._plans) > 64:
+                self._plans.clear()
+            p = build_cp_plan([list(x) for x in allv], self.cp, self.rank, self.mode)
+            t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
+            dev = {"send_perm": t(p.send_perm), "seq_perm": t(p.seq_perm),
+                   "segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.kv_len), int(p.kv_len.sum()))}
+            self._plans[key] = (p, dev)
+        return self._plans[key]
+
+    # ---------------------------------------------------------- collectives
+    def _a2a_rows(self, send, send_counts, recv_counts):
+        out = send.new_empty((int(sum(recv_counts)),) + tuple(send.shape[1:]))
+        dist.all_to_all_single(out, send, list(recv_counts), list(send_counts), group=self.group)
+        return out
+
+    def _redistribute(self, x, p, dev):
+        """local rows -> resident rows in plan order (cp_engine.py:330-371)."""
+        return self._a2a_rows(self.be.gather(x, dev["send_perm"]), p.send_counts, p.recv_counts)
+
+    def _restore(self, x_res, p, dev, n_local):
+        """resident rows -> local rows (cp_engine.py:468-525)."""
+        back = self._a2a_rows(x_res, p.recv_counts, p.send_counts)
+        out = x_res.new_empty((n_local,) + tuple(x_res.shape[1:]))
+        return self.be.scatter(back, dev["send_perm"], out)
+
+    def _gather_seq(self, x_res, p, dev):
+        """resident slabs of all ranks -> group rows in sequence order."""
+        pad = x_res.new_zeros((p.max_res,) + tuple(x_res.shape[1:]))
+        pad[: p.n_res] = x_res
+        full = x_res.new_empty((self.cp * p.max_res,) + tuple(x_res.shape[1:]))
+        dist.all_gather_into_tensor(full, pad, group=self.group)
+        return self.be.gather(full, dev["seq_perm"])
+
+    def _reduce_to_owner(self, x_seq, p, dev):
+        """sum of per-rank partials over group rows (sequence order) -> my resident rows."""
+        full = x_seq.new_zeros((self.cp * p.max_res,) + tuple(x_seq.shape[1:]))
+        self.be.scatter(x_seq, dev["seq_perm"], full)
+        mine = x_seq.new_empty((p.max_res,) + tuple(x_seq.shape[1:]))
+        dist.reduce_scatter_tensor(mine, full, group=self.group)
+        return mine[: p.n_res]
+
+    # --------------------------------------------------------------- passes
+    def forward(self, q, k, v, ts, local_lengths, w):
+        """Local (batch-sharded) q, k, v, ts -> local attention output.
+        Returns (out_local, ctx) where ctx feeds ``backward``."""
+        p, dev = self.plan_for(local_lengths, q.device)
+        q_r, k_r, v_r = (self._redistribute(x, p, dev) for x in (q, k, v))
+        ts_r = self._redistribute(ts.view(-1, 1), p, dev).view(-1)
+        k_s, v_s = self._gather_seq(k_r, p, dev), self._gather_seq(v_r, p, dev)
+        ts_s = self._gather_seq(ts_r.view(-1, 1), p, dev).view(-1)
+        o_r = self.be.fwd(q_r, k_s, v_s, ts_r, ts_s, dev["segs"], self.H, w, self.nb)
+        out = self._restore(o_r, p, dev, q.shape[0])
+        ctx = (p, dev, q_r, k_s, v_s, ts_r, ts_s, q.shape[0])
+        return out, ctx
+
+    def backward(self, ctx, g, w):
+        """Upstream gradient (local rows) -> (dq, dk, dv local; d_ts_weights summed over CP)."""
+        p, dev, q_r, k_s, v_s, ts_r, ts_s, n_local = ctx
+        g_r = self._redistribute(g, p, dev)
+        dq_r, dk_s, dv_s, dw = self.be.bwd(q_r, k_s, v_s, ts_r, ts_s, dev["segs"], g_r, self.H, w, self.nb)
+        dk_r = self._reduce_to_owner(dk_s, p, dev).to(q_r.dtype)
+        dv_r = self._reduce_to_owner(dv_s, p, dev).to(q_r.dtype)
+        dist.all_reduce(dw, group=self.group)
+        dq = self._restore(dq_r, p, dev, n_local)
+        dk = self._restore(dk_r, p, dev, n_local)
+        dv = self._restore(dv_r, p, dev, n_local)
+        return dq, dk, dv, dw
+
+    def bench_step(self, q, k, v, ts, local_offsets, g, w):
+        lengths = np.diff(np.asarray(local_offsets))
+
+        def step(prof=None):
+            _, ctx = self.forward(q, k, v, ts, lengths, w)
+            return self.backward(ctx, g, w)
+
+        return step
+
+
+class _CPAttentionFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, q, k, v, ts_weights, ts, lengths, layer):
+        out, c = layer.forward(q, k, v, ts, lengths, ts_weights)
+        ctx.c, ctx.layer = c, layer
+        ctx.save_for_backward(ts_weights)
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        (w,) = ctx.saved_tensors
+        dq, dk, dv, dw = ctx.layer.backward(ctx.c, g.to(ctx.c[2].dtype).contiguous(), w)
+        return dq, dk, dv, dw.to(w.dtype), None, None, None
+
+
+def cp_hstu_attention(layer: CPAttention, q, k, v, ts, local_lengths, ts_weights):
+    """Differentiable CP attention (gradients to q, k, v and ts_weights)."""
+    return _CPAttentionFn.apply(q, k, v, ts_weights, ts, np.asarray(local_lengths), layer)

@@ -6,17 +6,18 @@
 //
 // kv-tile-major persistent kernel: a work item is (segment, 128-row kv tile)
 // x head; it loops over the q tiles that can see the kv tile.
-//   warp 0      TMA producer: K_j, V_j once per item; Q_i, dO_i double buffered
-//   warp 1      MMA issuer:
-//                 (1) S^T  = K Q^T      -> TMEM [0,128)   (lane = kv row)
-//                 (2) dP^T = V dO^T     -> TMEM [128,256)
-//                 (3) dV  += P^T dO     A = P^T from TMEM (aliases S^T cols 0..63)
-//                 (4) dK  += dS^T Q     A = dS^T in smem (K-major)
-//                 (5) dQ_i = dS K       A = the same smem viewed MN-major -> TMEM [128,256)
-//   warp 2      TMEM allocator (512 columns: S^T | dP^T / dQ | dV | dK)
-//   warps 4..7  epilogue: thread = kv row for (S^T, dP^T) -> (P^T, dS^T, d_w);
-//               thread = q row when draining dQ_i (fp32 red.global.add into
-//               the dq accumulator); dK / dV written once per item.
+//   warp 0       TMA producer: K_j, V_j once per item; Q_i, dO_i, ts_q (2 stages)
+//   warp 1       MMA issuer:
+//                  (1) S^T  = K Q^T      -> TMEM [0,128)   (lane = kv row)
+//                  (2) dP^T = V dO^T     -> TMEM [128,256)
+//                  (3) dV  += P^T dO     A = P^T from TMEM (aliases S^T cols 0..63)
+//                  (4) dK  += dS^T Q     A = dS^T in smem (K-major)
+//                  (5) dQ_i = dS K       A = the same smem viewed MN-major -> TMEM [128,256)
+//   warp 2       TMEM allocator (512 columns: S^T | dP^T / dQ | dV | dK)
+//   warps 4..11  epilogue, two groups of 4 warps (q-column halves): thread =
+//                kv row for (S^T, dP^T) -> (P^T, dS^T, d_w); thread = q row
+//                when draining dQ_i (fp32 red.global.add into the dq
+//                accumulator); group 0 writes dV, group 1 dK once per item.
 // dS carries the 1/sqrt(d) scale so (4), (5) and d_w need no extra pass.
 #include <algorithm>
 
@@ -25,20 +26,22 @@
 
 namespace jh {
 
+constexpr int kBwdEpiWarps = 8;
+constexpr int kBwdThreads = 128 + 32 * kBwdEpiWarps;
+
 template <int D>
 struct BwdCfg {
   static constexpr int TILE = 128 * D * 2;  // one 128-row bf16 operand tile
   static constexpr int PANELS = D / 64;
   static constexpr int K_OFF = 0;
   static constexpr int V_OFF = TILE;
-  static constexpr int Q_OFF = 2 * TILE;             // [2] stages
-  static constexpr int DO_OFF = 4 * TILE;            // [2] stages
-  static constexpr int DS_OFF = 6 * TILE;            // 128 x 128 bf16 (2 panels)
-  static constexpr int TSQ_OFF = DS_OFF + 32768;     // int64 [2][128]
-  static constexpr int QMIN_OFF = TSQ_OFF + 2048;    // int64 [2][4]
-  static constexpr int MAX_NB = (D == 64) ? 256 : 64;  // D=128 leaves 2 KB of smem for everything else
-  static constexpr int W_OFF = QMIN_OFF + 64;        // float [MAX_NB]
-  static constexpr int PW_OFF = W_OFF + MAX_NB * 4;  // float [<=1024] (pos extension, D=64)
+  static constexpr int Q_OFF = 2 * TILE;          // [2] stages
+  static constexpr int DO_OFF = 4 * TILE;         // [2] stages
+  static constexpr int DS_OFF = 6 * TILE;         // 128 x 128 bf16 (2 panels)
+  static constexpr int TSQ_OFF = DS_OFF + 32768;  // int64 [2][kTsSlot]
+  static constexpr int MAX_NB = (D == 64) ? 256 : 32;  // D=128 leaves ~2 KB of smem for the rest
+  static constexpr int W_OFF = TSQ_OFF + 2 * kTsSlot * 8;  // float [MAX_NB]
+  static constexpr int PW_OFF = W_OFF + MAX_NB * 4;    // float [<=1024] (pos extension, D=64)
   static constexpr int BINS_OFF = PW_OFF + (D == 64 ? 4096 : 0);  // double bins [MAX_NB (+1024)]
   static constexpr int NBINS = MAX_NB + (D == 64 ? 1024 : 0);
   static constexpr int BAR_OFF = BINS_OFF + NBINS * 8;
@@ -53,17 +56,16 @@ JH_DEV void red_add_v4(float* addr, float a, float b, float c, float d) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
     hstu_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
-                    const __grid_constant__ AttnParams p) {
+                    const __grid_constant__ CUtensorMap tm_tsq, const __grid_constant__ AttnParams p) {
   using C = BwdCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
   int64_t* s_tsq = reinterpret_cast<int64_t*>(smem + C::TSQ_OFF);
-  int64_t* s_qmin = reinterpret_cast<int64_t*>(smem + C::QMIN_OFF);
   float* s_w = reinterpret_cast<float*>(smem + C::W_OFF);
   float* s_pw = reinterpret_cast<float*>(smem + C::PW_OFF);
-  double* s_bins = reinterpret_cast<double*>(smem + C::BINS_OFF);  // [nb] then [P]
+  double* s_bins = reinterpret_cast<double*>(smem + C::BINS_OFF);  // [MAX_NB] then [P]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* kv_full = bars + 0;
   uint64_t* kv_empty = bars + 1;
@@ -99,12 +101,12 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&qd_empty[i], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(epi_done, 128);
+    mbar_init(epi_done, 32 * kBwdEpiWarps);
     mbar_init(pv_done, 1);
     mbar_init(dq_full, 1);
-    mbar_init(dq_empty, 128);
+    mbar_init(dq_empty, 32 * kBwdEpiWarps);
     mbar_init(dkv_full, 1);
-    mbar_init(dkv_empty, 128);
+    mbar_init(dkv_empty, 32 * kBwdEpiWarps);
     fence_barrier_init();
   }
   if (warp == 0 && lane_id() == 0) {
@@ -112,6 +114,7 @@ __global__ void __launch_bounds__(256, 1)
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
     tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_tsq);
   }
   if (warp == 2) tmem_alloc(s_tmem, 512);
   tc_fence_before();
@@ -154,13 +157,14 @@ __global__ void __launch_bounds__(256, 1)
         for (int t = t0; t < nt; ++t) {
           const int st = qd_it & 1;
           mbar_wait(&qd_empty[st], ((qd_it >> 1) & 1) ^ 1);
-          mbar_expect_tx(&qd_full[st], 2 * C::TILE);
+          mbar_expect_tx(&qd_full[st], 2 * C::TILE + kTsBytes);
           const int32_t qrow = (int32_t)(sg.q_row0 + (int64_t)t * kBM);
           for (int pn = 0; pn < C::PANELS; ++pn) {
             tma_load_2d(smem + C::Q_OFF + st * C::TILE + pn * 16384, &tm_q, h * D + pn * 64, qrow, &qd_full[st]);
             tma_load_2d(smem + C::DO_OFF + st * C::TILE + pn * 16384, &tm_do, h * D + pn * 64, qrow,
                         &qd_full[st]);
           }
+          tma_load_1d(s_tsq + st * kTsSlot, &tm_tsq, qrow & ~1, &qd_full[st]);
           ++qd_it;
         }
       }
@@ -168,9 +172,9 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1) {
     // ================= MMA issuer
     if (elect_one()) {
-      constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);   // S^T, dP^T
-      constexpr uint32_t id_kv = idesc_bf16(128, D, 0, 1);    // dV (A tmem), dK (A smem K-major)
-      constexpr uint32_t id_q = idesc_bf16(128, D, 1, 1);     // dQ (A smem MN-major)
+      constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);  // S^T, dP^T
+      constexpr uint32_t id_kv = idesc_bf16(128, D, 0, 1);   // dV (A tmem), dK (A smem K-major)
+      constexpr uint32_t id_q = idesc_bf16(128, D, 1, 1);    // dQ (A smem MN-major)
       const uint32_t k_base = smem_u32(smem + C::K_OFF);
       const uint32_t v_base = smem_u32(smem + C::V_OFF);
       const uint32_t ds_base = smem_u32(smem + C::DS_OFF);
@@ -209,10 +213,13 @@ __global__ void __launch_bounds__(256, 1)
           if (t == t0) mbar_wait(dkv_empty, (it_cnt & 1) ^ 1);  // dK/dV of the previous item drained
           tc_fence_after();
           const uint32_t acc0 = (t == t0) ? 0u : 1u;
-          // (3) dV += P^T dO
+          // (3) dV += P^T dO.  Packed P^T of q columns [64g, 64g+64) sits in
+          // TMEM columns [64g, 64g+32) (each epilogue group overwrites only
+          // S^T columns it has already read).
 #pragma unroll
           for (int kk = 0; kk < kBM / 16; ++kk)
-            umma_ts(tDV, tS + kk * 8, sdesc_sw128(do_base + kk * 2048, 16384, 1024), id_kv, (kk > 0) ? 1u : acc0);
+            umma_ts(tDV, tS + kk * 8 + (kk >= 4 ? 32 : 0), sdesc_sw128(do_base + kk * 2048, 16384, 1024), id_kv,
+                    (kk > 0) ? 1u : acc0);
           umma_commit(pv_done);
           ++pv_cnt;
           // (4) dK += dS^T Q
@@ -238,16 +245,20 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    // ================= epilogue
-    const int r = tid - 128;  // kv row (S^T/dP^T/dK/dV) or q row (dQ)
-    const int ew = warp & 3;
-    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
+    // ================= epilogue: thread = (row r, column half wg)
+    const int et = tid - 128;
+    const int wg = et >> 7;
+    const int r = et & 127;  // kv row (S^T/dP^T/dK/dV) or q row (dQ)
+    const int lane = r & 31;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const float c1 = 0.5f * rsqrtf((float)D);
     const int64_t cap = p.bias.cap;
-    uint8_t* ds_smem = smem + C::DS_OFF;
-    float sat_w = 0.f, sat_p = 0.f;  // fp32 partials of the saturated buckets (per q tile)
-    double acc_w = 0.0, acc_p = 0.0;
-    uint32_t it_cnt = 0, s_cnt = 0, dq_cnt = 0, tsq_cnt = 0;
+    uint8_t* ds_smem = smem + C::DS_OFF + wg * 16384;  // this group's 64 q columns = one panel
+    float cb = s_w[nb - 1];
+    if (has_pos) cb += s_pw[P - 1];
+    cb *= c1;
+    double acc_w = 0.0, acc_p = 0.0;  // saturated-bucket partials (fp64 across tiles)
+    uint32_t it_cnt = 0, s_cnt = 0, dq_cnt = 0, qd_it = 0;
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
       const int2 it = p.wl.bwd[g / H];
       const int h = g % H;
@@ -256,151 +267,135 @@ __global__ void __launch_bounds__(256, 1)
       q_tiles(sg, it.y, t0, nt);
       const int64_t kv0 = (int64_t)it.y * kBN;
       const int64_t kpos = kv0 + r;
-      const int64_t kv_valid_lim = sg.kv_len;
-      const bool krow_ok = kpos < kv_valid_lim;
+      const bool krow_ok = kpos < sg.kv_len;
       const int64_t krow = sg.kv_row0 + kpos;
       if (t0 >= nt) {
         // no query sees this kv tile: its dK/dV rows are zero
         if (krow_ok && !p.dk_accum) {
-          for (int c = 0; c < D; c += 8) {
-            *reinterpret_cast<int4*>(p.dk + krow * p.ld_dk + h * D + c) = make_int4(0, 0, 0, 0);
-            *reinterpret_cast<int4*>(p.dv + krow * p.ld_dv + h * D + c) = make_int4(0, 0, 0, 0);
-          }
+          __nv_bfloat16* dst = wg ? (p.dk + krow * p.ld_dk) : (p.dv + krow * p.ld_dv);
+          for (int c = 0; c < D; c += 8) *reinterpret_cast<int4*>(dst + h * D + c) = make_int4(0, 0, 0, 0);
         }
         continue;
       }
-      const int64_t tk = krow_ok ? p.ts_k[krow] : INT64_MAX;
-      // first q tile's timestamps
-      int64_t tq_next;
-      {
-        const int64_t qi = (int64_t)t0 * kBM + r;
-        tq_next = qi < sg.lq ? p.ts_q[sg.q_row0 + qi] : INT64_MAX;
-      }
+      const int64_t tk = krow_ok ? p.ts_k[krow] : (INT64_MIN >> 2);
+      const int64_t tk_max = warp_max_i64(tk);
+      const int64_t k_lo = kv0 + (r & ~31), k_hi = k_lo + 31;  // this warp's kv positions
+      const bool warp_k_ok = k_hi < sg.kv_len;
       for (int t = t0; t < nt; ++t) {
-        const int sb = tsq_cnt & 1;
-        ++tsq_cnt;
+        const int st = qd_it & 1;
         const int64_t qrow0 = sg.q_row0 + (int64_t)t * kBM;
-        const int64_t qp_min = sg.qp0 + (int64_t)t * kBM;
+        const int64_t qp_tile = sg.qp0 + (int64_t)t * kBM;
         const int64_t nq = min((int64_t)kBM, sg.lq - (int64_t)t * kBM);
-        const int64_t tq_cur = tq_next;
-        if (t + 1 < nt) {
-          const int64_t qi = (int64_t)(t + 1) * kBM + r;
-          tq_next = qi < sg.lq ? p.ts_q[sg.q_row0 + qi] : INT64_MAX;
-        }
-        s_tsq[sb * 128 + r] = tq_cur;
-        int64_t m = tq_cur;
-        for (int o = 16; o; o >>= 1) {
-          int64_t y = __shfl_xor_sync(0xffffffffu, m, o);
-          m = y < m ? y : m;
-        }
-        if ((r & 31) == 0) s_qmin[sb * 4 + ew] = m;
-        named_bar_sync(1, 128);
-        int64_t qmin = s_qmin[sb * 4];
-        for (int e = 1; e < 4; ++e) qmin = s_qmin[sb * 4 + e] < qmin ? s_qmin[sb * 4 + e] : qmin;
-        // tile classes: full (no mask anywhere), saturated (constant bias)
-        const bool full = (kv0 + kBN - 1 <= qp_min) && (kv0 + kBN <= kv_valid_lim) && (nq == kBM);
-        bool sat = full && (!has_pos || qp_min - (kv0 + kBN - 1) >= P - 1);
-        sat = __all_sync(0xffffffffu, sat && (!krow_ok || qmin - tk >= cap));
-        float cb = s_w[nb - 1];
-        if (has_pos) cb += s_pw[P - 1];
-        cb *= c1;
-
+        mbar_wait(&qd_full[st], (qd_it >> 1) & 1);
+        ++qd_it;
+        const int64_t* tsq = s_tsq + st * kTsSlot + (qrow0 & 1);
         mbar_wait(s_full, s_cnt & 1);
         ++s_cnt;
         tc_fence_after();
+        float sat_w = 0.f, sat_p = 0.f;
 #pragma unroll 1
-        for (int c0 = 0; c0 < kBM; c0 += 32) {
-          uint32_t sv[32], dv[32];
-          tmem_ld32(tS + lane_off + c0, sv);
-          tmem_ld32(tDP + lane_off + c0, dv);
-          tmem_ld_wait();
+        for (int c0 = 64 * wg; c0 < 64 * wg + 64; c0 += 32) {
+          const int64_t qc0 = qp_tile + c0, qc1 = qc0 + 31;
           uint32_t pk[16], dk[16];
-          if (sat) {
+          if (qc1 < k_lo || c0 >= nq) {
+            // every pair of this chunk has its key in the future, or no query
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              float pp[2], dd[2];
-#pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                const float hh = fmaf(__uint_as_float(sv[i + u]), c1, cb);
-                const float th = tanh_approx(hh);
-                pp[u] = fmaf(hh, th, hh);
-                const float gp = __uint_as_float(dv[i + u]);
-                const float ds = fmaf(th, gp, gp) * (fmaf(-hh, th, hh) + 1.f) * c1;
-                dd[u] = ds;
-                sat_w += ds;
-              }
-              pk[i >> 1] = pack_bf16(pp[0], pp[1]);
-              dk[i >> 1] = pack_bf16(dd[0], dd[1]);
-            }
+            for (int i = 0; i < 16; ++i) pk[i] = dk[i] = 0u;
           } else {
+            uint32_t sv[32], dv[32];
+            tmem_ld32(tS + lane_off + c0, sv);
+            tmem_ld32(tDP + lane_off + c0, dv);
+            const bool full = (qc0 >= k_hi) && (c0 + 32 <= nq) && warp_k_ok;
+            bool sat = false;
+            if (full) {
+              const int64_t tq_min = warp_min_i64(tsq[c0 + lane]);
+              sat = (tq_min - tk_max >= cap) && (!has_pos || qc0 - k_hi >= P - 1);
+            }
+            tmem_ld_wait();
+            if (sat) {
+              float tile_sum = 0.f;
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              float pp[2], dd[2];
+              for (int i = 0; i < 32; i += 2) {
+                float pp[2], dd[2];
 #pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                const int qi = c0 + i + u;
-                const int64_t qpos = qp_min + qi;
-                const bool ok = krow_ok && (qi < nq) && (kpos <= qpos);
-                const int64_t tq = s_tsq[sb * 128 + qi];
-                const int b = bucket_of(tq - tk, p.bias.thr, p.bias.base, cap);
-                float bias = s_w[b];
-                int rel = 0;
-                if (has_pos) {
-                  int64_t rr = qpos - kpos;
-                  rel = (int)(rr < 0 ? 0 : (rr > P - 1 ? P - 1 : rr));
-                  bias += s_pw[rel];
+                for (int u = 0; u < 2; ++u) {
+                  const float hh = fmaf(__uint_as_float(sv[i + u]), c1, cb);
+                  const float th = tanh_approx(hh);
+                  pp[u] = fmaf(hh, th, hh);
+                  const float gp = __uint_as_float(dv[i + u]);
+                  dd[u] = fmaf(th, gp, gp) * (fmaf(-hh, th, hh) + 1.f) * c1;
+                  tile_sum += dd[u];
                 }
-                const float hh = (__uint_as_float(sv[i + u]) + bias) * c1;
-                const float th = tanh_approx(hh);
-                const float gp = __uint_as_float(dv[i + u]);
-                const float ds = ok ? fmaf(th, gp, gp) * (fmaf(-hh, th, hh) + 1.f) * c1 : 0.f;
-                pp[u] = ok ? fmaf(hh, th, hh) : 0.f;
-                dd[u] = ds;
-                if (ok) {
-                  if (b == nb - 1)
-                    sat_w += ds;
-                  else
-                    atomicAdd(&s_bins[b], (double)ds);
+                pk[i >> 1] = pack_bf16(pp[0], pp[1]);
+                dk[i >> 1] = pack_bf16(dd[0], dd[1]);
+              }
+              sat_w += tile_sum;
+              if (has_pos) sat_p += tile_sum;  // saturated chunks hit both last buckets
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; i += 2) {
+                float pp[2], dd[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                  const int qi = c0 + i + u;
+                  const int64_t qpos = qp_tile + qi;
+                  const bool ok = krow_ok && (qi < nq) && (kpos <= qpos);
+                  const int b = bucket_of(tsq[qi] - tk, p.bias.thr, p.bias.base, cap);
+                  float bias = s_w[b];
+                  int rel = 0;
                   if (has_pos) {
-                    if (rel == P - 1)
-                      sat_p += ds;
+                    int64_t rr = qpos - kpos;
+                    rel = (int)(rr < 0 ? 0 : (rr > P - 1 ? P - 1 : rr));
+                    bias += s_pw[rel];
+                  }
+                  const float hh = (__uint_as_float(sv[i + u]) + bias) * c1;
+                  const float th = tanh_approx(hh);
+                  const float gp = __uint_as_float(dv[i + u]);
+                  const float ds = ok ? fmaf(th, gp, gp) * (fmaf(-hh, th, hh) + 1.f) * c1 : 0.f;
+                  pp[u] = ok ? fmaf(hh, th, hh) : 0.f;
+                  dd[u] = ds;
+                  if (ok) {
+                    if (b == nb - 1)
+                      sat_w += ds;
                     else
-                      atomicAdd(&s_bins[C::MAX_NB + rel], (double)ds);
+                      atomicAdd(&s_bins[b], (double)ds);
+                    if (has_pos) {
+                      if (rel == P - 1)
+                        sat_p += ds;
+                      else
+                        atomicAdd(&s_bins[C::MAX_NB + rel], (double)ds);
+                    }
                   }
                 }
+                pk[i >> 1] = pack_bf16(pp[0], pp[1]);
+                dk[i >> 1] = pack_bf16(dd[0], dd[1]);
               }
-              pk[i >> 1] = pack_bf16(pp[0], pp[1]);
-              dk[i >> 1] = pack_bf16(dd[0], dd[1]);
             }
           }
-          tmem_st16(tS + lane_off + (c0 >> 1), pk);
-          // dS^T row r, q cols c0..c0+31 -> swizzled K-major smem (panel = c0/64)
-          uint8_t* prow = ds_smem + (c0 >> 6) * 16384;
+          tmem_st16(tS + lane_off + 64 * wg + ((c0 & 63) >> 1), pk);
+          // dS^T row r, q cols c0..c0+31 -> 128B-swizzled K-major smem panel
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
             const uint32_t col = (c0 & 63) + q4 * 8;
-            *reinterpret_cast<int4*>(prow + sw128_offset(r, col)) =
+            *reinterpret_cast<int4*>(ds_smem + sw128_offset(r, col)) =
                 make_int4(dk[4 * q4], dk[4 * q4 + 1], dk[4 * q4 + 2], dk[4 * q4 + 3]);
           }
         }
-        if (sat && has_pos) sat_p = sat_w;  // saturated tiles hit both last buckets
         acc_w += (double)sat_w;
-        acc_p += (double)(has_pos ? sat_p : 0.f);
-        sat_w = 0.f;
-        sat_p = 0.f;
+        acc_p += (double)sat_p;
         tmem_st_wait();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         mbar_arrive(epi_done);
 
-        // ---- drain dQ_i (thread = q row) into the fp32 accumulator
+        // ---- drain dQ_i (thread = q row, group = column half) into the fp32 accumulator
         mbar_wait(dq_full, dq_cnt & 1);
         ++dq_cnt;
         tc_fence_after();
         const bool qrow_ok = r < nq;
         float* dqa = p.wl.dq_accum + (qrow0 + r) * HD + h * D;
 #pragma unroll 1
-        for (int c0 = 0; c0 < D; c0 += 32) {
+        for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 32) {
           uint32_t v[32];
           tmem_ld32(tDP + lane_off + c0, v);
           tmem_ld_wait();
@@ -414,20 +409,19 @@ __global__ void __launch_bounds__(256, 1)
         tc_fence_before();
         mbar_arrive(dq_empty);
       }
-      // ---- dK, dV for this kv tile (thread = kv row)
+      // ---- dV (group 0) / dK (group 1) for this kv tile (thread = kv row)
       mbar_wait(dkv_full, it_cnt & 1);
       ++it_cnt;
       tc_fence_after();
-#pragma unroll 1
-      for (int part = 0; part < 2; ++part) {
-        const uint32_t tsrc = part ? tDK : tDV;
+      {
+        const uint32_t tsrc = wg ? tDK : tDV;
+        float* acc = wg ? p.dk_accum : p.dv_accum;
 #pragma unroll 1
         for (int c0 = 0; c0 < D; c0 += 32) {
           uint32_t v[32];
           tmem_ld32(tsrc + lane_off + c0, v);
           tmem_ld_wait();
           if (!krow_ok) continue;
-          float* acc = part ? p.dk_accum : p.dv_accum;
           if (acc) {
             float* dst = acc + krow * HD + h * D + c0;
 #pragma unroll
@@ -435,8 +429,7 @@ __global__ void __launch_bounds__(256, 1)
               red_add_v4(dst + i, __uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
                          __uint_as_float(v[i + 3]));
           } else {
-            __nv_bfloat16* dst = part ? (p.dk + krow * p.ld_dk) : (p.dv + krow * p.ld_dv);
-            dst += h * D + c0;
+            __nv_bfloat16* dst = (wg ? (p.dk + krow * p.ld_dk) : (p.dv + krow * p.ld_dv)) + h * D + c0;
             uint32_t pk[16];
 #pragma unroll
             for (int i = 0; i < 32; i += 2) pk[i >> 1] = pack_bf16(__uint_as_float(v[i]), __uint_as_float(v[i + 1]));
@@ -450,19 +443,20 @@ __global__ void __launch_bounds__(256, 1)
       mbar_arrive(dkv_empty);
     }
     // ---- flush d_ts_weights / d_pos partials
+#pragma unroll
     for (int o = 16; o; o >>= 1) {
       acc_w += __shfl_xor_sync(0xffffffffu, acc_w, o);
       acc_p += __shfl_xor_sync(0xffffffffu, acc_p, o);
     }
-    if ((r & 31) == 0) {
+    if (lane == 0) {
       atomicAdd(&s_bins[nb - 1], acc_w);
       if (has_pos) atomicAdd(&s_bins[C::MAX_NB + P - 1], acc_p);
     }
-    named_bar_sync(1, 128);
-    for (int i = r; i < nb; i += 128)
+    named_bar_sync(1, 32 * kBwdEpiWarps);
+    for (int i = et; i < nb; i += 32 * kBwdEpiWarps)
       if (s_bins[i] != 0.0) atomicAdd(&p.d_ts_weights[i], s_bins[i]);
     if (has_pos)
-      for (int i = r; i < P; i += 128)
+      for (int i = et; i < P; i += 32 * kBwdEpiWarps)
         if (s_bins[C::MAX_NB + i] != 0.0) atomicAdd(&p.d_pos_weights[i], s_bins[C::MAX_NB + i]);
   }
   tc_fence_before();
@@ -485,8 +479,7 @@ __global__ void dq_convert_kernel(const float* __restrict__ acc, __nv_bfloat16* 
 }
 
 template <int D>
-int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tdo,
-               const AttnParams& p, const jh_attn_args& a, int grid, cudaStream_t s) {
+int launch_bwd(const TMaps& tm, const AttnParams& p, const jh_attn_args& a, int grid, cudaStream_t s) {
   using C = BwdCfg<D>;
   static_assert(C::SMEM <= 232448, "bwd smem budget");
   if (a.num_buckets > C::MAX_NB) {
@@ -503,19 +496,19 @@ int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& 
     attr = true;
   }
   const int64_t HD = (int64_t)a.num_heads * a.head_dim;
-  if (cudaMemsetAsync(p.wl.dq_accum, 0, (size_t)a.q_rows * HD * 4, s) != cudaSuccess) return -1;
-  hstu_bwd_kernel<D><<<grid, 256, C::SMEM, s>>>(tq, tk, tv, tdo, p);
-  if (cudaGetLastError() != cudaSuccess) return -1;
+  if (cudaError_t e = cudaMemsetAsync(p.wl.dq_accum, 0, (size_t)a.q_rows * HD * 4, s)) return (int)e;
+  if (a.prof_event_start) cudaEventRecord((cudaEvent_t)a.prof_event_start, s);
+  hstu_bwd_kernel<D><<<grid, kBwdThreads, C::SMEM, s>>>(tm.q, tm.k, tm.v, tm.dout, tm.tsq, p);
+  if (a.prof_event_end) cudaEventRecord((cudaEvent_t)a.prof_event_end, s);
+  if (cudaError_t e = cudaGetLastError()) return (int)e;
   int64_t work = a.q_rows * HD / 8;
   int cgrid = (int)std::min<int64_t>((work + 255) / 256, (int64_t)grid * 16);
   if (cgrid < 1) cgrid = 1;
   dq_convert_kernel<<<cgrid, 256, 0, s>>>(p.wl.dq_accum, (__nv_bfloat16*)a.dq, a.q_rows, HD, a.ld_dq);
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  return (int)cudaGetLastError();
 }
 
-template int launch_bwd<64>(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
-                            const AttnParams&, const jh_attn_args&, int, cudaStream_t);
-template int launch_bwd<128>(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
-                             const AttnParams&, const jh_attn_args&, int, cudaStream_t);
+template int launch_bwd<64>(const TMaps&, const AttnParams&, const jh_attn_args&, int, cudaStream_t);
+template int launch_bwd<128>(const TMaps&, const AttnParams&, const jh_attn_args&, int, cudaStream_t);
 
 }  // namespace jh

@@ -8,6 +8,11 @@ namespace jh {
 
 constexpr int kBM = 128;  // q rows per tile
 constexpr int kBN = 128;  // kv rows per tile
+// Timestamp tiles are TMA-loaded from an even (16-byte aligned) start row:
+// 136 int64 cover any 128-row tile; element i of the tile is at [(row0 & 1) + i].
+constexpr int kTsBox = 136;
+constexpr int kTsBytes = kTsBox * 8;
+constexpr int kTsSlot = 144;  // int64 stride between smem slots (1152 B)
 
 struct SegArgs {
   const int64_t* q_offsets;
@@ -147,6 +152,11 @@ static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, 
     }
   }
 }
+
+// q, k, v, dout (bf16 2-D) and ts_q, ts_k (int64 1-D) tensor maps
+struct TMaps {
+  CUtensorMap q, k, v, dout, tsq, tsk;
+};
 
 // Parameters shared by the fwd / bwd attention kernels.
 struct AttnParams {

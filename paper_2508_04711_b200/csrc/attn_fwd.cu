@@ -6,13 +6,18 @@
 //
 // Persistent, warp-specialised kernel, one CTA per SM (grid = #SMs), work
 // items (segment, 128-row q tile) x head from the device-built list.
-//   warp 0      TMA producer: Q tile (double buffered), K/V tiles (NS stages)
-//   warp 1      MMA issuer (one lane): S = Q K^T -> TMEM (2 buffers),
-//               O += P V with P read from TMEM (tcgen05 .kind::f16, A in TMEM)
-//   warp 2      TMEM allocator (512 columns)
-//   warps 4..7  epilogue: thread = q row.  S row -> (+bias, *scale, SiLU via
-//               one tanh.approx, causal/jagged mask) -> bf16 P -> TMEM;
-//               final O -> bf16 -> global.
+//   warp 0       TMA producer: Q + ts_q tile (2 buffers), K + ts_k / V tiles
+//                (NS stages, K runs one tile ahead of V; K is released as soon
+//                as S = Q K^T has consumed it, V after O += P V)
+//   warp 1       MMA issuer (one lane): S = Q K^T -> TMEM (2 buffers),
+//                O += P V with P read from TMEM (tcgen05 .kind::f16, A in TMEM)
+//   warp 2       TMEM allocator (512 columns)
+//   warps 4..11  epilogue, two groups of 4 warps; thread = (q row, 64-column
+//                half).  Per 32-column chunk (warp-uniform): fully masked ->
+//                P = 0; unmasked and bias-saturated -> P = h + h*tanh(h) with
+//                h = acc*c + c_bias (2 FFMA + 1 MUFU); otherwise the exact
+//                integer bucket, positional bias and causal/jagged mask.
+//                Final O -> bf16 -> global.
 // TMEM columns: S0 [0,128) S1 [128,256) O [256,256+D) P0 [384,448) P1 [448,512)
 // There is no softmax normaliser: SiLU partials are additive, so O simply
 // accumulates in TMEM across kv tiles (no rescale).
@@ -20,51 +25,58 @@
 
 namespace jh {
 
+constexpr int kEpiWarps = 8;
+constexpr int kFwdThreads = 128 + 32 * kEpiWarps;
+constexpr int kTsRing = 4;  // ts_k tile ring (deeper than the K ring)
+
 template <int D>
 struct FwdCfg {
-  static constexpr int NS = (D == 64) ? 4 : 2;          // kv stages
-  static constexpr int PANELS = D / 64;                 // 64-col swizzle panels
-  static constexpr int TILE_BYTES = 128 * D * 2;        // one 128-row operand tile
+  static constexpr int NS = (D == 64) ? 4 : 2;  // K / V stages
+  static constexpr int PANELS = D / 64;         // 64-col swizzle panels
+  static constexpr int TILE_BYTES = 128 * D * 2;
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = 2 * TILE_BYTES;
   static constexpr int V_OFF = K_OFF + NS * TILE_BYTES;
-  static constexpr int TS_OFF = V_OFF + NS * TILE_BYTES;  // int64 tsk[2][128]
-  static constexpr int KMAX_OFF = TS_OFF + 2 * 128 * 8;   // int64 kmax[2][4]
-  static constexpr int W_OFF = KMAX_OFF + 2 * 4 * 8;      // float w[256]
-  static constexpr int PW_OFF = W_OFF + 256 * 4;          // float pw[<=1024]
-  static constexpr int THR_OFF = PW_OFF + 1024 * 4;       // int64 thr[64]
-  static constexpr int BASE_OFF = THR_OFF + 64 * 8;       // int32 base[64]
-  static constexpr int BAR_OFF = BASE_OFF + 64 * 4;       // mbarriers
-  static constexpr int NBARS = 2 + 2 + 3 * NS + 2 + 2 + 2 + 2;
+  static constexpr int TSQ_OFF = V_OFF + NS * TILE_BYTES;     // int64 [2][kTsSlot]
+  static constexpr int TSK_OFF = TSQ_OFF + 2 * kTsSlot * 8;   // int64 [kTsRing][kTsSlot]
+  static constexpr int W_OFF = TSK_OFF + kTsRing * kTsSlot * 8;  // float w[256]
+  static constexpr int PW_OFF = W_OFF + 256 * 4;           // float pw[<=1024]
+  static constexpr int THR_OFF = PW_OFF + 1024 * 4;        // int64 thr[64]
+  static constexpr int BASE_OFF = THR_OFF + 64 * 8;        // int32 base[64]
+  static constexpr int BAR_OFF = BASE_OFF + 64 * 4;        // mbarriers
+  static constexpr int NBARS = 4 + 4 * NS + 2 * kTsRing + 6 + 2;
   static constexpr int TMEMPTR_OFF = BAR_OFF + NBARS * 8;
-  static constexpr int SMEM = TMEMPTR_OFF + 16 + 1024;  // + alignment slack
+  static constexpr int SMEM = TMEMPTR_OFF + 16;
 };
 
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kFwdThreads, 1)
     hstu_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ AttnParams p) {
+                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_tsq,
+                    const __grid_constant__ CUtensorMap tm_tsk, const __grid_constant__ AttnParams p) {
   using C = FwdCfg<D>;
   constexpr int NS = C::NS;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  int64_t* s_tsk = reinterpret_cast<int64_t*>(smem + C::TS_OFF);
-  int64_t* s_kmax = reinterpret_cast<int64_t*>(smem + C::KMAX_OFF);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  int64_t* s_tsq = reinterpret_cast<int64_t*>(smem + C::TSQ_OFF);
+  int64_t* s_tsk = reinterpret_cast<int64_t*>(smem + C::TSK_OFF);
   float* s_w = reinterpret_cast<float*>(smem + C::W_OFF);
   float* s_pw = reinterpret_cast<float*>(smem + C::PW_OFF);
   int64_t* s_thr = reinterpret_cast<int64_t*>(smem + C::THR_OFF);
   int32_t* s_base = reinterpret_cast<int32_t*>(smem + C::BASE_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
-  uint64_t* q_full = bars;             // [2]
-  uint64_t* q_empty = bars + 2;        // [2]
-  uint64_t* k_full = bars + 4;         // [NS]
-  uint64_t* v_full = k_full + NS;      // [NS]
-  uint64_t* kv_empty = v_full + NS;    // [NS]
-  uint64_t* s_full = kv_empty + NS;    // [2]
-  uint64_t* p_full = s_full + 2;       // [2]
-  uint64_t* p_empty = p_full + 2;      // [2]
-  uint64_t* o_full = p_empty + 2;      // [1]
-  uint64_t* o_empty = o_full + 1;      // [1]
+  uint64_t* q_full = bars;                 // [2]  TMA Q + ts_q
+  uint64_t* q_empty = bars + 2;            // [2]  last S MMA + epilogue read of ts_q
+  uint64_t* k_full = bars + 4;             // [NS]
+  uint64_t* k_empty = k_full + NS;         // [NS] S MMA done
+  uint64_t* v_full = k_empty + NS;         // [NS]
+  uint64_t* v_empty = v_full + NS;         // [NS] PV MMA done
+  uint64_t* ts_full = v_empty + NS;        // [kTsRing]
+  uint64_t* ts_empty = ts_full + kTsRing;  // [kTsRing] epilogue done with the tile
+  uint64_t* s_full = ts_empty + kTsRing;   // [2]
+  uint64_t* p_full = s_full + 2;           // [2]
+  uint64_t* p_empty = p_full + 2;          // [2]
+  uint64_t* o_full = p_empty + 2;          // [1]
+  uint64_t* o_empty = o_full + 1;          // [1]
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::TMEMPTR_OFF);
 
   const uint32_t warp = warp_id();
@@ -72,7 +84,7 @@ __global__ void __launch_bounds__(256, 1)
   const int H = p.num_heads;
   const int nb = p.bias.nb;
 
-  // ---- one-time setup
+  if (smem_u32(smem) & 1023) __trap();  // 128B-swizzled operand tiles need 1 KB alignment
   for (int i = tid; i < 64; i += blockDim.x) {
     s_thr[i] = p.bias.thr[i];
     s_base[i] = p.bias.base[i];
@@ -82,24 +94,31 @@ __global__ void __launch_bounds__(256, 1)
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
-      mbar_init(&q_empty[i], 1);
+      mbar_init(&q_empty[i], 1 + kEpiWarps);
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128);
+      mbar_init(&p_full[i], 32 * kEpiWarps);
       mbar_init(&p_empty[i], 1);
     }
     for (int i = 0; i < NS; ++i) {
       mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < kTsRing; ++i) {
+      mbar_init(&ts_full[i], 1);
+      mbar_init(&ts_empty[i], kEpiWarps);
     }
     mbar_init(o_full, 1);
-    mbar_init(o_empty, 128);
+    mbar_init(o_empty, 32 * kEpiWarps);
     fence_barrier_init();
   }
   if (warp == 0 && lane_id() == 0) {
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
+    tma_prefetch_desc(&tm_tsq);
+    tma_prefetch_desc(&tm_tsk);
   }
   if (warp == 2) tmem_alloc(s_tmem, 512);
   tc_fence_before();
@@ -113,35 +132,48 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0) {
     // ================= TMA producer
     if (elect_one()) {
-      uint32_t q_it = 0, kv_it = 0;
+      uint32_t q_it = 0, k_it = 0, v_it = 0, t_it = 0;
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
         const int2 it = p.wl.fwd[g / H];
         const int h = g % H;
         const Seg sg = load_seg(p.seg, it.x);
-        const int64_t kv_lim = fwd_kv_lim(sg, it.y);
-        const int n = (int)((kv_lim + kBN - 1) / kBN);
+        const int n = (int)((fwd_kv_lim(sg, it.y) + kBN - 1) / kBN);
         if (n == 0) continue;
         const int qb = q_it & 1;
         mbar_wait(&q_empty[qb], ((q_it >> 1) & 1) ^ 1);
-        mbar_expect_tx(&q_full[qb], C::TILE_BYTES);
+        mbar_expect_tx(&q_full[qb], C::TILE_BYTES + kTsBytes);
         const int32_t qrow = (int32_t)(sg.q_row0 + (int64_t)it.y * kBM);
-        for (int pnl = 0; pnl < C::PANELS; ++pnl)
-          tma_load_2d(smem + C::Q_OFF + qb * C::TILE_BYTES + pnl * 16384, &tm_q, h * D + pnl * 64, qrow,
-                      &q_full[qb]);
+        for (int pn = 0; pn < C::PANELS; ++pn)
+          tma_load_2d(smem + C::Q_OFF + qb * C::TILE_BYTES + pn * 16384, &tm_q, h * D + pn * 64, qrow, &q_full[qb]);
+        tma_load_1d(s_tsq + qb * kTsSlot, &tm_tsq, qrow & ~1, &q_full[qb]);
         ++q_it;
-        for (int j = 0; j < n; ++j) {
-          const int st = kv_it % NS;
-          mbar_wait(&kv_empty[st], ((kv_it / NS) & 1) ^ 1);
+        auto load_k = [&](int j) {
+          const int st = k_it % NS;
+          const int ts = t_it % kTsRing;
           const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)j * kBN);
+          mbar_wait(&k_empty[st], ((k_it / NS) & 1) ^ 1);
           mbar_expect_tx(&k_full[st], C::TILE_BYTES);
-          for (int pnl = 0; pnl < C::PANELS; ++pnl)
-            tma_load_2d(smem + C::K_OFF + st * C::TILE_BYTES + pnl * 16384, &tm_k, h * D + pnl * 64, krow,
-                        &k_full[st]);
+          for (int pn = 0; pn < C::PANELS; ++pn)
+            tma_load_2d(smem + C::K_OFF + st * C::TILE_BYTES + pn * 16384, &tm_k, h * D + pn * 64, krow, &k_full[st]);
+          mbar_wait(&ts_empty[ts], ((t_it / kTsRing) & 1) ^ 1);
+          mbar_expect_tx(&ts_full[ts], kTsBytes);
+          tma_load_1d(s_tsk + ts * kTsSlot, &tm_tsk, krow & ~1, &ts_full[ts]);
+          ++k_it;
+          ++t_it;
+        };
+        auto load_v = [&](int j) {
+          const int st = v_it % NS;
+          const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)j * kBN);
+          mbar_wait(&v_empty[st], ((v_it / NS) & 1) ^ 1);
           mbar_expect_tx(&v_full[st], C::TILE_BYTES);
-          for (int pnl = 0; pnl < C::PANELS; ++pnl)
-            tma_load_2d(smem + C::V_OFF + st * C::TILE_BYTES + pnl * 16384, &tm_v, h * D + pnl * 64, krow,
-                        &v_full[st]);
-          ++kv_it;
+          for (int pn = 0; pn < C::PANELS; ++pn)
+            tma_load_2d(smem + C::V_OFF + st * C::TILE_BYTES + pn * 16384, &tm_v, h * D + pn * 64, krow, &v_full[st]);
+          ++v_it;
+        };
+        load_k(0);
+        for (int j = 0; j < n; ++j) {
+          if (j + 1 < n) load_k(j + 1);
+          load_v(j);
         }
       }
     }
@@ -151,22 +183,21 @@ __global__ void __launch_bounds__(256, 1)
       constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_pv = idesc_bf16(128, D, 0, 1);
       const uint32_t tO = tmem + 256;
-      uint32_t q_it = 0, kv_it = 0, s_it = 0, o_it = 0;
+      uint32_t q_it = 0, k_it = 0, v_it = 0, s_it = 0, o_it = 0;
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
         const int2 it = p.wl.fwd[g / H];
         const Seg sg = load_seg(p.seg, it.x);
-        const int64_t kv_lim = fwd_kv_lim(sg, it.y);
-        const int n = (int)((kv_lim + kBN - 1) / kBN);
+        const int n = (int)((fwd_kv_lim(sg, it.y) + kBN - 1) / kBN);
         if (n == 0) continue;
         const int qb = q_it & 1;
         mbar_wait(&q_full[qb], (q_it >> 1) & 1);
         tc_fence_after();
         const uint32_t q_base = smem_u32(smem + C::Q_OFF + qb * C::TILE_BYTES);
-        auto issue_pv = [&](uint32_t sit, uint32_t kvit, bool first) {
-          const int pb = sit & 1;
-          const int st = kvit % NS;
-          mbar_wait(&p_full[pb], (sit >> 1) & 1);
-          mbar_wait(&v_full[st], (kvit / NS) & 1);
+        auto issue_pv = [&](uint32_t sidx, bool first) {
+          const int pb = sidx & 1;
+          const int st = v_it % NS;
+          mbar_wait(&p_full[pb], (sidx >> 1) & 1);
+          mbar_wait(&v_full[st], (v_it / NS) & 1);
           if (first) mbar_wait(o_empty, (o_it & 1) ^ 1);
           tc_fence_after();
           const uint32_t v_base = smem_u32(smem + C::V_OFF + st * C::TILE_BYTES);
@@ -175,13 +206,14 @@ __global__ void __launch_bounds__(256, 1)
           for (int kk = 0; kk < kBN / 16; ++kk)
             umma_ts(tO, tP + kk * 8, sdesc_sw128(v_base + kk * 2048, 16384, 1024), idesc_pv,
                     (first && kk == 0) ? 0u : 1u);
-          umma_commit(&kv_empty[st]);
+          umma_commit(&v_empty[st]);
           umma_commit(&p_empty[pb]);
+          ++v_it;
         };
         for (int j = 0; j < n; ++j) {
-          const int st = kv_it % NS;
+          const int st = k_it % NS;
           const int sb = s_it & 1;
-          mbar_wait(&k_full[st], (kv_it / NS) & 1);
+          mbar_wait(&k_full[st], (k_it / NS) & 1);
           tc_fence_after();
           const uint32_t k_base = smem_u32(smem + C::K_OFF + st * C::TILE_BYTES);
 #pragma unroll
@@ -191,27 +223,34 @@ __global__ void __launch_bounds__(256, 1)
                     idesc_s, kk > 0 ? 1u : 0u);
           }
           umma_commit(&s_full[sb]);
+          umma_commit(&k_empty[st]);
           if (j == n - 1) umma_commit(&q_empty[qb]);
-          if (j > 0) issue_pv(s_it - 1, kv_it - 1, j == 1);
+          ++k_it;
+          // PV of the previous tile, now that the next S is queued
+          if (j > 0) issue_pv(s_it - 1, j == 1);
           ++s_it;
-          ++kv_it;
         }
-        issue_pv(s_it - 1, kv_it - 1, n == 1);
+        issue_pv(s_it - 1, n == 1);
         umma_commit(o_full);
         ++o_it;
         ++q_it;
       }
     }
   } else if (warp >= 4) {
-    // ================= epilogue (thread = q row)
-    const int r = tid - 128;
+    // ================= epilogue: thread = (q row r, column half wg)
+    const int et = tid - 128;
+    const int wg = et >> 7;          // column group: S columns [64*wg, 64*wg+64)
+    const int r = et & 127;          // q row within the tile (= TMEM lane)
+    const int lane = r & 31;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const int ew = warp & 3;
     const float c1 = 0.5f * rsqrtf((float)D);  // SiLU(s) = h + h*tanh(h), h = s/2
     const int64_t cap = p.bias.cap;
-    const bool has_pos = p.num_pos > 0;
     const int P = p.num_pos;
-    uint32_t s_it = 0, o_it = 0;
+    const bool has_pos = P > 0;
+    float cb = s_w[nb - 1];
+    if (has_pos) cb += s_pw[P - 1];
+    cb *= c1;
+    uint32_t q_it = 0, s_it = 0, t_it = 0, o_it = 0;
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
       const int2 it = p.wl.fwd[g / H];
       const int h = g % H;
@@ -220,92 +259,97 @@ __global__ void __launch_bounds__(256, 1)
       const int n = (int)((kv_lim + kBN - 1) / kBN);
       const int64_t nq = min((int64_t)kBM, sg.lq - (int64_t)it.y * kBM);
       const bool row_ok = r < nq;
-      const int64_t qpos = sg.qp0 + (int64_t)it.y * kBM + r;
-      const int64_t qp_min = sg.qp0 + (int64_t)it.y * kBM;
+      const int64_t qp_tile = sg.qp0 + (int64_t)it.y * kBM;
+      const int64_t qpos = qp_tile + r;
       const int64_t qrow = sg.q_row0 + (int64_t)it.y * kBM + r;
       __nv_bfloat16* orow = p.out + qrow * p.ld_o + h * D;
       if (n == 0) {
         if (row_ok)
-          for (int c = 0; c < D; c += 8) *reinterpret_cast<int4*>(orow + c) = make_int4(0, 0, 0, 0);
+          for (int c = wg * (D / 2); c < (wg + 1) * (D / 2); c += 8)
+            *reinterpret_cast<int4*>(orow + c) = make_int4(0, 0, 0, 0);
         continue;
       }
-      const int64_t tq = row_ok ? p.ts_q[qrow] : 0;
-      int64_t tk_next = (r < kv_lim) ? p.ts_k[sg.kv_row0 + r] : INT64_MIN;
+      // this tile's query timestamps (TMA-staged with Q)
+      const int qb = q_it & 1;
+      mbar_wait(&q_full[qb], (q_it >> 1) & 1);
+      const int64_t tq = row_ok ? s_tsq[qb * kTsSlot + ((qrow - r) & 1) + r] : (INT64_MAX >> 2);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&q_empty[qb]);
+      ++q_it;
+      const int64_t tq_min = warp_min_i64(tq);
+      const int64_t row_lo = qp_tile + (r & ~31), row_hi = row_lo + 31;  // warp's q positions
       for (int j = 0; j < n; ++j) {
         const int sb = s_it & 1;
+        const int ts = t_it % kTsRing;
         const int64_t kv0 = (int64_t)j * kBN;
-        // stage this tile's key timestamps (+ tile max) in smem
-        const int64_t tk_cur = tk_next;
-        if (j + 1 < n) {
-          const int64_t kp = kv0 + kBN + r;
-          tk_next = kp < kv_lim ? p.ts_k[sg.kv_row0 + kp] : INT64_MIN;
-        }
-        s_tsk[sb * 128 + r] = tk_cur;
-        int64_t m = tk_cur;
-        for (int o = 16; o; o >>= 1) {
-          int64_t y = __shfl_xor_sync(0xffffffffu, m, o);
-          m = y > m ? y : m;
-        }
-        if ((r & 31) == 0) s_kmax[sb * 4 + ew] = m;
-        named_bar_sync(1, 128);
-        int64_t kmax = s_kmax[sb * 4];
-        for (int e = 1; e < 4; ++e) kmax = s_kmax[sb * 4 + e] > kmax ? s_kmax[sb * 4 + e] : kmax;
-        const bool full = (kv0 + kBN - 1 <= qp_min) && (kv0 + kBN <= kv_lim);
-        bool sat = full && (!has_pos || qp_min - (kv0 + kBN - 1) >= P - 1);
-        sat = __all_sync(0xffffffffu, sat && (!row_ok || tq - kmax >= cap));
-        float cb = s_w[nb - 1];
-        if (has_pos) cb += s_pw[P - 1];
-        cb *= c1;
-
+        mbar_wait(&ts_full[ts], (t_it / kTsRing) & 1);
         mbar_wait(&s_full[sb], (s_it >> 1) & 1);
         mbar_wait(&p_empty[sb], ((s_it >> 1) & 1) ^ 1);
         tc_fence_after();
+        const int64_t* tsk = s_tsk + ts * kTsSlot + ((sg.kv_row0 + kv0) & 1);
         const uint32_t tS = tmem + 128 * sb + lane_off;
         const uint32_t tP = tmem + 384 + 64 * sb + lane_off;
 #pragma unroll 1
-        for (int c0 = 0; c0 < kBN; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(tS + c0, v);
-          tmem_ld_wait();
+        for (int c0 = 64 * wg; c0 < 64 * wg + 64; c0 += 32) {
+          const int64_t kc0 = kv0 + c0, kc1 = kc0 + 31;
           uint32_t pk[16];
-          if (sat) {
+          if (kc0 > row_hi || kc0 >= kv_lim) {
+            // every pair of this chunk is in the future or past the segment
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              const float h0 = fmaf(__uint_as_float(v[i]), c1, cb);
-              const float h1 = fmaf(__uint_as_float(v[i + 1]), c1, cb);
-              pk[i >> 1] = pack_bf16(fmaf(h0, tanh_approx(h0), h0), fmaf(h1, tanh_approx(h1), h1));
-            }
+            for (int i = 0; i < 16; ++i) pk[i] = 0u;
           } else {
-            float pv[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const int64_t kpos = kv0 + c0 + i;
-              const int64_t tk = s_tsk[sb * 128 + c0 + i];
-              float bias = s_w[bucket_of(tq - tk, s_thr, s_base, cap)];
-              if (has_pos) {
-                int64_t rel = qpos - kpos;
-                rel = rel < 0 ? 0 : (rel > P - 1 ? P - 1 : rel);
-                bias += s_pw[rel];
-              }
-              const float hh = (__uint_as_float(v[i]) + bias) * c1;
-              const float y = fmaf(hh, tanh_approx(hh), hh);
-              pv[i] = (kpos <= qpos && kpos < kv_lim) ? y : 0.f;
+            uint32_t v[32];
+            tmem_ld32(tS + c0, v);
+            const bool full = (kc1 <= row_lo) && (kc1 < kv_lim);
+            bool sat = false;
+            if (full) {
+              const int64_t tk_max = warp_max_i64(tsk[c0 + lane]);
+              sat = (tq_min - tk_max >= cap) && (!has_pos || row_lo - kc1 >= P - 1);
             }
+            tmem_ld_wait();
+            if (sat) {
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) pk[i >> 1] = pack_bf16(pv[i], pv[i + 1]);
+              for (int i = 0; i < 32; i += 2) {
+                const float h0 = fmaf(__uint_as_float(v[i]), c1, cb);
+                const float h1 = fmaf(__uint_as_float(v[i + 1]), c1, cb);
+                pk[i >> 1] = pack_bf16(fmaf(h0, tanh_approx(h0), h0), fmaf(h1, tanh_approx(h1), h1));
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; i += 2) {
+                float y[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                  const int64_t kpos = kc0 + i + u;
+                  float bias = s_w[bucket_of(tq - tsk[c0 + i + u], s_thr, s_base, cap)];
+                  if (has_pos) {
+                    int64_t rel = qpos - kpos;
+                    rel = rel < 0 ? 0 : (rel > P - 1 ? P - 1 : rel);
+                    bias += s_pw[rel];
+                  }
+                  const float hh = (__uint_as_float(v[i + u]) + bias) * c1;
+                  const float yy = fmaf(hh, tanh_approx(hh), hh);
+                  y[u] = (kpos <= qpos && kpos < kv_lim) ? yy : 0.f;
+                }
+                pk[i >> 1] = pack_bf16(y[0], y[1]);
+              }
+            }
           }
           tmem_st16(tP + (c0 >> 1), pk);
         }
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[sb]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ts_empty[ts]);
         ++s_it;
+        ++t_it;
       }
-      // ---- O: TMEM -> bf16 -> global
+      // ---- O: TMEM -> bf16 -> global (each group drains half the columns)
       mbar_wait(o_full, o_it & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c0 = 0; c0 < D; c0 += 32) {
+      for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 32) {
         uint32_t v[32];
         tmem_ld32(tmem + 256 + lane_off + c0, v);
         tmem_ld_wait();
@@ -329,21 +373,24 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 template <int D>
-int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const AttnParams& p, int grid,
-               cudaStream_t s) {
+int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& ttq,
+               const CUtensorMap& ttk, const AttnParams& p, int grid, cudaStream_t s, void* ev0, void* ev1) {
   using C = FwdCfg<D>;
+  static_assert(C::SMEM <= 232448, "fwd smem budget");
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(hstu_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
-  hstu_fwd_kernel<D><<<grid, 256, C::SMEM, s>>>(tq, tk, tv, p);
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  if (ev0) cudaEventRecord((cudaEvent_t)ev0, s);
+  hstu_fwd_kernel<D><<<grid, kFwdThreads, C::SMEM, s>>>(tq, tk, tv, ttq, ttk, p);
+  if (ev1) cudaEventRecord((cudaEvent_t)ev1, s);
+  return (int)cudaGetLastError();
 }
 
-template int launch_fwd<64>(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const AttnParams&, int,
-                            cudaStream_t);
-template int launch_fwd<128>(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const AttnParams&, int,
-                             cudaStream_t);
+template int launch_fwd<64>(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                            const CUtensorMap&, const AttnParams&, int, cudaStream_t, void*, void*);
+template int launch_fwd<128>(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                             const CUtensorMap&, const AttnParams&, int, cudaStream_t, void*, void*);
 
 }  // namespace jh

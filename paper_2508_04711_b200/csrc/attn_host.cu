@@ -10,10 +10,10 @@
 namespace jh {
 
 template <int D>
-int launch_fwd(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const AttnParams&, int, cudaStream_t);
+int launch_fwd(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+               const AttnParams&, int, cudaStream_t, void*, void*);
 template <int D>
-int launch_bwd(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const AttnParams&,
-               const jh_attn_args&, int, cudaStream_t);
+int launch_bwd(const TMaps&, const AttnParams&, const jh_attn_args&, int, cudaStream_t);
 
 static int sm_count() {
   static int n = 0;
@@ -87,8 +87,7 @@ static int validate(const jh_attn_args* a, bool bwd) {
   return JH_OK;
 }
 
-static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, CUtensorMap* tq, CUtensorMap* tk,
-                   CUtensorMap* tv, CUtensorMap* tdo, cudaStream_t s) {
+static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cudaStream_t s) {
   const BiasTable* bt = bias_table_cached(a->num_buckets);
   if (!bt) return set_error(JH_ERR_INVALID, "num_buckets must be >= 1");
   memset(p, 0, sizeof(*p));
@@ -130,11 +129,15 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, CUtensorMap* 
   if (bwd && (uint8_t*)p->wl.dq_accum < ws + w.items_b + 8)
     return set_error(JH_ERR_INVALID, "workspace too small");
   const uint64_t HD = (uint64_t)a->num_heads * a->head_dim;
-  if (make_tmap_bf16_2d(tq, a->q, a->q_rows, HD, a->ld_q, 128) ||
-      make_tmap_bf16_2d(tk, a->k, a->kv_rows, HD, a->ld_k, 128) ||
-      make_tmap_bf16_2d(tv, a->v, a->kv_rows, HD, a->ld_v, 128))
+  if ((uintptr_t)a->ts_q % 16 || (uintptr_t)a->ts_k % 16)
+    return set_error(JH_ERR_INVALID, "ts_q / ts_k must be 16-byte aligned");
+  if (make_tmap_bf16_2d(&tm->q, a->q, a->q_rows, HD, a->ld_q, 128) ||
+      make_tmap_bf16_2d(&tm->k, a->k, a->kv_rows, HD, a->ld_k, 128) ||
+      make_tmap_bf16_2d(&tm->v, a->v, a->kv_rows, HD, a->ld_v, 128) ||
+      make_tmap_i64_1d(&tm->tsq, a->ts_q, a->q_rows, kTsBox) ||
+      make_tmap_i64_1d(&tm->tsk, a->ts_k, a->kv_rows, kTsBox))
     return set_error(JH_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  if (bwd && make_tmap_bf16_2d(tdo, a->dout, a->q_rows, HD, a->ld_do, 128))
+  if (bwd && make_tmap_bf16_2d(&tm->dout, a->dout, a->q_rows, HD, a->ld_do, 128))
     return set_error(JH_ERR_CUDA, "cuTensorMapEncodeTiled failed (dout)");
   build_work_kernel<<<1, 1024, 0, s>>>(p->seg, p->wl);
   cudaError_t e = cudaGetLastError();
@@ -164,12 +167,15 @@ int jh_attn_fwd(const jh_attn_args* a, void* stream) {
   if (a->q_rows == 0 || a->num_segments == 0) return JH_OK;
   cudaStream_t s = (cudaStream_t)stream;
   AttnParams p;
-  CUtensorMap tq, tk, tv, tdo;
-  rc = prepare(a, false, &p, &tq, &tk, &tv, &tdo, s);
+  TMaps tm;
+  rc = prepare(a, false, &p, &tm, s);
   if (rc) return rc;
   int grid = sm_count();
-  int lr = a->head_dim == 64 ? launch_fwd<64>(tq, tk, tv, p, grid, s) : launch_fwd<128>(tq, tk, tv, p, grid, s);
-  if (lr) return set_error(JH_ERR_CUDA, "hstu_fwd launch: %s", cudaGetErrorString(cudaGetLastError()));
+  int lr = a->head_dim == 64
+               ? launch_fwd<64>(tm.q, tm.k, tm.v, tm.tsq, tm.tsk, p, grid, s, a->prof_event_start, a->prof_event_end)
+               : launch_fwd<128>(tm.q, tm.k, tm.v, tm.tsq, tm.tsk, p, grid, s, a->prof_event_start, a->prof_event_end);
+  if (lr > 0) return set_error(JH_ERR_CUDA, "hstu_fwd launch: %s", cudaGetErrorString((cudaError_t)lr));
+  if (lr) return JH_ERR_UNSUPPORTED;
   return JH_OK;
 }
 
@@ -179,13 +185,13 @@ int jh_attn_bwd(const jh_attn_args* a, void* stream) {
   if (a->q_rows == 0 || a->num_segments == 0) return JH_OK;
   cudaStream_t s = (cudaStream_t)stream;
   AttnParams p;
-  CUtensorMap tq, tk, tv, tdo;
-  rc = prepare(a, true, &p, &tq, &tk, &tv, &tdo, s);
+  TMaps tm;
+  rc = prepare(a, true, &p, &tm, s);
   if (rc) return rc;
   int grid = sm_count();
-  int lr = a->head_dim == 64 ? launch_bwd<64>(tq, tk, tv, tdo, p, *a, grid, s)
-                             : launch_bwd<128>(tq, tk, tv, tdo, p, *a, grid, s);
-  if (lr) return set_error(JH_ERR_CUDA, "hstu_bwd launch: %s", cudaGetErrorString(cudaGetLastError()));
+  int lr = a->head_dim == 64 ? launch_bwd<64>(tm, p, *a, grid, s) : launch_bwd<128>(tm, p, *a, grid, s);
+  if (lr > 0) return set_error(JH_ERR_CUDA, "hstu_bwd launch: %s", cudaGetErrorString((cudaError_t)lr));
+  if (lr) return JH_ERR_UNSUPPORTED;
   return JH_OK;
 }
 

@@ -42,14 +42,27 @@ JH_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-JH_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+// try_wait with a suspend-time hint: the waiting thread sleeps in hardware
+// until the phase completes instead of spinning through issue slots.
+// A watchdog turns a pipeline deadlock (a protocol bug) into a trap after
+// ~2^36 cycles instead of a hung GPU.
+JH_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "JH_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra JH_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680)
       : "memory");
+  return ok != 0;
+}
+JH_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait(bar, parity)) {
+    if (clock64() - t0 > (1ll << 36)) __trap();
+  }
 }
 
 // Named barrier over a subset of warps (id 0 is __syncthreads).
@@ -68,6 +81,32 @@ JH_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* m, int32_t c0, int32_
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
+}
+
+// 1-D tile load (int64 timestamps), completing on an mbarrier.
+JH_DEV void tma_load_1d(void* smem_dst, const CUtensorMap* m, int32_t c0, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2}], [%3];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(smem_u32(bar))
+      : "memory");
+}
+
+JH_DEV int64_t warp_max_i64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    int64_t y = __shfl_xor_sync(0xffffffffu, v, o);
+    v = y > v ? y : v;
+  }
+  return v;
+}
+JH_DEV int64_t warp_min_i64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    int64_t y = __shfl_xor_sync(0xffffffffu, v, o);
+    v = y < v ? y : v;
+  }
+  return v;
 }
 
 // ---------------------------------------------------------------- tcgen05

@@ -31,4 +31,18 @@ int make_tmap_bf16_2d(CUtensorMap* out, const void* base, uint64_t rows, uint64_
   return r == CUDA_SUCCESS ? 0 : static_cast<int>(r);
 }
 
+int make_tmap_i64_1d(CUtensorMap* out, const void* base, uint64_t n, uint32_t box) {
+  auto enc = get_encode();
+  if (!enc) return -1;
+  if (n == 0) n = 1;
+  cuuint64_t dims[1] = {n};
+  cuuint64_t strides[1] = {8};
+  cuuint32_t bx[1] = {box};
+  cuuint32_t estr[1] = {1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_INT64, 1, const_cast<void*>(base), dims, strides, bx, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : static_cast<int>(r);
+}
+
 }  // namespace jh

@@ -13,4 +13,7 @@ namespace jh {
 int make_tmap_bf16_2d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
                       uint32_t box_rows);
 
+// 1-D int64 vector [n] (timestamps), box of `box` elements, OOB zero-filled.
+int make_tmap_i64_1d(CUtensorMap* out, const void* base, uint64_t n, uint32_t box);
+
 }  // namespace jh

@@ -195,8 +195,17 @@ def _workspace(q_rows, kv_total, nseg, H, d, device):
     return torch.empty(nbytes, dtype=torch.uint8, device=device), nbytes
 
 
+def _prof(a, prof):
+    """prof = (start, end) torch.cuda.Event pair recorded around the main kernel."""
+    if prof is not None:
+        for ev in prof:
+            if ev.cuda_event == 0:
+                ev.record()  # materialise the event handle
+        a.prof_event_start, a.prof_event_end = prof[0].cuda_event, prof[1].cuda_event
+
+
 def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=16, pos_weights=None,
-             q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, out=None):
+             q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, out=None, prof=None):
     """Fused jagged HSTU forward (jh_attn_fwd).  bf16 in/out, fp32 weights."""
     w = ts_weights.to(device=q.device, dtype=torch.float32).contiguous()
     pw = None if pos_weights is None else pos_weights.to(device=q.device, dtype=torch.float32).contiguous()
@@ -207,13 +216,14 @@ def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=
     ws, nbytes = _workspace(q.shape[0], q.shape[0] if kv_len_total is None else kv_len_total, a.num_segments,
                             num_heads, a.head_dim, q.device)
     a.workspace, a.workspace_bytes = ws.data_ptr(), nbytes
+    _prof(a, prof)
     check(_lib.lib().jh_attn_fwd(ctypes.byref(a), _stream(q)), "hstu_attention forward")
     _bump(2)  # work-list build + fused forward
     return out
 
 
 def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_buckets=16, pos_weights=None,
-             q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, accumulate_dkv=False):
+             q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, accumulate_dkv=False, prof=None):
     """Fused jagged HSTU backward (jh_attn_bwd).
 
     Returns (dq bf16, dk, dv, d_ts_weights f64, d_pos f64 or None); dk/dv are
@@ -244,6 +254,7 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
     ws, nbytes = _workspace(q.shape[0], q.shape[0] if kv_len_total is None else kv_len_total, a.num_segments,
                             num_heads, a.head_dim, q.device)
     a.workspace, a.workspace_bytes = ws.data_ptr(), nbytes
+    _prof(a, prof)
     check(_lib.lib().jh_attn_bwd(ctypes.byref(a), _stream(q)), "hstu_attention backward")
     _bump(4)  # work-list build + dq memset + fused backward + dq convert
     return dq, dk, dv, d_w, d_pos

@@ -52,4 +52,9 @@ def to_cuda(case):
 
 
 def row_rel(got, want):
+    """Reference metric (harness.py:189-206); NaN/Inf count as infinite error
+    (the reference guards finiteness separately, harness.py:289-290)."""
+    got = np.asarray(got, dtype=np.float64)
+    if not np.isfinite(got).all():
+        return float("inf"), float("inf")
     return oh.output_errors([got], [want])

@@ -1,0 +1,146 @@
+"""Multi-process (gloo, CPU) test of the SPMD jagged-CP layer's host logic.
+
+The CP routing (plan, all-to-all redistribution, KV all-gather + sequence
+re-order, dK/dV reduce-scatter to owners, restore) runs for real over
+torch.distributed with world_size 2 and 3; the per-rank compute is injected as
+a numpy backend (the GPU kernels are covered by the -m gpu tests).  Outputs
+and gradients must equal the single-device oracle on the concatenated batch
+(plan-independent, harness.py:171-186 reference_outputs).
+"""
+
+import math
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+
+
+def _bias(tq, tk, w, nb):
+    return np.asarray(w)[oracle.bucketize_array(tq[:, None] - tk[None, :], nb)]
+
+
+class NumpyBackend:
+    """Reference-semantics compute on CPU tensors (test double for GpuBackend)."""
+
+    def gather(self, src, perm):
+        return src.index_select(0, perm)
+
+    def scatter(self, src, perm, out):
+        out.index_copy_(0, perm, src)
+        return out
+
+    def _segs(self, segs):
+        qo, qp, ks, kl, _ = segs
+        return qo.numpy(), qp.numpy(), ks.numpy(), kl.numpy()
+
+    def fwd(self, q, k, v, ts_q, ts_k, segs, H, w, nb):
+        qo, qp, ks, kl = self._segs(segs)
+        Q, K, V = q.numpy(), k.numpy(), v.numpy()
+        tq, tk, w = ts_q.numpy(), ts_k.numpy(), w.numpy()
+        d = Q.shape[1] // H
+        out = np.zeros_like(Q)
+        for s in range(len(qp)):
+            a, b = qo[s], qo[s + 1]
+            kr = slice(ks[s], ks[s] + kl[s])
+            mask = np.arange(kl[s])[None, :] <= (qp[s] + np.arange(b - a))[:, None]
+            bias = _bias(tq[a:b], tk[kr], w, nb)
+            for h in range(H):
+                c = slice(h * d, (h + 1) * d)
+                sc = (Q[a:b, c] @ K[kr, c].T + bias) / math.sqrt(d)
+                out[a:b, c] = np.where(mask, oracle.silu(sc), 0.0) @ V[kr, c]
+        return torch.from_numpy(out)
+
+    def bwd(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb):
+        qo, qp, ks, kl = self._segs(segs)
+        Q, K, V, G = q.numpy(), k.numpy(), v.numpy(), g.numpy()
+        tq, tk, w = ts_q.numpy(), ts_k.numpy(), w.numpy()
+        d = Q.shape[1] // H
+        dq, dk, dv = np.zeros_like(Q), np.zeros_like(K), np.zeros_like(V)
+        dw = np.zeros(nb)
+        for s in range(len(qp)):
+            a, b = qo[s], qo[s + 1]
+            kr = slice(ks[s], ks[s] + kl[s])
+            mask = np.arange(kl[s])[None, :] <= (qp[s] + np.arange(b - a))[:, None]
+            buckets = oracle.bucketize_array(tq[a:b, None] - tk[None, kr], nb)
+            bias = w[buckets]
+            for h in range(H):
+                c = slice(h * d, (h + 1) * d)
+                sc = (Q[a:b, c] @ K[kr, c].T + bias) / math.sqrt(d)
+                sig = oracle.sigmoid(sc)
+                A = np.where(mask, sc * sig, 0.0)
+                dv[kr, c] += A.T @ G[a:b, c]
+                dS = np.where(mask, (G[a:b, c] @ V[kr, c].T) * sig * (1 + sc * (1 - sig)), 0.0) / math.sqrt(d)
+                dq[a:b, c] += dS @ K[kr, c]
+                dk[kr, c] += dS.T @ Q[a:b, c]
+                dw += np.bincount(buckets.ravel(), weights=dS.ravel(), minlength=nb)
+        return (torch.from_numpy(dq), torch.from_numpy(dk), torch.from_numpy(dv), torch.from_numpy(dw))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _batch(seed, rank, lengths, D):
+    rng = np.random.default_rng([seed, rank])
+    T = int(sum(lengths))
+    offs = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    q, k, v, g = (rng.standard_normal((T, D)) for _ in range(4))
+    ts = np.zeros(T, dtype=np.int64)
+    for b, L in enumerate(lengths):
+        ts[offs[b]:offs[b] + L] = int(rng.integers(0, 10**9)) + np.cumsum(rng.integers(1, 10**6, size=L))
+    return dict(q=q, k=k, v=v, g=g, ts=ts, offsets=offs)
+
+
+def _worker(rank, world, port, lens, H, D, mode, result_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2508_04711_b200.cp_layer import CPAttention
+    b = _batch(3, rank, lens[rank], H * D)
+    w = torch.from_numpy(oracle.normal_init_ts_weights(16, 11))
+    layer = CPAttention(dist.group.WORLD, H, 16, balance_mode=mode, backend=NumpyBackend())
+    t = {key: torch.from_numpy(b[key]) for key in ("q", "k", "v", "g", "ts")}
+    out, ctx = layer.forward(t["q"], t["k"], t["v"], t["ts"], np.diff(b["offsets"]), w)
+    dq, dk, dv, dw = layer.backward(ctx, t["g"], w)
+    np.savez(os.path.join(result_dir, f"r{rank}.npz"), out=out.numpy(), dq=dq.numpy(), dk=dk.numpy(),
+             dv=dv.numpy(), dw=dw.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,lens,mode", [
+    (2, [[7, 0, 33], [12, 1]], "balanced_minichunk"),
+    (3, [[20, 5], [], [9, 40, 2]], "balanced_minichunk"),
+    (2, [[31, 4], [17]], "naive_contiguous"),
+])
+def test_cp_layer_matches_single_device(tmp_path, world, lens, mode):
+    H, D = 2, 4
+    mp.spawn(_worker, args=(world, _free_port(), lens, H, D, mode, str(tmp_path)), nprocs=world, join=True)
+    batches = [_batch(3, r, lens[r], H * D) for r in range(world)]
+    cat = oracle.concat_batches(batches)
+    g = np.concatenate([b["g"] for b in batches])
+    w = oracle.normal_init_ts_weights(16, 11)
+    want = oracle.hstu_forward(cat["q"], cat["k"], cat["v"], cat["ts"], cat["offsets"], w, 16, H)
+    wq, wk, wv, ww, _ = oracle.hstu_backward(cat["q"], cat["k"], cat["v"], cat["ts"], cat["offsets"], g, w, 16, H)
+    row = 0
+    for r in range(world):
+        res = np.load(os.path.join(tmp_path, f"r{r}.npz"))
+        n = batches[r]["q"].shape[0]
+        sl = slice(row, row + n)
+        for name, got, ref in (("out", res["out"], want[sl]), ("dq", res["dq"], wq[sl]), ("dk", res["dk"], wk[sl]),
+                               ("dv", res["dv"], wv[sl])):
+            assert got.shape == ref.shape and (got.size == 0 or np.abs(got - ref).max() < 1e-10), (r, name)
+        assert np.abs(res["dw"] - ww).max() < 1e-10
+        row += n
