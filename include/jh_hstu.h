@@ -131,6 +131,10 @@ typedef struct jh_attn_args {
    * before / after the main fused kernel (NULL = off) */
   void* prof_event_start;
   void* prof_event_end;
+  /* optional debug timeline: uint64 [5 roles][4096 events][2] written by CTA
+   * `trace_cta` (NULL = off) */
+  void* trace;
+  int32_t trace_cta;
 } jh_attn_args;
 
 /* kv_len_total = sum over segments of kv_len[s] (= q_rows when kv_len is NULL). */

@@ -42,6 +42,7 @@ class JhAttnArgs(ctypes.Structure):
         ("d_ts_weights", c_vp), ("d_pos_weights", c_vp),
         ("workspace", c_vp), ("workspace_bytes", ctypes.c_size_t),
         ("prof_event_start", c_vp), ("prof_event_end", c_vp),
+        ("trace", c_vp), ("trace_cta", ctypes.c_int32),
     ]
 
 

@@ -181,6 +181,21 @@ struct AttnParams {
   double* d_pos_weights;
   WorkLists wl;
   DevBiasTable bias;
+  // debug timeline (NULL = off): CTA trace_cta records (code, arg, clock64)
+  // per role into trace[role * kTraceCap * 2 ...]
+  unsigned long long* trace;
+  int32_t trace_cta;
 };
+
+constexpr int kTraceCap = 4096;
+
+// One event from the calling thread (callers pass only one thread per role).
+JH_DEV void trace_ev(const AttnParams& p, int role, uint32_t& cnt, uint32_t code, uint32_t arg) {
+  if (p.trace == nullptr || (int)blockIdx.x != p.trace_cta || cnt >= (uint32_t)kTraceCap) return;
+  unsigned long long* t = p.trace + ((size_t)role * kTraceCap + cnt) * 2;
+  t[0] = ((unsigned long long)code << 32) | arg;
+  t[1] = (unsigned long long)clock64();
+  ++cnt;
+}
 
 }  // namespace jh

@@ -41,10 +41,10 @@ struct FwdCfg {
   static constexpr int TSK_OFF = TSQ_OFF + 2 * kTsSlot * 8;   // int64 [kTsRing][kTsSlot]
   static constexpr int W_OFF = TSK_OFF + kTsRing * kTsSlot * 8;  // float w[256]
   static constexpr int PW_OFF = W_OFF + 256 * 4;           // float pw[<=1024]
-  static constexpr int THR_OFF = PW_OFF + 1024 * 4;        // int64 thr[64]
-  static constexpr int BASE_OFF = THR_OFF + 64 * 8;        // int32 base[64]
-  static constexpr int BAR_OFF = BASE_OFF + 64 * 4;        // mbarriers
-  static constexpr int NBARS = 4 + 4 * NS + 2 * kTsRing + 6 + 2;
+  static constexpr int TAB_OFF = PW_OFF + 1024 * 4;        // SmemBias (160 B)
+  static constexpr int KMAX_OFF = TAB_OFF + 256;           // int64 [kTsRing][4] per-chunk max ts_k
+  static constexpr int BAR_OFF = KMAX_OFF + kTsRing * 32;  // mbarriers
+  static constexpr int NBARS = 4 + 4 * NS + 3 * kTsRing + 6 + 2;
   static constexpr int TMEMPTR_OFF = BAR_OFF + NBARS * 8;
   static constexpr int SMEM = TMEMPTR_OFF + 16;
 };
@@ -61,8 +61,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   int64_t* s_tsk = reinterpret_cast<int64_t*>(smem + C::TSK_OFF);
   float* s_w = reinterpret_cast<float*>(smem + C::W_OFF);
   float* s_pw = reinterpret_cast<float*>(smem + C::PW_OFF);
-  int64_t* s_thr = reinterpret_cast<int64_t*>(smem + C::THR_OFF);
-  int32_t* s_base = reinterpret_cast<int32_t*>(smem + C::BASE_OFF);
+  SmemBias* s_bias = reinterpret_cast<SmemBias*>(smem + C::TAB_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* q_full = bars;                 // [2]  TMA Q + ts_q
   uint64_t* q_empty = bars + 2;            // [2]  last S MMA + epilogue read of ts_q
@@ -72,6 +71,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* v_empty = v_full + NS;         // [NS] PV MMA done
   uint64_t* ts_full = v_empty + NS;        // [kTsRing]
   uint64_t* ts_empty = ts_full + kTsRing;  // [kTsRing] epilogue done with the tile
+  uint64_t* tsx_full = bars + 4 + 4 * NS + 2 * kTsRing + 6 + 2;  // [kTsRing] chunk maxima ready
+  int64_t* s_kmax = reinterpret_cast<int64_t*>(smem + C::KMAX_OFF);
   uint64_t* s_full = ts_empty + kTsRing;   // [2]
   uint64_t* p_full = s_full + 2;           // [2]
   uint64_t* p_empty = p_full + 2;          // [2]
@@ -85,10 +86,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int nb = p.bias.nb;
 
   if (smem_u32(smem) & 1023) __trap();  // 128B-swizzled operand tiles need 1 KB alignment
-  for (int i = tid; i < 64; i += blockDim.x) {
-    s_thr[i] = p.bias.thr[i];
-    s_base[i] = p.bias.base[i];
-  }
+  smem_bias_fill(s_bias, p.bias, tid, blockDim.x);
   for (int i = tid; i < nb; i += blockDim.x) s_w[i] = p.ts_weights[i];
   for (int i = tid; i < p.num_pos; i += blockDim.x) s_pw[i] = p.pos_weights[i];
   if (tid == 0) {
@@ -108,6 +106,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     for (int i = 0; i < kTsRing; ++i) {
       mbar_init(&ts_full[i], 1);
       mbar_init(&ts_empty[i], kEpiWarps);
+      mbar_init(&tsx_full[i], 1);
     }
     mbar_init(o_full, 1);
     mbar_init(o_empty, 32 * kEpiWarps);
@@ -132,7 +131,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp == 0) {
     // ================= TMA producer
     if (elect_one()) {
-      uint32_t q_it = 0, k_it = 0, v_it = 0, t_it = 0;
+      uint32_t q_it = 0, k_it = 0, v_it = 0, t_it = 0, tcnt = 0;
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
         const int2 it = p.wl.fwd[g / H];
         const int h = g % H;
@@ -141,6 +140,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (n == 0) continue;
         const int qb = q_it & 1;
         mbar_wait(&q_empty[qb], ((q_it >> 1) & 1) ^ 1);
+        trace_ev(p, 0, tcnt, 1, g);
         mbar_expect_tx(&q_full[qb], C::TILE_BYTES + kTsBytes);
         const int32_t qrow = (int32_t)(sg.q_row0 + (int64_t)it.y * kBM);
         for (int pn = 0; pn < C::PANELS; ++pn)
@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const int ts = t_it % kTsRing;
           const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)j * kBN);
           mbar_wait(&k_empty[st], ((k_it / NS) & 1) ^ 1);
+          trace_ev(p, 0, tcnt, 2, j);
           mbar_expect_tx(&k_full[st], C::TILE_BYTES);
           for (int pn = 0; pn < C::PANELS; ++pn)
             tma_load_2d(smem + C::K_OFF + st * C::TILE_BYTES + pn * 16384, &tm_k, h * D + pn * 64, krow, &k_full[st]);
@@ -165,6 +166,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const int st = v_it % NS;
           const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)j * kBN);
           mbar_wait(&v_empty[st], ((v_it / NS) & 1) ^ 1);
+          trace_ev(p, 0, tcnt, 3, j);
           mbar_expect_tx(&v_full[st], C::TILE_BYTES);
           for (int pn = 0; pn < C::PANELS; ++pn)
             tma_load_2d(smem + C::V_OFF + st * C::TILE_BYTES + pn * 16384, &tm_v, h * D + pn * 64, krow, &v_full[st]);
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_pv = idesc_bf16(128, D, 0, 1);
       const uint32_t tO = tmem + 256;
-      uint32_t q_it = 0, k_it = 0, v_it = 0, s_it = 0, o_it = 0;
+      uint32_t q_it = 0, k_it = 0, v_it = 0, s_it = 0, o_it = 0, tcnt = 0;
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
         const int2 it = p.wl.fwd[g / H];
         const Seg sg = load_seg(p.seg, it.x);
@@ -197,6 +199,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const int pb = sidx & 1;
           const int st = v_it % NS;
           mbar_wait(&p_full[pb], (sidx >> 1) & 1);
+          trace_ev(p, 1, tcnt, 11, sidx);
           mbar_wait(&v_full[st], (v_it / NS) & 1);
           if (first) mbar_wait(o_empty, (o_it & 1) ^ 1);
           tc_fence_after();
@@ -214,6 +217,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const int st = k_it % NS;
           const int sb = s_it & 1;
           mbar_wait(&k_full[st], (k_it / NS) & 1);
+          trace_ev(p, 1, tcnt, 10, s_it);
           tc_fence_after();
           const uint32_t k_base = smem_u32(smem + C::K_OFF + st * C::TILE_BYTES);
 #pragma unroll
@@ -236,6 +240,29 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         ++q_it;
       }
     }
+  } else if (warp == 3) {
+    // ================= ts_k tile statistics: per 32-column chunk maximum
+    // (used by the epilogue's warp-uniform saturation test)
+    const int lane = lane_id();
+    uint32_t t_it = 0;
+    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      const int2 it = p.wl.fwd[g / H];
+      const Seg sg = load_seg(p.seg, it.x);
+      const int n = (int)((fwd_kv_lim(sg, it.y) + kBN - 1) / kBN);
+      for (int j = 0; j < n; ++j) {
+        const int ts = t_it % kTsRing;
+        mbar_wait(&ts_full[ts], (t_it / kTsRing) & 1);
+        const int64_t* tsk = s_tsk + ts * kTsSlot + ((sg.kv_row0 + (int64_t)j * kBN) & 1);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int64_t m = warp_max_i64(tsk[32 * c + lane]);
+          if (lane == 0) s_kmax[ts * 4 + c] = m;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tsx_full[ts]);
+        ++t_it;
+      }
+    }
   } else if (warp >= 4) {
     // ================= epilogue: thread = (q row r, column half wg)
     const int et = tid - 128;
@@ -250,7 +277,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     float cb = s_w[nb - 1];
     if (has_pos) cb += s_pw[P - 1];
     cb *= c1;
-    uint32_t q_it = 0, s_it = 0, t_it = 0, o_it = 0;
+    uint32_t q_it = 0, s_it = 0, t_it = 0, o_it = 0, tcnt = 0;
+    const bool tr = (tid == 128);
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
       const int2 it = p.wl.fwd[g / H];
       const int h = g % H;
@@ -282,50 +310,84 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int sb = s_it & 1;
         const int ts = t_it % kTsRing;
         const int64_t kv0 = (int64_t)j * kBN;
-        mbar_wait(&ts_full[ts], (t_it / kTsRing) & 1);
+        mbar_wait(&tsx_full[ts], (t_it / kTsRing) & 1);  // chunk maxima (implies ts_full)
         mbar_wait(&s_full[sb], (s_it >> 1) & 1);
+        if (tr) trace_ev(p, 4, tcnt, 40, s_it);
         mbar_wait(&p_empty[sb], ((s_it >> 1) & 1) ^ 1);
         tc_fence_after();
         const int64_t* tsk = s_tsk + ts * kTsSlot + ((sg.kv_row0 + kv0) & 1);
         const uint32_t tS = tmem + 128 * sb + lane_off;
         const uint32_t tP = tmem + 384 + 64 * sb + lane_off;
-#pragma unroll 1
-        for (int c0 = 64 * wg; c0 < 64 * wg + 64; c0 += 32) {
+        // chunk classes (warp-uniform): 0 all masked, 1 unmasked + saturated bias, 2 general
+        int cls_bits = 0;
+#pragma unroll
+        for (int ci = 0; ci < 2; ++ci) {
+          const int c0 = 64 * wg + 32 * ci;
           const int64_t kc0 = kv0 + c0, kc1 = kc0 + 31;
-          uint32_t pk[16];
-          if (kc0 > row_hi || kc0 >= kv_lim) {
-            // every pair of this chunk is in the future or past the segment
+          int cls = 0;  // every pair is in the future or past the segment
+          if (!(kc0 > row_hi || kc0 >= kv_lim)) {
+            cls = 2;
+            if ((kc1 <= row_lo) && (kc1 < kv_lim)) {
+              const int64_t tk_max = s_kmax[ts * 4 + (c0 >> 5)];
+              if ((tq_min - tk_max >= cap) && (!has_pos || row_lo - kc1 >= P - 1)) cls = 1;
+            }
+          }
+          cls_bits |= cls << (2 * ci);
+        }
+        auto silu_fast = [&](const uint32_t* v, uint32_t* pk) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float h0 = fmaf(__uint_as_float(v[i]), c1, cb);
+            const float h1 = fmaf(__uint_as_float(v[i + 1]), c1, cb);
+            const float2 t = tanh2_approx(h0, h1);
+            pk[i >> 1] = pack_bf16(fmaf(h0, t.x, h0), fmaf(h1, t.y, h1));
+          }
+        };
+        if (cls_bits == 5) {
+          // both chunks unmasked and saturated (the common case): one TMEM round trip
+          uint32_t va[32], vb[32], pk[16];
+          tmem_ld32(tS + 64 * wg, va);
+          tmem_ld32(tS + 64 * wg + 32, vb);
+          tmem_ld_wait();
+          silu_fast(va, pk);
+          tmem_st16(tP + 32 * wg, pk);
+          silu_fast(vb, pk);
+          tmem_st16(tP + 32 * wg + 16, pk);
+        } else
+#pragma unroll 1
+        for (int ci = 0; ci < 2; ++ci) {
+          const int c0 = 64 * wg + 32 * ci;
+          const int cls = (cls_bits >> (2 * ci)) & 3;
+          if (cls == 1) {
+            uint32_t v[32], pk[16];
+            tmem_ld32(tS + c0, v);
+            tmem_ld_wait();
+            silu_fast(v, pk);
+            tmem_st16(tP + (c0 >> 1), pk);
+          } else if (cls == 0) {
+            uint32_t pk[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) pk[i] = 0u;
+            tmem_st16(tP + (c0 >> 1), pk);
           } else {
-            uint32_t v[32];
-            tmem_ld32(tS + c0, v);
-            const bool full = (kc1 <= row_lo) && (kc1 < kv_lim);
-            bool sat = false;
-            if (full) {
-              const int64_t tk_max = warp_max_i64(tsk[c0 + lane]);
-              sat = (tq_min - tk_max >= cap) && (!has_pos || row_lo - kc1 >= P - 1);
-            }
-            tmem_ld_wait();
-            if (sat) {
+            // general chunk (diagonal / short time gaps): exact per-element
+            // bucket, positional bias and mask, 8 columns per step
+            const int64_t kc0 = kv0 + c0;
+#pragma unroll 1
+            for (int g8 = 0; g8 < 32; g8 += 8) {
+              uint32_t v[8], pk[4];
+              tmem_ld8(tS + c0 + g8, v);
+              tmem_ld_wait();
 #pragma unroll
-              for (int i = 0; i < 32; i += 2) {
-                const float h0 = fmaf(__uint_as_float(v[i]), c1, cb);
-                const float h1 = fmaf(__uint_as_float(v[i + 1]), c1, cb);
-                pk[i >> 1] = pack_bf16(fmaf(h0, tanh_approx(h0), h0), fmaf(h1, tanh_approx(h1), h1));
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; i += 2) {
+              for (int i = 0; i < 8; i += 2) {
                 float y[2];
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
-                  const int64_t kpos = kc0 + i + u;
-                  float bias = s_w[bucket_of(tq - tsk[c0 + i + u], s_thr, s_base, cap)];
+                  const int64_t kpos = kc0 + g8 + i + u;
+                  float bias = s_w[bucket_smem(tq - tsk[c0 + g8 + i + u], s_bias, cap)];
                   if (has_pos) {
-                    int64_t rel = qpos - kpos;
-                    rel = rel < 0 ? 0 : (rel > P - 1 ? P - 1 : rel);
-                    bias += s_pw[rel];
+                    const int64_t rel = qpos - kpos;
+                    bias += s_pw[rel < 0 ? 0 : (rel > P - 1 ? P - 1 : (int)rel)];
                   }
                   const float hh = (__uint_as_float(v[i + u]) + bias) * c1;
                   const float yy = fmaf(hh, tanh_approx(hh), hh);
@@ -333,13 +395,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                 }
                 pk[i >> 1] = pack_bf16(y[0], y[1]);
               }
+              tmem_st4(tP + ((c0 + g8) >> 1), pk);
             }
           }
-          tmem_st16(tP + (c0 >> 1), pk);
         }
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[sb]);
+        if (tr) trace_ev(p, 4, tcnt, 41, s_it);
         __syncwarp();
         if (lane == 0) mbar_arrive(&ts_empty[ts]);
         ++s_it;
@@ -347,6 +410,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
       // ---- O: TMEM -> bf16 -> global (each group drains half the columns)
       mbar_wait(o_full, o_it & 1);
+      if (tr) trace_ev(p, 4, tcnt, 42, o_it);
       tc_fence_after();
 #pragma unroll 1
       for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 32) {
@@ -364,6 +428,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(o_empty);
+      if (tr) trace_ev(p, 4, tcnt, 43, o_it);
       ++o_it;
     }
   }

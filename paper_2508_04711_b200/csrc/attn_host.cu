@@ -90,6 +90,8 @@ static int validate(const jh_attn_args* a, bool bwd) {
 static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cudaStream_t s) {
   const BiasTable* bt = bias_table_cached(a->num_buckets);
   if (!bt) return set_error(JH_ERR_INVALID, "num_buckets must be >= 1");
+  if (bt->cap >= 0xFFFFFFFFll)
+    return set_error(JH_ERR_UNSUPPORTED, "fused attention supports num_buckets <= 23 (got %d)", a->num_buckets);
   memset(p, 0, sizeof(*p));
   p->seg = SegArgs{a->q_offsets, a->q_pos0, a->kv_start, a->kv_len, a->num_segments};
   p->ts_q = a->ts_q;
@@ -116,6 +118,8 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
   }
   p->bias.cap = bt->cap;
   p->bias.nb = a->num_buckets;
+  p->trace = (unsigned long long*)a->trace;
+  p->trace_cta = a->trace_cta;
   // workspace carve-up (bound computed with the caller's kv total unknown:
   // the bwd list is placed after a q_rows-sized fwd list, see ws_layout)
   WsLayout w = ws_layout(a->q_rows, std::max<int64_t>(a->q_rows, 0), a->num_segments, a->num_heads, a->head_dim);

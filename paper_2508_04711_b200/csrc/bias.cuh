@@ -21,4 +21,40 @@ JH_DEV int bucket_of(int64_t d, const int64_t* thr, const int32_t* base, int64_t
   return base[o] + (d >= thr[o] ? 1 : 0);
 }
 
+// Compact shared-memory form of the table for cap < 2^32 - 1 (num_buckets <= 23):
+// 32 uint32 thresholds + 32 uint8 bases (160 B).
+struct SmemBias {
+  uint32_t thr[32];
+  uint8_t base[32];
+};
+
+// Fill from the kernel-parameter table (call with all threads, then sync).
+JH_DEV void smem_bias_fill(SmemBias* s, const DevBiasTable& t, int tid, int nthreads) {
+  for (int i = tid; i < 32; i += nthreads) {
+    s->thr[i] = t.thr[i] > 0xFFFFFFFFll ? 0xFFFFFFFFu : static_cast<uint32_t>(t.thr[i]);
+    s->base[i] = static_cast<uint8_t>(t.base[i]);
+  }
+}
+
+// Bucket of one delta with the shared table (requires cap < 2^32 - 1, i.e.
+// num_buckets <= 23; the fused kernels check this on the host).
+JH_DEV int bucket_smem(int64_t d, const SmemBias* s, int64_t cap) {
+  const uint32_t du = d <= 0 ? 0u : (d >= cap ? static_cast<uint32_t>(cap) : static_cast<uint32_t>(d));
+  const int o = 31 - __clz(du + 1u);
+  return s->base[o] + (du >= s->thr[o] ? 1 : 0);
+}
+
+// Bucket of one delta.  `small` (cap < 2^32 - 1) uses the shared table, else
+// the 64-bit parameter table.
+JH_DEV int bucket_any(int64_t d, const SmemBias* s, bool small, const DevBiasTable& t) {
+  if (small) {
+    d = d < 0 ? 0 : d;
+    d = d > t.cap ? t.cap : d;
+    const uint32_t du = static_cast<uint32_t>(d);
+    const int o = 31 - __clz(du + 1u);
+    return s->base[o] + (du >= s->thr[o] ? 1 : 0);
+  }
+  return bucket_of(d, t.thr, t.base, t.cap);
+}
+
 }  // namespace jh

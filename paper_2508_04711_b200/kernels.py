@@ -195,6 +195,15 @@ def _workspace(q_rows, kv_total, nseg, H, d, device):
     return torch.empty(nbytes, dtype=torch.uint8, device=device), nbytes
 
 
+_TRACE = {"buf": None, "cta": 0}
+
+
+def set_trace(buf: torch.Tensor | None, cta: int = 0) -> None:
+    """Debug timeline: the next attention launches record per-role events of
+    CTA ``cta`` into ``buf`` (int64 [5, 4096, 2]: (code<<32 | arg, clock64))."""
+    _TRACE["buf"], _TRACE["cta"] = buf, int(cta)
+
+
 def _prof(a, prof):
     """prof = (start, end) torch.cuda.Event pair recorded around the main kernel."""
     if prof is not None:
@@ -202,6 +211,8 @@ def _prof(a, prof):
             if ev.cuda_event == 0:
                 ev.record()  # materialise the event handle
         a.prof_event_start, a.prof_event_end = prof[0].cuda_event, prof[1].cuda_event
+    if _TRACE["buf"] is not None:
+        a.trace, a.trace_cta = _TRACE["buf"].data_ptr(), _TRACE["cta"]
 
 
 def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=16, pos_weights=None,

@@ -9,7 +9,8 @@ from paper_2508_04711_b200 import kernels
 lens = [int(x) for x in sys.argv[1].split(",")]
 H, d = int(sys.argv[2]), int(sys.argv[3])
 which = sys.argv[4] if len(sys.argv) > 4 else "fwd"
-case = make_case(lens, H * d, seed=1)
+seed = int(sys.argv[5]) if len(sys.argv) > 5 else 1
+case = make_case(lens, H * d, seed=seed)
 c = to_cuda(case)
 try:
     if which == "fwd":
@@ -21,6 +22,7 @@ try:
         dq, dk, dv, dw, _ = kernels.attn_bwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], c["g"], H, c["w"], 16)
         torch.cuda.synchronize()
         wq, wk, wv, ww, _ = oracle.hstu_backward(case["q"], case["k"], case["v"], case["ts"], case["offsets"], case["g"], case["w"], 16, H)
-        print(lens, H, d, which, "rel", [row_rel(a.float().cpu().numpy(), b)[1] for a, b in ((dq, wq), (dk, wk), (dv, wv))])
+        dwe = float(np.abs(dw.cpu().numpy() - ww).max() / np.abs(ww).max())
+        print(lens, H, d, which, "rel", [row_rel(a.float().cpu().numpy(), b)[1] for a, b in ((dq, wq), (dk, wk), (dv, wv))], "dw", dwe)
 except Exception as e:
     print(lens, H, d, which, "ERROR", str(e).splitlines()[0])
