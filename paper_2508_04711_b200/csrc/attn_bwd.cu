@@ -6,17 +6,19 @@
 // with A = tril . SiLU(S), S = (Q K^T + bias) / sqrt(d).
 //
 // (1) hstu_bwd_dkv_kernel -- kv-tile-major: a work item is (segment, 128-row
-//     kv tile) x head; it loops over the q tiles that can see the kv tile.
-//       warp 0      TMA: K_j, V_j per item; Q_i, dO_i, ts_q per q tile (2 stages)
-//       warp 1      MMA: S^T = K Q^T, dP^T = V dO^T, dV += P^T dO (A = P^T in
-//                   TMEM), dK += dS^T Q (A = dS^T in smem)
-//       warp 2      TMEM allocator; warp 3: per-chunk min of ts_q (saturation test)
-//       warps 4-11  compute, thread = (kv row, 64-q-column half):
+//     kv tile) x head; it loops over the 64-row q half tiles that can see it.
+//       warp 0      TMA: K_j, V_j per item (reloaded once the item's last S^T/dP^T ran)
+//       warp 2      TMA: Q_h, dO_h, ts_q per half (kQStages ring); TMEM allocator
+//       warp 1      MMA: S^T = K Q^T, dP^T = V dO^T (128 x 64, two TMEM buffers),
+//                   dV += P^T dO (A = P^T in TMEM), dK += dS^T Q (A = dS^T in smem)
+//       warp 3      per-chunk min of ts_q (saturation test)
+//       warps 4-11  compute, thread = (kv row, 32-q-column chunk of the half):
 //                   phase P  : S^T -> P^T (TMEM) and SiLU'(S) (f16, TMEM)
 //                   phase dS : dP^T -> dS^T = dP SiLU'(S)/sqrt(d) (smem), d_ts_weights
 //       warps 12-15 drain dK / dV (bf16 store, or fp32 accumulate for CP)
-//     TMEM: S^T [0,128) -- per column group g: P^T at [64g,64g+32), SiLU' at
-//           [64g+32,64g+64) | dP^T [128,256) | dV | dK
+//     TMEM: S^T buffers [0,64) [64,128) (P^T of a 32-column chunk overwrites the
+//           chunk's first 16 columns; SiLU'(S) stays in registers) | dP^T
+//           buffers [128,256) | dV | dK
 // (2) hstu_bwd_dq_kernel -- q-tile-major (the forward's work list): loops over
 //     the kv tiles the q tile sees; dQ accumulates in TMEM and is written once.
 //       warp 0 TMA (Q, dO, ts_q once; K + ts_k double, V single buffered)
@@ -36,28 +38,41 @@ constexpr int kDqThreads = 384;   // dQ kernel
 constexpr int kCompWarps = 8;
 
 // ===================================================================== dKV
+// The q side advances in 64-row half tiles so that S^T / dP^T can be double
+// buffered in TMEM: while the compute warps turn half i into P^T and dS^T,
+// the tensor core already computes S^T / dP^T of half i+1.
+constexpr int kQH = 64;     // q rows per half tile
+constexpr int kQStages = 3;  // Q / dO / ts_q ring depth
+
 template <int D>
 struct DkvCfg {
-  static constexpr int TILE = 128 * D * 2;
+  static constexpr int TILE = 128 * D * 2;       // K or V tile
+  static constexpr int HTILE = kQH * D * 2;      // Q or dO half tile
   static constexpr int PANELS = D / 64;
   static constexpr int K_OFF = 0;
   static constexpr int V_OFF = TILE;
-  static constexpr int Q_OFF = 2 * TILE;          // [2] stages
-  static constexpr int DO_OFF = 4 * TILE;         // [2] stages
-  static constexpr int DS_OFF = 6 * TILE;         // dS^T: 128 kv x 128 q bf16 (2 panels)
-  static constexpr int TSQ_OFF = DS_OFF + 32768;  // int64 [2][kTsSlot]
+  static constexpr int Q_OFF = 2 * TILE;                          // [kQStages]
+  static constexpr int DO_OFF = Q_OFF + kQStages * HTILE;         // [kQStages]
+  static constexpr int DS_OFF = DO_OFF + kQStages * HTILE;        // [2] dS^T: 128 kv x 64 q bf16 (1 panel)
+  static constexpr int TSQ_OFF = DS_OFF + 2 * 16384;              // int64 [kQStages][kTsSlotH]
   static constexpr int MAX_NB = (D == 64) ? 256 : 32;
-  static constexpr int W_OFF = TSQ_OFF + 2 * kTsSlot * 8;           // float [MAX_NB]
-  static constexpr int PW_OFF = W_OFF + MAX_NB * 4;                 // float [1024] (D=64 only)
-  static constexpr int BINS_OFF = PW_OFF + (D == 64 ? 4096 : 0);    // float [MAX_NB (+1024)]
-  static constexpr int NBINS = MAX_NB + (D == 64 ? 1024 : 0);
-  static constexpr int TAB_OFF = BINS_OFF + NBINS * 4;              // SmemBias (160 B)
-  static constexpr int QMIN_OFF = TAB_OFF + 160;                    // int64 [2][4]
-  static constexpr int BAR_OFF = QMIN_OFF + 64;
-  static constexpr int NBARS = 16;
-  static constexpr int TMEMPTR_OFF = BAR_OFF + NBARS * 8;
-  static constexpr int SMEM = TMEMPTR_OFF + 16;
+  static constexpr int OCT_OFF = TSQ_OFF + kQStages * kTsSlotH * 8;  // OctEntry [32]
+  static constexpr int PW_OFF = OCT_OFF + 32 * 16;                   // float [1024] x c1 (D=64 only)
+  // (the 8 int64 of padding after each ts_q box hold the stage's two chunk
+  // minima; slot 0's padding also holds the TMEM base address)
+  static constexpr int BAR_OFF = PW_OFF + (D == 64 ? 4096 : 0);
+  static constexpr int NBARS = 26;
+  static constexpr int SMEM = BAR_OFF + NBARS * 8;
 };
+
+// q half tiles [h0, nh) of segment `sg` that can see kv tile j (h0 == nh: none)
+JH_DEV void dkv_halves(const Seg& sg, int j, int& h0, int& nh) {
+  nh = (int)((sg.lq + kQH - 1) / kQH);
+  int64_t first = (int64_t)j * kBN - sg.qp0;
+  first = first < 0 ? 0 : first;
+  h0 = (int)(first / kQH);
+  if ((int64_t)j * kBN >= seg_kv_vis(sg)) h0 = nh;
+}
 
 template <int D>
 __global__ void __launch_bounds__(kBwdThreads, 1)
@@ -67,25 +82,24 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   using C = DkvCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
   int64_t* s_tsq = reinterpret_cast<int64_t*>(smem + C::TSQ_OFF);
-  float* s_w = reinterpret_cast<float*>(smem + C::W_OFF);
-  float* s_pw = reinterpret_cast<float*>(smem + C::PW_OFF);
-  float* s_bins = reinterpret_cast<float*>(smem + C::BINS_OFF);  // non-last buckets, then positions
-  SmemBias* s_bias = reinterpret_cast<SmemBias*>(smem + C::TAB_OFF);
-  int64_t* s_qmin = reinterpret_cast<int64_t*>(smem + C::QMIN_OFF);
+  OctEntry* s_oct = reinterpret_cast<OctEntry*>(smem + C::OCT_OFF);
+  float* s_pwc = reinterpret_cast<float*>(smem + C::PW_OFF);  // pos weights x c1
+  // chunk minima of stage st: s_tsq[st * kTsSlotH + kTsBoxH + {0, 1}]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* kv_full = bars + 0;
   uint64_t* kv_empty = bars + 1;
-  uint64_t* qd_full = bars + 2;    // [2]
-  uint64_t* qd_empty = bars + 4;   // [2] MMA (dK_i) + compute warps
-  uint64_t* qx_full = bars + 6;    // [2] chunk minima of ts_q
-  uint64_t* s_full = bars + 8;
-  uint64_t* dp_full = bars + 9;
-  uint64_t* p_full = bars + 10;    // P^T + SiLU' in TMEM, S^T consumed
-  uint64_t* ds_full = bars + 11;   // dS^T in smem; dP^T, SiLU' consumed
-  uint64_t* ds_empty = bars + 12;  // dK_i done with dS^T
-  uint64_t* dkv_full = bars + 13;
-  uint64_t* dkv_empty = bars + 14;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::TMEMPTR_OFF);
+  uint64_t* qd_full = bars + 2;                  // [kQStages]
+  uint64_t* qd_empty = qd_full + kQStages;       // [kQStages] MMA (dK of the half) + compute warps (ts_q)
+  uint64_t* qx_full = qd_empty + kQStages;       // [kQStages] chunk minima of ts_q
+  uint64_t* s_full = qx_full + kQStages;         // [2] S^T / dP^T buffers
+  uint64_t* dp_full = s_full + 2;                // [2]
+  uint64_t* p_full = dp_full + 2;                // [2] P^T in TMEM, S^T consumed
+  uint64_t* ds_full = p_full + 2;                // [2] dS^T in smem; dP^T consumed
+  uint64_t* ds_empty = ds_full + 2;              // [2] dK done with dS^T
+  uint64_t* dkv_full = ds_empty + 2;
+  uint64_t* dkv_empty = dkv_full + 1;
+  static_assert(2 + 3 * kQStages + 10 + 2 <= C::NBARS, "barrier count");
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_tsq + kTsBoxH + 2);
 
   const uint32_t warp = warp_id();
   const int tid = threadIdx.x;
@@ -95,25 +109,31 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const bool has_pos = P > 0;
   const int64_t HD = (int64_t)H * D;
 
+  const float c1 = 0.5f * rsqrtf((float)D);  // SiLU(s) = h (1 + tanh h), h = s / (2 sqrt(d))
   if (smem_u32(smem) & 1023) __trap();
-  for (int i = tid; i < nb; i += blockDim.x) s_w[i] = p.ts_weights[i];
+  oct_table_fill(s_oct, p.bias, p.ts_weights, c1, tid, blockDim.x);
   if (D == 64)
-    for (int i = tid; i < P; i += blockDim.x) s_pw[i] = p.pos_weights[i];
-  for (int i = tid; i < C::NBINS; i += blockDim.x) s_bins[i] = 0.f;
-  smem_bias_fill(s_bias, p.bias, tid, blockDim.x);
+    for (int i = tid; i < P; i += blockDim.x) s_pwc[i] = p.pos_weights[i] * c1;
+  // this CTA's fp32 partial bins (buckets, then positions) in the workspace
+  float* g_bins = p.wl.bins + (size_t)blockIdx.x * kBinsPerCta;
+  for (int i = tid; i < nb; i += blockDim.x) g_bins[i] = 0.f;
+  for (int i = tid; i < P; i += blockDim.x) g_bins[256 + i] = 0.f;
+  __threadfence_block();
   if (tid == 0) {
     mbar_init(kv_full, 1);
     mbar_init(kv_empty, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kQStages; ++i) {
       mbar_init(&qd_full[i], 1);
       mbar_init(&qd_empty[i], 1 + kCompWarps);
       mbar_init(&qx_full[i], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(dp_full, 1);
-    mbar_init(p_full, 32 * kCompWarps);
-    mbar_init(ds_full, 32 * kCompWarps);
-    mbar_init(ds_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&dp_full[i], 1);
+      mbar_init(&p_full[i], 32 * kCompWarps);
+      mbar_init(&ds_full[i], 32 * kCompWarps);
+      mbar_init(&ds_empty[i], 1);
+    }
     mbar_init(dkv_full, 1);
     mbar_init(dkv_empty, 128);
     fence_barrier_init();
@@ -130,29 +150,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
-  const uint32_t tS = tmem, tDP = tmem + 128, tDV = tmem + 256, tDK = tmem + 256 + D;
+  // TMEM: S^T [64x, 64x+64) and dP^T [128+64x, ...) for buffer x, dV, dK
+  const uint32_t tDP = tmem + 128, tDV = tmem + 256, tDK = tmem + 256 + D;
 
   const int total = p.wl.hdr->n_bwd * H;
-  auto q_tiles = [&](const Seg& sg, int j, int& t0, int& nt) {
-    nt = (int)((sg.lq + kBM - 1) / kBM);
-    int64_t first = (int64_t)j * kBN - sg.qp0;
-    first = first < 0 ? 0 : first;
-    t0 = (int)(first / kBM);
-    if ((int64_t)j * kBN >= seg_kv_vis(sg)) t0 = nt;  // kv tile no query can see
-  };
 
   if (warp == 0) {
-    // ================= TMA producer
+    // ================= TMA producer: K_j, V_j per item
     if (elect_one()) {
-      uint32_t it_cnt = 0, qd_it = 0, tcnt = 0;
+      uint32_t it_cnt = 0, tcnt = 0;
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
         const int2 it = p.wl.bwd[g / H];
         const int h = g % H;
         const Seg sg = load_seg(p.seg, it.x);
-        int t0, nt;
-        q_tiles(sg, it.y, t0, nt);
-        if (t0 >= nt) continue;
-        mbar_wait(kv_empty, (it_cnt & 1) ^ 1);
+        int h0, nh;
+        dkv_halves(sg, it.y, h0, nh);
+        if (h0 >= nh) continue;
+        mbar_wait(kv_empty, (it_cnt & 1) ^ 1);  // last S^T / dP^T of the previous item done
         trace_ev(p, 0, tcnt, 1, g);
         mbar_expect_tx(kv_full, 2 * C::TILE);
         const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)it.y * kBN);
@@ -161,93 +175,106 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tma_load_2d(smem + C::V_OFF + pn * 16384, &tm_v, h * D + pn * 64, krow, kv_full);
         }
         ++it_cnt;
-        for (int t = t0; t < nt; ++t) {
-          const int st = qd_it & 1;
-          mbar_wait(&qd_empty[st], ((qd_it >> 1) & 1) ^ 1);
-          trace_ev(p, 0, tcnt, 2, t);
-          mbar_expect_tx(&qd_full[st], 2 * C::TILE + kTsBytes);
-          const int32_t qrow = (int32_t)(sg.q_row0 + (int64_t)t * kBM);
+      }
+    }
+  } else if (warp == 2) {
+    // ================= TMA producer: Q_h, dO_h, ts_q per half tile (runs ahead
+    // across item boundaries, independent of the K/V buffer)
+    if (elect_one()) {
+      uint32_t hc = 0;
+      for (int g = blockIdx.x; g < total; g += gridDim.x) {
+        const int2 it = p.wl.bwd[g / H];
+        const int h = g % H;
+        const Seg sg = load_seg(p.seg, it.x);
+        int h0, nh;
+        dkv_halves(sg, it.y, h0, nh);
+        for (int t = h0; t < nh; ++t, ++hc) {
+          const int st = hc % kQStages;
+          mbar_wait(&qd_empty[st], ((hc / kQStages) & 1) ^ 1);
+          mbar_expect_tx(&qd_full[st], 2 * C::HTILE + kTsBytesH);
+          const int32_t qrow = (int32_t)(sg.q_row0 + (int64_t)t * kQH);
           for (int pn = 0; pn < C::PANELS; ++pn) {
-            tma_load_2d(smem + C::Q_OFF + st * C::TILE + pn * 16384, &tm_q, h * D + pn * 64, qrow, &qd_full[st]);
-            tma_load_2d(smem + C::DO_OFF + st * C::TILE + pn * 16384, &tm_do, h * D + pn * 64, qrow,
+            tma_load_2d(smem + C::Q_OFF + st * C::HTILE + pn * 8192, &tm_q, h * D + pn * 64, qrow, &qd_full[st]);
+            tma_load_2d(smem + C::DO_OFF + st * C::HTILE + pn * 8192, &tm_do, h * D + pn * 64, qrow,
                         &qd_full[st]);
           }
-          tma_load_1d(s_tsq + st * kTsSlot, &tm_tsq, qrow & ~1, &qd_full[st]);
-          ++qd_it;
+          tma_load_1d(s_tsq + st * kTsSlotH, &tm_tsq, qrow & ~1, &qd_full[st]);
         }
       }
     }
   } else if (warp == 1) {
     // ================= MMA issuer
     if (elect_one()) {
-      constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);  // S^T, dP^T
+      constexpr uint32_t id_s = idesc_bf16(128, kQH, 0, 0);  // S^T, dP^T: 128 kv x 64 q
       constexpr uint32_t id_kv = idesc_bf16(128, D, 0, 1);   // dV (A tmem), dK (A smem K-major)
       const uint32_t k_base = smem_u32(smem + C::K_OFF);
       const uint32_t v_base = smem_u32(smem + C::V_OFF);
-      const uint32_t ds_base = smem_u32(smem + C::DS_OFF);
-      uint32_t it_cnt = 0, qd_it = 0, p_cnt = 0, ds_cnt = 0, tcnt = 0;
-      auto q_base = [&](uint32_t qi) { return smem_u32(smem + C::Q_OFF + (qi & 1) * C::TILE); };
-      auto do_base = [&](uint32_t qi) { return smem_u32(smem + C::DO_OFF + (qi & 1) * C::TILE); };
-      auto issue_S_dP = [&](uint32_t qi) {
-        mbar_wait(&qd_full[qi & 1], (qi >> 1) & 1);
-        trace_ev(p, 1, tcnt, 10, qi);
+      uint32_t it_cnt = 0, hc = 0, tcnt = 0;
+      auto q_base = [&](uint32_t hi) { return smem_u32(smem + C::Q_OFF + (hi % kQStages) * C::HTILE); };
+      auto do_base = [&](uint32_t hi) { return smem_u32(smem + C::DO_OFF + (hi % kQStages) * C::HTILE); };
+      auto issue_S_dP = [&](uint32_t hi, bool last) {
+        const uint32_t x = hi & 1;
+        mbar_wait(&qd_full[hi % kQStages], (hi / kQStages) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          umma_ss(tS, sdesc_sw128(k_base + off, 16, 1024), sdesc_sw128(q_base(qi) + off, 16, 1024), id_s,
+          const uint32_t ka = (kk >> 2) * 16384 + (kk & 3) * 32;
+          const uint32_t kb = (kk >> 2) * 8192 + (kk & 3) * 32;
+          umma_ss(tmem + 64 * x, sdesc_sw128(k_base + ka, 16, 1024), sdesc_sw128(q_base(hi) + kb, 16, 1024), id_s,
                   kk > 0 ? 1u : 0u);
         }
-        umma_commit(s_full);
+        umma_commit(&s_full[x]);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          umma_ss(tDP, sdesc_sw128(v_base + off, 16, 1024), sdesc_sw128(do_base(qi) + off, 16, 1024), id_s,
+          const uint32_t ka = (kk >> 2) * 16384 + (kk & 3) * 32;
+          const uint32_t kb = (kk >> 2) * 8192 + (kk & 3) * 32;
+          umma_ss(tDP + 64 * x, sdesc_sw128(v_base + ka, 16, 1024), sdesc_sw128(do_base(hi) + kb, 16, 1024), id_s,
                   kk > 0 ? 1u : 0u);
         }
-        umma_commit(dp_full);
+        umma_commit(&dp_full[x]);
+        if (last) umma_commit(kv_empty);  // K_j / V_j no longer read: next item's may load
       };
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
         const int2 it = p.wl.bwd[g / H];
         const Seg sg = load_seg(p.seg, it.x);
-        int t0, nt;
-        q_tiles(sg, it.y, t0, nt);
-        if (t0 >= nt) continue;
-        const int n = nt - t0;
+        int h0, nh;
+        dkv_halves(sg, it.y, h0, nh);
+        if (h0 >= nh) continue;
+        const int n = nh - h0;
         mbar_wait(kv_full, it_cnt & 1);
-        issue_S_dP(qd_it);
+        trace_ev(p, 1, tcnt, 11, g);
+        issue_S_dP(hc, n == 1);
+        if (n > 1) issue_S_dP(hc + 1, n == 2);
         for (int i = 0; i < n; ++i) {
-          const uint32_t qi = qd_it + i;
-          // dV += P^T dO.  P^T of q columns [32c, 32c+32) (chunk c) sits at TMEM
-          // columns [32c, 32c+16) of the S^T region (SiLU' in the other half)
-          mbar_wait(p_full, p_cnt & 1);
-          trace_ev(p, 1, tcnt, 12, qi);
-          ++p_cnt;
+          const uint32_t hi = hc + i;
+          const uint32_t x = hi & 1, xp = (hi >> 1) & 1;
+          // dV += P^T dO.  P^T of chunk c (q columns [32c, 32c+32)) sits at TMEM
+          // columns [32c, 32c+16) of the S^T buffer (SiLU' in the other 16)
+          mbar_wait(&p_full[x], xp);
+          trace_ev(p, 1, tcnt, 12, hi);
           if (i == 0) mbar_wait(dkv_empty, (it_cnt & 1) ^ 1);  // dK/dV of the previous item drained
           tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < kBM / 16; ++kk)
-            umma_ts(tDV, tS + 32 * (kk >> 1) + 8 * (kk & 1), sdesc_sw128(do_base(qi) + kk * 2048, 16384, 1024), id_kv,
-                    (kk > 0 || i > 0) ? 1u : 0u);
+          for (int kk = 0; kk < kQH / 16; ++kk)
+            umma_ts(tDV, tmem + 64 * x + 32 * (kk >> 1) + 8 * (kk & 1),
+                    sdesc_sw128(do_base(hi) + kk * 2048, 8192, 1024), id_kv, (kk > 0 || i > 0) ? 1u : 0u);
           // dK += dS^T Q
-          mbar_wait(ds_full, ds_cnt & 1);
-          trace_ev(p, 1, tcnt, 13, qi);
-          ++ds_cnt;
+          mbar_wait(&ds_full[x], xp);
+          trace_ev(p, 1, tcnt, 13, hi);
           tc_fence_after();
+          const uint32_t ds_base = smem_u32(smem + C::DS_OFF + x * 16384);
 #pragma unroll
-          for (int kk = 0; kk < kBM / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-            umma_ss(tDK, sdesc_sw128(ds_base + off, 16, 1024), sdesc_sw128(q_base(qi) + kk * 2048, 16384, 1024),
+          for (int kk = 0; kk < kQH / 16; ++kk)
+            umma_ss(tDK, sdesc_sw128(ds_base + kk * 32, 16, 1024), sdesc_sw128(q_base(hi) + kk * 2048, 8192, 1024),
                     id_kv, (kk > 0 || i > 0) ? 1u : 0u);
-          }
-          umma_commit(ds_empty);
-          umma_commit(&qd_empty[qi & 1]);
-          // next tile's S^T / dP^T (S^T region: P^T read by dV in issue order; SiLU' consumed)
-          if (i + 1 < n) issue_S_dP(qi + 1);
+          umma_commit(&ds_empty[x]);
+          umma_commit(&qd_empty[hi % kQStages]);
+          // S^T / dP^T of half i+2 into buffer x (P^T read by dV_i in issue order;
+          // dP^T and SiLU' consumed before ds_full)
+          if (i + 2 < n) issue_S_dP(hi + 2, i + 3 == n);
         }
-        qd_it += n;
+        hc += n;
         umma_commit(dkv_full);
-        umma_commit(kv_empty);
         trace_ev(p, 1, tcnt, 15, g);
         ++it_cnt;
       }
@@ -255,49 +282,48 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   } else if (warp == 3) {
     // ================= ts_q statistics: per 32-column chunk minimum
     const int lane = lane_id();
-    uint32_t qd_it = 0;
+    uint32_t hc = 0;
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
       const int2 it = p.wl.bwd[g / H];
       const Seg sg = load_seg(p.seg, it.x);
-      int t0, nt;
-      q_tiles(sg, it.y, t0, nt);
-      for (int t = t0; t < nt; ++t) {
-        const int st = qd_it & 1;
-        mbar_wait(&qd_full[st], (qd_it >> 1) & 1);
-        const int64_t* tsq = s_tsq + st * kTsSlot + ((sg.q_row0 + (int64_t)t * kBM) & 1);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int64_t m = warp_min_i64(tsq[32 * c + lane]);
-          if (lane == 0) s_qmin[st * 4 + c] = m;
+      int h0, nh;
+      dkv_halves(sg, it.y, h0, nh);
+      for (int t = h0; t < nh; ++t, ++hc) {
+        const int st = hc % kQStages;
+        mbar_wait(&qd_full[st], (hc / kQStages) & 1);
+        const int64_t* tsq = s_tsq + st * kTsSlotH + ((sg.q_row0 + (int64_t)t * kQH) & 1);
+        const int64_t m0 = warp_min_i64(tsq[lane]);
+        const int64_t m1 = warp_min_i64(tsq[32 + lane]);
+        if (lane == 0) {
+          s_tsq[st * kTsSlotH + kTsBoxH] = m0;
+          s_tsq[st * kTsSlotH + kTsBoxH + 1] = m1;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&qx_full[st]);
-        ++qd_it;
       }
     }
   } else if (warp >= 4 && warp < 12) {
-    // ================= compute: thread = (kv row r, q-column half wg)
+    // ================= compute: thread = (kv row r, 32-q-column chunk wg of the half)
     const int et = tid - 128;
     const int wg = et >> 7;
     const int r = et & 127;
     const int lane = r & 31;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t tSg = tS + lane_off + 64 * wg;  // this group's S^T / P^T / SiLU' columns
-    const float c1 = 0.5f * rsqrtf((float)D);
     const int64_t cap = p.bias.cap;
-    uint8_t* ds_smem = smem + C::DS_OFF + wg * 16384;  // this group's 64 q columns = one panel
-    float cb = s_w[nb - 1];
-    if (has_pos) cb += s_pw[P - 1];
+    const int c0 = 32 * wg;  // q column offset of this thread's chunk within the half
+    float cb = p.ts_weights[nb - 1];
+    if (has_pos) cb += p.pos_weights[P - 1];
     cb *= c1;
-    double acc_w = 0.0, acc_p = 0.0;  // last-bucket partials
-    uint32_t qd_it = 0, s_cnt = 0, dp_cnt = 0, ds_cnt = 0, tcnt = 0;
-    const bool tr = (tid == 128);
+    double acc_w = 0.0, acc_p = 0.0;  // saturated-chunk partials of the last buckets
+    uint32_t hc = 0, tcnt = 0;
+    const bool tr = (tid == 128 || tid == 256);
+    const int trole = tid == 128 ? 2 : 3;
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
       const int2 it = p.wl.bwd[g / H];
       const Seg sg = load_seg(p.seg, it.x);
-      int t0, nt;
-      q_tiles(sg, it.y, t0, nt);
-      if (t0 >= nt) continue;
+      int h0, nh;
+      dkv_halves(sg, it.y, h0, nh);
+      if (h0 >= nh) continue;
       const int64_t kv0 = (int64_t)it.y * kBN;
       const int64_t kpos = kv0 + r;
       const bool krow_ok = kpos < sg.kv_len;
@@ -305,189 +331,185 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int64_t tk_max = warp_max_i64(tk);
       const int64_t k_lo = kv0 + (r & ~31), k_hi = k_lo + 31;  // this warp's kv positions
       const bool warp_k_ok = k_hi < sg.kv_len;
-      for (int t = t0; t < nt; ++t) {
-        const int st = qd_it & 1;
-        const int64_t qrow0 = sg.q_row0 + (int64_t)t * kBM;
-        const int64_t qp_tile = sg.qp0 + (int64_t)t * kBM;
-        const int nq = (int)min((int64_t)kBM, sg.lq - (int64_t)t * kBM);
-        mbar_wait(&qx_full[st], (qd_it >> 1) & 1);
-        const int64_t* tsq = s_tsq + st * kTsSlot + (qrow0 & 1);
-        int cls_bits = 0;  // per chunk: 0 masked, 1 saturated, 2 general
-#pragma unroll
-        for (int ci = 0; ci < 2; ++ci) {
-          const int c0 = 64 * wg + 32 * ci;
-          const int64_t qc0 = qp_tile + c0;
-          int cls = 0;
-          if (!(qc0 + 31 < k_lo || c0 >= nq)) {
-            cls = 2;
-            if ((qc0 >= k_hi) && (c0 + 32 <= nq) && warp_k_ok &&
-                (s_qmin[st * 4 + (c0 >> 5)] - tk_max >= cap) && (!has_pos || qc0 - k_hi >= P - 1))
-              cls = 1;
-          }
-          cls_bits |= cls << (2 * ci);
+      for (int t = h0; t < nh; ++t, ++hc) {
+        const int st = hc % kQStages;
+        const uint32_t x = hc & 1, xp = (hc >> 1) & 1;
+        const int64_t qrow0 = sg.q_row0 + (int64_t)t * kQH;
+        const int64_t qp_half = sg.qp0 + (int64_t)t * kQH;
+        const int nq = (int)min((int64_t)kQH, sg.lq - (int64_t)t * kQH);
+        mbar_wait(&qx_full[st], (hc / kQStages) & 1);
+        const int64_t* tsq = s_tsq + st * kTsSlotH + (qrow0 & 1) + c0;  // this chunk's 32 query timestamps
+        // chunk class: 0 masked, 1 unmasked with saturated bias, 2 general
+        const int64_t qc0 = qp_half + c0;
+        int cls = 0;
+        if (!(qc0 + 31 < k_lo || c0 >= nq)) {
+          cls = 2;
+          if ((qc0 >= k_hi) && (c0 + 32 <= nq) && warp_k_ok &&
+              (s_tsq[st * kTsSlotH + kTsBoxH + wg] - tk_max >= cap) && (!has_pos || qc0 - k_hi >= P - 1))
+            cls = 1;
         }
+        const uint32_t cbase = tmem + 64 * x + c0 + lane_off;  // S^T chunk -> P^T [cbase, +16)
+        // general chunks: relative position of column 0 and the number of in-range columns
+        const int rel0 = (int)(qc0 - kpos);
+        const int ncol = krow_ok ? nq - c0 : 0;
+        // SiLU'(S) of the chunk (f16 pairs) stays in registers from phase P to phase dS
+        // (saturated chunks) or in a small per-thread local buffer (general chunks,
+        // rolled loops keep that rarely-run code small), with the buckets and mask
+        uint32_t kp[16];
+        uint32_t kl[16], bl[8];
+        uint32_t okm = 0;
         // ---------------- phase P: S^T -> P^T, SiLU'
-        mbar_wait(s_full, s_cnt & 1);
-        if (tr) trace_ev(p, 2, tcnt, 21, t);
-        ++s_cnt;
+        mbar_wait(&s_full[x], xp);
+        if (tr) trace_ev(p, trole, tcnt, 21, t);
         tc_fence_after();
-        // per chunk (32 S^T columns at cbase): P^T -> [cbase, cbase+16), SiLU' -> [cbase+16, cbase+32),
-        // i.e. each chunk is overwritten in place, only after all of its S^T values were read
+        if (cls == 1) {
+          uint32_t v[32], pk[16];
+          tmem_ld32(cbase, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float h0f = fmaf(__uint_as_float(v[i]), c1, cb);
+            const float h1f = fmaf(__uint_as_float(v[i + 1]), c1, cb);
+            const float t0 = tanh_approx(h0f), t1 = tanh_approx(h1f);  // f32: d_ts_weights accuracy
+            pk[i >> 1] = pack_bf16(fmaf(h0f, t0, h0f), fmaf(h1f, t1, h1f));
+            __half2 hk = __floats2half2_rn((1.f + t0) * (fmaf(-h0f, t0, h0f) + 1.f),
+                                           (1.f + t1) * (fmaf(-h1f, t1, h1f) + 1.f));
+            kp[i >> 1] = *reinterpret_cast<uint32_t*>(&hk);
+          }
+          tmem_st16(cbase, pk);
+        } else if (cls == 0) {
+          uint32_t z[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) z[i] = 0u;
+          tmem_st16(cbase, z);
+        } else {
+          // general chunk: exact per-element bucket, positional bias and mask
 #pragma unroll 1
-        for (int ci = 0; ci < 2; ++ci) {
-          const int cls = (cls_bits >> (2 * ci)) & 3;
-          const int c0 = 64 * wg + 32 * ci;
-          const uint32_t cbase = tSg + 32 * ci;
-          if (cls == 1) {
-            uint32_t v[32], pk[16], kp[16];
-            tmem_ld32(cbase, v);
+          for (int g8 = 0; g8 < 32; g8 += 8) {
+            uint32_t v[8], pk[4];
+            tmem_ld8(cbase + g8, v);
+            float bc[8];
+            uint32_t bw0 = 0, bw1 = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              int b;
+              oct_lookup(clamp_delta(tsq[g8 + j] - tk, cap), s_oct, b, bc[j]);
+              if (j < 4)
+                bw0 |= (uint32_t)b << (8 * j);
+              else
+                bw1 |= (uint32_t)b << (8 * (j - 4));
+              const bool ok = (g8 + j < ncol) && (rel0 + g8 + j >= 0);
+              okm |= (ok ? 1u : 0u) << (g8 + j);
+            }
+            if (has_pos) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) bc[j] += s_pwc[min(max(rel0 + g8 + j, 0), P - 1)];
+            }
+            bl[g8 >> 2] = bw0;
+            bl[(g8 >> 2) + 1] = bw1;
             tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              const float h0 = fmaf(__uint_as_float(v[i]), c1, cb);
-              const float h1 = fmaf(__uint_as_float(v[i + 1]), c1, cb);
-              const float2 th = make_float2(tanh_approx(h0), tanh_approx(h1));  // f32: d_ts_weights accuracy
-              pk[i >> 1] = pack_bf16(fmaf(h0, th.x, h0), fmaf(h1, th.y, h1));
-              __half2 hk = __floats2half2_rn((1.f + th.x) * (fmaf(-h0, th.x, h0) + 1.f),
-                                             (1.f + th.y) * (fmaf(-h1, th.y, h1) + 1.f));
-              kp[i >> 1] = *reinterpret_cast<uint32_t*>(&hk);
-            }
-            tmem_st16(cbase, pk);
-            tmem_st16(cbase + 16, kp);
-          } else if (cls == 0) {
-            uint32_t z[16];
+            for (int j = 0; j < 8; j += 2) {
+              float pp[2], dd[2];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) z[i] = 0u;
-            tmem_st16(cbase, z);
-            tmem_st16(cbase + 16, z);
-          } else {
-            // general chunk: 8 columns per step; P^T words land on columns already
-            // read, SiLU' words wait in a small local buffer until all 32 are read
-            uint32_t kl[16];
-#pragma unroll 1
-            for (int g8 = 0; g8 < 32; g8 += 8) {
-              uint32_t v[8], pk[4];
-              tmem_ld8(cbase + g8, v);
-              tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 8; i += 2) {
-                float pp[2], dd[2];
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                  const int qi = c0 + g8 + i + u;
-                  const int64_t qpos = qp_tile + qi;
-                  const bool ok = krow_ok && (qi < nq) && (kpos <= qpos);
-                  float bias = s_w[bucket_smem(tsq[qi] - tk, s_bias, cap)];
-                  if (has_pos) {
-                    const int64_t rr = qpos - kpos;
-                    bias += s_pw[rr < 0 ? 0 : (rr > P - 1 ? P - 1 : (int)rr)];
-                  }
-                  const float hh = (__uint_as_float(v[i + u]) + bias) * c1;
-                  const float th = tanh_approx(hh);
-                  pp[u] = ok ? fmaf(hh, th, hh) : 0.f;
-                  dd[u] = ok ? (1.f + th) * (fmaf(-hh, th, hh) + 1.f) : 0.f;
-                }
-                pk[i >> 1] = pack_bf16(pp[0], pp[1]);
-                __half2 hk = __floats2half2_rn(dd[0], dd[1]);
-                kl[(g8 + i) >> 1] = *reinterpret_cast<uint32_t*>(&hk);
+              for (int u = 0; u < 2; ++u) {
+                const bool ok = (okm >> (g8 + j + u)) & 1u;
+                const float hh = fmaf(__uint_as_float(v[j + u]), c1, bc[j + u]);
+                const float th = tanh_approx(hh);
+                pp[u] = ok ? fmaf(hh, th, hh) : 0.f;
+                dd[u] = ok ? (1.f + th) * (fmaf(-hh, th, hh) + 1.f) : 0.f;
               }
-              tmem_st4(cbase + (g8 >> 1), pk);
+              pk[j >> 1] = pack_bf16(pp[0], pp[1]);
+              __half2 hk = __floats2half2_rn(dd[0], dd[1]);
+              kl[(g8 + j) >> 1] = *reinterpret_cast<uint32_t*>(&hk);
             }
-            uint32_t kp[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) kp[i] = kl[i];
-            tmem_st16(cbase + 16, kp);
+            tmem_st4(cbase + (g8 >> 1), pk);
           }
         }
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(p_full);
-        if (tr) trace_ev(p, 2, tcnt, 22, t);
+        mbar_arrive(&p_full[x]);
+        if (tr) trace_ev(p, trole, tcnt, 22, t);
         // ---------------- phase dS: dP^T, SiLU' -> dS^T (smem), d_ts_weights
-        mbar_wait(dp_full, dp_cnt & 1);
-        ++dp_cnt;
-        if (ds_cnt > 0) mbar_wait(ds_empty, (ds_cnt - 1) & 1);  // dK of the previous tile done with dS^T
-        ++ds_cnt;
-        if (tr) trace_ev(p, 2, tcnt, 24, t);
+        mbar_wait(&dp_full[x], xp);
+        if (hc >= 2) mbar_wait(&ds_empty[x], xp ^ 1);  // dK of half hc-2 done with this dS^T buffer
+        if (tr) trace_ev(p, trole, tcnt, 24, t);
         tc_fence_after();
+        uint8_t* ds_smem = smem + C::DS_OFF + x * 16384;
+        const uint32_t dpbase = tDP + 64 * x + c0 + lane_off;
         float sat_w = 0.f, sat_p = 0.f;
+        if (cls == 1) {
+          uint32_t dv[32], dk[16];
+          tmem_ld32(dpbase, dv);
+          tmem_ld_wait();
+          float csum = 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float2 kd = __half22float2(*reinterpret_cast<const __half2*>(&kp[i >> 1]));
+            const float d0 = __uint_as_float(dv[i]) * kd.x * c1;
+            const float d1 = __uint_as_float(dv[i + 1]) * kd.y * c1;
+            dk[i >> 1] = pack_bf16(d0, d1);
+            csum += d0 + d1;
+          }
+          sat_w = csum;
+          if (has_pos) sat_p = csum;  // saturated chunks hit both last buckets
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4)
+            *reinterpret_cast<int4*>(ds_smem + sw128_offset(r, c0 + q4 * 8)) =
+                make_int4(dk[4 * q4], dk[4 * q4 + 1], dk[4 * q4 + 2], dk[4 * q4 + 3]);
+        } else if (cls == 0) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4)
+            *reinterpret_cast<int4*>(ds_smem + sw128_offset(r, c0 + q4 * 8)) = make_int4(0, 0, 0, 0);
+        } else {
+          // general chunk: exact bucket scatter.  Runs of equal buckets along the row
+          // accumulate in a register and are flushed with predicated fire-and-forget
+          // fp32 reductions into this CTA's bins
+          uint32_t rb = (uint32_t)(nb - 1);
+          float rs = 0.f;
 #pragma unroll 1
-        for (int ci = 0; ci < 2; ++ci) {
-          const int c0 = 64 * wg + 32 * ci;
-          const int cls = (cls_bits >> (2 * ci)) & 3;
-          const uint32_t cbase = tSg + 32 * ci;
-          if (cls == 1) {
-            uint32_t dv[32], kp[16], dk[16];
-            tmem_ld32(tDP + lane_off + c0, dv);
-            tmem_ld16(cbase + 16, kp);
+          for (int g8 = 0; g8 < 32; g8 += 8) {
+            uint32_t dv[8], dk[4];
+            tmem_ld8(dpbase + g8, dv);
+            const uint32_t bw0 = bl[g8 >> 2], bw1 = bl[(g8 >> 2) + 1];
+            uint32_t kw[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) kw[j] = kl[(g8 >> 1) + j];
             tmem_ld_wait();
-            float csum = 0.f;
+            float dd[8];
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              const float2 kd = __half22float2(*reinterpret_cast<const __half2*>(&kp[i >> 1]));
-              const float d0 = __uint_as_float(dv[i]) * kd.x * c1;
-              const float d1 = __uint_as_float(dv[i + 1]) * kd.y * c1;
-              dk[i >> 1] = pack_bf16(d0, d1);
-              csum += d0 + d1;
+            for (int j = 0; j < 8; j += 2) {
+              const float2 kd = __half22float2(*reinterpret_cast<const __half2*>(&kw[j >> 1]));
+              dd[j] = __uint_as_float(dv[j]) * kd.x * c1;
+              dd[j + 1] = __uint_as_float(dv[j + 1]) * kd.y * c1;
+              dk[j >> 1] = pack_bf16(dd[j], dd[j + 1]);
             }
-            sat_w += csum;
-            if (has_pos) sat_p += csum;  // saturated chunks hit both last buckets
+            *reinterpret_cast<int4*>(ds_smem + sw128_offset(r, c0 + g8)) = make_int4(dk[0], dk[1], dk[2], dk[3]);
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4)
-              *reinterpret_cast<int4*>(ds_smem + sw128_offset(r, (c0 & 63) + q4 * 8)) =
-                  make_int4(dk[4 * q4], dk[4 * q4 + 1], dk[4 * q4 + 2], dk[4 * q4 + 3]);
-          } else if (cls == 0) {
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4)
-              *reinterpret_cast<int4*>(ds_smem + sw128_offset(r, (c0 & 63) + q4 * 8)) = make_int4(0, 0, 0, 0);
-          } else {
-            // general chunk, 8 columns per step: exact bucket scatter into the bins
-#pragma unroll 1
-            for (int g8 = 0; g8 < 32; g8 += 8) {
-              uint32_t dv[8], kp[4], dk[4];
-              tmem_ld8(tDP + lane_off + c0 + g8, dv);
-              tmem_ld4(cbase + 16 + (g8 >> 1), kp);
-              tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 8; i += 2) {
-                const float2 kd = __half22float2(*reinterpret_cast<const __half2*>(&kp[i >> 1]));
-                float dd[2] = {__uint_as_float(dv[i]) * kd.x * c1, __uint_as_float(dv[i + 1]) * kd.y * c1};
-                dk[i >> 1] = pack_bf16(dd[0], dd[1]);
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                  const int qi = c0 + g8 + i + u;
-                  const int64_t qpos = qp_tile + qi;
-                  if (krow_ok && qi < nq && kpos <= qpos) {
-                    const int b = bucket_smem(tsq[qi] - tk, s_bias, cap);
-                    if (b == nb - 1)
-                      sat_w += dd[u];
-                    else
-                      atomicAdd(&s_bins[b], dd[u]);
-                    if (has_pos) {
-                      const int64_t rr = qpos - kpos;
-                      const int rel = rr > P - 1 ? P - 1 : (int)rr;
-                      if (rel == P - 1)
-                        sat_p += dd[u];
-                      else
-                        atomicAdd(&s_bins[C::MAX_NB + rel], dd[u]);
-                    }
-                  }
-                }
+            for (int j = 0; j < 8; ++j) {
+              const bool ok = (okm >> (g8 + j)) & 1u;
+              const uint32_t b = ((j < 4 ? bw0 : bw1) >> (8 * (j & 3))) & 0xFFu;
+              const bool ch = ok && b != rb;
+              red_add_f32_if(g_bins + rb, rs, ch && rs != 0.f);
+              rb = ch ? b : rb;
+              rs = ch ? dd[j] : rs + dd[j];  // dd = 0 on masked elements
+              if (has_pos) {
+                const int rel = min(rel0 + g8 + j, P - 1);
+                red_add_f32_if(g_bins + 256 + max(rel, 0), dd[j], ok && rel != P - 1);
+                sat_p += (ok && rel == P - 1) ? dd[j] : 0.f;
               }
-              *reinterpret_cast<int4*>(ds_smem + sw128_offset(r, (c0 & 63) + g8)) =
-                  make_int4(dk[0], dk[1], dk[2], dk[3]);
             }
           }
+          red_add_f32_if(g_bins + rb, rs, rs != 0.f);
         }
         acc_w += (double)sat_w;
         acc_p += (double)sat_p;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
-        mbar_arrive(ds_full);
-        if (tr) trace_ev(p, 2, tcnt, 25, t);
+        mbar_arrive(&ds_full[x]);
+        if (tr) trace_ev(p, trole, tcnt, 25, t);
         __syncwarp();
         if (lane == 0) mbar_arrive(&qd_empty[st]);  // done with this stage's ts_q
-        ++qd_it;
       }
     }
     // ---- d_ts_weights / d_pos: last buckets as fp64 partials, the rest from smem bins
@@ -500,12 +522,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (acc_w != 0.0) atomicAdd(&p.d_ts_weights[nb - 1], acc_w);
       if (has_pos && acc_p != 0.0) atomicAdd(&p.d_pos_weights[P - 1], acc_p);
     }
+    __threadfence();
     named_bar_sync(1, 32 * kCompWarps);
-    for (int i = et; i < nb; i += 32 * kCompWarps)
-      if (s_bins[i] != 0.f) atomicAdd(&p.d_ts_weights[i], (double)s_bins[i]);
+    for (int i = et; i < nb; i += 32 * kCompWarps) {
+      const float v = __ldcg(g_bins + i);
+      if (v != 0.f) atomicAdd(&p.d_ts_weights[i], (double)v);
+    }
     if (has_pos)
-      for (int i = et; i < P; i += 32 * kCompWarps)
-        if (s_bins[C::MAX_NB + i] != 0.f) atomicAdd(&p.d_pos_weights[i], (double)s_bins[C::MAX_NB + i]);
+      for (int i = et; i < P - 1; i += 32 * kCompWarps) {
+        const float v = __ldcg(g_bins + 256 + i);
+        if (v != 0.f) atomicAdd(&p.d_pos_weights[i], (double)v);
+      }
   } else if (warp >= 12) {
     // ================= dK / dV drain (thread = kv row)
     const int r = tid - 384;
@@ -515,12 +542,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int2 it = p.wl.bwd[g / H];
       const int h = g % H;
       const Seg sg = load_seg(p.seg, it.x);
-      int t0, nt;
-      q_tiles(sg, it.y, t0, nt);
+      int h0, nh;
+      dkv_halves(sg, it.y, h0, nh);
       const int64_t kpos = (int64_t)it.y * kBN + r;
       const bool krow_ok = kpos < sg.kv_len;
       const int64_t krow = sg.kv_row0 + kpos;
-      if (t0 >= nt) {
+      if (h0 >= nh) {
         // no query sees this kv tile: its dK/dV rows are zero
         if (krow_ok && !p.dk_accum)
           for (int c = 0; c < D; c += 8) {
@@ -537,13 +564,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const uint32_t tsrc = part ? tDK : tDV;
         float* acc = part ? p.dk_accum : p.dv_accum;
 #pragma unroll 1
-        for (int c0 = 0; c0 < D; c0 += 32) {
+        for (int cc = 0; cc < D; cc += 32) {
           uint32_t v[32];
-          tmem_ld32(tsrc + lane_off + c0, v);
+          tmem_ld32(tsrc + lane_off + cc, v);
           tmem_ld_wait();
           if (!krow_ok) continue;
           if (acc) {
-            float* dst = acc + krow * HD + h * D + c0;
+            float* dst = acc + krow * HD + h * D + cc;
 #pragma unroll
             for (int i = 0; i < 32; i += 4)
               asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + i), "f"(__uint_as_float(v[i])),
@@ -551,7 +578,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                            "f"(__uint_as_float(v[i + 3]))
                            : "memory");
           } else {
-            __nv_bfloat16* dst = (part ? (p.dk + krow * p.ld_dk) : (p.dv + krow * p.ld_dv)) + h * D + c0;
+            __nv_bfloat16* dst = (part ? (p.dk + krow * p.ld_dk) : (p.dv + krow * p.ld_dv)) + h * D + cc;
             uint32_t pk[16];
 #pragma unroll
             for (int i = 0; i < 32; i += 2) pk[i >> 1] = pack_bf16(__uint_as_float(v[i]), __uint_as_float(v[i + 1]));
@@ -982,7 +1009,7 @@ int launch_bwd(const TMaps& tm, const AttnParams& p, const jh_attn_args& a, int 
     attr = true;
   }
   if (a.prof_event_start) cudaEventRecord((cudaEvent_t)a.prof_event_start, s);
-  hstu_bwd_dkv_kernel<D><<<grid, kBwdThreads, C::SMEM, s>>>(tm.q, tm.k, tm.v, tm.dout, tm.tsq, p);
+  hstu_bwd_dkv_kernel<D><<<grid, kBwdThreads, C::SMEM, s>>>(tm.q64, tm.k, tm.v, tm.do64, tm.tsq72, p);
   if (cudaError_t e = cudaGetLastError()) return (int)e;
   hstu_bwd_dq_kernel<D><<<grid, kDqThreads, Q::SMEM, s>>>(tm.q, tm.k, tm.v, tm.dout, tm.tsq, tm.tsk, p,
                                                          (__nv_bfloat16*)a.dq, a.ld_dq);

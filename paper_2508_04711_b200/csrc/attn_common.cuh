@@ -13,6 +13,10 @@ constexpr int kBN = 128;  // kv rows per tile
 constexpr int kTsBox = 136;
 constexpr int kTsBytes = kTsBox * 8;
 constexpr int kTsSlot = 144;  // int64 stride between smem slots (1152 B)
+// 64-row half tiles (dKV kernel): ts box 72 (64 + parity, 16B multiple)
+constexpr int kTsBoxH = 72;
+constexpr int kTsBytesH = kTsBoxH * 8;
+constexpr int kTsSlotH = 80;  // TMA smem destinations must be 128-byte aligned
 
 struct SegArgs {
   const int64_t* q_offsets;
@@ -54,12 +58,14 @@ struct WorkHeader {
   int32_t pad[14];
 };
 
-// Workspace: [WorkHeader][fwd items int2 x max_f][bwd items int2 x max_b][dq_accum fp32]
+// Workspace: [WorkHeader][fwd items int2 x max_f][bwd items int2 x max_b] ...
+// [per-CTA d_ts_weights / d_pos_weights partial bins, fp32 kBinsPerCta each]
+constexpr int kBinsPerCta = 256 + 1024;
 struct WorkLists {
   WorkHeader* hdr;
   int2* fwd;
   int2* bwd;
-  float* dq_accum;
+  float* bins;
 };
 
 constexpr int kLevels = 4096;
@@ -153,9 +159,10 @@ static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, 
   }
 }
 
-// q, k, v, dout (bf16 2-D) and ts_q, ts_k (int64 1-D) tensor maps
+// q, k, v, dout (bf16 2-D, 128-row boxes) and ts_q, ts_k (int64 1-D) tensor maps
 struct TMaps {
   CUtensorMap q, k, v, dout, tsq, tsk;
+  CUtensorMap q64, do64, tsq72;  // 64-row boxes for the dKV kernel
 };
 
 // Parameters shared by the fwd / bwd attention kernels.

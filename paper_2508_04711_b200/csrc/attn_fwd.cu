@@ -314,6 +314,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_wait(&s_full[sb], (s_it >> 1) & 1);
         if (tr) trace_ev(p, 4, tcnt, 40, s_it);
         mbar_wait(&p_empty[sb], ((s_it >> 1) & 1) ^ 1);
+        if (tr) trace_ev(p, 4, tcnt, 48, s_it);
         tc_fence_after();
         const int64_t* tsk = s_tsk + ts * kTsSlot + ((sg.kv_row0 + kv0) & 1);
         const uint32_t tS = tmem + 128 * sb + lane_off;
@@ -339,20 +340,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int i = 0; i < 32; i += 2) {
             const float h0 = fmaf(__uint_as_float(v[i]), c1, cb);
             const float h1 = fmaf(__uint_as_float(v[i + 1]), c1, cb);
-            const float2 t = tanh2_approx(h0, h1);
-            pk[i >> 1] = pack_bf16(fmaf(h0, t.x, h0), fmaf(h1, t.y, h1));
+            pk[i >> 1] = pack_bf16(fmaf(h0, tanh_approx(h0), h0), fmaf(h1, tanh_approx(h1), h1));
           }
         };
         if (cls_bits == 5) {
           // both chunks unmasked and saturated (the common case): one TMEM round trip
           uint32_t va[32], vb[32], pk[16];
+          if (tr) trace_ev(p, 4, tcnt, 44, s_it);
           tmem_ld32(tS + 64 * wg, va);
           tmem_ld32(tS + 64 * wg + 32, vb);
           tmem_ld_wait();
+          if (tr) trace_ev(p, 4, tcnt, 45, s_it);
           silu_fast(va, pk);
           tmem_st16(tP + 32 * wg, pk);
           silu_fast(vb, pk);
           tmem_st16(tP + 32 * wg + 16, pk);
+          if (tr) trace_ev(p, 4, tcnt, 46, s_it);
         } else
 #pragma unroll 1
         for (int ci = 0; ci < 2; ++ci) {
@@ -400,6 +403,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
         }
         tmem_st_wait();
+        if (tr) trace_ev(p, 4, tcnt, 47, s_it);
         tc_fence_before();
         mbar_arrive(&p_full[sb]);
         if (tr) trace_ev(p, 4, tcnt, 41, s_it);

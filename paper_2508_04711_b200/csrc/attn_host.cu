@@ -27,8 +27,10 @@ static int sm_count() {
 }
 
 struct WsLayout {
-  size_t items_f, items_b, dq, total;
+  size_t items_f, items_b, bins, total;
 };
+
+static size_t bins_bytes() { return (size_t)sm_count() * kBinsPerCta * 4; }
 
 static WsLayout ws_layout(int64_t q_rows, int64_t kv_total, int64_t nseg, int32_t H, int32_t D) {
   WsLayout w;
@@ -36,8 +38,8 @@ static WsLayout ws_layout(int64_t q_rows, int64_t kv_total, int64_t nseg, int32_
   int64_t max_b = kv_total / kBN + nseg + 1;
   w.items_f = sizeof(WorkHeader);
   w.items_b = w.items_f + ((size_t)max_f * 8 + 255) / 256 * 256;
-  w.dq = w.items_b + ((size_t)max_b * 8 + 255) / 256 * 256;
-  w.total = w.dq + (size_t)std::max<int64_t>(q_rows, 0) * H * D * 4;
+  w.bins = w.items_b + ((size_t)max_b * 8 + 255) / 256 * 256;
+  w.total = w.bins + bins_bytes();
   return w;
 }
 
@@ -82,8 +84,8 @@ static int validate(const jh_attn_args* a, bool bwd) {
     }
   }
   WsLayout w = ws_layout(a->q_rows, a->q_rows, a->num_segments, a->num_heads, a->head_dim);
-  if (!a->workspace || a->workspace_bytes < (bwd ? w.total : w.dq))
-    return set_error(JH_ERR_INVALID, "workspace too small (need >= %zu bytes)", bwd ? w.total : w.dq);
+  if (!a->workspace || a->workspace_bytes < (bwd ? w.total : w.bins))
+    return set_error(JH_ERR_INVALID, "workspace too small (need >= %zu bytes)", bwd ? w.total : w.bins);
   return JH_OK;
 }
 
@@ -127,10 +129,9 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
   p->wl.hdr = (WorkHeader*)ws;
   p->wl.fwd = (int2*)(ws + w.items_f);
   p->wl.bwd = (int2*)(ws + w.items_b);
-  // dq accumulator at the end of the caller's workspace (its size is q_rows*H*d*4)
-  size_t dq_bytes = (size_t)a->q_rows * a->num_heads * a->head_dim * 4;
-  p->wl.dq_accum = bwd ? (float*)(ws + ((a->workspace_bytes - dq_bytes) & ~size_t(255))) : nullptr;
-  if (bwd && (uint8_t*)p->wl.dq_accum < ws + w.items_b + 8)
+  // per-CTA gradient bins at the end of the caller's workspace
+  p->wl.bins = bwd ? (float*)(ws + ((a->workspace_bytes - bins_bytes()) & ~size_t(255))) : nullptr;
+  if (bwd && (uint8_t*)p->wl.bins < ws + w.items_b + 8)
     return set_error(JH_ERR_INVALID, "workspace too small");
   const uint64_t HD = (uint64_t)a->num_heads * a->head_dim;
   if ((uintptr_t)a->ts_q % 16 || (uintptr_t)a->ts_k % 16)
@@ -141,8 +142,11 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
       make_tmap_i64_1d(&tm->tsq, a->ts_q, a->q_rows, kTsBox) ||
       make_tmap_i64_1d(&tm->tsk, a->ts_k, a->kv_rows, kTsBox))
     return set_error(JH_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  if (bwd && make_tmap_bf16_2d(&tm->dout, a->dout, a->q_rows, HD, a->ld_do, 128))
-    return set_error(JH_ERR_CUDA, "cuTensorMapEncodeTiled failed (dout)");
+  if (bwd && (make_tmap_bf16_2d(&tm->dout, a->dout, a->q_rows, HD, a->ld_do, 128) ||
+              make_tmap_bf16_2d(&tm->q64, a->q, a->q_rows, HD, a->ld_q, 64) ||
+              make_tmap_bf16_2d(&tm->do64, a->dout, a->q_rows, HD, a->ld_do, 64) ||
+              make_tmap_i64_1d(&tm->tsq72, a->ts_q, a->q_rows, kTsBoxH)))
+    return set_error(JH_ERR_CUDA, "cuTensorMapEncodeTiled failed (bwd maps)");
   build_work_kernel<<<1, 1024, 0, s>>>(p->seg, p->wl);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(JH_ERR_CUDA, "build_work: %s", cudaGetErrorString(e));
@@ -158,7 +162,7 @@ extern "C" {
 size_t jh_attn_workspace_bytes(int64_t q_rows, int64_t kv_len_total, int64_t num_segments, int32_t num_heads,
                                int32_t head_dim) {
   // the layout is q_rows-bounded for the fwd list; the bwd list bound uses
-  // max(kv_len_total, q_rows); dq accumulator last
+  // max(kv_len_total, q_rows); per-CTA bins last
   int64_t kvt = std::max(kv_len_total, q_rows);
   WsLayout a = ws_layout(q_rows, q_rows, num_segments, num_heads, head_dim);
   WsLayout b = ws_layout(q_rows, kvt, num_segments, num_heads, head_dim);

@@ -57,4 +57,40 @@ JH_DEV int bucket_any(int64_t d, const SmemBias* s, bool small, const DevBiasTab
   return bucket_of(d, t.thr, t.base, t.cap);
 }
 
+// Per-octave lookup entry for the fused kernels (cap < 2^32 - 1): the
+// octave's threshold and base bucket plus the two candidate weights already
+// scaled by the kernel's constant (one 16-byte shared load per element).
+struct __align__(16) OctEntry {
+  uint32_t thr;
+  int32_t base;
+  float wlo, whi;
+};
+
+// Fill 32 entries from the parameter table and the bucket weights (global).
+JH_DEV void oct_table_fill(OctEntry* t, const DevBiasTable& bt, const float* w, float scale, int tid, int nthreads) {
+  for (int o = tid; o < 32; o += nthreads) {
+    const int b = bt.base[o];
+    const int b1 = b + 1 < bt.nb ? b + 1 : bt.nb - 1;
+    OctEntry e;
+    e.thr = bt.thr[o] > 0xFFFFFFFFll ? 0xFFFFFFFFu : static_cast<uint32_t>(bt.thr[o]);
+    e.base = b;
+    e.wlo = w[b] * scale;
+    e.whi = w[b1] * scale;
+    t[o] = e;
+  }
+}
+
+// Time delta clamped to [0, cap] (cap < 2^32 - 1) as a 32-bit value.
+JH_DEV uint32_t clamp_delta(int64_t d, int64_t cap) {
+  return d <= 0 ? 0u : (d >= cap ? static_cast<uint32_t>(cap) : static_cast<uint32_t>(d));
+}
+
+// Bucket and scaled weight of a clamped delta.
+JH_DEV void oct_lookup(uint32_t du, const OctEntry* t, int& bucket, float& wscaled) {
+  const OctEntry e = t[31 - __clz(du + 1u)];
+  const bool hi = du >= e.thr;
+  bucket = e.base + (hi ? 1 : 0);
+  wscaled = hi ? e.whi : e.wlo;
+}
+
 }  // namespace jh

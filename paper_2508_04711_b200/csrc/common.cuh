@@ -216,6 +216,18 @@ JH_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
 JH_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------- math
+// Fire-and-forget fp32 reduction into global memory (no return value, no retry loop).
+JH_DEV void red_add_f32(float* addr, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
+}
+
+// Predicated fire-and-forget reduction (no branch around it).
+JH_DEV void red_add_f32_if(float* addr, float v, bool pred) {
+  asm volatile("{ .reg .pred p; setp.ne.b32 p, %2, 0; @p red.global.add.f32 [%0], %1; }" ::"l"(addr), "f"(v),
+               "r"((int)pred)
+               : "memory");
+}
+
 JH_DEV float tanh_approx(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
