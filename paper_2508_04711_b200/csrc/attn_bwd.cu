@@ -609,10 +609,9 @@ struct DqCfg {
   static constexpr int DS_OFF = 5 * TILE;                 // dS: 128 q x 128 kv bf16 (2 panels)
   static constexpr int TSQ_OFF = DS_OFF + 32768;          // int64 [kTsSlot]
   static constexpr int TSK_OFF = TSQ_OFF + kTsSlot * 8;   // int64 [2][kTsSlot]
-  static constexpr int W_OFF = TSK_OFF + 2 * kTsSlot * 8; // float [256]
-  static constexpr int PW_OFF = W_OFF + 1024;             // float [1024]
-  static constexpr int TAB_OFF = PW_OFF + 4096;           // SmemBias
-  static constexpr int KMAX_OFF = TAB_OFF + 160;          // int64 [2][4]
+  static constexpr int OCT_OFF = TSK_OFF + 2 * kTsSlot * 8; // OctEntry [32]
+  static constexpr int PW_OFF = OCT_OFF + 32 * 16;           // float [1024] x c1
+  static constexpr int KMAX_OFF = PW_OFF + 4096;             // int64 [2][4]
   static constexpr int BAR_OFF = KMAX_OFF + 64;
   static constexpr int NBARS = 20;
   static constexpr int TMEMPTR_OFF = BAR_OFF + NBARS * 8;
@@ -629,9 +628,8 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   int64_t* s_tsq = reinterpret_cast<int64_t*>(smem + C::TSQ_OFF);
   int64_t* s_tsk = reinterpret_cast<int64_t*>(smem + C::TSK_OFF);
-  float* s_w = reinterpret_cast<float*>(smem + C::W_OFF);
-  float* s_pw = reinterpret_cast<float*>(smem + C::PW_OFF);
-  SmemBias* s_bias = reinterpret_cast<SmemBias*>(smem + C::TAB_OFF);
+  OctEntry* s_oct = reinterpret_cast<OctEntry*>(smem + C::OCT_OFF);
+  float* s_pwc = reinterpret_cast<float*>(smem + C::PW_OFF);  // pos weights x c1
   int64_t* s_kmax = reinterpret_cast<int64_t*>(smem + C::KMAX_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* q_full = bars + 0;
@@ -657,9 +655,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   const bool has_pos = P > 0;
 
   if (smem_u32(smem) & 1023) __trap();
-  for (int i = tid; i < nb; i += blockDim.x) s_w[i] = p.ts_weights[i];
-  for (int i = tid; i < P; i += blockDim.x) s_pw[i] = p.pos_weights[i];
-  smem_bias_fill(s_bias, p.bias, tid, blockDim.x);
+  const float c1 = 0.5f * rsqrtf((float)D);
+  oct_table_fill(s_oct, p.bias, p.ts_weights, c1, tid, blockDim.x);
+  for (int i = tid; i < P; i += blockDim.x) s_pwc[i] = p.pos_weights[i] * c1;
   if (tid == 0) {
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1 + kCompWarps);
@@ -838,12 +836,12 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     const int r = et & 127;
     const int lane = r & 31;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const float c1 = 0.5f * rsqrtf((float)D);
     const int64_t cap = p.bias.cap;
-    float cb = s_w[nb - 1];
-    if (has_pos) cb += s_pw[P - 1];
+    float cb = p.ts_weights[nb - 1];
+    if (has_pos) cb += p.pos_weights[P - 1];
     cb *= c1;
-    uint32_t q_it = 0, k_it = 0, s_it = 0, dp_cnt = 0, ds_cnt = 0, o_it = 0;
+    uint32_t q_it = 0, k_it = 0, s_it = 0, dp_cnt = 0, ds_cnt = 0, o_it = 0, tcnt = 0;
+    const bool tr = (tid == 128);  // timeline role 4 (the dKV kernel uses roles 0-3)
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
       const int2 it = p.wl.fwd[g / H];
       const int h = g % H;
@@ -889,11 +887,14 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           }
           cls_bits |= cls << (2 * ci);
         }
+        if (tr) trace_ev(p, 4, tcnt, 30, j);
         mbar_wait(&s_full[sb], (s_it >> 1) & 1);
+        if (tr) trace_ev(p, 4, tcnt, 31, j);
         mbar_wait(dp_full, dp_cnt & 1);
         ++dp_cnt;
         if (ds_cnt > 0) mbar_wait(ds_empty, (ds_cnt - 1) & 1);
         ++ds_cnt;
+        if (tr) trace_ev(p, 4, tcnt, 32, j);
         tc_fence_after();
         const uint32_t tS = tmem + 128 * sb + lane_off;
 #pragma unroll 1
@@ -925,26 +926,34 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             for (int q4 = 0; q4 < 4; ++q4)
               *reinterpret_cast<int4*>(prow + sw128_offset(r, (c0 & 63) + q4 * 8)) = make_int4(0, 0, 0, 0);
           } else {
+            // general chunk: exact per-element bucket, positional bias and mask
+            const int relc = (int)(qpos - kv0 - c0);                           // qpos - kpos of column 0
+            const int ncol = row_ok ? (int)min(kv_lim - kv0 - c0, (int64_t)32) : 0;  // in-range columns
 #pragma unroll 1
             for (int g8 = 0; g8 < 32; g8 += 8) {
               uint32_t sv[8], dv[8], dsk[4];
               tmem_ld8(tS + c0 + g8, sv);
               tmem_ld8(tDP + lane_off + c0 + g8, dv);
+              float bc[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                int b;
+                oct_lookup(clamp_delta(tq - tsk[c0 + g8 + i], cap), s_oct, b, bc[i]);
+              }
+              if (has_pos) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) bc[i] += s_pwc[min(max(relc - g8 - i, 0), P - 1)];
+              }
               tmem_ld_wait();
 #pragma unroll
               for (int i = 0; i < 8; i += 2) {
                 float dd[2];
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
-                  const int64_t kpos = kv0 + c0 + g8 + i + u;
-                  float bias = s_w[bucket_smem(tq - tsk[c0 + g8 + i + u], s_bias, cap)];
-                  if (has_pos) {
-                    const int64_t rel = qpos - kpos;
-                    bias += s_pw[rel < 0 ? 0 : (rel > P - 1 ? P - 1 : (int)rel)];
-                  }
-                  const float hh = (__uint_as_float(sv[i + u]) + bias) * c1;
+                  const int k = g8 + i + u;
+                  const float hh = fmaf(__uint_as_float(sv[i + u]), c1, bc[i + u]);
                   const float th = tanh_approx(hh);
-                  const bool ok = row_ok && kpos <= qpos && kpos < kv_lim;
+                  const bool ok = k < ncol && k <= relc;
                   dd[u] = ok ? __uint_as_float(dv[i + u]) * (1.f + th) * (fmaf(-hh, th, hh) + 1.f) * c1 : 0.f;
                 }
                 dsk[i >> 1] = pack_bf16(dd[0], dd[1]);
@@ -957,6 +966,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         mbar_arrive(ds_full);
+        if (tr) trace_ev(p, 4, tcnt, 33, j);
         __syncwarp();
         if (lane == 0) mbar_arrive(&k_empty[st]);  // done with this stage's ts_k
         ++k_it;

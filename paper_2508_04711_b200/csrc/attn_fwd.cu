@@ -39,10 +39,9 @@ struct FwdCfg {
   static constexpr int V_OFF = K_OFF + NS * TILE_BYTES;
   static constexpr int TSQ_OFF = V_OFF + NS * TILE_BYTES;     // int64 [2][kTsSlot]
   static constexpr int TSK_OFF = TSQ_OFF + 2 * kTsSlot * 8;   // int64 [kTsRing][kTsSlot]
-  static constexpr int W_OFF = TSK_OFF + kTsRing * kTsSlot * 8;  // float w[256]
-  static constexpr int PW_OFF = W_OFF + 256 * 4;           // float pw[<=1024]
-  static constexpr int TAB_OFF = PW_OFF + 1024 * 4;        // SmemBias (160 B)
-  static constexpr int KMAX_OFF = TAB_OFF + 256;           // int64 [kTsRing][4] per-chunk max ts_k
+  static constexpr int OCT_OFF = TSK_OFF + kTsRing * kTsSlot * 8;  // OctEntry [32]
+  static constexpr int PW_OFF = OCT_OFF + 32 * 16;          // float pw[<=1024] x c1
+  static constexpr int KMAX_OFF = PW_OFF + 1024 * 4;        // int64 [kTsRing][4] per-chunk max ts_k
   static constexpr int BAR_OFF = KMAX_OFF + kTsRing * 32;  // mbarriers
   static constexpr int NBARS = 4 + 4 * NS + 3 * kTsRing + 6 + 2;
   static constexpr int TMEMPTR_OFF = BAR_OFF + NBARS * 8;
@@ -59,9 +58,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   int64_t* s_tsq = reinterpret_cast<int64_t*>(smem + C::TSQ_OFF);
   int64_t* s_tsk = reinterpret_cast<int64_t*>(smem + C::TSK_OFF);
-  float* s_w = reinterpret_cast<float*>(smem + C::W_OFF);
-  float* s_pw = reinterpret_cast<float*>(smem + C::PW_OFF);
-  SmemBias* s_bias = reinterpret_cast<SmemBias*>(smem + C::TAB_OFF);
+  OctEntry* s_oct = reinterpret_cast<OctEntry*>(smem + C::OCT_OFF);
+  float* s_pwc = reinterpret_cast<float*>(smem + C::PW_OFF);  // pos weights x c1
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* q_full = bars;                 // [2]  TMA Q + ts_q
   uint64_t* q_empty = bars + 2;            // [2]  last S MMA + epilogue read of ts_q
@@ -86,9 +84,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int nb = p.bias.nb;
 
   if (smem_u32(smem) & 1023) __trap();  // 128B-swizzled operand tiles need 1 KB alignment
-  smem_bias_fill(s_bias, p.bias, tid, blockDim.x);
-  for (int i = tid; i < nb; i += blockDim.x) s_w[i] = p.ts_weights[i];
-  for (int i = tid; i < p.num_pos; i += blockDim.x) s_pw[i] = p.pos_weights[i];
+  const float c1 = 0.5f * rsqrtf((float)D);  // SiLU(s) = h + h*tanh(h), h = s/2 (scaled by 1/sqrt(d))
+  oct_table_fill(s_oct, p.bias, p.ts_weights, c1, tid, blockDim.x);
+  for (int i = tid; i < p.num_pos; i += blockDim.x) s_pwc[i] = p.pos_weights[i] * c1;
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
@@ -270,12 +268,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int r = et & 127;          // q row within the tile (= TMEM lane)
     const int lane = r & 31;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const float c1 = 0.5f * rsqrtf((float)D);  // SiLU(s) = h + h*tanh(h), h = s/2
     const int64_t cap = p.bias.cap;
     const int P = p.num_pos;
     const bool has_pos = P > 0;
-    float cb = s_w[nb - 1];
-    if (has_pos) cb += s_pw[P - 1];
+    float cb = p.ts_weights[nb - 1];
+    if (has_pos) cb += p.pos_weights[P - 1];
     cb *= c1;
     uint32_t q_it = 0, s_it = 0, t_it = 0, o_it = 0, tcnt = 0;
     const bool tr = (tid == 128);
@@ -375,26 +372,32 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           } else {
             // general chunk (diagonal / short time gaps): exact per-element
             // bucket, positional bias and mask, 8 columns per step
-            const int64_t kc0 = kv0 + c0;
+            const int relc = (int)(qpos - kv0 - c0);                        // qpos - kpos of column 0
+            const int ncol = (int)min(kv_lim - kv0 - c0, (int64_t)32);      // in-range columns
 #pragma unroll 1
             for (int g8 = 0; g8 < 32; g8 += 8) {
               uint32_t v[8], pk[4];
               tmem_ld8(tS + c0 + g8, v);
+              float bc[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                int b;
+                oct_lookup(clamp_delta(tq - tsk[c0 + g8 + i], cap), s_oct, b, bc[i]);
+              }
+              if (has_pos) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) bc[i] += s_pwc[min(max(relc - g8 - i, 0), P - 1)];
+              }
               tmem_ld_wait();
 #pragma unroll
               for (int i = 0; i < 8; i += 2) {
                 float y[2];
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
-                  const int64_t kpos = kc0 + g8 + i + u;
-                  float bias = s_w[bucket_smem(tq - tsk[c0 + g8 + i + u], s_bias, cap)];
-                  if (has_pos) {
-                    const int64_t rel = qpos - kpos;
-                    bias += s_pw[rel < 0 ? 0 : (rel > P - 1 ? P - 1 : (int)rel)];
-                  }
-                  const float hh = (__uint_as_float(v[i + u]) + bias) * c1;
+                  const int k = g8 + i + u;
+                  const float hh = fmaf(__uint_as_float(v[i + u]), c1, bc[i + u]);
                   const float yy = fmaf(hh, tanh_approx(hh), hh);
-                  y[u] = (kpos <= qpos && kpos < kv_lim) ? yy : 0.f;
+                  y[u] = (k <= relc && k < ncol) ? yy : 0.f;
                 }
                 pk[i >> 1] = pack_bf16(y[0], y[1]);
               }
