@@ -66,51 +66,81 @@ def _flops(lengths) -> float:
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """SM clock / throttle-reason sampler running during the timed region
+    (NVML every ~1 ms in a thread; nvidia-smi -lms as a fallback)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.rows = []
+        self.thread = None
+
+    def _nvml_loop(self, nv, handle):
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        mx = nv.nvmlDeviceGetMaxClockInfo(handle, nv.NVML_CLOCK_SM)
+        while not self.stop:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(handle, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(handle)
+                self.rows.append((float(sm), float(mx), ["Active" if rs & b else "Not Active" for b in bits]))
+            except Exception:
+                pass
+            time.sleep(0.001)
 
     def __enter__(self):
+        self.stop = False
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import threading
+            import pynvml as nv
+            nv.nvmlInit()
+            handle = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, handle), daemon=True)
+            self.thread.start()
         except Exception:
-            self.proc = None
-        time.sleep(0.2)
+            self.thread = None
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                     "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            except Exception:
+                self.proc = None
+            time.sleep(0.5)
         return self
 
     def __exit__(self, *a):
-        self.out = ""
+        self.stop = True
+        if self.thread is not None:
+            self.thread.join(timeout=2)
         if self.proc is not None:
             time.sleep(0.1)
             self.proc.terminate()
             try:
-                self.out, _ = self.proc.communicate(timeout=5)
+                out, _ = self.proc.communicate(timeout=5)
             except Exception:
                 self.proc.kill()
+                out = ""
+            for line in (out or "").strip().splitlines():
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 6:
+                    try:
+                        self.rows.append((float(parts[0]), float(parts[1]), parts[2:6]))
+                    except ValueError:
+                        pass
 
     def summary(self):
-        rows = []
-        for line in (self.out or "").strip().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 6:
-                try:
-                    rows.append((float(parts[0]), float(parts[1]), parts[2:6]))
-                except ValueError:
-                    pass
+        rows = self.rows
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, flags in rows for i, f in enumerate(flags) if f.lower() == "active"})
-        busy = [r[0] for r in rows]
-        return {"sm_mhz": float(np.median(busy)), "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
-                "samples": len(rows)}
+        reasons = sorted({self.NAMES[i] for _, _, flags in rows for i, f in enumerate(flags)
+                          if f.lower() == "active"})
+        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows),
+                "source": "nvml" if self.thread is not None else "nvidia-smi"}
 
 
 # --------------------------------------------------------------------- GPU arm

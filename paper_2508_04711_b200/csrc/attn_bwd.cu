@@ -10,20 +10,23 @@
 //       warp 0      TMA: K_j, V_j per item (reloaded once the item's last S^T/dP^T ran)
 //       warp 2      TMA: Q_h, dO_h, ts_q per half (kQStages ring); TMEM allocator
 //       warp 1      MMA: S^T = K Q^T, dP^T = V dO^T (128 x 64, two TMEM buffers),
-//                   dV += P^T dO (A = P^T in TMEM), dK += dS^T Q (A = dS^T in smem)
+//                   dV += P^T dO, dK += dS^T Q (A = P^T / dS^T in TMEM)
 //       warp 3      per-chunk min of ts_q (saturation test)
 //       warps 4-11  compute, thread = (kv row, 32-q-column chunk of the half):
 //                   phase P  : S^T -> P^T (TMEM) and SiLU'(S) (f16, TMEM)
-//                   phase dS : dP^T -> dS^T = dP SiLU'(S)/sqrt(d) (smem), d_ts_weights
+//                   phase dS : dP^T -> dS^T = dP SiLU'(S)/sqrt(d) (TMEM), d_ts_weights
 //       warps 12-15 drain dK / dV (bf16 store, or fp32 accumulate for CP)
-//     TMEM: S^T buffers [0,64) [64,128) (P^T of a 32-column chunk overwrites the
-//           chunk's first 16 columns; SiLU'(S) stays in registers) | dP^T
+//     TMEM: S^T buffers [0,64) [64,128): per 32-column chunk, P^T (bf16) overwrites
+//           the first 16 columns and dS^T (bf16) the last 16 -- both are the A
+//           operands of the dV / dK MMAs; SiLU'(S) stays in registers | dP^T
 //           buffers [128,256) | dV | dK
 // (2) hstu_bwd_dq_kernel -- q-tile-major (the forward's work list): loops over
-//     the kv tiles the q tile sees; dQ accumulates in TMEM and is written once.
-//       warp 0 TMA (Q, dO, ts_q once; K + ts_k double, V single buffered)
-//       warp 1 MMA: S = Q K^T (2 TMEM buffers), dP = dO V^T, dQ += dS K
-//       warp 3 per-chunk max of ts_k; warps 4-11 compute dS (smem) and write dQ.
+//     the 64-row kv half tiles the q tile sees; dQ accumulates in TMEM.
+//       warp 0 TMA: Q, dO, ts_q per item;  warp 2 TMA: K_h, V_h, ts_k per half
+//       warp 1 MMA: S = Q K_h^T, dP = dO V_h^T (128 x 64, two TMEM buffers each),
+//              dQ += dS K_h (A = dS in TMEM over S; two dQ buffers, one per item in flight)
+//       warp 3 per-chunk max of ts_k; warps 4-11 compute dS (TMEM);
+//       warps 12-15 drain dQ (bf16) while the next item runs.
 // No atomics on the gradient tensors: every dQ / dK / dV row is written by
 // exactly one CTA; d_ts_weights reduces per-CTA partials with fp64 atomics.
 #include <algorithm>
@@ -33,8 +36,7 @@
 
 namespace jh {
 
-constexpr int kBwdThreads = 512;  // dKV kernel
-constexpr int kDqThreads = 384;   // dQ kernel
+constexpr int kBwdThreads = 512;  // both backward kernels
 constexpr int kCompWarps = 8;
 
 // ===================================================================== dKV
@@ -42,7 +44,7 @@ constexpr int kCompWarps = 8;
 // buffered in TMEM: while the compute warps turn half i into P^T and dS^T,
 // the tensor core already computes S^T / dP^T of half i+1.
 constexpr int kQH = 64;     // q rows per half tile
-constexpr int kQStages = 3;  // Q / dO / ts_q ring depth
+constexpr int kQStages = 4;  // Q / dO / ts_q ring depth
 
 template <int D>
 struct DkvCfg {
@@ -53,8 +55,7 @@ struct DkvCfg {
   static constexpr int V_OFF = TILE;
   static constexpr int Q_OFF = 2 * TILE;                          // [kQStages]
   static constexpr int DO_OFF = Q_OFF + kQStages * HTILE;         // [kQStages]
-  static constexpr int DS_OFF = DO_OFF + kQStages * HTILE;        // [2] dS^T: 128 kv x 64 q bf16 (1 panel)
-  static constexpr int TSQ_OFF = DS_OFF + 2 * 16384;              // int64 [kQStages][kTsSlotH]
+  static constexpr int TSQ_OFF = DO_OFF + kQStages * HTILE;       // int64 [kQStages][kTsSlotH]
   static constexpr int MAX_NB = (D == 64) ? 256 : 32;
   static constexpr int OCT_OFF = TSQ_OFF + kQStages * kTsSlotH * 8;  // OctEntry [32]
   static constexpr int PW_OFF = OCT_OFF + 32 * 16;                   // float [1024] x c1 (D=64 only)
@@ -94,11 +95,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* s_full = qx_full + kQStages;         // [2] S^T / dP^T buffers
   uint64_t* dp_full = s_full + 2;                // [2]
   uint64_t* p_full = dp_full + 2;                // [2] P^T in TMEM, S^T consumed
-  uint64_t* ds_full = p_full + 2;                // [2] dS^T in smem; dP^T consumed
-  uint64_t* ds_empty = ds_full + 2;              // [2] dK done with dS^T
-  uint64_t* dkv_full = ds_empty + 2;
+  uint64_t* ds_full = p_full + 2;                // [2] dS^T in TMEM; dP^T consumed
+  uint64_t* dkv_full = ds_full + 2;
   uint64_t* dkv_empty = dkv_full + 1;
-  static_assert(2 + 3 * kQStages + 10 + 2 <= C::NBARS, "barrier count");
+  static_assert(2 + 3 * kQStages + 8 + 2 <= C::NBARS, "barrier count");
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_tsq + kTsBoxH + 2);
 
   const uint32_t warp = warp_id();
@@ -132,7 +132,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(&dp_full[i], 1);
       mbar_init(&p_full[i], 32 * kCompWarps);
       mbar_init(&ds_full[i], 32 * kCompWarps);
-      mbar_init(&ds_empty[i], 1);
     }
     mbar_init(dkv_full, 1);
     mbar_init(dkv_empty, 128);
@@ -262,15 +261,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           mbar_wait(&ds_full[x], xp);
           trace_ev(p, 1, tcnt, 13, hi);
           tc_fence_after();
-          const uint32_t ds_base = smem_u32(smem + C::DS_OFF + x * 16384);
+          // A = dS^T from TMEM: chunk c's 32 q columns at [64x + 32c + 16, +16)
 #pragma unroll
           for (int kk = 0; kk < kQH / 16; ++kk)
-            umma_ss(tDK, sdesc_sw128(ds_base + kk * 32, 16, 1024), sdesc_sw128(q_base(hi) + kk * 2048, 8192, 1024),
-                    id_kv, (kk > 0 || i > 0) ? 1u : 0u);
-          umma_commit(&ds_empty[x]);
+            umma_ts(tDK, tmem + 64 * x + 32 * (kk >> 1) + 16 + 8 * (kk & 1),
+                    sdesc_sw128(q_base(hi) + kk * 2048, 8192, 1024), id_kv, (kk > 0 || i > 0) ? 1u : 0u);
           umma_commit(&qd_empty[hi % kQStages]);
-          // S^T / dP^T of half i+2 into buffer x (P^T read by dV_i in issue order;
-          // dP^T and SiLU' consumed before ds_full)
+          // S^T / dP^T of half i+2 into buffer x (P^T, dS^T read by dV_i / dK_i in
+          // issue order; dP^T consumed before ds_full)
           if (i + 2 < n) issue_S_dP(hi + 2, i + 3 == n);
         }
         hc += n;
@@ -432,10 +430,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (tr) trace_ev(p, trole, tcnt, 22, t);
         // ---------------- phase dS: dP^T, SiLU' -> dS^T (smem), d_ts_weights
         mbar_wait(&dp_full[x], xp);
-        if (hc >= 2) mbar_wait(&ds_empty[x], xp ^ 1);  // dK of half hc-2 done with this dS^T buffer
         if (tr) trace_ev(p, trole, tcnt, 24, t);
         tc_fence_after();
-        uint8_t* ds_smem = smem + C::DS_OFF + x * 16384;
         const uint32_t dpbase = tDP + 64 * x + c0 + lane_off;
         float sat_w = 0.f, sat_p = 0.f;
         if (cls == 1) {
@@ -453,14 +449,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           sat_w = csum;
           if (has_pos) sat_p = csum;  // saturated chunks hit both last buckets
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4)
-            *reinterpret_cast<int4*>(ds_smem + sw128_offset(r, c0 + q4 * 8)) =
-                make_int4(dk[4 * q4], dk[4 * q4 + 1], dk[4 * q4 + 2], dk[4 * q4 + 3]);
+          tmem_st16(cbase + 16, dk);
         } else if (cls == 0) {
+          uint32_t z[16];
 #pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4)
-            *reinterpret_cast<int4*>(ds_smem + sw128_offset(r, c0 + q4 * 8)) = make_int4(0, 0, 0, 0);
+          for (int i = 0; i < 16; ++i) z[i] = 0u;
+          tmem_st16(cbase + 16, z);
         } else {
           // general chunk: exact bucket scatter.  Runs of equal buckets along the row
           // accumulate in a register and are flushed with predicated fire-and-forget
@@ -484,7 +478,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               dd[j + 1] = __uint_as_float(dv[j + 1]) * kd.y * c1;
               dk[j >> 1] = pack_bf16(dd[j], dd[j + 1]);
             }
-            *reinterpret_cast<int4*>(ds_smem + sw128_offset(r, c0 + g8)) = make_int4(dk[0], dk[1], dk[2], dk[3]);
+            tmem_st4(cbase + 16 + (g8 >> 1), dk);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const bool ok = (okm >> (g8 + j)) & 1u;
@@ -504,7 +498,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         acc_w += (double)sat_w;
         acc_p += (double)sat_p;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&ds_full[x]);
         if (tr) trace_ev(p, trole, tcnt, 25, t);
@@ -598,54 +592,53 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 }
 
 // ====================================================================== dQ
+// q-tile-major (the forward's work list).  The kv side advances in 64-row half
+// tiles so that S / dP are double buffered in TMEM; dQ accumulates in one of two
+// TMEM buffers and is drained by dedicated warps while the next item runs.
+constexpr int kKStages = 4;  // K / V / ts_k half-tile ring depth
+
 template <int D>
 struct DqCfg {
-  static constexpr int TILE = 128 * D * 2;
+  static constexpr int TILE = 128 * D * 2;   // Q or dO tile
+  static constexpr int HTILE = kQH * D * 2;  // K or V half tile
   static constexpr int PANELS = D / 64;
   static constexpr int Q_OFF = 0;
   static constexpr int DO_OFF = TILE;
-  static constexpr int K_OFF = 2 * TILE;                  // [2] stages
-  static constexpr int V_OFF = 4 * TILE;                  // [1]
-  static constexpr int DS_OFF = 5 * TILE;                 // dS: 128 q x 128 kv bf16 (2 panels)
-  static constexpr int TSQ_OFF = DS_OFF + 32768;          // int64 [kTsSlot]
-  static constexpr int TSK_OFF = TSQ_OFF + kTsSlot * 8;   // int64 [2][kTsSlot]
-  static constexpr int OCT_OFF = TSK_OFF + 2 * kTsSlot * 8; // OctEntry [32]
-  static constexpr int PW_OFF = OCT_OFF + 32 * 16;           // float [1024] x c1
-  static constexpr int KMAX_OFF = PW_OFF + 4096;             // int64 [2][4]
-  static constexpr int BAR_OFF = KMAX_OFF + 64;
-  static constexpr int NBARS = 20;
-  static constexpr int TMEMPTR_OFF = BAR_OFF + NBARS * 8;
-  static constexpr int SMEM = TMEMPTR_OFF + 16;
+  static constexpr int K_OFF = 2 * TILE;                          // [kKStages]
+  static constexpr int V_OFF = K_OFF + kKStages * HTILE;          // [kKStages]
+  static constexpr int TSQ_OFF = V_OFF + kKStages * HTILE;        // int64 [kTsSlot] (+ TMEM address in the pad)
+  static constexpr int TSK_OFF = TSQ_OFF + kTsSlot * 8;           // int64 [kKStages][kTsSlotH] (+ chunk maxima)
+  static constexpr int OCT_OFF = TSK_OFF + kKStages * kTsSlotH * 8;  // OctEntry [32]
+  static constexpr int PW_OFF = OCT_OFF + 32 * 16;                   // float [1024] x c1 (D=64 only)
+  static constexpr int BAR_OFF = PW_OFF + (D == 64 ? 4096 : 0);
+  static constexpr int NBARS = 2 + 3 * kKStages + 10;
+  static constexpr int SMEM = BAR_OFF + NBARS * 8;
 };
 
 template <int D>
-__global__ void __launch_bounds__(kDqThreads, 1)
-    hstu_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                       const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    hstu_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                       const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                        const __grid_constant__ CUtensorMap tm_tsq, const __grid_constant__ CUtensorMap tm_tsk,
                        const __grid_constant__ AttnParams p, __nv_bfloat16* __restrict__ dq, int64_t ld_dq) {
   using C = DqCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
   int64_t* s_tsq = reinterpret_cast<int64_t*>(smem + C::TSQ_OFF);
-  int64_t* s_tsk = reinterpret_cast<int64_t*>(smem + C::TSK_OFF);
+  int64_t* s_tsk = reinterpret_cast<int64_t*>(smem + C::TSK_OFF);  // chunk maxima at [st][kTsBoxH + {0,1}]
   OctEntry* s_oct = reinterpret_cast<OctEntry*>(smem + C::OCT_OFF);
-  float* s_pwc = reinterpret_cast<float*>(smem + C::PW_OFF);  // pos weights x c1
-  int64_t* s_kmax = reinterpret_cast<int64_t*>(smem + C::KMAX_OFF);
+  float* s_pwc = reinterpret_cast<float*>(smem + C::PW_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* q_full = bars + 0;
-  uint64_t* q_empty = bars + 1;   // MMA (last S, dP, dQ of the item) + compute warps (ts_q)
-  uint64_t* k_full = bars + 2;    // [2] K + ts_k
-  uint64_t* k_empty = bars + 4;   // [2] dQ_j done (last reader of K_j) + compute (ts_k)
-  uint64_t* kx_full = bars + 6;   // [2] chunk maxima of ts_k
-  uint64_t* v_full = bars + 8;
-  uint64_t* v_empty = bars + 9;
-  uint64_t* s_full = bars + 10;   // [2]
-  uint64_t* dp_full = bars + 12;
-  uint64_t* ds_full = bars + 13;  // dS in smem; S_j, dP_j consumed
-  uint64_t* ds_empty = bars + 14; // dQ_j done with dS
-  uint64_t* dq_full = bars + 15;
-  uint64_t* dq_empty = bars + 16;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::TMEMPTR_OFF);
+  uint64_t* q_empty = bars + 1;              // last S / dP of the item + compute warps (ts_q)
+  uint64_t* kh_full = bars + 2;              // [kKStages] K_h, V_h, ts_k
+  uint64_t* kh_empty = kh_full + kKStages;   // [kKStages] dQ of the half (last reader of K_h) + compute (ts_k)
+  uint64_t* kx_full = kh_empty + kKStages;   // [kKStages] chunk maxima of ts_k
+  uint64_t* s_full = kx_full + kKStages;     // [2]
+  uint64_t* dp_full = s_full + 2;            // [2]
+  uint64_t* ds_full = dp_full + 2;           // [2] dS in TMEM (over S); dP consumed
+  uint64_t* dq_full = ds_full + 2;           // [2] dQ accumulators
+  uint64_t* dq_empty = dq_full + 2;          // [2]
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_tsq + kTsBox);
 
   const uint32_t warp = warp_id();
   const int tid = threadIdx.x;
@@ -653,27 +646,27 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   const int nb = p.bias.nb;
   const int P = p.num_pos;
   const bool has_pos = P > 0;
+  const float c1 = 0.5f * rsqrtf((float)D);
 
   if (smem_u32(smem) & 1023) __trap();
-  const float c1 = 0.5f * rsqrtf((float)D);
   oct_table_fill(s_oct, p.bias, p.ts_weights, c1, tid, blockDim.x);
-  for (int i = tid; i < P; i += blockDim.x) s_pwc[i] = p.pos_weights[i] * c1;
+  if (D == 64)
+    for (int i = tid; i < P; i += blockDim.x) s_pwc[i] = p.pos_weights[i] * c1;
   if (tid == 0) {
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1 + kCompWarps);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1 + kCompWarps);
+    for (int i = 0; i < kKStages; ++i) {
+      mbar_init(&kh_full[i], 1);
+      mbar_init(&kh_empty[i], 1 + kCompWarps);
       mbar_init(&kx_full[i], 1);
-      mbar_init(&s_full[i], 1);
     }
-    mbar_init(v_full, 1);
-    mbar_init(v_empty, 1);
-    mbar_init(dp_full, 1);
-    mbar_init(ds_full, 32 * kCompWarps);
-    mbar_init(ds_empty, 1);
-    mbar_init(dq_full, 1);
-    mbar_init(dq_empty, 32 * kCompWarps);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&dp_full[i], 1);
+      mbar_init(&ds_full[i], 32 * kCompWarps);
+      mbar_init(&dq_full[i], 1);
+      mbar_init(&dq_empty[i], 128);
+    }
     fence_barrier_init();
   }
   if (warp == 0 && lane_id() == 0) {
@@ -689,20 +682,21 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
-  const uint32_t tDP = tmem + 256, tDQ = tmem + 384;
+  // TMEM: S buffers [0,64) [64,128), dP buffers [128,192) [192,256), dQ buffers 256 + D*y
+  const uint32_t tDP = tmem + 128, tDQ = tmem + 256;
 
   const int total = p.wl.hdr->n_fwd * H;
+  auto kv_halves = [&](const Seg& sg, int qt) { return (int)((fwd_kv_lim(sg, qt) + kQH - 1) / kQH); };
 
   if (warp == 0) {
-    // ================= TMA producer
+    // ================= TMA producer: Q, dO, ts_q per item
     if (elect_one()) {
-      uint32_t q_it = 0, k_it = 0, v_it = 0;
+      uint32_t q_it = 0;
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
         const int2 it = p.wl.fwd[g / H];
         const int h = g % H;
         const Seg sg = load_seg(p.seg, it.x);
-        const int n = (int)((fwd_kv_lim(sg, it.y) + kBN - 1) / kBN);
-        if (n == 0) continue;
+        if (kv_halves(sg, it.y) == 0) continue;
         mbar_wait(q_empty, (q_it & 1) ^ 1);
         mbar_expect_tx(q_full, 2 * C::TILE + kTsBytes);
         const int32_t qrow = (int32_t)(sg.q_row0 + (int64_t)it.y * kBM);
@@ -712,286 +706,268 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         }
         tma_load_1d(s_tsq, &tm_tsq, qrow & ~1, q_full);
         ++q_it;
-        auto load_k = [&](int j) {
-          const int st = k_it & 1;
-          const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)j * kBN);
-          mbar_wait(&k_empty[st], ((k_it >> 1) & 1) ^ 1);
-          mbar_expect_tx(&k_full[st], C::TILE + kTsBytes);
-          for (int pn = 0; pn < C::PANELS; ++pn)
-            tma_load_2d(smem + C::K_OFF + st * C::TILE + pn * 16384, &tm_k, h * D + pn * 64, krow, &k_full[st]);
-          tma_load_1d(s_tsk + st * kTsSlot, &tm_tsk, krow & ~1, &k_full[st]);
-          ++k_it;
-        };
-        auto load_v = [&](int j) {
-          const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)j * kBN);
-          mbar_wait(v_empty, (v_it & 1) ^ 1);
-          mbar_expect_tx(v_full, C::TILE);
-          for (int pn = 0; pn < C::PANELS; ++pn)
-            tma_load_2d(smem + C::V_OFF + pn * 16384, &tm_v, h * D + pn * 64, krow, v_full);
-          ++v_it;
-        };
-        load_k(0);
-        for (int j = 0; j < n; ++j) {
-          if (j + 1 < n) load_k(j + 1);
-          load_v(j);
+      }
+    }
+  } else if (warp == 2) {
+    // ================= TMA producer: K_h, V_h, ts_k per kv half tile
+    if (elect_one()) {
+      uint32_t kc = 0;
+      for (int g = blockIdx.x; g < total; g += gridDim.x) {
+        const int2 it = p.wl.fwd[g / H];
+        const int h = g % H;
+        const Seg sg = load_seg(p.seg, it.x);
+        const int n = kv_halves(sg, it.y);
+        for (int t = 0; t < n; ++t, ++kc) {
+          const int st = kc % kKStages;
+          mbar_wait(&kh_empty[st], ((kc / kKStages) & 1) ^ 1);
+          mbar_expect_tx(&kh_full[st], 2 * C::HTILE + kTsBytesH);
+          const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)t * kQH);
+          for (int pn = 0; pn < C::PANELS; ++pn) {
+            tma_load_2d(smem + C::K_OFF + st * C::HTILE + pn * 8192, &tm_k, h * D + pn * 64, krow, &kh_full[st]);
+            tma_load_2d(smem + C::V_OFF + st * C::HTILE + pn * 8192, &tm_v, h * D + pn * 64, krow, &kh_full[st]);
+          }
+          tma_load_1d(s_tsk + st * kTsSlotH, &tm_tsk, krow & ~1, &kh_full[st]);
         }
       }
     }
   } else if (warp == 1) {
     // ================= MMA issuer
     if (elect_one()) {
-      constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);  // S = Q K^T, dP = dO V^T
-      constexpr uint32_t id_q = idesc_bf16(128, D, 0, 1);    // dQ += dS K (A K-major smem, B MN-major)
+      constexpr uint32_t id_s = idesc_bf16(128, kQH, 0, 0);  // S = Q K_h^T, dP = dO V_h^T: 128 q x 64 kv
+      constexpr uint32_t id_q = idesc_bf16(128, D, 0, 1);    // dQ += dS K_h (A K-major smem, B MN-major)
       const uint32_t q_base = smem_u32(smem + C::Q_OFF);
       const uint32_t do_base = smem_u32(smem + C::DO_OFF);
-      const uint32_t v_base = smem_u32(smem + C::V_OFF);
-      const uint32_t ds_base = smem_u32(smem + C::DS_OFF);
-      uint32_t q_it = 0, k_it = 0, v_it = 0, s_it = 0, ds_cnt = 0, o_it = 0;
-      auto k_base = [&](uint32_t ki) { return smem_u32(smem + C::K_OFF + (ki & 1) * C::TILE); };
-      auto issue_S = [&](uint32_t ki, uint32_t sb) {
-        mbar_wait(&k_full[ki & 1], (ki >> 1) & 1);
+      uint32_t q_it = 0, kc = 0, o_it = 0;
+      auto k_base = [&](uint32_t ki) { return smem_u32(smem + C::K_OFF + (ki % kKStages) * C::HTILE); };
+      auto v_base = [&](uint32_t ki) { return smem_u32(smem + C::V_OFF + (ki % kKStages) * C::HTILE); };
+      auto issue_S_dP = [&](uint32_t ki, bool last) {
+        const uint32_t x = ki & 1;
+        mbar_wait(&kh_full[ki % kKStages], (ki / kKStages) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          umma_ss(tmem + 128 * sb, sdesc_sw128(q_base + off, 16, 1024), sdesc_sw128(k_base(ki) + off, 16, 1024),
-                  id_s, kk > 0 ? 1u : 0u);
-        }
-        umma_commit(&s_full[sb]);
-      };
-      auto issue_dP = [&]() {
-        mbar_wait(v_full, v_it & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          umma_ss(tDP, sdesc_sw128(do_base + off, 16, 1024), sdesc_sw128(v_base + off, 16, 1024), id_s,
+          const uint32_t ka = (kk >> 2) * 16384 + (kk & 3) * 32;
+          const uint32_t kb = (kk >> 2) * 8192 + (kk & 3) * 32;
+          umma_ss(tmem + 64 * x, sdesc_sw128(q_base + ka, 16, 1024), sdesc_sw128(k_base(ki) + kb, 16, 1024), id_s,
                   kk > 0 ? 1u : 0u);
         }
-        umma_commit(dp_full);
-        umma_commit(v_empty);
-        ++v_it;
+        umma_commit(&s_full[x]);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ka = (kk >> 2) * 16384 + (kk & 3) * 32;
+          const uint32_t kb = (kk >> 2) * 8192 + (kk & 3) * 32;
+          umma_ss(tDP + 64 * x, sdesc_sw128(do_base + ka, 16, 1024), sdesc_sw128(v_base(ki) + kb, 16, 1024), id_s,
+                  kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&dp_full[x]);
+        if (last) umma_commit(q_empty);  // Q / dO no longer read: the next item's may load
       };
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
         const int2 it = p.wl.fwd[g / H];
         const Seg sg = load_seg(p.seg, it.x);
-        const int n = (int)((fwd_kv_lim(sg, it.y) + kBN - 1) / kBN);
+        const int n = kv_halves(sg, it.y);
         if (n == 0) continue;
+        const uint32_t y = o_it & 1;
         mbar_wait(q_full, q_it & 1);
-        const uint32_t k0 = k_it, s0 = s_it;
-        issue_S(k0, s0 & 1);
-        issue_dP();
-        if (n > 1) issue_S(k0 + 1, (s0 + 1) & 1);
-        for (int j = 0; j < n; ++j) {
-          mbar_wait(ds_full, ds_cnt & 1);
-          ++ds_cnt;
-          if (j == 0) mbar_wait(dq_empty, (o_it & 1) ^ 1);  // previous item's dQ written out
+        issue_S_dP(kc, n == 1);
+        if (n > 1) issue_S_dP(kc + 1, n == 2);
+        for (int i = 0; i < n; ++i) {
+          const uint32_t ki = kc + i;
+          const uint32_t x = ki & 1;
+          mbar_wait(&ds_full[x], (ki >> 1) & 1);
+          if (i == 0) mbar_wait(&dq_empty[y], ((o_it >> 1) & 1) ^ 1);  // this dQ buffer drained
           tc_fence_after();
-          // dQ += dS K_j
+          // dQ += dS K_h: A = dS in TMEM (chunk c's 32 kv columns as bf16 pairs at
+          // [64x + 32c, +16)), B = K_h (64 kv x D, MN-major smem)
 #pragma unroll
-          for (int kk = 0; kk < kBN / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-            umma_ss(tDQ, sdesc_sw128(ds_base + off, 16, 1024), sdesc_sw128(k_base(k0 + j) + kk * 2048, 16384, 1024),
-                    id_q, (kk > 0 || j > 0) ? 1u : 0u);
-          }
-          umma_commit(ds_empty);
-          umma_commit(&k_empty[(k0 + j) & 1]);
-          if (j + 1 < n) issue_dP();                           // dP region: dP_j consumed (ds_full)
-          if (j + 2 < n) issue_S(k0 + j + 2, (s0 + j) & 1);    // S buffer of tile j consumed (ds_full)
+          for (int kk = 0; kk < kQH / 16; ++kk)
+            umma_ts(tDQ + D * y, tmem + 64 * x + 32 * (kk >> 1) + 8 * (kk & 1),
+                    sdesc_sw128(k_base(ki) + kk * 2048, 8192, 1024), id_q, (kk > 0 || i > 0) ? 1u : 0u);
+          umma_commit(&kh_empty[ki % kKStages]);
+          if (i + 2 < n) issue_S_dP(ki + 2, i + 3 == n);
         }
-        k_it += n;
-        s_it += n;
-        umma_commit(dq_full);
-        umma_commit(q_empty);
+        kc += n;
+        umma_commit(&dq_full[y]);
         ++o_it;
         ++q_it;
       }
     }
   } else if (warp == 3) {
-    // ================= ts_k statistics: per 32-column chunk maximum
+    // ================= ts_k statistics: per 32-column chunk maximum of each half
     const int lane = lane_id();
-    uint32_t k_it = 0;
+    uint32_t kc = 0;
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
       const int2 it = p.wl.fwd[g / H];
       const Seg sg = load_seg(p.seg, it.x);
-      const int n = (int)((fwd_kv_lim(sg, it.y) + kBN - 1) / kBN);
-      for (int j = 0; j < n; ++j) {
-        const int st = k_it & 1;
-        mbar_wait(&k_full[st], (k_it >> 1) & 1);
-        const int64_t* tsk = s_tsk + st * kTsSlot + ((sg.kv_row0 + (int64_t)j * kBN) & 1);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int64_t m = warp_max_i64(tsk[32 * c + lane]);
-          if (lane == 0) s_kmax[st * 4 + c] = m;
+      const int n = kv_halves(sg, it.y);
+      for (int t = 0; t < n; ++t, ++kc) {
+        const int st = kc % kKStages;
+        mbar_wait(&kh_full[st], (kc / kKStages) & 1);
+        const int64_t* tsk = s_tsk + st * kTsSlotH + ((sg.kv_row0 + (int64_t)t * kQH) & 1);
+        const int64_t m0 = warp_max_i64(tsk[lane]);
+        const int64_t m1 = warp_max_i64(tsk[32 + lane]);
+        if (lane == 0) {
+          s_tsk[st * kTsSlotH + kTsBoxH] = m0;
+          s_tsk[st * kTsSlotH + kTsBoxH + 1] = m1;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&kx_full[st]);
-        ++k_it;
       }
     }
-  } else if (warp >= 4) {
-    // ================= compute: thread = (q row r, kv-column half wg)
+  } else if (warp >= 4 && warp < 12) {
+    // ================= compute: thread = (q row r, 32-kv-column chunk wg of the half)
     const int et = tid - 128;
     const int wg = et >> 7;
     const int r = et & 127;
     const int lane = r & 31;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const int64_t cap = p.bias.cap;
+    const int c0 = 32 * wg;
     float cb = p.ts_weights[nb - 1];
     if (has_pos) cb += p.pos_weights[P - 1];
     cb *= c1;
-    uint32_t q_it = 0, k_it = 0, s_it = 0, dp_cnt = 0, ds_cnt = 0, o_it = 0, tcnt = 0;
+    uint32_t q_it = 0, kc = 0, tcnt = 0;
     const bool tr = (tid == 128);  // timeline role 4 (the dKV kernel uses roles 0-3)
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
       const int2 it = p.wl.fwd[g / H];
-      const int h = g % H;
       const Seg sg = load_seg(p.seg, it.x);
       const int64_t kv_lim = fwd_kv_lim(sg, it.y);
-      const int n = (int)((kv_lim + kBN - 1) / kBN);
+      const int n = (int)((kv_lim + kQH - 1) / kQH);
+      if (n == 0) continue;
       const int64_t nq = min((int64_t)kBM, sg.lq - (int64_t)it.y * kBM);
       const bool row_ok = r < nq;
       const int64_t qp_tile = sg.qp0 + (int64_t)it.y * kBM;
       const int64_t qpos = qp_tile + r;
-      const int64_t qrow = sg.q_row0 + (int64_t)it.y * kBM + r;
-      __nv_bfloat16* dqrow = dq + qrow * ld_dq + h * D;
-      if (n == 0) {
-        if (row_ok)
-          for (int c = wg * (D / 2); c < (wg + 1) * (D / 2); c += 8)
-            *reinterpret_cast<int4*>(dqrow + c) = make_int4(0, 0, 0, 0);
-        continue;
-      }
       mbar_wait(q_full, q_it & 1);
-      const int64_t tq = row_ok ? s_tsq[((qrow - r) & 1) + r] : (INT64_MAX >> 2);
+      const int64_t tq = row_ok ? s_tsq[((sg.q_row0 + (int64_t)it.y * kBM) & 1) + r] : (INT64_MAX >> 2);
       __syncwarp();
       if (lane == 0) mbar_arrive(q_empty);
       ++q_it;
       const int64_t tq_min = warp_min_i64(tq);
       const int64_t row_lo = qp_tile + (r & ~31), row_hi = row_lo + 31;
-      for (int j = 0; j < n; ++j) {
-        const int st = k_it & 1;
-        const int sb = s_it & 1;
-        const int64_t kv0 = (int64_t)j * kBN;
-        mbar_wait(&kx_full[st], (k_it >> 1) & 1);
-        const int64_t* tsk = s_tsk + st * kTsSlot + ((sg.kv_row0 + kv0) & 1);
-        int cls_bits = 0;
-#pragma unroll
-        for (int ci = 0; ci < 2; ++ci) {
-          const int c0 = 64 * wg + 32 * ci;
-          const int64_t kc0 = kv0 + c0, kc1 = kc0 + 31;
-          int cls = 0;
-          if (!(kc0 > row_hi || kc0 >= kv_lim)) {
-            cls = 2;
-            if ((kc1 <= row_lo) && (kc1 < kv_lim) && (tq_min - s_kmax[st * 4 + (c0 >> 5)] >= cap) &&
-                (!has_pos || row_lo - kc1 >= P - 1))
-              cls = 1;
-          }
-          cls_bits |= cls << (2 * ci);
+      for (int t = 0; t < n; ++t, ++kc) {
+        const int st = kc % kKStages;
+        const uint32_t x = kc & 1, xp = (kc >> 1) & 1;
+        const int64_t kv0 = (int64_t)t * kQH + c0;  // this chunk's first kv position
+        mbar_wait(&kx_full[st], (kc / kKStages) & 1);
+        const int64_t* tsk = s_tsk + st * kTsSlotH + ((sg.kv_row0 + (int64_t)t * kQH) & 1) + c0;
+        const int64_t kc1 = kv0 + 31;
+        int cls = 0;
+        if (!(kv0 > row_hi || kv0 >= kv_lim)) {
+          cls = 2;
+          if ((kc1 <= row_lo) && (kc1 < kv_lim) && (tq_min - s_tsk[st * kTsSlotH + kTsBoxH + wg] >= cap) &&
+              (!has_pos || row_lo - kc1 >= P - 1))
+            cls = 1;
         }
-        if (tr) trace_ev(p, 4, tcnt, 30, j);
-        mbar_wait(&s_full[sb], (s_it >> 1) & 1);
-        if (tr) trace_ev(p, 4, tcnt, 31, j);
-        mbar_wait(dp_full, dp_cnt & 1);
-        ++dp_cnt;
-        if (ds_cnt > 0) mbar_wait(ds_empty, (ds_cnt - 1) & 1);
-        ++ds_cnt;
-        if (tr) trace_ev(p, 4, tcnt, 32, j);
+        if (tr) trace_ev(p, 4, tcnt, 30, t);
+        mbar_wait(&s_full[x], xp);
+        mbar_wait(&dp_full[x], xp);
+        if (tr) trace_ev(p, 4, tcnt, 32, t);
         tc_fence_after();
-        const uint32_t tS = tmem + 128 * sb + lane_off;
+        const uint32_t tS = tmem + 64 * x + c0 + lane_off;
+        const uint32_t tP = tDP + 64 * x + c0 + lane_off;
+        if (cls == 1) {
+          uint32_t sv[32], dv[32], dsk[16];
+          tmem_ld32(tS, sv);
+          tmem_ld32(tP, dv);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float h0 = fmaf(__uint_as_float(sv[i]), c1, cb);
+            const float h1 = fmaf(__uint_as_float(sv[i + 1]), c1, cb);
+            const float t0 = tanh_approx(h0), t1 = tanh_approx(h1);
+            const float d0 = __uint_as_float(dv[i]) * (1.f + t0) * (fmaf(-h0, t0, h0) + 1.f) * c1;
+            const float d1 = __uint_as_float(dv[i + 1]) * (1.f + t1) * (fmaf(-h1, t1, h1) + 1.f) * c1;
+            dsk[i >> 1] = pack_bf16(d0, d1);
+          }
+          tmem_st16(tS, dsk);  // dS over the chunk's (consumed) S columns
+        } else if (cls == 0) {
+          uint32_t z[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) z[i] = 0u;
+          tmem_st16(tS, z);
+        } else {
+          // general chunk: exact per-element bucket, positional bias and mask
+          const int relc = (int)(qpos - kv0);                                       // qpos - kpos of column 0
+          const int ncol = row_ok ? (int)min(kv_lim - kv0, (int64_t)32) : 0;        // in-range columns
 #pragma unroll 1
-        for (int ci = 0; ci < 2; ++ci) {
-          const int c0 = 64 * wg + 32 * ci;
-          const int cls = (cls_bits >> (2 * ci)) & 3;
-          // dS row r (q), kv cols c0..c0+31 -> 128B-swizzled K-major smem (panel = c0 / 64)
-          uint8_t* prow = smem + C::DS_OFF + (c0 >> 6) * 16384;
-          if (cls == 1) {
-            uint32_t sv[32], dv[32], dsk[16];
-            tmem_ld32(tS + c0, sv);
-            tmem_ld32(tDP + lane_off + c0, dv);
+          for (int g8 = 0; g8 < 32; g8 += 8) {
+            uint32_t sv[8], dv[8], dsk[4];
+            tmem_ld8(tS + g8, sv);
+            tmem_ld8(tP + g8, dv);
+            float bc[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              int b;
+              oct_lookup(clamp_delta(tq - tsk[g8 + i], cap), s_oct, b, bc[i]);
+            }
+            if (has_pos) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) bc[i] += s_pwc[min(max(relc - g8 - i, 0), P - 1)];
+            }
             tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              const float h0 = fmaf(__uint_as_float(sv[i]), c1, cb);
-              const float h1 = fmaf(__uint_as_float(sv[i + 1]), c1, cb);
-              const float2 th = make_float2(tanh_approx(h0), tanh_approx(h1));
-              const float d0 = __uint_as_float(dv[i]) * (1.f + th.x) * (fmaf(-h0, th.x, h0) + 1.f) * c1;
-              const float d1 = __uint_as_float(dv[i + 1]) * (1.f + th.y) * (fmaf(-h1, th.y, h1) + 1.f) * c1;
-              dsk[i >> 1] = pack_bf16(d0, d1);
+            for (int i = 0; i < 8; i += 2) {
+              float dd[2];
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const int k = g8 + i + u;
+                const float hh = fmaf(__uint_as_float(sv[i + u]), c1, bc[i + u]);
+                const float th = tanh_approx(hh);
+                const bool ok = k < ncol && k <= relc;
+                dd[u] = ok ? __uint_as_float(dv[i + u]) * (1.f + th) * (fmaf(-hh, th, hh) + 1.f) * c1 : 0.f;
+              }
+              dsk[i >> 1] = pack_bf16(dd[0], dd[1]);
             }
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4)
-              *reinterpret_cast<int4*>(prow + sw128_offset(r, (c0 & 63) + q4 * 8)) =
-                  make_int4(dsk[4 * q4], dsk[4 * q4 + 1], dsk[4 * q4 + 2], dsk[4 * q4 + 3]);
-          } else if (cls == 0) {
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4)
-              *reinterpret_cast<int4*>(prow + sw128_offset(r, (c0 & 63) + q4 * 8)) = make_int4(0, 0, 0, 0);
-          } else {
-            // general chunk: exact per-element bucket, positional bias and mask
-            const int relc = (int)(qpos - kv0 - c0);                           // qpos - kpos of column 0
-            const int ncol = row_ok ? (int)min(kv_lim - kv0 - c0, (int64_t)32) : 0;  // in-range columns
-#pragma unroll 1
-            for (int g8 = 0; g8 < 32; g8 += 8) {
-              uint32_t sv[8], dv[8], dsk[4];
-              tmem_ld8(tS + c0 + g8, sv);
-              tmem_ld8(tDP + lane_off + c0 + g8, dv);
-              float bc[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                int b;
-                oct_lookup(clamp_delta(tq - tsk[c0 + g8 + i], cap), s_oct, b, bc[i]);
-              }
-              if (has_pos) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) bc[i] += s_pwc[min(max(relc - g8 - i, 0), P - 1)];
-              }
-              tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 8; i += 2) {
-                float dd[2];
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                  const int k = g8 + i + u;
-                  const float hh = fmaf(__uint_as_float(sv[i + u]), c1, bc[i + u]);
-                  const float th = tanh_approx(hh);
-                  const bool ok = k < ncol && k <= relc;
-                  dd[u] = ok ? __uint_as_float(dv[i + u]) * (1.f + th) * (fmaf(-hh, th, hh) + 1.f) * c1 : 0.f;
-                }
-                dsk[i >> 1] = pack_bf16(dd[0], dd[1]);
-              }
-              *reinterpret_cast<int4*>(prow + sw128_offset(r, (c0 & 63) + g8)) =
-                  make_int4(dsk[0], dsk[1], dsk[2], dsk[3]);
-            }
+            tmem_st4(tS + (g8 >> 1), dsk);  // S columns g8/2 .. g8/2+3 were already read
           }
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(ds_full);
-        if (tr) trace_ev(p, 4, tcnt, 33, j);
+        mbar_arrive(&ds_full[x]);
+        if (tr) trace_ev(p, 4, tcnt, 33, t);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&k_empty[st]);  // done with this stage's ts_k
-        ++k_it;
-        ++s_it;
+        if (lane == 0) mbar_arrive(&kh_empty[st]);  // done with this stage's ts_k
       }
-      // ---- dQ: TMEM -> bf16 -> global (each group writes half the columns)
-      mbar_wait(dq_full, o_it & 1);
+    }
+  } else if (warp >= 12) {
+    // ================= dQ drain: TMEM -> bf16 -> global (thread = q row)
+    const int r = tid - 384;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    uint32_t o_it = 0;
+    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      const int2 it = p.wl.fwd[g / H];
+      const int h = g % H;
+      const Seg sg = load_seg(p.seg, it.x);
+      const int n = kv_halves(sg, it.y);
+      const int64_t nq = min((int64_t)kBM, sg.lq - (int64_t)it.y * kBM);
+      const bool row_ok = r < nq;
+      __nv_bfloat16* dqrow = dq + (sg.q_row0 + (int64_t)it.y * kBM + r) * ld_dq + h * D;
+      if (n == 0) {
+        if (row_ok)
+          for (int c = 0; c < D; c += 8) *reinterpret_cast<int4*>(dqrow + c) = make_int4(0, 0, 0, 0);
+        continue;
+      }
+      const uint32_t y = o_it & 1;
+      mbar_wait(&dq_full[y], (o_it >> 1) & 1);
       ++o_it;
       tc_fence_after();
 #pragma unroll 1
-      for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 32) {
+      for (int cc = 0; cc < D; cc += 32) {
         uint32_t v[32];
-        tmem_ld32(tDQ + lane_off + c0, v);
+        tmem_ld32(tDQ + D * y + lane_off + cc, v);
         tmem_ld_wait();
         if (row_ok) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 32; i += 2) pk[i >> 1] = pack_bf16(__uint_as_float(v[i]), __uint_as_float(v[i + 1]));
-          int4* d4 = reinterpret_cast<int4*>(dqrow + c0);
+          int4* d4 = reinterpret_cast<int4*>(dqrow + cc);
 #pragma unroll
           for (int i = 0; i < 4; ++i) d4[i] = make_int4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
         }
       }
       tc_fence_before();
-      mbar_arrive(dq_empty);
+      mbar_arrive(&dq_empty[y]);
     }
   }
   tc_fence_before();
@@ -1021,8 +997,8 @@ int launch_bwd(const TMaps& tm, const AttnParams& p, const jh_attn_args& a, int 
   if (a.prof_event_start) cudaEventRecord((cudaEvent_t)a.prof_event_start, s);
   hstu_bwd_dkv_kernel<D><<<grid, kBwdThreads, C::SMEM, s>>>(tm.q64, tm.k, tm.v, tm.do64, tm.tsq72, p);
   if (cudaError_t e = cudaGetLastError()) return (int)e;
-  hstu_bwd_dq_kernel<D><<<grid, kDqThreads, Q::SMEM, s>>>(tm.q, tm.k, tm.v, tm.dout, tm.tsq, tm.tsk, p,
-                                                         (__nv_bfloat16*)a.dq, a.ld_dq);
+  hstu_bwd_dq_kernel<D><<<grid, kBwdThreads, Q::SMEM, s>>>(tm.q, tm.dout, tm.k64, tm.v64, tm.tsq, tm.tsk72, p,
+                                                          (__nv_bfloat16*)a.dq, a.ld_dq);
   if (a.prof_event_end) cudaEventRecord((cudaEvent_t)a.prof_event_end, s);
   return (int)cudaGetLastError();
 }

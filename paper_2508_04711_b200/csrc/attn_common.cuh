@@ -162,7 +162,8 @@ static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, 
 // q, k, v, dout (bf16 2-D, 128-row boxes) and ts_q, ts_k (int64 1-D) tensor maps
 struct TMaps {
   CUtensorMap q, k, v, dout, tsq, tsk;
-  CUtensorMap q64, do64, tsq72;  // 64-row boxes for the dKV kernel
+  CUtensorMap q64, do64, tsq72;  // 64-row boxes for the dKV kernel (q side)
+  CUtensorMap k64, v64, tsk72;  // 64-row boxes for the dQ kernel (kv side)
 };
 
 // Parameters shared by the fwd / bwd attention kernels.

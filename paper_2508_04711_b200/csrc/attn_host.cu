@@ -145,7 +145,10 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
   if (bwd && (make_tmap_bf16_2d(&tm->dout, a->dout, a->q_rows, HD, a->ld_do, 128) ||
               make_tmap_bf16_2d(&tm->q64, a->q, a->q_rows, HD, a->ld_q, 64) ||
               make_tmap_bf16_2d(&tm->do64, a->dout, a->q_rows, HD, a->ld_do, 64) ||
-              make_tmap_i64_1d(&tm->tsq72, a->ts_q, a->q_rows, kTsBoxH)))
+              make_tmap_i64_1d(&tm->tsq72, a->ts_q, a->q_rows, kTsBoxH) ||
+              make_tmap_bf16_2d(&tm->k64, a->k, a->kv_rows, HD, a->ld_k, 64) ||
+              make_tmap_bf16_2d(&tm->v64, a->v, a->kv_rows, HD, a->ld_v, 64) ||
+              make_tmap_i64_1d(&tm->tsk72, a->ts_k, a->kv_rows, kTsBoxH)))
     return set_error(JH_ERR_CUDA, "cuTensorMapEncodeTiled failed (bwd maps)");
   build_work_kernel<<<1, 1024, 0, s>>>(p->seg, p->wl);
   cudaError_t e = cudaGetLastError();
