@@ -188,7 +188,8 @@ def run_gpu(args):
     else:
         def step_fn(prof=None):
             kernels.attn_fwd(q, k, v, ts, ts, offs, H, w, NB, prof=None if prof is None else prof[0])
-            return kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, NB, prof=None if prof is None else prof[1])
+            return kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, NB, prof=None if prof is None else prof[1],
+                                    max_kv_len=MAXLEN)
         tokens_total = T
         flat_lens = [int(x) for x in lens]
 
@@ -248,7 +249,7 @@ def run_gpu(args):
         ach_b = Fb / (bwd_ms / 1e3) / 1e12
         ach_f = Ff / (fwd_ms / 1e3) / 1e12
         result["roofline"] = {
-            "bound": "tensor", "kernel": "hstu_bwd_kernel<128>", "achieved": ach_b, "peak": peak,
+            "bound": "tensor", "kernel": "jh_attn_bwd: hstu_bwd_dkv_kernel<128> + hstu_bwd_dq_kernel<128>", "achieved": ach_b, "peak": peak,
             "unit": "TFLOP/s", "frac": ach_b / peak, "traffic": _traffic("bwd"),
             "peak_kind": f"{peak_kind} burst bf16 (MEASURED_PEAKS.json)",
             "algorithmic_flops_per_launch": Fb, "ms_per_launch": bwd_ms,

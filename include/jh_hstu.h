@@ -135,11 +135,21 @@ typedef struct jh_attn_args {
    * `trace_cta` (NULL = off) */
   void* trace;
   int32_t trace_cta;
+  /* backward scratch for the bf16 dS tiles handed from the dK/dV kernel to the
+   * dQ kernel: at least jh_attn_ds_scratch_bytes(...) bytes (jh_attn_bwd only) */
+  void* ds_scratch;
+  size_t ds_scratch_bytes;
 } jh_attn_args;
 
 /* kv_len_total = sum over segments of kv_len[s] (= q_rows when kv_len is NULL). */
 JH_API size_t jh_attn_workspace_bytes(int64_t q_rows, int64_t kv_len_total, int64_t num_segments, int32_t num_heads,
                                       int32_t head_dim);
+
+/* Backward dS scratch bound.  max_kv_len >= every segment's kv_len (= its
+ * length when kv_len is NULL).  If the bound is violated at run time the
+ * backward writes NaN into dq instead of overrunning the scratch. */
+JH_API size_t jh_attn_ds_scratch_bytes(int64_t kv_len_total, int64_t num_segments, int32_t num_heads,
+                                       int64_t max_kv_len);
 
 /* Forward: attention.py:125 hstu_attention_reference / :151 blockwise_partial. */
 JH_API int jh_attn_fwd(const jh_attn_args* a, void* stream);

@@ -43,6 +43,7 @@ class JhAttnArgs(ctypes.Structure):
         ("workspace", c_vp), ("workspace_bytes", ctypes.c_size_t),
         ("prof_event_start", c_vp), ("prof_event_end", c_vp),
         ("trace", c_vp), ("trace_cta", ctypes.c_int32),
+        ("ds_scratch", c_vp), ("ds_scratch_bytes", ctypes.c_size_t),
     ]
 
 
@@ -56,6 +57,7 @@ SIGNATURES = {
     "jh_dbias_scatter": (ctypes.c_int, [c_vp, ctypes.c_int64, c_vp, ctypes.c_int64, c_vp, ctypes.c_int, c_vp, c_vp]),
     "jh_attn_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
                                                   ctypes.c_int32]),
+    "jh_attn_ds_scratch_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64]),
     "jh_attn_fwd": (ctypes.c_int, [ctypes.POINTER(JhAttnArgs), c_vp]),
     "jh_attn_bwd": (ctypes.c_int, [ctypes.POINTER(JhAttnArgs), c_vp]),
     "jh_gather_rows": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int64, ctypes.c_int64, c_vp]),

@@ -117,14 +117,14 @@ class GpuBackend:
         return self.k.scatter_rows(src, perm, out)
 
     def fwd(self, q, k, v, ts_q, ts_k, segs, H, w, nb):
-        qo, qp, ks, kl, kvt = segs
+        qo, qp, ks, kl, kvt, _ = segs
         return self.k.attn_fwd(q, k, v, ts_q, ts_k, qo, H, w, nb, q_pos0=qp, kv_start=ks, kv_len=kl,
                                kv_len_total=kvt)
 
     def bwd(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb):
-        qo, qp, ks, kl, kvt = segs
+        qo, qp, ks, kl, kvt, max_kv = segs
         dq, dk, dv, dw, _ = self.k.attn_bwd(q, k, v, ts_q, ts_k, qo, g, H, w, nb, q_pos0=qp, kv_start=ks,
-                                            kv_len=kl, kv_len_total=kvt, accumulate_dkv=True)
+                                            kv_len=kl, kv_len_total=kvt, accumulate_dkv=True, max_kv_len=max_kv)
         return dq, dk, dv, dw
 
 
@@ -153,7 +153,8 @@ class CPAttention:
             p = build_cp_plan([list(x) for x in allv], self.cp, self.rank, self.mode)
             t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
             dev = {"send_perm": t(p.send_perm), "seq_perm": t(p.seq_perm),
-                   "segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.kv_len), int(p.kv_len.sum()))}
+                   "segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.kv_len), int(p.kv_len.sum()),
+                            int(p.kv_len.max(initial=0)))}
             self._plans[key] = (p, dev)
         return self._plans[key]
 

@@ -12,7 +12,8 @@
 //       warp 1      MMA: S^T = K Q^T, dP^T = V dO^T (128 x 64, two TMEM buffers),
 //                   dV += P^T dO, dK += dS^T Q (A = P^T / dS^T in TMEM)
 //       warp 3      per-chunk min of ts_q (saturation test)
-//       warps 4-11  compute, thread = (kv row, 32-q-column chunk of the half):
+//       warps 4-11  compute, two warpgroups in ping-pong over the halves (group
+//                   hc % 2 owns TMEM buffer hc % 2), thread = (kv row, half):
 //                   phase P  : S^T -> P^T (TMEM) and SiLU'(S) (f16, TMEM)
 //                   phase dS : dP^T -> dS^T = dP SiLU'(S)/sqrt(d) (TMEM), d_ts_weights
 //       warps 12-15 drain dK / dV (bf16 store, or fp32 accumulate for CP)
@@ -20,13 +21,9 @@
 //           the first 16 columns and dS^T (bf16) the last 16 -- both are the A
 //           operands of the dV / dK MMAs; SiLU'(S) stays in registers | dP^T
 //           buffers [128,256) | dV | dK
-// (2) hstu_bwd_dq_kernel -- q-tile-major (the forward's work list): loops over
-//     the 64-row kv half tiles the q tile sees; dQ accumulates in TMEM.
-//       warp 0 TMA: Q, dO, ts_q per item;  warp 2 TMA: K_h, V_h, ts_k per half
-//       warp 1 MMA: S = Q K_h^T, dP = dO V_h^T (128 x 64, two TMEM buffers each),
-//              dQ += dS K_h (A = dS in TMEM over S; two dQ buffers, one per item in flight)
-//       warp 3 per-chunk max of ts_k; warps 4-11 compute dS (TMEM);
-//       warps 12-15 drain dQ (bf16) while the next item runs.
+//     The dS^T tile of every half is also written (bf16) to a scratch buffer.
+// (2) hstu_bwd_dq_kernel -- dQ = dS K as a streaming GEMM over that scratch
+//     (q-tile-major, TMA-fed, dQ double-buffered in TMEM), no recomputation.
 // No atomics on the gradient tensors: every dQ / dK / dV row is written by
 // exactly one CTA; d_ts_weights reduces per-CTA partials with fp64 atomics.
 #include <algorithm>
@@ -45,6 +42,7 @@ constexpr int kCompWarps = 8;
 // the tensor core already computes S^T / dP^T of half i+1.
 constexpr int kQH = 64;     // q rows per half tile
 constexpr int kQStages = 4;  // Q / dO / ts_q ring depth
+static_assert(kQStages % 2 == 0, "a ring stage must always belong to the same compute warpgroup");
 
 template <int D>
 struct DkvCfg {
@@ -124,14 +122,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(kv_empty, 1);
     for (int i = 0; i < kQStages; ++i) {
       mbar_init(&qd_full[i], 1);
-      mbar_init(&qd_empty[i], 1 + kCompWarps);
+      mbar_init(&qd_empty[i], 1 + kCompWarps / 2);  // MMA + the owning warpgroup
       mbar_init(&qx_full[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&dp_full[i], 1);
-      mbar_init(&p_full[i], 32 * kCompWarps);
-      mbar_init(&ds_full[i], 32 * kCompWarps);
+      mbar_init(&p_full[i], 16 * kCompWarps);  // one warpgroup
+      mbar_init(&ds_full[i], 16 * kCompWarps);
     }
     mbar_init(dkv_full, 1);
     mbar_init(dkv_empty, 128);
@@ -301,14 +299,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
   } else if (warp >= 4 && warp < 12) {
-    // ================= compute: thread = (kv row r, 32-q-column chunk wg of the half)
+    // ================= compute: two warpgroups in ping-pong -- warpgroup wg owns the
+    // halves with hc % 2 == wg (TMEM buffer wg); thread = (kv row r, both 32-q-column
+    // chunks of the half), so one group's TMEM / barrier latency hides behind the
+    // other group's math
     const int et = tid - 128;
     const int wg = et >> 7;
     const int r = et & 127;
     const int lane = r & 31;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const int64_t cap = p.bias.cap;
-    const int c0 = 32 * wg;  // q column offset of this thread's chunk within the half
     float cb = p.ts_weights[nb - 1];
     if (has_pos) cb += p.pos_weights[P - 1];
     cb *= c1;
@@ -316,6 +316,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint32_t hc = 0, tcnt = 0;
     const bool tr = (tid == 128 || tid == 256);
     const int trole = tid == 128 ? 2 : 3;
+    // dS scratch capacity (caller's max_kv_len bound); on overflow dQ becomes NaN
+    const bool ds_ok = p.wl.hdr->ds_blocks * H <= p.ds_cap_blocks;
+    if (!ds_ok && et == 0) p.wl.hdr->ds_overflow = 1;
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
       const int2 it = p.wl.bwd[g / H];
       const Seg sg = load_seg(p.seg, it.x);
@@ -329,172 +332,200 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int64_t tk_max = warp_max_i64(tk);
       const int64_t k_lo = kv0 + (r & ~31), k_hi = k_lo + 31;  // this warp's kv positions
       const bool warp_k_ok = k_hi < sg.kv_len;
+      // this thread's dS^T row in the scratch block of (segment, head, kv tile, half 0)
+      const int h = g % H;
+      uint8_t* ds_row = reinterpret_cast<uint8_t*>(p.ds) +
+                        ((p.wl.ds_base[it.x] * H + (int64_t)(h * ds_nkt(sg) + it.y) * nh) * kDsBlockBytes) + r * 128;
       for (int t = h0; t < nh; ++t, ++hc) {
+        if ((int)(hc & 1) != wg) continue;
+        int4* ds_out = reinterpret_cast<int4*>(ds_row + (int64_t)t * kDsBlockBytes);
         const int st = hc % kQStages;
         const uint32_t x = hc & 1, xp = (hc >> 1) & 1;
         const int64_t qrow0 = sg.q_row0 + (int64_t)t * kQH;
         const int64_t qp_half = sg.qp0 + (int64_t)t * kQH;
         const int nq = (int)min((int64_t)kQH, sg.lq - (int64_t)t * kQH);
         mbar_wait(&qx_full[st], (hc / kQStages) & 1);
-        const int64_t* tsq = s_tsq + st * kTsSlotH + (qrow0 & 1) + c0;  // this chunk's 32 query timestamps
-        // chunk class: 0 masked, 1 unmasked with saturated bias, 2 general
-        const int64_t qc0 = qp_half + c0;
-        int cls = 0;
-        if (!(qc0 + 31 < k_lo || c0 >= nq)) {
-          cls = 2;
-          if ((qc0 >= k_hi) && (c0 + 32 <= nq) && warp_k_ok &&
-              (s_tsq[st * kTsSlotH + kTsBoxH + wg] - tk_max >= cap) && (!has_pos || qc0 - k_hi >= P - 1))
-            cls = 1;
+        // chunk classes: 0 masked, 1 unmasked with saturated bias, 2 general
+        int cls[2];
+#pragma unroll
+        for (int ci = 0; ci < 2; ++ci) {
+          const int64_t qc0 = qp_half + 32 * ci;
+          cls[ci] = 0;
+          if (!(qc0 + 31 < k_lo || 32 * ci >= nq)) {
+            cls[ci] = 2;
+            if ((qc0 >= k_hi) && (32 * ci + 32 <= nq) && warp_k_ok &&
+                (s_tsq[st * kTsSlotH + kTsBoxH + ci] - tk_max >= cap) && (!has_pos || qc0 - k_hi >= P - 1))
+              cls[ci] = 1;
+          }
         }
-        const uint32_t cbase = tmem + 64 * x + c0 + lane_off;  // S^T chunk -> P^T [cbase, +16)
-        // general chunks: relative position of column 0 and the number of in-range columns
-        const int rel0 = (int)(qc0 - kpos);
-        const int ncol = krow_ok ? nq - c0 : 0;
-        // SiLU'(S) of the chunk (f16 pairs) stays in registers from phase P to phase dS
-        // (saturated chunks) or in a small per-thread local buffer (general chunks,
-        // rolled loops keep that rarely-run code small), with the buckets and mask
-        uint32_t kp[16];
-        uint32_t kl[16], bl[8];
-        uint32_t okm = 0;
+        // SiLU'(S) (f16 pairs) stays in registers from phase P to phase dS (saturated
+        // chunks) or in a small per-thread local buffer (general chunks: rolled loops
+        // keep that rarely-run code small), with the buckets and the mask
+        uint32_t kp[2][16];
+        uint32_t kl[2][16], bl[2][8];
+        uint32_t okm[2] = {0u, 0u};
         // ---------------- phase P: S^T -> P^T, SiLU'
         mbar_wait(&s_full[x], xp);
         if (tr) trace_ev(p, trole, tcnt, 21, t);
         tc_fence_after();
-        if (cls == 1) {
-          uint32_t v[32], pk[16];
-          tmem_ld32(cbase, v);
-          tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            const float h0f = fmaf(__uint_as_float(v[i]), c1, cb);
-            const float h1f = fmaf(__uint_as_float(v[i + 1]), c1, cb);
-            const float t0 = tanh_approx(h0f), t1 = tanh_approx(h1f);  // f32: d_ts_weights accuracy
-            pk[i >> 1] = pack_bf16(fmaf(h0f, t0, h0f), fmaf(h1f, t1, h1f));
-            __half2 hk = __floats2half2_rn((1.f + t0) * (fmaf(-h0f, t0, h0f) + 1.f),
-                                           (1.f + t1) * (fmaf(-h1f, t1, h1f) + 1.f));
-            kp[i >> 1] = *reinterpret_cast<uint32_t*>(&hk);
-          }
-          tmem_st16(cbase, pk);
-        } else if (cls == 0) {
-          uint32_t z[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) z[i] = 0u;
-          tmem_st16(cbase, z);
-        } else {
-          // general chunk: exact per-element bucket, positional bias and mask
-#pragma unroll 1
-          for (int g8 = 0; g8 < 32; g8 += 8) {
-            uint32_t v[8], pk[4];
-            tmem_ld8(cbase + g8, v);
-            float bc[8];
-            uint32_t bw0 = 0, bw1 = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              int b;
-              oct_lookup(clamp_delta(tsq[g8 + j] - tk, cap), s_oct, b, bc[j]);
-              if (j < 4)
-                bw0 |= (uint32_t)b << (8 * j);
-              else
-                bw1 |= (uint32_t)b << (8 * (j - 4));
-              const bool ok = (g8 + j < ncol) && (rel0 + g8 + j >= 0);
-              okm |= (ok ? 1u : 0u) << (g8 + j);
-            }
-            if (has_pos) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j) bc[j] += s_pwc[min(max(rel0 + g8 + j, 0), P - 1)];
-            }
-            bl[g8 >> 2] = bw0;
-            bl[(g8 >> 2) + 1] = bw1;
+        for (int ci = 0; ci < 2; ++ci) {
+          const int c0 = 32 * ci;
+          const uint32_t cbase = tmem + 64 * x + c0 + lane_off;  // S^T chunk -> P^T [cbase, +16)
+          if (cls[ci] == 1) {
+            uint32_t v[32], pk[16];
+            tmem_ld32(cbase, v);
             tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 8; j += 2) {
-              float pp[2], dd[2];
-#pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                const bool ok = (okm >> (g8 + j + u)) & 1u;
-                const float hh = fmaf(__uint_as_float(v[j + u]), c1, bc[j + u]);
-                const float th = tanh_approx(hh);
-                pp[u] = ok ? fmaf(hh, th, hh) : 0.f;
-                dd[u] = ok ? (1.f + th) * (fmaf(-hh, th, hh) + 1.f) : 0.f;
-              }
-              pk[j >> 1] = pack_bf16(pp[0], pp[1]);
-              __half2 hk = __floats2half2_rn(dd[0], dd[1]);
-              kl[(g8 + j) >> 1] = *reinterpret_cast<uint32_t*>(&hk);
+            for (int i = 0; i < 32; i += 2) {
+              const float h0f = fmaf(__uint_as_float(v[i]), c1, cb);
+              const float h1f = fmaf(__uint_as_float(v[i + 1]), c1, cb);
+              const float t0 = tanh_approx(h0f), t1 = tanh_approx(h1f);  // f32: d_ts_weights accuracy
+              pk[i >> 1] = pack_bf16(fmaf(h0f, t0, h0f), fmaf(h1f, t1, h1f));
+              __half2 hk = __floats2half2_rn((1.f + t0) * (fmaf(-h0f, t0, h0f) + 1.f),
+                                             (1.f + t1) * (fmaf(-h1f, t1, h1f) + 1.f));
+              kp[ci][i >> 1] = *reinterpret_cast<uint32_t*>(&hk);
             }
-            tmem_st4(cbase + (g8 >> 1), pk);
+            tmem_st16(cbase, pk);
+          } else if (cls[ci] == 0) {
+            uint32_t z[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) z[i] = 0u;
+            tmem_st16(cbase, z);
+          } else {
+            // general chunk: exact per-element bucket, positional bias and mask
+            const int64_t* tsq = s_tsq + st * kTsSlotH + (qrow0 & 1) + c0;  // the chunk's query timestamps
+            const int rel0 = (int)(qp_half + c0 - kpos);
+            const int ncol = krow_ok ? nq - c0 : 0;
+#pragma unroll 1
+            for (int g8 = 0; g8 < 32; g8 += 8) {
+              uint32_t v[8], pk[4];
+              tmem_ld8(cbase + g8, v);
+              float bc[8];
+              uint32_t bw0 = 0, bw1 = 0, om = 0;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                int b;
+                oct_lookup(clamp_delta(tsq[g8 + j] - tk, cap), s_oct, b, bc[j]);
+                if (j < 4)
+                  bw0 |= (uint32_t)b << (8 * j);
+                else
+                  bw1 |= (uint32_t)b << (8 * (j - 4));
+                const bool ok = (g8 + j < ncol) && (rel0 + g8 + j >= 0);
+                om |= (ok ? 1u : 0u) << j;
+              }
+              if (has_pos) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) bc[j] += s_pwc[min(max(rel0 + g8 + j, 0), P - 1)];
+              }
+              okm[ci] |= om << g8;
+              bl[ci][g8 >> 2] = bw0;
+              bl[ci][(g8 >> 2) + 1] = bw1;
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 8; j += 2) {
+                float pp[2], dd[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                  const bool ok = (om >> (j + u)) & 1u;
+                  const float hh = fmaf(__uint_as_float(v[j + u]), c1, bc[j + u]);
+                  const float th = tanh_approx(hh);
+                  pp[u] = ok ? fmaf(hh, th, hh) : 0.f;
+                  dd[u] = ok ? (1.f + th) * (fmaf(-hh, th, hh) + 1.f) : 0.f;
+                }
+                pk[j >> 1] = pack_bf16(pp[0], pp[1]);
+                __half2 hk = __floats2half2_rn(dd[0], dd[1]);
+                kl[ci][(g8 + j) >> 1] = *reinterpret_cast<uint32_t*>(&hk);
+              }
+              tmem_st4(cbase + (g8 >> 1), pk);
+            }
           }
         }
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[x]);
         if (tr) trace_ev(p, trole, tcnt, 22, t);
-        // ---------------- phase dS: dP^T, SiLU' -> dS^T (smem), d_ts_weights
+        // ---------------- phase dS: dP^T, SiLU' -> dS^T (TMEM), d_ts_weights
         mbar_wait(&dp_full[x], xp);
         if (tr) trace_ev(p, trole, tcnt, 24, t);
         tc_fence_after();
-        const uint32_t dpbase = tDP + 64 * x + c0 + lane_off;
         float sat_w = 0.f, sat_p = 0.f;
-        if (cls == 1) {
-          uint32_t dv[32], dk[16];
-          tmem_ld32(dpbase, dv);
-          tmem_ld_wait();
-          float csum = 0.f;
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            const float2 kd = __half22float2(*reinterpret_cast<const __half2*>(&kp[i >> 1]));
-            const float d0 = __uint_as_float(dv[i]) * kd.x * c1;
-            const float d1 = __uint_as_float(dv[i + 1]) * kd.y * c1;
-            dk[i >> 1] = pack_bf16(d0, d1);
-            csum += d0 + d1;
-          }
-          sat_w = csum;
-          if (has_pos) sat_p = csum;  // saturated chunks hit both last buckets
-          tmem_st16(cbase + 16, dk);
-        } else if (cls == 0) {
-          uint32_t z[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) z[i] = 0u;
-          tmem_st16(cbase + 16, z);
-        } else {
-          // general chunk: exact bucket scatter.  Runs of equal buckets along the row
-          // accumulate in a register and are flushed with predicated fire-and-forget
-          // fp32 reductions into this CTA's bins
-          uint32_t rb = (uint32_t)(nb - 1);
-          float rs = 0.f;
-#pragma unroll 1
-          for (int g8 = 0; g8 < 32; g8 += 8) {
-            uint32_t dv[8], dk[4];
-            tmem_ld8(dpbase + g8, dv);
-            const uint32_t bw0 = bl[g8 >> 2], bw1 = bl[(g8 >> 2) + 1];
-            uint32_t kw[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) kw[j] = kl[(g8 >> 1) + j];
+        for (int ci = 0; ci < 2; ++ci) {
+          const int c0 = 32 * ci;
+          const uint32_t cbase = tmem + 64 * x + c0 + lane_off;  // dS^T -> [cbase + 16, +16)
+          const uint32_t dpbase = tDP + 64 * x + c0 + lane_off;
+          if (cls[ci] == 1) {
+            uint32_t dv[32], dk[16];
+            tmem_ld32(dpbase, dv);
             tmem_ld_wait();
-            float dd[8];
+            float csum = 0.f;
 #pragma unroll
-            for (int j = 0; j < 8; j += 2) {
-              const float2 kd = __half22float2(*reinterpret_cast<const __half2*>(&kw[j >> 1]));
-              dd[j] = __uint_as_float(dv[j]) * kd.x * c1;
-              dd[j + 1] = __uint_as_float(dv[j + 1]) * kd.y * c1;
-              dk[j >> 1] = pack_bf16(dd[j], dd[j + 1]);
+            for (int i = 0; i < 32; i += 2) {
+              const float2 kd = __half22float2(*reinterpret_cast<const __half2*>(&kp[ci][i >> 1]));
+              const float d0 = __uint_as_float(dv[i]) * kd.x * c1;
+              const float d1 = __uint_as_float(dv[i + 1]) * kd.y * c1;
+              dk[i >> 1] = pack_bf16(d0, d1);
+              csum += d0 + d1;
             }
-            tmem_st4(cbase + 16 + (g8 >> 1), dk);
+            sat_w += csum;
+            if (has_pos) sat_p += csum;  // saturated chunks hit both last buckets
+            tmem_st16(cbase + 16, dk);
+            if (ds_ok)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const bool ok = (okm >> (g8 + j)) & 1u;
-              const uint32_t b = ((j < 4 ? bw0 : bw1) >> (8 * (j & 3))) & 0xFFu;
-              const bool ch = ok && b != rb;
-              red_add_f32_if(g_bins + rb, rs, ch && rs != 0.f);
-              rb = ch ? b : rb;
-              rs = ch ? dd[j] : rs + dd[j];  // dd = 0 on masked elements
-              if (has_pos) {
-                const int rel = min(rel0 + g8 + j, P - 1);
-                red_add_f32_if(g_bins + 256 + max(rel, 0), dd[j], ok && rel != P - 1);
-                sat_p += (ok && rel == P - 1) ? dd[j] : 0.f;
+              for (int q4 = 0; q4 < 4; ++q4)
+                ds_out[4 * ci + q4] = make_int4(dk[4 * q4], dk[4 * q4 + 1], dk[4 * q4 + 2], dk[4 * q4 + 3]);
+          } else if (cls[ci] == 0) {
+            uint32_t z[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) z[i] = 0u;
+            tmem_st16(cbase + 16, z);
+            if (ds_ok)
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4) ds_out[4 * ci + q4] = make_int4(0, 0, 0, 0);
+          } else {
+            // general chunk: exact bucket scatter.  Runs of equal buckets along the row
+            // accumulate in a register and are flushed with predicated fire-and-forget
+            // fp32 reductions into this CTA's bins
+            const int rel0 = (int)(qp_half + c0 - kpos);
+            uint32_t rb = (uint32_t)(nb - 1);
+            float rs = 0.f;
+#pragma unroll 1
+            for (int g8 = 0; g8 < 32; g8 += 8) {
+              uint32_t dv[8], dk[4];
+              tmem_ld8(dpbase + g8, dv);
+              const uint32_t bw0 = bl[ci][g8 >> 2], bw1 = bl[ci][(g8 >> 2) + 1];
+              uint32_t kw[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) kw[j] = kl[ci][(g8 >> 1) + j];
+              tmem_ld_wait();
+              float dd[8];
+#pragma unroll
+              for (int j = 0; j < 8; j += 2) {
+                const float2 kd = __half22float2(*reinterpret_cast<const __half2*>(&kw[j >> 1]));
+                dd[j] = __uint_as_float(dv[j]) * kd.x * c1;
+                dd[j + 1] = __uint_as_float(dv[j + 1]) * kd.y * c1;
+                dk[j >> 1] = pack_bf16(dd[j], dd[j + 1]);
+              }
+              tmem_st4(cbase + 16 + (g8 >> 1), dk);
+              if (ds_ok) ds_out[4 * ci + (g8 >> 3)] = make_int4(dk[0], dk[1], dk[2], dk[3]);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const bool ok = (okm[ci] >> (g8 + j)) & 1u;
+                const uint32_t b = ((j < 4 ? bw0 : bw1) >> (8 * (j & 3))) & 0xFFu;
+                const bool ch = ok && b != rb;
+                red_add_f32_if(g_bins + rb, rs, ch && rs != 0.f);
+                rb = ch ? b : rb;
+                rs = ch ? dd[j] : rs + dd[j];  // dd = 0 on masked elements
+                if (has_pos) {
+                  const int rel = min(rel0 + g8 + j, P - 1);
+                  red_add_f32_if(g_bins + 256 + max(rel, 0), dd[j], ok && rel != P - 1);
+                  sat_p += (ok && rel == P - 1) ? dd[j] : 0.f;
+                }
               }
             }
+            red_add_f32_if(g_bins + rb, rs, rs != 0.f);
           }
-          red_add_f32_if(g_bins + rb, rs, rs != 0.f);
         }
         acc_w += (double)sat_w;
         acc_p += (double)sat_p;
@@ -541,6 +572,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int64_t kpos = (int64_t)it.y * kBN + r;
       const bool krow_ok = kpos < sg.kv_len;
       const int64_t krow = sg.kv_row0 + kpos;
+      if ((h0 & 1) && h0 < nh && p.wl.hdr->ds_blocks * H <= p.ds_cap_blocks) {
+        // the dQ kernel reads q halves in pairs: the partner of the first visible
+        // half sees nothing of this kv tile, its dS^T block is zero
+        int4* z = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(p.ds) +
+                                          (p.wl.ds_base[it.x] * H + (int64_t)(h * ds_nkt(sg) + it.y) * nh + h0 - 1) *
+                                              kDsBlockBytes + r * 128);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) z[i] = make_int4(0, 0, 0, 0);
+      }
       if (h0 >= nh) {
         // no query sees this kv tile: its dK/dV rows are zero
         if (krow_ok && !p.dk_accum)
@@ -592,354 +632,133 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 }
 
 // ====================================================================== dQ
-// q-tile-major (the forward's work list).  The kv side advances in 64-row half
-// tiles so that S / dP are double buffered in TMEM; dQ accumulates in one of two
-// TMEM buffers and is drained by dedicated warps while the next item runs.
-constexpr int kKStages = 4;  // K / V / ts_k half-tile ring depth
+// dQ = dS K as a plain streaming GEMM over the dS tiles the dKV kernel left in
+// the scratch (bf16, already scaled): q-tile-major (the forward's work list),
+// one item = (segment, 128-row q tile) x head, looping over the kv tiles it sees.
+//   warp 0 TMA: the two dS^T blocks of q halves (2i, 2i+1) + K_j per stage
+//   warp 1 MMA: dQ += dS K_j (A = dS, MN-major: the blocks are [kv][q]; B = K_j,
+//          MN-major), dQ double-buffered in TMEM
+//   warp 2 TMEM allocator;  warps 4-7 drain dQ (bf16) while the next item runs
+constexpr int kDqStages = 3;
+constexpr int kDqThreads = 256;
 
 template <int D>
 struct DqCfg {
-  static constexpr int TILE = 128 * D * 2;   // Q or dO tile
-  static constexpr int HTILE = kQH * D * 2;  // K or V half tile
+  static constexpr int TILE = 128 * D * 2;       // K tile
+  static constexpr int DSB = 2 * kDsBlockBytes;  // two dS^T blocks = dS^T of a 128-row q tile
+  static constexpr int STAGE = DSB + TILE;
   static constexpr int PANELS = D / 64;
-  static constexpr int Q_OFF = 0;
-  static constexpr int DO_OFF = TILE;
-  static constexpr int K_OFF = 2 * TILE;                          // [kKStages]
-  static constexpr int V_OFF = K_OFF + kKStages * HTILE;          // [kKStages]
-  static constexpr int TSQ_OFF = V_OFF + kKStages * HTILE;        // int64 [kTsSlot] (+ TMEM address in the pad)
-  static constexpr int TSK_OFF = TSQ_OFF + kTsSlot * 8;           // int64 [kKStages][kTsSlotH] (+ chunk maxima)
-  static constexpr int OCT_OFF = TSK_OFF + kKStages * kTsSlotH * 8;  // OctEntry [32]
-  static constexpr int PW_OFF = OCT_OFF + 32 * 16;                   // float [1024] x c1 (D=64 only)
-  static constexpr int BAR_OFF = PW_OFF + (D == 64 ? 4096 : 0);
-  static constexpr int NBARS = 2 + 3 * kKStages + 10;
-  static constexpr int SMEM = BAR_OFF + NBARS * 8;
+  static constexpr int BAR_OFF = kDqStages * STAGE;
+  static constexpr int NBARS = 2 * kDqStages + 4;
+  static constexpr int TMEMPTR_OFF = BAR_OFF + NBARS * 8;
+  static constexpr int SMEM = TMEMPTR_OFF + 16;
 };
 
 template <int D>
-__global__ void __launch_bounds__(kBwdThreads, 1)
-    hstu_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
-                       const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                       const __grid_constant__ CUtensorMap tm_tsq, const __grid_constant__ CUtensorMap tm_tsk,
+__global__ void __launch_bounds__(kDqThreads, 1)
+    hstu_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_ds, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ AttnParams p, __nv_bfloat16* __restrict__ dq, int64_t ld_dq) {
   using C = DqCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  int64_t* s_tsq = reinterpret_cast<int64_t*>(smem + C::TSQ_OFF);
-  int64_t* s_tsk = reinterpret_cast<int64_t*>(smem + C::TSK_OFF);  // chunk maxima at [st][kTsBoxH + {0,1}]
-  OctEntry* s_oct = reinterpret_cast<OctEntry*>(smem + C::OCT_OFF);
-  float* s_pwc = reinterpret_cast<float*>(smem + C::PW_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
-  uint64_t* q_full = bars + 0;
-  uint64_t* q_empty = bars + 1;              // last S / dP of the item + compute warps (ts_q)
-  uint64_t* kh_full = bars + 2;              // [kKStages] K_h, V_h, ts_k
-  uint64_t* kh_empty = kh_full + kKStages;   // [kKStages] dQ of the half (last reader of K_h) + compute (ts_k)
-  uint64_t* kx_full = kh_empty + kKStages;   // [kKStages] chunk maxima of ts_k
-  uint64_t* s_full = kx_full + kKStages;     // [2]
-  uint64_t* dp_full = s_full + 2;            // [2]
-  uint64_t* ds_full = dp_full + 2;           // [2] dS in TMEM (over S); dP consumed
-  uint64_t* dq_full = ds_full + 2;           // [2] dQ accumulators
+  uint64_t* full = bars;                   // [kDqStages]
+  uint64_t* empty = bars + kDqStages;      // [kDqStages]
+  uint64_t* dq_full = bars + 2 * kDqStages;  // [2]
   uint64_t* dq_empty = dq_full + 2;          // [2]
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_tsq + kTsBox);
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::TMEMPTR_OFF);
 
   const uint32_t warp = warp_id();
   const int tid = threadIdx.x;
   const int H = p.num_heads;
-  const int nb = p.bias.nb;
-  const int P = p.num_pos;
-  const bool has_pos = P > 0;
-  const float c1 = 0.5f * rsqrtf((float)D);
-
   if (smem_u32(smem) & 1023) __trap();
-  oct_table_fill(s_oct, p.bias, p.ts_weights, c1, tid, blockDim.x);
-  if (D == 64)
-    for (int i = tid; i < P; i += blockDim.x) s_pwc[i] = p.pos_weights[i] * c1;
   if (tid == 0) {
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1 + kCompWarps);
-    for (int i = 0; i < kKStages; ++i) {
-      mbar_init(&kh_full[i], 1);
-      mbar_init(&kh_empty[i], 1 + kCompWarps);
-      mbar_init(&kx_full[i], 1);
+    for (int i = 0; i < kDqStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&dp_full[i], 1);
-      mbar_init(&ds_full[i], 32 * kCompWarps);
       mbar_init(&dq_full[i], 1);
       mbar_init(&dq_empty[i], 128);
     }
     fence_barrier_init();
   }
   if (warp == 0 && lane_id() == 0) {
-    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_ds);
     tma_prefetch_desc(&tm_k);
-    tma_prefetch_desc(&tm_v);
-    tma_prefetch_desc(&tm_do);
-    tma_prefetch_desc(&tm_tsq);
-    tma_prefetch_desc(&tm_tsk);
   }
-  if (warp == 2) tmem_alloc(s_tmem, 512);
+  if (warp == 2) tmem_alloc(s_tmem, 2 * D < 32 ? 32 : 2 * D);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
-  // TMEM: S buffers [0,64) [64,128), dP buffers [128,192) [192,256), dQ buffers 256 + D*y
-  const uint32_t tDP = tmem + 128, tDQ = tmem + 256;
-
   const int total = p.wl.hdr->n_fwd * H;
-  auto kv_halves = [&](const Seg& sg, int qt) { return (int)((fwd_kv_lim(sg, qt) + kQH - 1) / kQH); };
+  auto kv_tiles = [&](const Seg& sg, int qt) { return (int)((fwd_kv_lim(sg, qt) + kBN - 1) / kBN); };
 
   if (warp == 0) {
-    // ================= TMA producer: Q, dO, ts_q per item
-    if (elect_one()) {
-      uint32_t q_it = 0;
-      for (int g = blockIdx.x; g < total; g += gridDim.x) {
-        const int2 it = p.wl.fwd[g / H];
-        const int h = g % H;
-        const Seg sg = load_seg(p.seg, it.x);
-        if (kv_halves(sg, it.y) == 0) continue;
-        mbar_wait(q_empty, (q_it & 1) ^ 1);
-        mbar_expect_tx(q_full, 2 * C::TILE + kTsBytes);
-        const int32_t qrow = (int32_t)(sg.q_row0 + (int64_t)it.y * kBM);
-        for (int pn = 0; pn < C::PANELS; ++pn) {
-          tma_load_2d(smem + C::Q_OFF + pn * 16384, &tm_q, h * D + pn * 64, qrow, q_full);
-          tma_load_2d(smem + C::DO_OFF + pn * 16384, &tm_do, h * D + pn * 64, qrow, q_full);
-        }
-        tma_load_1d(s_tsq, &tm_tsq, qrow & ~1, q_full);
-        ++q_it;
-      }
-    }
-  } else if (warp == 2) {
-    // ================= TMA producer: K_h, V_h, ts_k per kv half tile
+    // ================= TMA producer
     if (elect_one()) {
       uint32_t kc = 0;
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
         const int2 it = p.wl.fwd[g / H];
         const int h = g % H;
         const Seg sg = load_seg(p.seg, it.x);
-        const int n = kv_halves(sg, it.y);
-        for (int t = 0; t < n; ++t, ++kc) {
-          const int st = kc % kKStages;
-          mbar_wait(&kh_empty[st], ((kc / kKStages) & 1) ^ 1);
-          mbar_expect_tx(&kh_full[st], 2 * C::HTILE + kTsBytesH);
-          const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)t * kQH);
-          for (int pn = 0; pn < C::PANELS; ++pn) {
-            tma_load_2d(smem + C::K_OFF + st * C::HTILE + pn * 8192, &tm_k, h * D + pn * 64, krow, &kh_full[st]);
-            tma_load_2d(smem + C::V_OFF + st * C::HTILE + pn * 8192, &tm_v, h * D + pn * 64, krow, &kh_full[st]);
-          }
-          tma_load_1d(s_tsk + st * kTsSlotH, &tm_tsk, krow & ~1, &kh_full[st]);
+        const int n = kv_tiles(sg, it.y);
+        const int nh = ds_nh(sg), nkt = ds_nkt(sg);
+        for (int j = 0; j < n; ++j, ++kc) {
+          const int st = kc % kDqStages;
+          mbar_wait(&empty[st], ((kc / kDqStages) & 1) ^ 1);
+          mbar_expect_tx(&full[st], C::STAGE);
+          uint8_t* sb = smem + st * C::STAGE;
+          // blocks (j, 2i) and (j, 2i+1); the second one may not exist (odd half
+          // count): whatever is loaded only feeds q rows past the segment
+          const int64_t blk = p.wl.ds_base[it.x] * H + (int64_t)(h * nkt + j) * nh + 2 * it.y;
+          tma_load_2d(sb, &tm_ds, 0, (int32_t)(blk * 128), &full[st]);
+          tma_load_2d(sb + kDsBlockBytes, &tm_ds, 0, (int32_t)((blk + 1) * 128), &full[st]);
+          const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)j * kBN);
+          for (int pn = 0; pn < C::PANELS; ++pn)
+            tma_load_2d(sb + C::DSB + pn * 16384, &tm_k, h * D + pn * 64, krow, &full[st]);
         }
       }
     }
   } else if (warp == 1) {
     // ================= MMA issuer
     if (elect_one()) {
-      constexpr uint32_t id_s = idesc_bf16(128, kQH, 0, 0);  // S = Q K_h^T, dP = dO V_h^T: 128 q x 64 kv
-      constexpr uint32_t id_q = idesc_bf16(128, D, 0, 1);    // dQ += dS K_h (A K-major smem, B MN-major)
-      const uint32_t q_base = smem_u32(smem + C::Q_OFF);
-      const uint32_t do_base = smem_u32(smem + C::DO_OFF);
-      uint32_t q_it = 0, kc = 0, o_it = 0;
-      auto k_base = [&](uint32_t ki) { return smem_u32(smem + C::K_OFF + (ki % kKStages) * C::HTILE); };
-      auto v_base = [&](uint32_t ki) { return smem_u32(smem + C::V_OFF + (ki % kKStages) * C::HTILE); };
-      auto issue_S_dP = [&](uint32_t ki, bool last) {
-        const uint32_t x = ki & 1;
-        mbar_wait(&kh_full[ki % kKStages], (ki / kKStages) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t ka = (kk >> 2) * 16384 + (kk & 3) * 32;
-          const uint32_t kb = (kk >> 2) * 8192 + (kk & 3) * 32;
-          umma_ss(tmem + 64 * x, sdesc_sw128(q_base + ka, 16, 1024), sdesc_sw128(k_base(ki) + kb, 16, 1024), id_s,
-                  kk > 0 ? 1u : 0u);
-        }
-        umma_commit(&s_full[x]);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t ka = (kk >> 2) * 16384 + (kk & 3) * 32;
-          const uint32_t kb = (kk >> 2) * 8192 + (kk & 3) * 32;
-          umma_ss(tDP + 64 * x, sdesc_sw128(do_base + ka, 16, 1024), sdesc_sw128(v_base(ki) + kb, 16, 1024), id_s,
-                  kk > 0 ? 1u : 0u);
-        }
-        umma_commit(&dp_full[x]);
-        if (last) umma_commit(q_empty);  // Q / dO no longer read: the next item's may load
-      };
+      constexpr uint32_t id_q = idesc_bf16(128, D, 1, 1);  // A = dS (MN-major), B = K_j (MN-major)
+      uint32_t kc = 0, o_it = 0;
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
         const int2 it = p.wl.fwd[g / H];
         const Seg sg = load_seg(p.seg, it.x);
-        const int n = kv_halves(sg, it.y);
+        const int n = kv_tiles(sg, it.y);
         if (n == 0) continue;
         const uint32_t y = o_it & 1;
-        mbar_wait(q_full, q_it & 1);
-        issue_S_dP(kc, n == 1);
-        if (n > 1) issue_S_dP(kc + 1, n == 2);
-        for (int i = 0; i < n; ++i) {
-          const uint32_t ki = kc + i;
-          const uint32_t x = ki & 1;
-          mbar_wait(&ds_full[x], (ki >> 1) & 1);
-          if (i == 0) mbar_wait(&dq_empty[y], ((o_it >> 1) & 1) ^ 1);  // this dQ buffer drained
+        mbar_wait(&dq_empty[y], ((o_it >> 1) & 1) ^ 1);
+        for (int j = 0; j < n; ++j, ++kc) {
+          const int st = kc % kDqStages;
+          mbar_wait(&full[st], (kc / kDqStages) & 1);
           tc_fence_after();
-          // dQ += dS K_h: A = dS in TMEM (chunk c's 32 kv columns as bf16 pairs at
-          // [64x + 32c, +16)), B = K_h (64 kv x D, MN-major smem)
+          const uint32_t a_base = smem_u32(smem + st * C::STAGE);
+          const uint32_t b_base = a_base + C::DSB;
 #pragma unroll
-          for (int kk = 0; kk < kQH / 16; ++kk)
-            umma_ts(tDQ + D * y, tmem + 64 * x + 32 * (kk >> 1) + 8 * (kk & 1),
-                    sdesc_sw128(k_base(ki) + kk * 2048, 8192, 1024), id_q, (kk > 0 || i > 0) ? 1u : 0u);
-          umma_commit(&kh_empty[ki % kKStages]);
-          if (i + 2 < n) issue_S_dP(ki + 2, i + 3 == n);
+          for (int kk = 0; kk < kBN / 16; ++kk)
+            umma_ss(tmem + D * y, sdesc_sw128(a_base + kk * 2048, kDsBlockBytes, 1024),
+                    sdesc_sw128(b_base + kk * 2048, 16384, 1024), id_q, (kk > 0 || j > 0) ? 1u : 0u);
+          umma_commit(&empty[st]);
         }
-        kc += n;
         umma_commit(&dq_full[y]);
         ++o_it;
-        ++q_it;
       }
     }
-  } else if (warp == 3) {
-    // ================= ts_k statistics: per 32-column chunk maximum of each half
-    const int lane = lane_id();
-    uint32_t kc = 0;
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
-      const int2 it = p.wl.fwd[g / H];
-      const Seg sg = load_seg(p.seg, it.x);
-      const int n = kv_halves(sg, it.y);
-      for (int t = 0; t < n; ++t, ++kc) {
-        const int st = kc % kKStages;
-        mbar_wait(&kh_full[st], (kc / kKStages) & 1);
-        const int64_t* tsk = s_tsk + st * kTsSlotH + ((sg.kv_row0 + (int64_t)t * kQH) & 1);
-        const int64_t m0 = warp_max_i64(tsk[lane]);
-        const int64_t m1 = warp_max_i64(tsk[32 + lane]);
-        if (lane == 0) {
-          s_tsk[st * kTsSlotH + kTsBoxH] = m0;
-          s_tsk[st * kTsSlotH + kTsBoxH + 1] = m1;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&kx_full[st]);
-      }
-    }
-  } else if (warp >= 4 && warp < 12) {
-    // ================= compute: thread = (q row r, 32-kv-column chunk wg of the half)
-    const int et = tid - 128;
-    const int wg = et >> 7;
-    const int r = et & 127;
-    const int lane = r & 31;
+  } else if (warp >= 4) {
+    // ================= dQ drain (thread = q row)
+    const int r = tid - 128;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const int64_t cap = p.bias.cap;
-    const int c0 = 32 * wg;
-    float cb = p.ts_weights[nb - 1];
-    if (has_pos) cb += p.pos_weights[P - 1];
-    cb *= c1;
-    uint32_t q_it = 0, kc = 0, tcnt = 0;
-    const bool tr = (tid == 128);  // timeline role 4 (the dKV kernel uses roles 0-3)
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
-      const int2 it = p.wl.fwd[g / H];
-      const Seg sg = load_seg(p.seg, it.x);
-      const int64_t kv_lim = fwd_kv_lim(sg, it.y);
-      const int n = (int)((kv_lim + kQH - 1) / kQH);
-      if (n == 0) continue;
-      const int64_t nq = min((int64_t)kBM, sg.lq - (int64_t)it.y * kBM);
-      const bool row_ok = r < nq;
-      const int64_t qp_tile = sg.qp0 + (int64_t)it.y * kBM;
-      const int64_t qpos = qp_tile + r;
-      mbar_wait(q_full, q_it & 1);
-      const int64_t tq = row_ok ? s_tsq[((sg.q_row0 + (int64_t)it.y * kBM) & 1) + r] : (INT64_MAX >> 2);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(q_empty);
-      ++q_it;
-      const int64_t tq_min = warp_min_i64(tq);
-      const int64_t row_lo = qp_tile + (r & ~31), row_hi = row_lo + 31;
-      for (int t = 0; t < n; ++t, ++kc) {
-        const int st = kc % kKStages;
-        const uint32_t x = kc & 1, xp = (kc >> 1) & 1;
-        const int64_t kv0 = (int64_t)t * kQH + c0;  // this chunk's first kv position
-        mbar_wait(&kx_full[st], (kc / kKStages) & 1);
-        const int64_t* tsk = s_tsk + st * kTsSlotH + ((sg.kv_row0 + (int64_t)t * kQH) & 1) + c0;
-        const int64_t kc1 = kv0 + 31;
-        int cls = 0;
-        if (!(kv0 > row_hi || kv0 >= kv_lim)) {
-          cls = 2;
-          if ((kc1 <= row_lo) && (kc1 < kv_lim) && (tq_min - s_tsk[st * kTsSlotH + kTsBoxH + wg] >= cap) &&
-              (!has_pos || row_lo - kc1 >= P - 1))
-            cls = 1;
-        }
-        if (tr) trace_ev(p, 4, tcnt, 30, t);
-        mbar_wait(&s_full[x], xp);
-        mbar_wait(&dp_full[x], xp);
-        if (tr) trace_ev(p, 4, tcnt, 32, t);
-        tc_fence_after();
-        const uint32_t tS = tmem + 64 * x + c0 + lane_off;
-        const uint32_t tP = tDP + 64 * x + c0 + lane_off;
-        if (cls == 1) {
-          uint32_t sv[32], dv[32], dsk[16];
-          tmem_ld32(tS, sv);
-          tmem_ld32(tP, dv);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            const float h0 = fmaf(__uint_as_float(sv[i]), c1, cb);
-            const float h1 = fmaf(__uint_as_float(sv[i + 1]), c1, cb);
-            const float t0 = tanh_approx(h0), t1 = tanh_approx(h1);
-            const float d0 = __uint_as_float(dv[i]) * (1.f + t0) * (fmaf(-h0, t0, h0) + 1.f) * c1;
-            const float d1 = __uint_as_float(dv[i + 1]) * (1.f + t1) * (fmaf(-h1, t1, h1) + 1.f) * c1;
-            dsk[i >> 1] = pack_bf16(d0, d1);
-          }
-          tmem_st16(tS, dsk);  // dS over the chunk's (consumed) S columns
-        } else if (cls == 0) {
-          uint32_t z[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) z[i] = 0u;
-          tmem_st16(tS, z);
-        } else {
-          // general chunk: exact per-element bucket, positional bias and mask
-          const int relc = (int)(qpos - kv0);                                       // qpos - kpos of column 0
-          const int ncol = row_ok ? (int)min(kv_lim - kv0, (int64_t)32) : 0;        // in-range columns
-#pragma unroll 1
-          for (int g8 = 0; g8 < 32; g8 += 8) {
-            uint32_t sv[8], dv[8], dsk[4];
-            tmem_ld8(tS + g8, sv);
-            tmem_ld8(tP + g8, dv);
-            float bc[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              int b;
-              oct_lookup(clamp_delta(tq - tsk[g8 + i], cap), s_oct, b, bc[i]);
-            }
-            if (has_pos) {
-#pragma unroll
-              for (int i = 0; i < 8; ++i) bc[i] += s_pwc[min(max(relc - g8 - i, 0), P - 1)];
-            }
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 8; i += 2) {
-              float dd[2];
-#pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                const int k = g8 + i + u;
-                const float hh = fmaf(__uint_as_float(sv[i + u]), c1, bc[i + u]);
-                const float th = tanh_approx(hh);
-                const bool ok = k < ncol && k <= relc;
-                dd[u] = ok ? __uint_as_float(dv[i + u]) * (1.f + th) * (fmaf(-hh, th, hh) + 1.f) * c1 : 0.f;
-              }
-              dsk[i >> 1] = pack_bf16(dd[0], dd[1]);
-            }
-            tmem_st4(tS + (g8 >> 1), dsk);  // S columns g8/2 .. g8/2+3 were already read
-          }
-        }
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&ds_full[x]);
-        if (tr) trace_ev(p, 4, tcnt, 33, t);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&kh_empty[st]);  // done with this stage's ts_k
-      }
-    }
-  } else if (warp >= 12) {
-    // ================= dQ drain: TMEM -> bf16 -> global (thread = q row)
-    const int r = tid - 384;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const bool bad = p.wl.hdr->ds_overflow != 0;  // dS scratch overflow: poison dq
     uint32_t o_it = 0;
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
       const int2 it = p.wl.fwd[g / H];
       const int h = g % H;
       const Seg sg = load_seg(p.seg, it.x);
-      const int n = kv_halves(sg, it.y);
+      const int n = kv_tiles(sg, it.y);
       const int64_t nq = min((int64_t)kBM, sg.lq - (int64_t)it.y * kBM);
       const bool row_ok = r < nq;
       __nv_bfloat16* dqrow = dq + (sg.q_row0 + (int64_t)it.y * kBM + r) * ld_dq + h * D;
@@ -955,12 +774,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll 1
       for (int cc = 0; cc < D; cc += 32) {
         uint32_t v[32];
-        tmem_ld32(tDQ + D * y + lane_off + cc, v);
+        tmem_ld32(tmem + D * y + lane_off + cc, v);
         tmem_ld_wait();
         if (row_ok) {
           uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) pk[i >> 1] = pack_bf16(__uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+          for (int i = 0; i < 32; i += 2)
+            pk[i >> 1] = bad ? 0x7FC07FC0u : pack_bf16(__uint_as_float(v[i]), __uint_as_float(v[i + 1]));
           int4* d4 = reinterpret_cast<int4*>(dqrow + cc);
 #pragma unroll
           for (int i = 0; i < 4; ++i) d4[i] = make_int4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
@@ -972,7 +792,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc(tmem, 512);
+  if (warp == 2) tmem_dealloc(tmem, 2 * D < 32 ? 32 : 2 * D);
 }
 
 template <int D>
@@ -997,8 +817,7 @@ int launch_bwd(const TMaps& tm, const AttnParams& p, const jh_attn_args& a, int 
   if (a.prof_event_start) cudaEventRecord((cudaEvent_t)a.prof_event_start, s);
   hstu_bwd_dkv_kernel<D><<<grid, kBwdThreads, C::SMEM, s>>>(tm.q64, tm.k, tm.v, tm.do64, tm.tsq72, p);
   if (cudaError_t e = cudaGetLastError()) return (int)e;
-  hstu_bwd_dq_kernel<D><<<grid, kBwdThreads, Q::SMEM, s>>>(tm.q, tm.dout, tm.k64, tm.v64, tm.tsq, tm.tsk72, p,
-                                                          (__nv_bfloat16*)a.dq, a.ld_dq);
+  hstu_bwd_dq_kernel<D><<<grid, kDqThreads, Q::SMEM, s>>>(tm.ds, tm.k, p, (__nv_bfloat16*)a.dq, a.ld_dq);
   if (a.prof_event_end) cudaEventRecord((cudaEvent_t)a.prof_event_end, s);
   return (int)cudaGetLastError();
 }

@@ -55,18 +55,29 @@ JH_DEV int64_t seg_kv_vis(const Seg& g) {
 
 struct WorkHeader {
   int32_t n_fwd, n_bwd;
-  int32_t pad[14];
+  int64_t ds_blocks;    // dS scratch blocks of all segments (one head)
+  int32_t ds_overflow;  // set by the dKV kernel when the scratch is too small
+  int32_t pad[11];
 };
 
-// Workspace: [WorkHeader][fwd items int2 x max_f][bwd items int2 x max_b] ...
+// Workspace: [WorkHeader][fwd items int2 x max_f][bwd items int2 x max_b]
+// [dS block base per segment, int64 x (nseg + 1)] ...
 // [per-CTA d_ts_weights / d_pos_weights partial bins, fp32 kBinsPerCta each]
 constexpr int kBinsPerCta = 256 + 1024;
 struct WorkLists {
   WorkHeader* hdr;
   int2* fwd;
   int2* bwd;
+  int64_t* ds_base;
   float* bins;
 };
+
+// Backward dS scratch: per (segment, head) a dense grid of blocks, one per
+// (128-row kv tile j, 64-row q half t), each the bf16 dS^T tile [128 kv][64 q]
+// (16 KB, row-major); block (s, h, j, t) = ds_base[s] * H + (h * nkt + j) * nh + t.
+constexpr int kDsBlockBytes = 128 * 64 * 2;
+JH_DEV int ds_nkt(const Seg& g) { return (int)((seg_kv_vis(g) + kBN - 1) / kBN); }
+JH_DEV int ds_nh(const Seg& g) { return (int)((g.lq + 63) / 64); }
 
 constexpr int kLevels = 4096;
 
@@ -157,6 +168,48 @@ static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, 
       wl.bwd[idx] = make_int2((int)s, j);
     }
   }
+  // dS scratch: exclusive scan of the per-segment block counts (chunks of 1024)
+  if (wl.ds_base != nullptr) {
+    __shared__ long long carry_s;
+    __shared__ long long wsum[32];
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < sa.num_segments; base += blockDim.x) {
+      const int64_t s = base + threadIdx.x;
+      long long v = 0;
+      if (s < sa.num_segments) {
+        Seg g = load_seg(sa, s);
+        v = (long long)ds_nkt(g) * ds_nh(g);
+      }
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+      long long incl = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) wsum[wid] = incl;
+      __syncthreads();
+      if (wid == 0) {
+        long long x = wsum[lane], xi = x;
+        for (int o = 1; o < 32; o <<= 1) {
+          long long y = __shfl_up_sync(0xffffffffu, xi, o);
+          if (lane >= o) xi += y;
+        }
+        wsum[lane] = xi - x;
+      }
+      __syncthreads();
+      const long long c = carry_s;
+      if (s < sa.num_segments) wl.ds_base[s] = c + wsum[wid] + incl - v;
+      __syncthreads();
+      if (threadIdx.x == blockDim.x - 1) carry_s = c + wsum[wid] + incl;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      wl.ds_base[sa.num_segments] = carry_s;
+      wl.hdr->ds_blocks = carry_s;
+      wl.hdr->ds_overflow = 0;
+    }
+  }
 }
 
 // q, k, v, dout (bf16 2-D, 128-row boxes) and ts_q, ts_k (int64 1-D) tensor maps
@@ -164,6 +217,7 @@ struct TMaps {
   CUtensorMap q, k, v, dout, tsq, tsk;
   CUtensorMap q64, do64, tsq72;  // 64-row boxes for the dKV kernel (q side)
   CUtensorMap k64, v64, tsk72;  // 64-row boxes for the dQ kernel (kv side)
+  CUtensorMap ds;               // dS scratch as a [blocks * 128, 64] bf16 matrix, 128-row boxes
 };
 
 // Parameters shared by the fwd / bwd attention kernels.
@@ -187,6 +241,8 @@ struct AttnParams {
   float* dv_accum;
   double* d_ts_weights;
   double* d_pos_weights;
+  __nv_bfloat16* ds;      // dS scratch (kDsBlockBytes blocks)
+  int64_t ds_cap_blocks;  // its capacity
   WorkLists wl;
   DevBiasTable bias;
   // debug timeline (NULL = off): CTA trace_cta records (code, arg, clock64)

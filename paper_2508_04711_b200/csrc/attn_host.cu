@@ -27,7 +27,7 @@ static int sm_count() {
 }
 
 struct WsLayout {
-  size_t items_f, items_b, bins, total;
+  size_t items_f, items_b, ds_base, bins, total;
 };
 
 static size_t bins_bytes() { return (size_t)sm_count() * kBinsPerCta * 4; }
@@ -38,7 +38,8 @@ static WsLayout ws_layout(int64_t q_rows, int64_t kv_total, int64_t nseg, int32_
   int64_t max_b = kv_total / kBN + nseg + 1;
   w.items_f = sizeof(WorkHeader);
   w.items_b = w.items_f + ((size_t)max_f * 8 + 255) / 256 * 256;
-  w.bins = w.items_b + ((size_t)max_b * 8 + 255) / 256 * 256;
+  w.ds_base = w.items_b + ((size_t)max_b * 8 + 255) / 256 * 256;
+  w.bins = w.ds_base + ((size_t)(nseg + 1) * 8 + 255) / 256 * 256;
   w.total = w.bins + bins_bytes();
   return w;
 }
@@ -84,8 +85,10 @@ static int validate(const jh_attn_args* a, bool bwd) {
     }
   }
   WsLayout w = ws_layout(a->q_rows, a->q_rows, a->num_segments, a->num_heads, a->head_dim);
-  if (!a->workspace || a->workspace_bytes < (bwd ? w.total : w.bins))
-    return set_error(JH_ERR_INVALID, "workspace too small (need >= %zu bytes)", bwd ? w.total : w.bins);
+  if (!a->workspace || a->workspace_bytes < (bwd ? w.total : w.ds_base))
+    return set_error(JH_ERR_INVALID, "workspace too small (need >= %zu bytes)", bwd ? w.total : w.ds_base);
+  if (bwd && a->q_rows > 0 && (!a->ds_scratch || a->ds_scratch_bytes < (size_t)kDsBlockBytes || !aligned16(a->ds_scratch)))
+    return set_error(JH_ERR_INVALID, "ds_scratch missing or too small (see jh_attn_ds_scratch_bytes)");
   return JH_OK;
 }
 
@@ -129,9 +132,16 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
   p->wl.hdr = (WorkHeader*)ws;
   p->wl.fwd = (int2*)(ws + w.items_f);
   p->wl.bwd = (int2*)(ws + w.items_b);
+  p->ds = bwd ? (__nv_bfloat16*)a->ds_scratch : nullptr;
+  p->ds_cap_blocks = bwd ? (int64_t)(a->ds_scratch_bytes / kDsBlockBytes) : 0;
   // per-CTA gradient bins at the end of the caller's workspace
-  p->wl.bins = bwd ? (float*)(ws + ((a->workspace_bytes - bins_bytes()) & ~size_t(255))) : nullptr;
-  if (bwd && (uint8_t*)p->wl.bins < ws + w.items_b + 8)
+  // (the bwd item list is bounded by the caller's kv total, unknown here: the
+  // dS block bases and the per-CTA bins are carved from the end of the workspace)
+  const size_t bins_off = (a->workspace_bytes - bins_bytes()) & ~size_t(255);
+  const size_t dsb_off = (bins_off - (size_t)(a->num_segments + 1) * 8) & ~size_t(255);
+  p->wl.bins = bwd ? (float*)(ws + bins_off) : nullptr;
+  p->wl.ds_base = bwd ? (int64_t*)(ws + dsb_off) : nullptr;
+  if (bwd && ws + dsb_off < ws + w.items_b + 8)
     return set_error(JH_ERR_INVALID, "workspace too small");
   const uint64_t HD = (uint64_t)a->num_heads * a->head_dim;
   if ((uintptr_t)a->ts_q % 16 || (uintptr_t)a->ts_k % 16)
@@ -148,7 +158,8 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
               make_tmap_i64_1d(&tm->tsq72, a->ts_q, a->q_rows, kTsBoxH) ||
               make_tmap_bf16_2d(&tm->k64, a->k, a->kv_rows, HD, a->ld_k, 64) ||
               make_tmap_bf16_2d(&tm->v64, a->v, a->kv_rows, HD, a->ld_v, 64) ||
-              make_tmap_i64_1d(&tm->tsk72, a->ts_k, a->kv_rows, kTsBoxH)))
+              make_tmap_i64_1d(&tm->tsk72, a->ts_k, a->kv_rows, kTsBoxH) ||
+              make_tmap_bf16_2d(&tm->ds, a->ds_scratch, (uint64_t)p->ds_cap_blocks * 128, 64, 64, 128)))
     return set_error(JH_ERR_CUDA, "cuTensorMapEncodeTiled failed (bwd maps)");
   build_work_kernel<<<1, 1024, 0, s>>>(p->seg, p->wl);
   cudaError_t e = cudaGetLastError();
@@ -161,6 +172,14 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
 using namespace jh;
 
 extern "C" {
+
+size_t jh_attn_ds_scratch_bytes(int64_t kv_len_total, int64_t num_segments, int32_t num_heads, int64_t max_kv_len) {
+  // sum_s ceil(kv_s / 128) * ceil(lq_s / 64) <= (ceil(kv_total / 128) + nseg) * ceil(max_kv / 64)
+  // (a segment's q rows never exceed its kv rows)
+  if (kv_len_total <= 0 || num_segments <= 0 || num_heads <= 0 || max_kv_len <= 0) return (size_t)kDsBlockBytes;
+  const int64_t blocks = ((kv_len_total + kBN - 1) / kBN + num_segments) * ((max_kv_len + 63) / 64);
+  return (size_t)blocks * num_heads * kDsBlockBytes;
+}
 
 size_t jh_attn_workspace_bytes(int64_t q_rows, int64_t kv_len_total, int64_t num_segments, int32_t num_heads,
                                int32_t head_dim) {

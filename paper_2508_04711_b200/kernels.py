@@ -234,11 +234,14 @@ def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=
 
 
 def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_buckets=16, pos_weights=None,
-             q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, accumulate_dkv=False, prof=None):
+             q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, accumulate_dkv=False, prof=None,
+             max_kv_len=None):
     """Fused jagged HSTU backward (jh_attn_bwd).
 
     Returns (dq bf16, dk, dv, d_ts_weights f64, d_pos f64 or None); dk/dv are
-    bf16, or fp32 accumulators when ``accumulate_dkv`` (CP partials)."""
+    bf16, or fp32 accumulators when ``accumulate_dkv`` (CP partials).
+    ``max_kv_len`` bounds every segment's kv length (sizes the dS scratch);
+    when omitted it is read back from the device (one synchronisation)."""
     w = ts_weights.to(device=q.device, dtype=torch.float32).contiguous()
     pw = None if pos_weights is None else pos_weights.to(device=q.device, dtype=torch.float32).contiguous()
     a = _attn_args(q, k, v, ts_q, ts_k, q_offsets, num_heads, w, num_buckets, pw, q_pos0, kv_start, kv_len)
@@ -262,9 +265,19 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
     if pw is not None:
         d_pos = torch.zeros(pw.numel(), dtype=torch.float64, device=q.device)
         a.d_pos_weights = d_pos.data_ptr()
-    ws, nbytes = _workspace(q.shape[0], q.shape[0] if kv_len_total is None else kv_len_total, a.num_segments,
-                            num_heads, a.head_dim, q.device)
+    kvt = q.shape[0] if kv_len_total is None else kv_len_total
+    ws, nbytes = _workspace(q.shape[0], kvt, a.num_segments, num_heads, a.head_dim, q.device)
     a.workspace, a.workspace_bytes = ws.data_ptr(), nbytes
+    if max_kv_len is None:
+        if a.num_segments == 0:
+            max_kv_len = 0
+        elif kv_len is not None:
+            max_kv_len = int(kv_len.max().item())
+        else:
+            max_kv_len = int((q_offsets[1:] - q_offsets[:-1]).max().item())
+    ds_bytes = _lib.lib().jh_attn_ds_scratch_bytes(kvt, a.num_segments, num_heads, int(max_kv_len))
+    ds = torch.empty(ds_bytes, dtype=torch.uint8, device=q.device)
+    a.ds_scratch, a.ds_scratch_bytes = ds.data_ptr(), ds_bytes
     _prof(a, prof)
     check(_lib.lib().jh_attn_bwd(ctypes.byref(a), _stream(q)), "hstu_attention backward")
     _bump(4)  # work-list build + dq memset + fused backward + dq convert

@@ -40,7 +40,7 @@ class NumpyBackend:
         return out
 
     def _segs(self, segs):
-        qo, qp, ks, kl, _ = segs
+        qo, qp, ks, kl = segs[:4]
         return qo.numpy(), qp.numpy(), ks.numpy(), kl.numpy()
 
     def fwd(self, q, k, v, ts_q, ts_k, segs, H, w, nb):
