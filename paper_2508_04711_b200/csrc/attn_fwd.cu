@@ -9,16 +9,20 @@
 //   warp 0       TMA producer: Q + ts_q tile (2 buffers), K + ts_k / V tiles
 //                (NS stages, K runs one tile ahead of V; K is released as soon
 //                as S = Q K^T has consumed it, V after O += P V)
-//   warp 1       MMA issuer (one lane): S = Q K^T -> TMEM (2 buffers),
-//                O += P V with P read from TMEM (tcgen05 .kind::f16, A in TMEM)
-//   warp 2       TMEM allocator (512 columns)
-//   warps 4..11  epilogue, two groups of 4 warps; thread = (q row, 64-column
-//                half).  Per 32-column chunk (warp-uniform): fully masked ->
-//                P = 0; unmasked and bias-saturated -> P = h + h*tanh(h) with
-//                h = acc*c + c_bias (2 FFMA + 1 MUFU); otherwise the exact
-//                integer bucket, positional bias and causal/jagged mask.
-//                Final O -> bf16 -> global.
-// TMEM columns: S0 [0,128) S1 [128,256) O [256,256+D) P0 [384,448) P1 [448,512)
+//   warp 1       MMA issuer (one lane): S = Q K^T -> TMEM (3 buffers, S runs
+//                two tiles ahead of PV), O += P V with P read from TMEM
+//                (tcgen05 .kind::f16, A in TMEM)
+//   warp 2       TMEM allocator (512 columns); warp 3: per-chunk max of ts_k
+//   warps 4..11  epilogue, two warpgroups in ping-pong over the kv tiles (tile
+//                i -> group i % 2, S buffer i % 3), so one group's TMEM / barrier
+//                latency hides behind the other's MUFU work.  Thread = q row, all 128
+//                columns of its tiles.  Per 32-column chunk (warp-uniform):
+//                fully masked -> P = 0; unmasked and bias-saturated ->
+//                P = h + h*tanh(h), h = acc*c + c_bias (2 FFMA + 1 MUFU);
+//                otherwise the exact integer bucket, positional bias and mask.
+//                P (bf16) overwrites the first 16 columns of its S chunk.
+//   warps 12..15 drain O (bf16) of the finished item while the next one runs
+// TMEM columns: S0 [0,128) S1 [128,256) S2 [256,384) O [384,384+D)
 // There is no softmax normaliser: SiLU partials are additive, so O simply
 // accumulates in TMEM across kv tiles (no rescale).
 #include "attn_common.cuh"
@@ -26,7 +30,7 @@
 namespace jh {
 
 constexpr int kEpiWarps = 8;
-constexpr int kFwdThreads = 128 + 32 * kEpiWarps;
+constexpr int kFwdThreads = 128 + 32 * kEpiWarps + 128;
 constexpr int kTsRing = 4;  // ts_k tile ring (deeper than the K ring)
 
 template <int D>
@@ -43,7 +47,7 @@ struct FwdCfg {
   static constexpr int PW_OFF = OCT_OFF + 32 * 16;          // float pw[<=1024] x c1
   static constexpr int KMAX_OFF = PW_OFF + 1024 * 4;        // int64 [kTsRing][4] per-chunk max ts_k
   static constexpr int BAR_OFF = KMAX_OFF + kTsRing * 32;  // mbarriers
-  static constexpr int NBARS = 4 + 4 * NS + 3 * kTsRing + 6 + 2;
+  static constexpr int NBARS = 4 + 4 * NS + 3 * kTsRing + 8;
   static constexpr int TMEMPTR_OFF = BAR_OFF + NBARS * 8;
   static constexpr int SMEM = TMEMPTR_OFF + 16;
 };
@@ -69,13 +73,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* v_empty = v_full + NS;         // [NS] PV MMA done
   uint64_t* ts_full = v_empty + NS;        // [kTsRing]
   uint64_t* ts_empty = ts_full + kTsRing;  // [kTsRing] epilogue done with the tile
-  uint64_t* tsx_full = bars + 4 + 4 * NS + 2 * kTsRing + 6 + 2;  // [kTsRing] chunk maxima ready
+  uint64_t* tsx_full = bars + 4 + 4 * NS + 2 * kTsRing + 8;  // [kTsRing] chunk maxima ready
   int64_t* s_kmax = reinterpret_cast<int64_t*>(smem + C::KMAX_OFF);
-  uint64_t* s_full = ts_empty + kTsRing;   // [2]
-  uint64_t* p_full = s_full + 2;           // [2]
-  uint64_t* p_empty = p_full + 2;          // [2]
-  uint64_t* o_full = p_empty + 2;          // [1]
-  uint64_t* o_empty = o_full + 1;          // [1]
+  uint64_t* s_full = ts_empty + kTsRing;   // [3]
+  uint64_t* p_full = s_full + 3;           // [3] P (over S) written
+  uint64_t* o_full = p_full + 3;           // [1]
+  uint64_t* o_empty = o_full + 1;          // [1] drain warps hold O in registers
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::TMEMPTR_OFF);
 
   const uint32_t warp = warp_id();
@@ -91,10 +94,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1 + kEpiWarps);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 32 * kEpiWarps);
-      mbar_init(&p_empty[i], 1);
     }
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 16 * kEpiWarps);  // one warpgroup
+    }
+    mbar_init(o_full, 1);
+    mbar_init(o_empty, 128);  // drain warps
     for (int i = 0; i < NS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
@@ -103,11 +109,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     for (int i = 0; i < kTsRing; ++i) {
       mbar_init(&ts_full[i], 1);
-      mbar_init(&ts_empty[i], kEpiWarps);
+      mbar_init(&ts_empty[i], kEpiWarps / 2);  // the owning warpgroup
       mbar_init(&tsx_full[i], 1);
     }
-    mbar_init(o_full, 1);
-    mbar_init(o_empty, 32 * kEpiWarps);
     fence_barrier_init();
   }
   if (warp == 0 && lane_id() == 0) {
@@ -126,10 +130,28 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int n_items = p.wl.hdr->n_fwd;
   const int total = n_items * H;
 
+  // The K/S stream runs two kv tiles ahead of the V/PV stream, continuously
+  // across work items (a small ring carries the deferred tiles' coordinates).
+  constexpr int kLag = 2;
   if (warp == 0) {
-    // ================= TMA producer
+    // ================= TMA producer: Q + ts_q per item, K + ts_k per tile, V two tiles later
     if (elect_one()) {
-      uint32_t q_it = 0, k_it = 0, v_it = 0, t_it = 0, tcnt = 0;
+      uint32_t q_it = 0, k_it = 0, v_it = 0, tcnt = 0;
+      int32_t pend_row[4], pend_col[4];  // deferred V tiles (row, head column)
+      uint32_t n_pend = 0, pend_head = 0;
+      auto load_v = [&]() {
+        const int slot = pend_head & 3;
+        const int st = v_it % NS;
+        mbar_wait(&v_empty[st], ((v_it / NS) & 1) ^ 1);
+        trace_ev(p, 0, tcnt, 3, v_it);
+        mbar_expect_tx(&v_full[st], C::TILE_BYTES);
+        for (int pn = 0; pn < C::PANELS; ++pn)
+          tma_load_2d(smem + C::V_OFF + st * C::TILE_BYTES + pn * 16384, &tm_v, pend_col[slot] + pn * 64,
+                      pend_row[slot], &v_full[st]);
+        ++v_it;
+        ++pend_head;
+        --n_pend;
+      };
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
         const int2 it = p.wl.fwd[g / H];
         const int h = g % H;
@@ -145,45 +167,64 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           tma_load_2d(smem + C::Q_OFF + qb * C::TILE_BYTES + pn * 16384, &tm_q, h * D + pn * 64, qrow, &q_full[qb]);
         tma_load_1d(s_tsq + qb * kTsSlot, &tm_tsq, qrow & ~1, &q_full[qb]);
         ++q_it;
-        auto load_k = [&](int j) {
+        for (int j = 0; j < n; ++j) {
           const int st = k_it % NS;
-          const int ts = t_it % kTsRing;
+          const int ts = k_it % kTsRing;
           const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)j * kBN);
           mbar_wait(&k_empty[st], ((k_it / NS) & 1) ^ 1);
           trace_ev(p, 0, tcnt, 2, j);
           mbar_expect_tx(&k_full[st], C::TILE_BYTES);
           for (int pn = 0; pn < C::PANELS; ++pn)
             tma_load_2d(smem + C::K_OFF + st * C::TILE_BYTES + pn * 16384, &tm_k, h * D + pn * 64, krow, &k_full[st]);
-          mbar_wait(&ts_empty[ts], ((t_it / kTsRing) & 1) ^ 1);
+          mbar_wait(&ts_empty[ts], ((k_it / kTsRing) & 1) ^ 1);
           mbar_expect_tx(&ts_full[ts], kTsBytes);
           tma_load_1d(s_tsk + ts * kTsSlot, &tm_tsk, krow & ~1, &ts_full[ts]);
           ++k_it;
-          ++t_it;
-        };
-        auto load_v = [&](int j) {
-          const int st = v_it % NS;
-          const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)j * kBN);
-          mbar_wait(&v_empty[st], ((v_it / NS) & 1) ^ 1);
-          trace_ev(p, 0, tcnt, 3, j);
-          mbar_expect_tx(&v_full[st], C::TILE_BYTES);
-          for (int pn = 0; pn < C::PANELS; ++pn)
-            tma_load_2d(smem + C::V_OFF + st * C::TILE_BYTES + pn * 16384, &tm_v, h * D + pn * 64, krow, &v_full[st]);
-          ++v_it;
-        };
-        load_k(0);
-        for (int j = 0; j < n; ++j) {
-          if (j + 1 < n) load_k(j + 1);
-          load_v(j);
+          const int slot = (pend_head + n_pend) & 3;
+          pend_row[slot] = krow;
+          pend_col[slot] = h * D;
+          ++n_pend;
+          if (n_pend > kLag) load_v();
         }
       }
+      while (n_pend) load_v();
     }
   } else if (warp == 1) {
-    // ================= MMA issuer
+    // ================= MMA issuer: S(t) then PV(t - 2), one continuous stream
     if (elect_one()) {
       constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_pv = idesc_bf16(128, D, 0, 1);
-      const uint32_t tO = tmem + 256;
+      const uint32_t tO = tmem + 384;
       uint32_t q_it = 0, k_it = 0, v_it = 0, s_it = 0, o_it = 0, tcnt = 0;
+      uint32_t pend_flags[4];  // bit0 first tile of its item, bit1 last tile
+      uint32_t n_pend = 0, pend_head = 0, pv_it = 0;
+      auto issue_pv = [&]() {
+        const uint32_t sidx = pv_it;
+        const uint32_t fl = pend_flags[pend_head & 3];
+        const bool first = fl & 1u;
+        const int pb = sidx % 3;
+        const int st = v_it % NS;
+        mbar_wait(&p_full[pb], (sidx / 3) & 1);
+        trace_ev(p, 1, tcnt, 11, sidx);
+        mbar_wait(&v_full[st], (v_it / NS) & 1);
+        if (first) mbar_wait(o_empty, (o_it & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t v_base = smem_u32(smem + C::V_OFF + st * C::TILE_BYTES);
+        // A = P in TMEM: chunk c's 32 kv columns as bf16 pairs at [128 pb + 32c, +16)
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk)
+          umma_ts(tO, tmem + 128 * pb + 32 * (kk >> 1) + 8 * (kk & 1), sdesc_sw128(v_base + kk * 2048, 16384, 1024),
+                  idesc_pv, (first && kk == 0) ? 0u : 1u);
+        umma_commit(&v_empty[st]);
+        if (fl & 2u) {
+          umma_commit(o_full);
+          ++o_it;
+        }
+        ++v_it;
+        ++pv_it;
+        ++pend_head;
+        --n_pend;
+      };
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
         const int2 it = p.wl.fwd[g / H];
         const Seg sg = load_seg(p.seg, it.x);
@@ -193,27 +234,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_wait(&q_full[qb], (q_it >> 1) & 1);
         tc_fence_after();
         const uint32_t q_base = smem_u32(smem + C::Q_OFF + qb * C::TILE_BYTES);
-        auto issue_pv = [&](uint32_t sidx, bool first) {
-          const int pb = sidx & 1;
-          const int st = v_it % NS;
-          mbar_wait(&p_full[pb], (sidx >> 1) & 1);
-          trace_ev(p, 1, tcnt, 11, sidx);
-          mbar_wait(&v_full[st], (v_it / NS) & 1);
-          if (first) mbar_wait(o_empty, (o_it & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t v_base = smem_u32(smem + C::V_OFF + st * C::TILE_BYTES);
-          const uint32_t tP = tmem + 384 + 64 * pb;
-#pragma unroll
-          for (int kk = 0; kk < kBN / 16; ++kk)
-            umma_ts(tO, tP + kk * 8, sdesc_sw128(v_base + kk * 2048, 16384, 1024), idesc_pv,
-                    (first && kk == 0) ? 0u : 1u);
-          umma_commit(&v_empty[st]);
-          umma_commit(&p_empty[pb]);
-          ++v_it;
-        };
         for (int j = 0; j < n; ++j) {
           const int st = k_it % NS;
-          const int sb = s_it & 1;
+          const int sb = s_it % 3;  // buffer of tile s_it - 3, whose PV was issued before
           mbar_wait(&k_full[st], (k_it / NS) & 1);
           trace_ev(p, 1, tcnt, 10, s_it);
           tc_fence_after();
@@ -228,15 +251,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           umma_commit(&k_empty[st]);
           if (j == n - 1) umma_commit(&q_empty[qb]);
           ++k_it;
-          // PV of the previous tile, now that the next S is queued
-          if (j > 0) issue_pv(s_it - 1, j == 1);
           ++s_it;
+          pend_flags[(pend_head + n_pend) & 3] = (j == 0 ? 1u : 0u) | (j == n - 1 ? 2u : 0u);
+          ++n_pend;
+          if (n_pend > kLag) issue_pv();
         }
-        issue_pv(s_it - 1, n == 1);
-        umma_commit(o_full);
-        ++o_it;
         ++q_it;
       }
+      while (n_pend) issue_pv();
     }
   } else if (warp == 3) {
     // ================= ts_k tile statistics: per 32-column chunk maximum
@@ -261,10 +283,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         ++t_it;
       }
     }
-  } else if (warp >= 4) {
-    // ================= epilogue: thread = (q row r, column half wg)
+  } else if (warp >= 4 && warp < 12) {
+    // ================= epilogue: warpgroup wg owns the tiles with s_it % 2 == wg;
+    // thread = q row r, all 128 kv columns
     const int et = tid - 128;
-    const int wg = et >> 7;          // column group: S columns [64*wg, 64*wg+64)
+    const int wg = et >> 7;
     const int r = et & 127;          // q row within the tile (= TMEM lane)
     const int lane = r & 31;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
@@ -274,101 +297,66 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     float cb = p.ts_weights[nb - 1];
     if (has_pos) cb += p.pos_weights[P - 1];
     cb *= c1;
-    uint32_t q_it = 0, s_it = 0, t_it = 0, o_it = 0, tcnt = 0;
-    const bool tr = (tid == 128);
+    uint32_t q_it = 0, s_it = 0, tcnt = 0;
+    const bool tr = (tid == 128 || tid == 256);
+    const int trole = tid == 128 ? 3 : 4;
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
       const int2 it = p.wl.fwd[g / H];
-      const int h = g % H;
       const Seg sg = load_seg(p.seg, it.x);
       const int64_t kv_lim = fwd_kv_lim(sg, it.y);
       const int n = (int)((kv_lim + kBN - 1) / kBN);
+      if (n == 0) continue;
       const int64_t nq = min((int64_t)kBM, sg.lq - (int64_t)it.y * kBM);
       const bool row_ok = r < nq;
       const int64_t qp_tile = sg.qp0 + (int64_t)it.y * kBM;
       const int64_t qpos = qp_tile + r;
-      const int64_t qrow = sg.q_row0 + (int64_t)it.y * kBM + r;
-      __nv_bfloat16* orow = p.out + qrow * p.ld_o + h * D;
-      if (n == 0) {
-        if (row_ok)
-          for (int c = wg * (D / 2); c < (wg + 1) * (D / 2); c += 8)
-            *reinterpret_cast<int4*>(orow + c) = make_int4(0, 0, 0, 0);
-        continue;
-      }
       // this tile's query timestamps (TMA-staged with Q)
       const int qb = q_it & 1;
       mbar_wait(&q_full[qb], (q_it >> 1) & 1);
-      const int64_t tq = row_ok ? s_tsq[qb * kTsSlot + ((qrow - r) & 1) + r] : (INT64_MAX >> 2);
+      const int64_t tq = row_ok ? s_tsq[qb * kTsSlot + ((sg.q_row0 + (int64_t)it.y * kBM) & 1) + r] : (INT64_MAX >> 2);
       __syncwarp();
       if (lane == 0) mbar_arrive(&q_empty[qb]);
       ++q_it;
       const int64_t tq_min = warp_min_i64(tq);
       const int64_t row_lo = qp_tile + (r & ~31), row_hi = row_lo + 31;  // warp's q positions
-      for (int j = 0; j < n; ++j) {
-        const int sb = s_it & 1;
-        const int ts = t_it % kTsRing;
+      for (int j = 0; j < n; ++j, ++s_it) {
+        if ((int)(s_it & 1) != wg) continue;
+        const int sb = s_it % 3;
+        const int ts = s_it % kTsRing;
         const int64_t kv0 = (int64_t)j * kBN;
-        mbar_wait(&tsx_full[ts], (t_it / kTsRing) & 1);  // chunk maxima (implies ts_full)
-        mbar_wait(&s_full[sb], (s_it >> 1) & 1);
-        if (tr) trace_ev(p, 4, tcnt, 40, s_it);
-        mbar_wait(&p_empty[sb], ((s_it >> 1) & 1) ^ 1);
-        if (tr) trace_ev(p, 4, tcnt, 48, s_it);
+        mbar_wait(&tsx_full[ts], (s_it / kTsRing) & 1);  // chunk maxima (implies ts_full)
+        mbar_wait(&s_full[sb], (s_it / 3) & 1);
+        if (tr) trace_ev(p, trole, tcnt, 40, s_it);
         tc_fence_after();
         const int64_t* tsk = s_tsk + ts * kTsSlot + ((sg.kv_row0 + kv0) & 1);
         const uint32_t tS = tmem + 128 * sb + lane_off;
-        const uint32_t tP = tmem + 384 + 64 * sb + lane_off;
-        // chunk classes (warp-uniform): 0 all masked, 1 unmasked + saturated bias, 2 general
-        int cls_bits = 0;
-#pragma unroll
-        for (int ci = 0; ci < 2; ++ci) {
-          const int c0 = 64 * wg + 32 * ci;
+#pragma unroll 1
+        for (int c0 = 0; c0 < kBN; c0 += 32) {
+          // chunk class (warp-uniform): 0 all masked, 1 unmasked + saturated bias, 2 general
           const int64_t kc0 = kv0 + c0, kc1 = kc0 + 31;
           int cls = 0;  // every pair is in the future or past the segment
           if (!(kc0 > row_hi || kc0 >= kv_lim)) {
             cls = 2;
-            if ((kc1 <= row_lo) && (kc1 < kv_lim)) {
-              const int64_t tk_max = s_kmax[ts * 4 + (c0 >> 5)];
-              if ((tq_min - tk_max >= cap) && (!has_pos || row_lo - kc1 >= P - 1)) cls = 1;
-            }
+            if ((kc1 <= row_lo) && (kc1 < kv_lim) && (tq_min - s_kmax[ts * 4 + (c0 >> 5)] >= cap) &&
+                (!has_pos || row_lo - kc1 >= P - 1))
+              cls = 1;
           }
-          cls_bits |= cls << (2 * ci);
-        }
-        auto silu_fast = [&](const uint32_t* v, uint32_t* pk) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            const float h0 = fmaf(__uint_as_float(v[i]), c1, cb);
-            const float h1 = fmaf(__uint_as_float(v[i + 1]), c1, cb);
-            pk[i >> 1] = pack_bf16(fmaf(h0, tanh_approx(h0), h0), fmaf(h1, tanh_approx(h1), h1));
-          }
-        };
-        if (cls_bits == 5) {
-          // both chunks unmasked and saturated (the common case): one TMEM round trip
-          uint32_t va[32], vb[32], pk[16];
-          if (tr) trace_ev(p, 4, tcnt, 44, s_it);
-          tmem_ld32(tS + 64 * wg, va);
-          tmem_ld32(tS + 64 * wg + 32, vb);
-          tmem_ld_wait();
-          if (tr) trace_ev(p, 4, tcnt, 45, s_it);
-          silu_fast(va, pk);
-          tmem_st16(tP + 32 * wg, pk);
-          silu_fast(vb, pk);
-          tmem_st16(tP + 32 * wg + 16, pk);
-          if (tr) trace_ev(p, 4, tcnt, 46, s_it);
-        } else
-#pragma unroll 1
-        for (int ci = 0; ci < 2; ++ci) {
-          const int c0 = 64 * wg + 32 * ci;
-          const int cls = (cls_bits >> (2 * ci)) & 3;
           if (cls == 1) {
             uint32_t v[32], pk[16];
             tmem_ld32(tS + c0, v);
             tmem_ld_wait();
-            silu_fast(v, pk);
-            tmem_st16(tP + (c0 >> 1), pk);
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const float h0 = fmaf(__uint_as_float(v[i]), c1, cb);
+              const float h1 = fmaf(__uint_as_float(v[i + 1]), c1, cb);
+              pk[i >> 1] = pack_bf16(fmaf(h0, tanh_approx(h0), h0), fmaf(h1, tanh_approx(h1), h1));
+            }
+            tmem_st16(tS + c0, pk);  // P over the chunk's (consumed) S columns
           } else if (cls == 0) {
             uint32_t pk[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) pk[i] = 0u;
-            tmem_st16(tP + (c0 >> 1), pk);
+            tmem_st16(tS + c0, pk);
           } else {
             // general chunk (diagonal / short time gaps): exact per-element
             // bucket, positional bias and mask, 8 columns per step
@@ -401,42 +389,56 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                 }
                 pk[i >> 1] = pack_bf16(y[0], y[1]);
               }
-              tmem_st4(tP + ((c0 + g8) >> 1), pk);
+              tmem_st4(tS + c0 + (g8 >> 1), pk);  // S columns c0 .. c0+g8+7 were already read
             }
           }
         }
         tmem_st_wait();
-        if (tr) trace_ev(p, 4, tcnt, 47, s_it);
         tc_fence_before();
         mbar_arrive(&p_full[sb]);
-        if (tr) trace_ev(p, 4, tcnt, 41, s_it);
+        if (tr) trace_ev(p, trole, tcnt, 41, s_it);
         __syncwarp();
         if (lane == 0) mbar_arrive(&ts_empty[ts]);
-        ++s_it;
-        ++t_it;
       }
-      // ---- O: TMEM -> bf16 -> global (each group drains half the columns)
+    }
+  } else if (warp >= 12) {
+    // ================= O drain: TMEM -> bf16 -> global (thread = q row)
+    const int r = tid - 384;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    uint32_t o_it = 0;
+    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      const int2 it = p.wl.fwd[g / H];
+      const int h = g % H;
+      const Seg sg = load_seg(p.seg, it.x);
+      const int n = (int)((fwd_kv_lim(sg, it.y) + kBN - 1) / kBN);
+      const int64_t nq = min((int64_t)kBM, sg.lq - (int64_t)it.y * kBM);
+      const bool row_ok = r < nq;
+      __nv_bfloat16* orow = p.out + (sg.q_row0 + (int64_t)it.y * kBM + r) * p.ld_o + h * D;
+      if (n == 0) {
+        if (row_ok)
+          for (int c = 0; c < D; c += 8) *reinterpret_cast<int4*>(orow + c) = make_int4(0, 0, 0, 0);
+        continue;
+      }
       mbar_wait(o_full, o_it & 1);
-      if (tr) trace_ev(p, 4, tcnt, 42, o_it);
+      ++o_it;
       tc_fence_after();
-#pragma unroll 1
-      for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 32) {
+      // O -> bf16 registers first, release the accumulator, then store
+      uint32_t pk[D / 2];
+#pragma unroll
+      for (int c0 = 0; c0 < D; c0 += 32) {
         uint32_t v[32];
-        tmem_ld32(tmem + 256 + lane_off + c0, v);
+        tmem_ld32(tmem + 384 + lane_off + c0, v);
         tmem_ld_wait();
-        if (row_ok) {
-          uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) pk[i >> 1] = pack_bf16(__uint_as_float(v[i]), __uint_as_float(v[i + 1]));
-          int4* dst = reinterpret_cast<int4*>(orow + c0);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) dst[i] = make_int4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-        }
+        for (int i = 0; i < 32; i += 2) pk[(c0 + i) >> 1] = pack_bf16(__uint_as_float(v[i]), __uint_as_float(v[i + 1]));
       }
       tc_fence_before();
       mbar_arrive(o_empty);
-      if (tr) trace_ev(p, 4, tcnt, 43, o_it);
-      ++o_it;
+      if (row_ok) {
+        int4* dst = reinterpret_cast<int4*>(orow);
+#pragma unroll
+        for (int i = 0; i < D / 8; ++i) dst[i] = make_int4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      }
     }
   }
   tc_fence_before();
