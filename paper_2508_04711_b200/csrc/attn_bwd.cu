@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int64_t HD = (int64_t)H * D;
 
   const float c1 = 0.5f * rsqrtf((float)D);  // SiLU(s) = h (1 + tanh h), h = s / (2 sqrt(d))
+  cta_stamp(p, 0);
   if (smem_u32(smem) & 1023) __trap();
   oct_table_fill(s_oct, p.bias, p.ts_weights, c1, tid, blockDim.x);
   if (D == 64)
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // ================= TMA producer: K_j, V_j per item
     if (elect_one()) {
       uint32_t it_cnt = 0, tcnt = 0;
-      for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      JH_FOR_ITEMS(g, total) {
         const int2 it = p.wl.bwd[g / H];
         const int h = g % H;
         const Seg sg = load_seg(p.seg, it.x);
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // across item boundaries, independent of the K/V buffer)
     if (elect_one()) {
       uint32_t hc = 0;
-      for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      JH_FOR_ITEMS(g, total) {
         const int2 it = p.wl.bwd[g / H];
         const int h = g % H;
         const Seg sg = load_seg(p.seg, it.x);
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         umma_commit(&dp_full[x]);
         if (last) umma_commit(kv_empty);  // K_j / V_j no longer read: next item's may load
       };
-      for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      JH_FOR_ITEMS(g, total) {
         const int2 it = p.wl.bwd[g / H];
         const Seg sg = load_seg(p.seg, it.x);
         int h0, nh;
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // ================= ts_q statistics: per 32-column chunk minimum
     const int lane = lane_id();
     uint32_t hc = 0;
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    JH_FOR_ITEMS(g, total) {
       const int2 it = p.wl.bwd[g / H];
       const Seg sg = load_seg(p.seg, it.x);
       int h0, nh;
@@ -317,9 +318,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const bool tr = (tid == 128 || tid == 256);
     const int trole = tid == 128 ? 2 : 3;
     // dS scratch capacity (caller's max_kv_len bound); on overflow dQ becomes NaN
-    const bool ds_ok = p.wl.hdr->ds_blocks * H <= p.ds_cap_blocks;
+    const bool ds_ok = p.wl.hdr->ds_blocks * H <= p.ds_cap_blocks && !(p.dbg & 1);
     if (!ds_ok && et == 0) p.wl.hdr->ds_overflow = 1;
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    JH_FOR_ITEMS(g, total) {
       const int2 it = p.wl.bwd[g / H];
       const Seg sg = load_seg(p.seg, it.x);
       int h0, nh;
@@ -563,7 +564,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int r = tid - 384;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     uint32_t it_cnt = 0;
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    JH_FOR_ITEMS(g, total) {
       const int2 it = p.wl.bwd[g / H];
       const int h = g % H;
       const Seg sg = load_seg(p.seg, it.x);
@@ -628,6 +629,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  cta_stamp(p, 1);
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
@@ -670,6 +672,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   const uint32_t warp = warp_id();
   const int tid = threadIdx.x;
   const int H = p.num_heads;
+  cta_stamp(p, 0, 1);
   if (smem_u32(smem) & 1023) __trap();
   if (tid == 0) {
     for (int i = 0; i < kDqStages; ++i) {
@@ -698,7 +701,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     // ================= TMA producer
     if (elect_one()) {
       uint32_t kc = 0;
-      for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      JH_FOR_ITEMS(g, total) {
         const int2 it = p.wl.fwd[g / H];
         const int h = g % H;
         const Seg sg = load_seg(p.seg, it.x);
@@ -725,7 +728,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     if (elect_one()) {
       constexpr uint32_t id_q = idesc_bf16(128, D, 1, 1);  // A = dS (MN-major), B = K_j (MN-major)
       uint32_t kc = 0, o_it = 0;
-      for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      JH_FOR_ITEMS(g, total) {
         const int2 it = p.wl.fwd[g / H];
         const Seg sg = load_seg(p.seg, it.x);
         const int n = kv_tiles(sg, it.y);
@@ -754,7 +757,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const bool bad = p.wl.hdr->ds_overflow != 0;  // dS scratch overflow: poison dq
     uint32_t o_it = 0;
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    JH_FOR_ITEMS(g, total) {
       const int2 it = p.wl.fwd[g / H];
       const int h = g % H;
       const Seg sg = load_seg(p.seg, it.x);
@@ -792,6 +795,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  cta_stamp(p, 1, 1);
   if (warp == 2) tmem_dealloc(tmem, 2 * D < 32 ? 32 : 2 * D);
 }
 
@@ -812,6 +816,9 @@ int launch_bwd(const TMaps& tm, const AttnParams& p, const jh_attn_args& a, int 
   if (!attr) {
     cudaFuncSetAttribute(hstu_bwd_dkv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     cudaFuncSetAttribute(hstu_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
+    // one shared-memory carveout for every kernel of the library (no reconfiguration between them)
+    cudaFuncSetAttribute(hstu_bwd_dkv_kernel<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(hstu_bwd_dq_kernel<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr = true;
   }
   if (a.prof_event_start) cudaEventRecord((cudaEvent_t)a.prof_event_start, s);

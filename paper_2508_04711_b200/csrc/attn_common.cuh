@@ -79,135 +79,128 @@ constexpr int kDsBlockBytes = 128 * 64 * 2;
 JH_DEV int ds_nkt(const Seg& g) { return (int)((seg_kv_vis(g) + kBN - 1) / kBN); }
 JH_DEV int ds_nh(const Seg& g) { return (int)((g.lq + 63) / 64); }
 
-constexpr int kLevels = 4096;
+constexpr int kLevels = 1024;  // work-size histogram levels (one per builder thread)
+
+// Block-wide exclusive scan of one value per thread (1024 threads); returns the
+// exclusive prefix, *total gets the block sum.
+template <typename T>
+JH_DEV T block_exclusive_scan(T v, T* warp_sum, T* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  T incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) warp_sum[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    T x = warp_sum[lane], xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T y = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += y;
+    }
+    warp_sum[lane] = xi - x;
+    if (lane == 31) warp_sum[32] = xi;
+  }
+  __syncthreads();
+  const T r = warp_sum[wid] + incl - v;
+  *total = warp_sum[32];
+  __syncthreads();
+  return r;
+}
 
 // One block of 1024 threads.  fwd items (s, q_tile) ordered by #kv tiles
-// descending; bwd items (s, kv_tile) ordered by #q tiles descending.
-static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, WorkLists wl) {
+// descending; bwd items (s, kv_tile) ordered by #q tiles descending (counting
+// sort over a 1024-level histogram).  The segment each thread owns first is
+// decoded once and kept in registers across the passes.
+static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, WorkLists wl,
+                                                                   unsigned long long* stamp = nullptr) {
+  if (stamp != nullptr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    stamp[3072] = t;
+  }
   __shared__ int hist_f[kLevels], hist_b[kLevels];
-  __shared__ int warp_sum[32];
-  for (int i = threadIdx.x; i < kLevels; i += blockDim.x) hist_f[i] = hist_b[i] = 0;
+  __shared__ int isum[33];
+  __shared__ long long lsum[33];
+  const int tid = threadIdx.x;
+  hist_f[tid] = 0;
+  hist_b[tid] = 0;
+  const bool own = tid < sa.num_segments;
+  Seg g0{};
+  if (own) g0 = load_seg(sa, tid);
   __syncthreads();
-  for (int64_t s = threadIdx.x; s < sa.num_segments; s += blockDim.x) {
-    Seg g = load_seg(sa, s);
-    int nt = (int)((g.lq + kBM - 1) / kBM);
+  auto seg = [&](int64_t s) { return s == tid ? g0 : load_seg(sa, s); };
+  auto bwd_w = [](const Seg& g, int j) {
+    int64_t first = (int64_t)j * kBN - g.qp0;
+    first = first < 0 ? 0 : first;
+    return (int)((g.lq - first + kBM - 1) / kBM);
+  };
+  for (int64_t s = tid; s < sa.num_segments; s += blockDim.x) {
+    const Seg g = seg(s);
+    const int nt = (int)((g.lq + kBM - 1) / kBM);
     for (int t = 0; t < nt; ++t) {
-      int w = (int)((fwd_kv_lim(g, t) + kBN - 1) / kBN);
+      const int w = (int)((fwd_kv_lim(g, t) + kBN - 1) / kBN);
       atomicAdd(&hist_f[min(w, kLevels - 1)], 1);
     }
-    int64_t vis = seg_kv_vis(g);
-    int nj = (int)((vis + kBN - 1) / kBN);
-    int64_t qend = g.qp0 + g.lq;
-    for (int j = 0; j < nj; ++j) {
-      // q rows with position >= j*128
-      int64_t first = (int64_t)j * kBN - g.qp0;
-      first = first < 0 ? 0 : first;
-      int w = (int)((g.lq - first + kBM - 1) / kBM);
-      (void)qend;
-      atomicAdd(&hist_b[min(w, kLevels - 1)], 1);
+    const int nj = (int)((seg_kv_vis(g) + kBN - 1) / kBN);
+    for (int j = 0; j < nj; ++j) atomicAdd(&hist_b[min(bwd_w(g, j), kLevels - 1)], 1);
+  }
+  __syncthreads();
+  // descending starts: level L starts after all items of levels > L
+  {
+    const int lvl = kLevels - 1 - tid;
+    const int cf = hist_f[lvl], cb = hist_b[lvl];
+    int tf, tb;
+    const int sf = block_exclusive_scan(cf, isum, &tf);
+    const int sb = block_exclusive_scan(cb, isum, &tb);
+    hist_f[lvl] = sf;
+    hist_b[lvl] = sb;
+    if (tid == 0) {
+      wl.hdr->n_fwd = tf;
+      wl.hdr->n_bwd = tb;
     }
   }
   __syncthreads();
-  // descending exclusive scan: start[w] = sum_{w' > w} hist[w'] (in place)
-  for (int pass = 0; pass < 2; ++pass) {
-    int* h = pass ? hist_b : hist_f;
-    constexpr int per = kLevels / 1024;
-    int vals[per];
-    int local = 0;
-    // thread i owns levels reversed: idx = kLevels-1 - (i*per + k)
-    for (int k = 0; k < per; ++k) {
-      vals[k] = h[kLevels - 1 - (threadIdx.x * per + k)];
-      local += vals[k];
-    }
-    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int incl = local;
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) warp_sum[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-      int x = warp_sum[lane];
-      int xi = x;
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, xi, o);
-        if (lane >= o) xi += y;
-      }
-      warp_sum[lane] = xi - x;  // exclusive
-    }
-    __syncthreads();
-    int run = warp_sum[wid] + incl - local;
-    for (int k = 0; k < per; ++k) {
-      h[kLevels - 1 - (threadIdx.x * per + k)] = run;
-      run += vals[k];
-    }
-    if (threadIdx.x == blockDim.x - 1) {
-      if (pass)
-        wl.hdr->n_bwd = run;
-      else
-        wl.hdr->n_fwd = run;
-    }
-    __syncthreads();
-  }
-  for (int64_t s = threadIdx.x; s < sa.num_segments; s += blockDim.x) {
-    Seg g = load_seg(sa, s);
-    int nt = (int)((g.lq + kBM - 1) / kBM);
+  for (int64_t s = tid; s < sa.num_segments; s += blockDim.x) {
+    const Seg g = seg(s);
+    const int nt = (int)((g.lq + kBM - 1) / kBM);
     for (int t = 0; t < nt; ++t) {
-      int w = (int)((fwd_kv_lim(g, t) + kBN - 1) / kBN);
-      int idx = atomicAdd(&hist_f[min(w, kLevels - 1)], 1);
-      wl.fwd[idx] = make_int2((int)s, t);
+      const int w = (int)((fwd_kv_lim(g, t) + kBN - 1) / kBN);
+      wl.fwd[atomicAdd(&hist_f[min(w, kLevels - 1)], 1)] = make_int2((int)s, t);
     }
-    int64_t vis = seg_kv_vis(g);
-    int nj = (int)((vis + kBN - 1) / kBN);
-    for (int j = 0; j < nj; ++j) {
-      int64_t first = (int64_t)j * kBN - g.qp0;
-      first = first < 0 ? 0 : first;
-      int w = (int)((g.lq - first + kBM - 1) / kBM);
-      int idx = atomicAdd(&hist_b[min(w, kLevels - 1)], 1);
-      wl.bwd[idx] = make_int2((int)s, j);
-    }
+    const int nj = (int)((seg_kv_vis(g) + kBN - 1) / kBN);
+    for (int j = 0; j < nj; ++j) wl.bwd[atomicAdd(&hist_b[min(bwd_w(g, j), kLevels - 1)], 1)] = make_int2((int)s, j);
   }
   // dS scratch: exclusive scan of the per-segment block counts (chunks of 1024)
   if (wl.ds_base != nullptr) {
-    __shared__ long long carry_s;
-    __shared__ long long wsum[32];
-    if (threadIdx.x == 0) carry_s = 0;
-    __syncthreads();
+    long long carry = 0;
     for (int64_t base = 0; base < sa.num_segments; base += blockDim.x) {
-      const int64_t s = base + threadIdx.x;
+      const int64_t s = base + tid;
       long long v = 0;
       if (s < sa.num_segments) {
-        Seg g = load_seg(sa, s);
+        const Seg g = seg(s);
         v = (long long)ds_nkt(g) * ds_nh(g);
       }
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-      long long incl = v;
-      for (int o = 1; o < 32; o <<= 1) {
-        long long y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      if (lane == 31) wsum[wid] = incl;
-      __syncthreads();
-      if (wid == 0) {
-        long long x = wsum[lane], xi = x;
-        for (int o = 1; o < 32; o <<= 1) {
-          long long y = __shfl_up_sync(0xffffffffu, xi, o);
-          if (lane >= o) xi += y;
-        }
-        wsum[lane] = xi - x;
-      }
-      __syncthreads();
-      const long long c = carry_s;
-      if (s < sa.num_segments) wl.ds_base[s] = c + wsum[wid] + incl - v;
-      __syncthreads();
-      if (threadIdx.x == blockDim.x - 1) carry_s = c + wsum[wid] + incl;
-      __syncthreads();
+      long long tot;
+      const long long ex = block_exclusive_scan(v, lsum, &tot);
+      if (s < sa.num_segments) wl.ds_base[s] = carry + ex;
+      carry += tot;
     }
-    if (threadIdx.x == 0) {
-      wl.ds_base[sa.num_segments] = carry_s;
-      wl.hdr->ds_blocks = carry_s;
+    if (tid == 0) {
+      wl.ds_base[sa.num_segments] = carry;
+      wl.hdr->ds_blocks = carry;
       wl.hdr->ds_overflow = 0;
+    }
+  }
+  if (stamp != nullptr) {
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      stamp[3073] = t;
     }
   }
 }
@@ -249,13 +242,34 @@ struct AttnParams {
   // per role into trace[role * kTraceCap * 2 ...]
   unsigned long long* trace;
   int32_t trace_cta;
+  int32_t dbg;  // experiment switches (JH_DBG environment variable), 0 in production
 };
 
 constexpr int kTraceCap = 4096;
 
+// Per-CTA start / end stamps (trace_cta == -1): trace[2*cta] = start, [2*cta+1] = end
+// (globaltimer ns), for load-balance measurements.
+JH_DEV void cta_stamp(const AttnParams& p, int which, int kernel = 0) {
+  if (p.trace == nullptr || p.trace_cta != -1 || threadIdx.x != 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  p.trace[1024 * kernel + 2 * blockIdx.x + which] = t;
+  p.trace[1024 * kernel + 512 + 2 * blockIdx.x + which] = (unsigned long long)clock64();
+}
+
+// Static "snake" assignment of the longest-first work list to the persistent
+// CTAs: round k hands items [k*grid, (k+1)*grid) to CTAs in alternating
+// direction, which balances the per-CTA sums of the sorted item sizes far
+// better than plain round-robin.  Every role of a CTA walks the same sequence.
+JH_DEV int snake_item(int k) {
+  const int b = (k & 1) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;
+  return k * (int)gridDim.x + b;
+}
+#define JH_FOR_ITEMS(g, total) for (int _k = 0, g; (g = snake_item(_k)) < (total); ++_k)
+
 // One event from the calling thread (callers pass only one thread per role).
 JH_DEV void trace_ev(const AttnParams& p, int role, uint32_t& cnt, uint32_t code, uint32_t arg) {
-  if (p.trace == nullptr || (int)blockIdx.x != p.trace_cta || cnt >= (uint32_t)kTraceCap) return;
+  if (p.trace == nullptr || (int)blockIdx.x != p.trace_cta || cnt >= (uint32_t)kTraceCap) return;  // (-1: stamps)
   unsigned long long* t = p.trace + ((size_t)role * kTraceCap + cnt) * 2;
   t[0] = ((unsigned long long)code << 32) | arg;
   t[1] = (unsigned long long)clock64();

@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int H = p.num_heads;
   const int nb = p.bias.nb;
 
+  cta_stamp(p, 0, 2);
   if (smem_u32(smem) & 1023) __trap();  // 128B-swizzled operand tiles need 1 KB alignment
   const float c1 = 0.5f * rsqrtf((float)D);  // SiLU(s) = h + h*tanh(h), h = s/2 (scaled by 1/sqrt(d))
   oct_table_fill(s_oct, p.bias, p.ts_weights, c1, tid, blockDim.x);
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         ++pend_head;
         --n_pend;
       };
-      for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      JH_FOR_ITEMS(g, total) {
         const int2 it = p.wl.fwd[g / H];
         const int h = g % H;
         const Seg sg = load_seg(p.seg, it.x);
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         ++pend_head;
         --n_pend;
       };
-      for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      JH_FOR_ITEMS(g, total) {
         const int2 it = p.wl.fwd[g / H];
         const Seg sg = load_seg(p.seg, it.x);
         const int n = (int)((fwd_kv_lim(sg, it.y) + kBN - 1) / kBN);
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // (used by the epilogue's warp-uniform saturation test)
     const int lane = lane_id();
     uint32_t t_it = 0;
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    JH_FOR_ITEMS(g, total) {
       const int2 it = p.wl.fwd[g / H];
       const Seg sg = load_seg(p.seg, it.x);
       const int n = (int)((fwd_kv_lim(sg, it.y) + kBN - 1) / kBN);
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     uint32_t q_it = 0, s_it = 0, tcnt = 0;
     const bool tr = (tid == 128 || tid == 256);
     const int trole = tid == 128 ? 3 : 4;
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    JH_FOR_ITEMS(g, total) {
       const int2 it = p.wl.fwd[g / H];
       const Seg sg = load_seg(p.seg, it.x);
       const int64_t kv_lim = fwd_kv_lim(sg, it.y);
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int r = tid - 384;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     uint32_t o_it = 0;
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    JH_FOR_ITEMS(g, total) {
       const int2 it = p.wl.fwd[g / H];
       const int h = g % H;
       const Seg sg = load_seg(p.seg, it.x);
@@ -443,6 +444,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  cta_stamp(p, 1, 2);
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
@@ -454,6 +456,7 @@ int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& 
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(hstu_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(hstu_fwd_kernel<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr = true;
   }
   if (ev0) cudaEventRecord((cudaEvent_t)ev0, s);

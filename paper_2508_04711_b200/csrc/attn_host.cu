@@ -1,6 +1,7 @@
 // Host launch code for the attention kernels (jh_attn_fwd / jh_attn_bwd):
 // argument validation, tensor maps, work-list build, kernel launches.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "abi_internal.h"
@@ -125,6 +126,10 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
   p->bias.nb = a->num_buckets;
   p->trace = (unsigned long long*)a->trace;
   p->trace_cta = a->trace_cta;
+  {
+    const char* e = getenv("JH_DBG");
+    p->dbg = e ? atoi(e) : 0;
+  }
   // workspace carve-up (bound computed with the caller's kv total unknown:
   // the bwd list is placed after a q_rows-sized fwd list, see ws_layout)
   WsLayout w = ws_layout(a->q_rows, std::max<int64_t>(a->q_rows, 0), a->num_segments, a->num_heads, a->head_dim);
@@ -161,7 +166,12 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
               make_tmap_i64_1d(&tm->tsk72, a->ts_k, a->kv_rows, kTsBoxH) ||
               make_tmap_bf16_2d(&tm->ds, a->ds_scratch, (uint64_t)p->ds_cap_blocks * 128, 64, 64, 128)))
     return set_error(JH_ERR_CUDA, "cuTensorMapEncodeTiled failed (bwd maps)");
-  build_work_kernel<<<1, 1024, 0, s>>>(p->seg, p->wl);
+  static bool carve = false;
+  if (!carve) {
+    cudaFuncSetAttribute(build_work_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    carve = true;
+  }
+  build_work_kernel<<<1, 1024, 0, s>>>(p->seg, p->wl, p->trace_cta == -1 ? p->trace : nullptr);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(JH_ERR_CUDA, "build_work: %s", cudaGetErrorString(e));
   return JH_OK;
