@@ -363,10 +363,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             // bucket, positional bias and mask, 8 columns per step
             const int relc = (int)(qpos - kv0 - c0);                        // qpos - kpos of column 0
             const int ncol = (int)min(kv_lim - kv0 - c0, (int64_t)32);      // in-range columns
+            uint32_t vn[8];
+            tmem_ld8(tS + c0, vn);  // the next 8 columns' load stays in flight during each step
 #pragma unroll 1
             for (int g8 = 0; g8 < 32; g8 += 8) {
               uint32_t v[8], pk[4];
-              tmem_ld8(tS + c0 + g8, v);
               float bc[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
@@ -378,6 +379,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                 for (int i = 0; i < 8; ++i) bc[i] += s_pwc[min(max(relc - g8 - i, 0), P - 1)];
               }
               tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[i] = vn[i];
+              if (g8 < 24) tmem_ld8(tS + c0 + g8 + 8, vn);
 #pragma unroll
               for (int i = 0; i < 8; i += 2) {
                 float y[2];

@@ -205,6 +205,11 @@ JH_DEV void tmem_st4(uint32_t taddr, const uint32_t (&r)[4]) {
                : "memory");
 }
 
+JH_DEV void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
 JH_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -223,9 +228,9 @@ JH_DEV void red_add_f32(float* addr, float v) {
 
 // Predicated fire-and-forget reduction (no branch around it).
 JH_DEV void red_add_f32_if(float* addr, float v, bool pred) {
+  // no "memory" clobber: the bins are only read after a __threadfence at the end
   asm volatile("{ .reg .pred p; setp.ne.b32 p, %2, 0; @p red.global.add.f32 [%0], %1; }" ::"l"(addr), "f"(v),
-               "r"((int)pred)
-               : "memory");
+               "r"((int)pred));
 }
 
 JH_DEV float tanh_approx(float x) {
