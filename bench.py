@@ -205,6 +205,28 @@ def run_gpu(args):
         step_fn()
     barrier()
 
+    # N = 1: the step (work-list builds + 3 attention kernels + d_w zeroing) is
+    # captured once into a CUDA graph and replayed, so host launch overhead is
+    # not on the device timeline.  The per-kernel roofline timing below uses a
+    # separate eager pass with events around the kernels.
+    graph = None
+    if world == 1 and not args.no_graph:
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                step_fn()
+        stream.wait_stream(side)
+        barrier()
+        graph = torch.cuda.CUDAGraph()
+        n0 = kernels.launch_count()
+        with torch.cuda.graph(graph):
+            step_fn()
+        launches_per_step = kernels.launch_count() - n0
+        barrier()
+        graph.replay()
+        barrier()
+
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     kev = [((torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)),
@@ -215,10 +237,19 @@ def run_gpu(args):
         for i in range(K):
             flush.fill_(float(i))  # evict the step's inputs from L2 (512 MiB > 126 MB L2)
             ev[i][0].record(stream)
-            step_fn(prof=kev[i] if world == 1 else None)
+            if graph is not None:
+                graph.replay()
+            else:
+                step_fn(prof=kev[i] if world == 1 else None)
             ev[i][1].record(stream)
         barrier()
-    launches = kernels.launch_count() - launches0
+    launches = (kernels.launch_count() - launches0) if graph is None else launches_per_step * K
+    if graph is not None:
+        # eager pass for the per-kernel (roofline) timings
+        for i in range(K):
+            flush.fill_(float(i))
+            step_fn(prof=kev[i])
+        barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = float(sum(step_ms))
     if world > 1:
@@ -238,7 +269,8 @@ def run_gpu(args):
                                "H=4, d=128, nb=16" + ("" if world == 1 else f", jagged CP={world} (balanced)"),
                    "batch_per_rank": B, "max_seq_len": MAXLEN, "heads": H, "head_dim": D, "tokens": tokens_total,
                    "parallelism": "single" if world == 1 else f"cp{world}",
-                   "l2": "flushed between timed steps (512 MiB write, outside the timed events)"},
+                   "l2": "flushed between timed steps (512 MiB write, outside the timed events)",
+                   "cuda_graph": graph is not None},
         "tflops": F / (ms_per_step / 1e3) / 1e12,
         "tensor_frac_step": F / (ms_per_step / 1e3) / (world * peak * 1e12),
         "gpu_launches": int(launches),
@@ -398,6 +430,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a captured CUDA graph")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
