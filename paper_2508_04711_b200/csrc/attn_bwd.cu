@@ -25,7 +25,8 @@
 // (2) hstu_bwd_dq_kernel -- dQ = dS K as a streaming GEMM over that scratch
 //     (q-tile-major, TMA-fed, dQ double-buffered in TMEM), no recomputation.
 // No atomics on the gradient tensors: every dQ / dK / dV row is written by
-// exactly one CTA; d_ts_weights reduces per-CTA partials with fp64 atomics.
+// exactly one CTA; d_ts_weights: per-CTA fp64 totals of the dK/dV kernel, summed
+// in a fixed order by the dQ kernel.
 #include <algorithm>
 
 #include "abi_internal.h"
@@ -61,7 +62,8 @@ struct DkvCfg {
   // minima; slot 0's padding also holds the TMEM base address)
   static constexpr int BAR_OFF = PW_OFF + (D == 64 ? 4096 : 0);
   static constexpr int NBARS = 26;
-  static constexpr int SMEM = BAR_OFF + NBARS * 8;
+  static constexpr int RING_OFF = BAR_OFF + NBARS * 8;  // work-item ring: full[], empty[], slot[]
+  static constexpr int SMEM = RING_OFF + 2 * kItemRing * 8 + kItemRing * 4;
 };
 
 // q half tiles [h0, nh) of segment `sg` that can see kv tile j (h0 == nh: none)
@@ -98,6 +100,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* dkv_empty = dkv_full + 1;
   static_assert(2 + 3 * kQStages + 8 + 2 <= C::NBARS, "barrier count");
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_tsq + kTsBoxH + 2);
+  const ItemRing ring{reinterpret_cast<int32_t*>(smem + C::RING_OFF + 2 * kItemRing * 8),
+                      reinterpret_cast<uint64_t*>(smem + C::RING_OFF),
+                      reinterpret_cast<uint64_t*>(smem + C::RING_OFF + kItemRing * 8)};
 
   const uint32_t warp = warp_id();
   const int tid = threadIdx.x;
@@ -134,6 +139,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     mbar_init(dkv_full, 1);
     mbar_init(dkv_empty, 128);
+    ring_init(ring, 1 + 1 + 1 + kCompWarps + 4);  // consumers: Q TMA, MMA, ts stats, compute, drain
     fence_barrier_init();
   }
   if (warp == 0 && lane_id() == 0) {
@@ -157,7 +163,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // ================= TMA producer: K_j, V_j per item
     if (elect_one()) {
       uint32_t it_cnt = 0, tcnt = 0;
-      JH_FOR_ITEMS(g, total) {
+      uint32_t rk = 0;
+      for (int g; (g = ring_produce(ring, rk, &p.wl.hdr->next_item[1], total)) >= 0;) {
         const int2 it = p.wl.bwd[g / H];
         const int h = g % H;
         const Seg sg = load_seg(p.seg, it.x);
@@ -180,7 +187,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // across item boundaries, independent of the K/V buffer)
     if (elect_one()) {
       uint32_t hc = 0;
-      JH_FOR_ITEMS(g, total) {
+      uint32_t rk = 0;
+      for (int g; (g = ring_consume(ring, rk, false)) >= 0;) {
         const int2 it = p.wl.bwd[g / H];
         const int h = g % H;
         const Seg sg = load_seg(p.seg, it.x);
@@ -232,7 +240,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         umma_commit(&dp_full[x]);
         if (last) umma_commit(kv_empty);  // K_j / V_j no longer read: next item's may load
       };
-      JH_FOR_ITEMS(g, total) {
+      uint32_t rk = 0;
+      for (int g; (g = ring_consume(ring, rk, false)) >= 0;) {
         const int2 it = p.wl.bwd[g / H];
         const Seg sg = load_seg(p.seg, it.x);
         int h0, nh;
@@ -280,7 +289,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // ================= ts_q statistics: per 32-column chunk minimum
     const int lane = lane_id();
     uint32_t hc = 0;
-    JH_FOR_ITEMS(g, total) {
+    uint32_t rk = 0;
+    for (int g; (g = ring_consume(ring, rk, true)) >= 0;) {
       const int2 it = p.wl.bwd[g / H];
       const Seg sg = load_seg(p.seg, it.x);
       int h0, nh;
@@ -320,7 +330,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // dS scratch capacity (caller's max_kv_len bound); on overflow dQ becomes NaN
     const bool ds_ok = p.wl.hdr->ds_blocks * H <= p.ds_cap_blocks && !(p.dbg & 1);
     if (!ds_ok && et == 0) p.wl.hdr->ds_overflow = 1;
-    JH_FOR_ITEMS(g, total) {
+    uint32_t rk = 0;
+    for (int g; (g = ring_consume(ring, rk, true)) >= 0;) {
       const int2 it = p.wl.bwd[g / H];
       const Seg sg = load_seg(p.seg, it.x);
       int h0, nh;
@@ -544,27 +555,29 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       acc_w += __shfl_xor_sync(0xffffffffu, acc_w, o);
       acc_p += __shfl_xor_sync(0xffffffffu, acc_p, o);
     }
-    if (lane == 0) {
-      if (acc_w != 0.0) atomicAdd(&p.d_ts_weights[nb - 1], acc_w);
-      if (has_pos && acc_p != 0.0) atomicAdd(&p.d_pos_weights[P - 1], acc_p);
-    }
-    __threadfence();
+    // this CTA's saturated-chunk totals go to plain fp64 slots; the dQ kernel
+    // (next on the stream) sums them with every CTA's fp32 bins -- no contended
+    // atomics and no memory fence at the end of this kernel
+    double* s_red = reinterpret_cast<double*>(smem + C::TSQ_OFF);  // ts_q ring is idle now
     named_bar_sync(1, 32 * kCompWarps);
-    for (int i = et; i < nb; i += 32 * kCompWarps) {
-      const float v = __ldcg(g_bins + i);
-      if (v != 0.f) atomicAdd(&p.d_ts_weights[i], (double)v);
+    if (lane == 0) {
+      s_red[(et >> 5)] = acc_w;
+      s_red[kCompWarps + (et >> 5)] = acc_p;
     }
-    if (has_pos)
-      for (int i = et; i < P - 1; i += 32 * kCompWarps) {
-        const float v = __ldcg(g_bins + 256 + i);
-        if (v != 0.f) atomicAdd(&p.d_pos_weights[i], (double)v);
-      }
+    named_bar_sync(1, 32 * kCompWarps);
+    if (et == 0 && p.trace != nullptr && p.trace_cta == -1) p.trace[512 + 2 * blockIdx.x] = hc;  // halves done
+    if (et < 2) {
+      double v = 0.0;
+      for (int w2 = 0; w2 < kCompWarps; ++w2) v += s_red[et * kCompWarps + w2];
+      p.wl.partials[(size_t)blockIdx.x * 2 + et] = v;
+    }
   } else if (warp >= 12) {
     // ================= dK / dV drain (thread = kv row)
     const int r = tid - 384;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     uint32_t it_cnt = 0;
-    JH_FOR_ITEMS(g, total) {
+    uint32_t rk = 0;
+    for (int g; (g = ring_consume(ring, rk, true)) >= 0;) {
       const int2 it = p.wl.bwd[g / H];
       const int h = g % H;
       const Seg sg = load_seg(p.seg, it.x);
@@ -653,7 +666,8 @@ struct DqCfg {
   static constexpr int BAR_OFF = kDqStages * STAGE;
   static constexpr int NBARS = 2 * kDqStages + 4;
   static constexpr int TMEMPTR_OFF = BAR_OFF + NBARS * 8;
-  static constexpr int SMEM = TMEMPTR_OFF + 16;
+  static constexpr int RING_OFF = TMEMPTR_OFF + 16;  // work-item ring
+  static constexpr int SMEM = RING_OFF + 2 * kItemRing * 8 + kItemRing * 4;
 };
 
 template <int D>
@@ -668,6 +682,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   uint64_t* dq_full = bars + 2 * kDqStages;  // [2]
   uint64_t* dq_empty = dq_full + 2;          // [2]
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::TMEMPTR_OFF);
+  const ItemRing ring{reinterpret_cast<int32_t*>(smem + C::RING_OFF + 2 * kItemRing * 8),
+                      reinterpret_cast<uint64_t*>(smem + C::RING_OFF),
+                      reinterpret_cast<uint64_t*>(smem + C::RING_OFF + kItemRing * 8)};
 
   const uint32_t warp = warp_id();
   const int tid = threadIdx.x;
@@ -683,6 +700,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       mbar_init(&dq_full[i], 1);
       mbar_init(&dq_empty[i], 128);
     }
+    ring_init(ring, 1 + 4);  // consumers: MMA, drain warps
     fence_barrier_init();
   }
   if (warp == 0 && lane_id() == 0) {
@@ -701,7 +719,8 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     // ================= TMA producer
     if (elect_one()) {
       uint32_t kc = 0;
-      JH_FOR_ITEMS(g, total) {
+      uint32_t rk = 0;
+      for (int g; (g = ring_produce(ring, rk, &p.wl.hdr->next_item[2], total)) >= 0;) {
         const int2 it = p.wl.fwd[g / H];
         const int h = g % H;
         const Seg sg = load_seg(p.seg, it.x);
@@ -728,7 +747,8 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     if (elect_one()) {
       constexpr uint32_t id_q = idesc_bf16(128, D, 1, 1);  // A = dS (MN-major), B = K_j (MN-major)
       uint32_t kc = 0, o_it = 0;
-      JH_FOR_ITEMS(g, total) {
+      uint32_t rk = 0;
+      for (int g; (g = ring_consume(ring, rk, false)) >= 0;) {
         const int2 it = p.wl.fwd[g / H];
         const Seg sg = load_seg(p.seg, it.x);
         const int n = kv_tiles(sg, it.y);
@@ -751,13 +771,30 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         ++o_it;
       }
     }
+  } else if (warp == 3) {
+    // ================= d_ts_weights / d_pos: sum the dK/dV kernel's per-CTA totals
+    // (entry e handled by one thread of one CTA: a plain, ordered accumulate)
+    const int nb = p.bias.nb, P = p.num_pos;
+    const int n_e = 256 + P;
+    for (int e = blockIdx.x * 32 + lane_id(); e < n_e; e += gridDim.x * 32) {
+      if (e >= nb && e < 256) continue;
+      double v = 0.0;
+      for (int c = 0; c < (int)gridDim.x; ++c) v += (double)__ldcg(p.wl.bins + (size_t)c * kBinsPerCta + e);
+      if (e == nb - 1 || (P > 0 && e == 256 + P - 1))
+        for (int c = 0; c < (int)gridDim.x; ++c) v += p.wl.partials[(size_t)c * 2 + (e < 256 ? 0 : 1)];
+      if (e < 256)
+        p.d_ts_weights[e] += v;
+      else
+        p.d_pos_weights[e - 256] += v;
+    }
   } else if (warp >= 4) {
     // ================= dQ drain (thread = q row)
     const int r = tid - 128;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const bool bad = p.wl.hdr->ds_overflow != 0;  // dS scratch overflow: poison dq
     uint32_t o_it = 0;
-    JH_FOR_ITEMS(g, total) {
+    uint32_t rk = 0;
+    for (int g; (g = ring_consume(ring, rk, true)) >= 0;) {
       const int2 it = p.wl.fwd[g / H];
       const int h = g % H;
       const Seg sg = load_seg(p.seg, it.x);

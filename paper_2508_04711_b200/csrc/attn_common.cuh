@@ -57,7 +57,8 @@ struct WorkHeader {
   int32_t n_fwd, n_bwd;
   int64_t ds_blocks;    // dS scratch blocks of all segments (one head)
   int32_t ds_overflow;  // set by the dKV kernel when the scratch is too small
-  int32_t pad[11];
+  int32_t next_item[3]; // dynamic scheduler counters: fwd, dK/dV, dQ kernels
+  int32_t pad[8];
 };
 
 // Workspace: [WorkHeader][fwd items int2 x max_f][bwd items int2 x max_b]
@@ -69,7 +70,8 @@ struct WorkLists {
   int2* fwd;
   int2* bwd;
   int64_t* ds_base;
-  float* bins;
+  float* bins;        // per-CTA fp32 bins (dK/dV kernel, reductions)
+  double* partials;   // per-CTA fp64 totals [grid][kBinsPerCta], summed by the dQ kernel
 };
 
 // Backward dS scratch: per (segment, head) a dense grid of blocks, one per
@@ -161,6 +163,7 @@ static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, 
     if (tid == 0) {
       wl.hdr->n_fwd = tf;
       wl.hdr->n_bwd = tb;
+      wl.hdr->next_item[0] = wl.hdr->next_item[1] = wl.hdr->next_item[2] = 0;
     }
   }
   __syncthreads();
@@ -255,6 +258,49 @@ JH_DEV void cta_stamp(const AttnParams& p, int which, int kernel = 0) {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   p.trace[1024 * kernel + 2 * blockIdx.x + which] = t;
   p.trace[1024 * kernel + 512 + 2 * blockIdx.x + which] = (unsigned long long)clock64();
+}
+
+// Dynamic assignment of the longest-first work list to the persistent CTAs:
+// one thread per CTA (the ring producer) takes the next item index from a
+// global counter and publishes it in a small shared-memory ring that every
+// other role of the CTA consumes in the same order (longest-processing-time-
+// first scheduling without any static imbalance).
+constexpr int kItemRing = 2;
+struct ItemRing {
+  int32_t* slot;    // [kItemRing]
+  uint64_t* full;   // [kItemRing], count 1
+  uint64_t* empty;  // [kItemRing], count = number of consumers
+};
+JH_DEV void ring_init(const ItemRing& r, int consumers) {
+  for (int i = 0; i < kItemRing; ++i) {
+    mbar_init(&r.full[i], 1);
+    mbar_init(&r.empty[i], consumers);
+  }
+}
+// producer: returns the next item (or -1 when the list is exhausted)
+JH_DEV int ring_produce(const ItemRing& r, uint32_t& k, int32_t* counter, int total) {
+  const uint32_t s = k % kItemRing;
+  mbar_wait(&r.empty[s], ((k / kItemRing) & 1) ^ 1);
+  int g = atomicAdd(counter, 1);
+  if (g >= total) g = -1;
+  r.slot[s] = g;
+  mbar_arrive(&r.full[s]);
+  ++k;
+  return g;
+}
+// consumer: a whole warp (lane 0 arrives for it) or a single thread
+JH_DEV int ring_consume(const ItemRing& r, uint32_t& k, bool warp_wide) {
+  const uint32_t s = k % kItemRing;
+  mbar_wait(&r.full[s], (k / kItemRing) & 1);
+  const int g = *reinterpret_cast<volatile int32_t*>(&r.slot[s]);
+  if (warp_wide) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&r.empty[s]);
+  } else {
+    mbar_arrive(&r.empty[s]);
+  }
+  ++k;
+  return g;
 }
 
 // Static "snake" assignment of the longest-first work list to the persistent

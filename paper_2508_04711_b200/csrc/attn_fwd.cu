@@ -49,7 +49,8 @@ struct FwdCfg {
   static constexpr int BAR_OFF = KMAX_OFF + kTsRing * 32;  // mbarriers
   static constexpr int NBARS = 4 + 4 * NS + 3 * kTsRing + 8;
   static constexpr int TMEMPTR_OFF = BAR_OFF + NBARS * 8;
-  static constexpr int SMEM = TMEMPTR_OFF + 16;
+  static constexpr int RING_OFF = TMEMPTR_OFF + 16;  // work-item ring: full[], empty[], slot[]
+  static constexpr int SMEM = RING_OFF + 2 * kItemRing * 8 + kItemRing * 4;
 };
 
 template <int D>
@@ -80,6 +81,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* o_full = p_full + 3;           // [1]
   uint64_t* o_empty = o_full + 1;          // [1] drain warps hold O in registers
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::TMEMPTR_OFF);
+  const ItemRing ring{reinterpret_cast<int32_t*>(smem + C::RING_OFF + 2 * kItemRing * 8),
+                      reinterpret_cast<uint64_t*>(smem + C::RING_OFF),
+                      reinterpret_cast<uint64_t*>(smem + C::RING_OFF + kItemRing * 8)};
 
   const uint32_t warp = warp_id();
   const int tid = threadIdx.x;
@@ -113,6 +117,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&ts_empty[i], kEpiWarps / 2);  // the owning warpgroup
       mbar_init(&tsx_full[i], 1);
     }
+    ring_init(ring, 1 + 1 + kEpiWarps + 4);  // consumers: MMA, ts stats, epilogue warps, drain warps
     fence_barrier_init();
   }
   if (warp == 0 && lane_id() == 0) {
@@ -153,7 +158,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         ++pend_head;
         --n_pend;
       };
-      JH_FOR_ITEMS(g, total) {
+      uint32_t rk = 0;
+      for (int g; (g = ring_produce(ring, rk, &p.wl.hdr->next_item[0], total)) >= 0;) {
         const int2 it = p.wl.fwd[g / H];
         const int h = g % H;
         const Seg sg = load_seg(p.seg, it.x);
@@ -226,7 +232,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         ++pend_head;
         --n_pend;
       };
-      JH_FOR_ITEMS(g, total) {
+      uint32_t rk = 0;
+      for (int g; (g = ring_consume(ring, rk, false)) >= 0;) {
         const int2 it = p.wl.fwd[g / H];
         const Seg sg = load_seg(p.seg, it.x);
         const int n = (int)((fwd_kv_lim(sg, it.y) + kBN - 1) / kBN);
@@ -266,7 +273,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // (used by the epilogue's warp-uniform saturation test)
     const int lane = lane_id();
     uint32_t t_it = 0;
-    JH_FOR_ITEMS(g, total) {
+    uint32_t rk = 0;
+    for (int g; (g = ring_consume(ring, rk, true)) >= 0;) {
       const int2 it = p.wl.fwd[g / H];
       const Seg sg = load_seg(p.seg, it.x);
       const int n = (int)((fwd_kv_lim(sg, it.y) + kBN - 1) / kBN);
@@ -301,7 +309,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     uint32_t q_it = 0, s_it = 0, tcnt = 0;
     const bool tr = (tid == 128 || tid == 256);
     const int trole = tid == 128 ? 3 : 4;
-    JH_FOR_ITEMS(g, total) {
+    uint32_t rk = 0;
+    for (int g; (g = ring_consume(ring, rk, true)) >= 0;) {
       const int2 it = p.wl.fwd[g / H];
       const Seg sg = load_seg(p.seg, it.x);
       const int64_t kv_lim = fwd_kv_lim(sg, it.y);
@@ -411,7 +420,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int r = tid - 384;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     uint32_t o_it = 0;
-    JH_FOR_ITEMS(g, total) {
+    uint32_t rk = 0;
+    for (int g; (g = ring_consume(ring, rk, true)) >= 0;) {
       const int2 it = p.wl.fwd[g / H];
       const int h = g % H;
       const Seg sg = load_seg(p.seg, it.x);

@@ -31,7 +31,7 @@ struct WsLayout {
   size_t items_f, items_b, ds_base, bins, total;
 };
 
-static size_t bins_bytes() { return (size_t)sm_count() * kBinsPerCta * 4; }
+static size_t bins_bytes() { return (size_t)sm_count() * kBinsPerCta * (4 + 8); }  // fp32 bins + fp64 totals
 
 static WsLayout ws_layout(int64_t q_rows, int64_t kv_total, int64_t nseg, int32_t H, int32_t D) {
   WsLayout w;
@@ -145,6 +145,7 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
   const size_t bins_off = (a->workspace_bytes - bins_bytes()) & ~size_t(255);
   const size_t dsb_off = (bins_off - (size_t)(a->num_segments + 1) * 8) & ~size_t(255);
   p->wl.bins = bwd ? (float*)(ws + bins_off) : nullptr;
+  p->wl.partials = bwd ? (double*)(ws + bins_off + (size_t)sm_count() * kBinsPerCta * 4) : nullptr;
   p->wl.ds_base = bwd ? (int64_t*)(ws + dsb_off) : nullptr;
   if (bwd && ws + dsb_off < ws + w.items_b + 8)
     return set_error(JH_ERR_INVALID, "workspace too small");

@@ -41,3 +41,11 @@ for name, a in (("fwd", fwd), ("dkv", dkv), ("dq", dq)):
     print(f"{name}: first start {(a[:, 0].min() - t0) / 1e3:8.1f}  last start {(a[:, 0].max() - t0) / 1e3:8.1f}  "
           f"first end {(a[:, 1].min() - t0) / 1e3:8.1f}  last end {(a[:, 1].max() - t0) / 1e3:8.1f}")
 print(f"bwd build_work: {(r[3072] - t0) / 1e3:.1f} .. {(r[3073] - t0) / 1e3:.1f}")
+
+cyc = r[512:512 + 296].reshape(148, 2)
+halves = cyc[:, 0]
+busy = (dkv[:, 1] - dkv[:, 0]) / 1e3
+order = np.argsort(busy)
+print("dkv CTAs (busy us, halves): fastest", [(round(busy[i], 1), int(halves[i])) for i in order[:5]],
+      "slowest", [(round(busy[i], 1), int(halves[i])) for i in order[-5:]])
+print("halves per CTA min/mean/max", halves.min(), halves.mean(), halves.max())
