@@ -43,6 +43,7 @@ constexpr int kCompWarps = 8;
 // the tensor core already computes S^T / dP^T of half i+1.
 constexpr int kQH = 64;     // q rows per half tile
 constexpr int kQStages = 4;  // Q / dO / ts_q ring depth
+constexpr int kTbBuckets = 24;  // >= the fused kernels' num_buckets limit (23)
 static_assert(kQStages % 2 == 0, "a ring stage must always belong to the same compute warpgroup");
 
 template <int D>
@@ -63,7 +64,9 @@ struct DkvCfg {
   static constexpr int BAR_OFF = PW_OFF + (D == 64 ? 4096 : 0);
   static constexpr int NBARS = 26;
   static constexpr int RING_OFF = BAR_OFF + NBARS * 8;  // work-item ring: full[], empty[], slot[]
-  static constexpr int SMEM = RING_OFF + 2 * kItemRing * 8 + kItemRing * 4;
+  // thread-private d_ts_weights bins of the general chunks: float [kTbBuckets][256 compute threads]
+  static constexpr int TB_OFF = (RING_OFF + 2 * kItemRing * 8 + kItemRing * 4 + 15) & ~15;
+  static constexpr int SMEM = TB_OFF + kTbBuckets * 256 * 4;
 };
 
 // q half tiles [h0, nh) of segment `sg` that can see kv tile j (h0 == nh: none)
@@ -120,7 +123,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int i = tid; i < P; i += blockDim.x) s_pwc[i] = p.pos_weights[i] * c1;
   // this CTA's fp32 partial bins (buckets, then positions) in the workspace
   float* g_bins = p.wl.bins + (size_t)blockIdx.x * kBinsPerCta;
-  for (int i = tid; i < nb; i += blockDim.x) g_bins[i] = 0.f;
+  float* s_tb = reinterpret_cast<float*>(smem + C::TB_OFF);
+  for (int i = tid; i < kTbBuckets * 256; i += blockDim.x) s_tb[i] = 0.f;
   for (int i = tid; i < P; i += blockDim.x) g_bins[256 + i] = 0.f;
   __threadfence_block();
   if (tid == 0) {
@@ -301,9 +305,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int64_t* tsq = s_tsq + st * kTsSlotH + ((sg.q_row0 + (int64_t)t * kQH) & 1);
         const int64_t m0 = warp_min_i64(tsq[lane]);
         const int64_t m1 = warp_min_i64(tsq[32 + lane]);
-        if (lane == 0) {
+        const int64_t x0 = warp_max_i64(tsq[lane]);
+        const int64_t x1 = warp_max_i64(tsq[32 + lane]);
+        if (lane == 0) {  // pad layout: [min0, min1, (TMEM address in slot 0), max0, max1]
           s_tsq[st * kTsSlotH + kTsBoxH] = m0;
           s_tsq[st * kTsSlotH + kTsBoxH + 1] = m1;
+          s_tsq[st * kTsSlotH + kTsBoxH + 3] = x0;
+          s_tsq[st * kTsSlotH + kTsBoxH + 4] = x1;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&qx_full[st]);
@@ -342,6 +350,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const bool krow_ok = kpos < sg.kv_len;
       const int64_t tk = krow_ok ? p.ts_k[sg.kv_row0 + kpos] : (INT64_MIN >> 2);
       const int64_t tk_max = warp_max_i64(tk);
+      const int64_t tk_min = warp_min_i64(krow_ok ? tk : (INT64_MAX >> 2));  // over valid rows
+      const int32_t tk32 = (int32_t)(uint32_t)(uint64_t)tk;
       const int64_t k_lo = kv0 + (r & ~31), k_hi = k_lo + 31;  // this warp's kv positions
       const bool warp_k_ok = k_hi < sg.kv_len;
       // this thread's dS^T row in the scratch block of (segment, head, kv tile, half 0)
@@ -409,26 +419,52 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             const int64_t* tsq = s_tsq + st * kTsSlotH + (qrow0 & 1) + c0;  // the chunk's query timestamps
             const int rel0 = (int)(qp_half + c0 - kpos);
             const int ncol = krow_ok ? nq - c0 : 0;
+            // every delta of the chunk fits in 32 bits (warp-uniform): exact 32-bit
+            // arithmetic on the low words (differences < 2^31 in magnitude)
+            const bool fits32 = cap < 0x7FFFFFFFll &&
+                                s_tsq[st * kTsSlotH + kTsBoxH + 3 + ci] - tk_min < 0x7FFFFFFFll &&
+                                s_tsq[st * kTsSlotH + kTsBoxH + ci] - tk_max > -0x7FFFFFFFll;
+            const int32_t* tsq32 = reinterpret_cast<const int32_t*>(tsq);
 #pragma unroll 1
             for (int g8 = 0; g8 < 32; g8 += 8) {
               uint32_t v[8], pk[4];
               tmem_ld8(cbase + g8, v);
               float bc[8];
-              uint32_t bw0 = 0, bw1 = 0, om = 0;
+              uint32_t bw0 = 0, bw1 = 0, om = 0, du[8];
+              bool unsat = false;
+              if (fits32) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  du[j] = (uint32_t)min(max((int32_t)((uint32_t)tsq32[2 * (g8 + j)] - (uint32_t)tk32), 0), (int32_t)cap);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) du[j] = clamp_delta(tsq[g8 + j] - tk, cap);
+              }
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                int b;
-                oct_lookup(clamp_delta(tsq[g8 + j] - tk, cap), s_oct, b, bc[j]);
-                if (j < 4)
-                  bw0 |= (uint32_t)b << (8 * j);
-                else
-                  bw1 |= (uint32_t)b << (8 * (j - 4));
                 const bool ok = (g8 + j < ncol) && (rel0 + g8 + j >= 0);
                 om |= (ok ? 1u : 0u) << j;
+                unsat |= ok && du[j] < (uint32_t)cap;
               }
-              if (has_pos) {
+              if (!has_pos && !__any_sync(0xffffffffu, unsat)) {
+                // every visible pair of these 8 columns is in the last bucket (warp-uniform)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) bc[j] += s_pwc[min(max(rel0 + g8 + j, 0), P - 1)];
+                for (int j = 0; j < 8; ++j) bc[j] = cb;
+                bw0 = bw1 = (uint32_t)(nb - 1) * 0x01010101u;
+              } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  int b;
+                  oct_lookup(du[j], s_oct, b, bc[j]);
+                  if (j < 4)
+                    bw0 |= (uint32_t)b << (8 * j);
+                  else
+                    bw1 |= (uint32_t)b << (8 * (j - 4));
+                }
+                if (has_pos) {
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) bc[j] += s_pwc[min(max(rel0 + g8 + j, 0), P - 1)];
+                }
               }
               okm[ci] |= om << g8;
               bl[ci][g8 >> 2] = bw0;
@@ -496,12 +532,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
               for (int q4 = 0; q4 < 4; ++q4) ds_out[4 * ci + q4] = make_int4(0, 0, 0, 0);
           } else {
-            // general chunk: exact bucket scatter.  Runs of equal buckets along the row
-            // accumulate in a register and are flushed with predicated fire-and-forget
-            // fp32 reductions into this CTA's bins
+            // general chunk: exact bucket scatter.  The last bucket accumulates in a
+            // register; the other buckets present in each 8 columns (warp-wide mask)
+            // are summed one warp-uniform pass per bucket into thread-private bins
             const int rel0 = (int)(qp_half + c0 - kpos);
-            uint32_t rb = (uint32_t)(nb - 1);
-            float rs = 0.f;
+            float* my_tb = s_tb + et;
 #pragma unroll 1
             for (int g8 = 0; g8 < 32; g8 += 8) {
               uint32_t dv[8], dk[4];
@@ -521,14 +556,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               }
               tmem_st4(cbase + 16 + (g8 >> 1), dk);
               if (ds_ok) ds_out[4 * ci + (g8 >> 3)] = make_int4(dk[0], dk[1], dk[2], dk[3]);
+              uint32_t bj[8], msk = 0;
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 const bool ok = (okm[ci] >> (g8 + j)) & 1u;
-                const uint32_t b = ((j < 4 ? bw0 : bw1) >> (8 * (j & 3))) & 0xFFu;
-                const bool ch = ok && b != rb;
-                red_add_f32_if(g_bins + rb, rs, ch && rs != 0.f);
-                rb = ch ? b : rb;
-                rs = ch ? dd[j] : rs + dd[j];  // dd = 0 on masked elements
+                bj[j] = ok ? (((j < 4 ? bw0 : bw1) >> (8 * (j & 3))) & 0xFFu) : 31u;
+                msk |= 1u << bj[j];
+                sat_w += bj[j] == (uint32_t)(nb - 1) ? dd[j] : 0.f;
+              }
+              msk &= ~((1u << (nb - 1)) | 0x80000000u);
+              for (uint32_t m = __reduce_or_sync(0xffffffffu, msk); m; m &= m - 1) {
+                const uint32_t k = __ffs(m) - 1;
+                float sk = 0.f;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) sk += bj[j] == k ? dd[j] : 0.f;
+                my_tb[k * 256] += sk;
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const bool ok = (okm[ci] >> (g8 + j)) & 1u;
                 if (has_pos) {
                   const int rel = min(rel0 + g8 + j, P - 1);
                   red_add_f32_if(g_bins + 256 + max(rel, 0), dd[j], ok && rel != P - 1);
@@ -536,7 +582,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 }
               }
             }
-            red_add_f32_if(g_bins + rb, rs, rs != 0.f);
           }
         }
         acc_w += (double)sat_w;
@@ -566,6 +611,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     named_bar_sync(1, 32 * kCompWarps);
     if (et == 0 && p.trace != nullptr && p.trace_cta == -1) p.trace[512 + 2 * blockIdx.x] = hc;  // halves done
+    // general-chunk bins: warp w sums buckets w, w+8, ... over the 256 thread slots
+    for (int b = (et >> 5); b < nb; b += kCompWarps) {
+      float v = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v += s_tb[b * 256 + lane + 32 * i];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) g_bins[b] = v;
+    }
     if (et < 2) {
       double v = 0.0;
       for (int w2 = 0; w2 < kCompWarps; ++w2) v += s_red[et * kCompWarps + w2];
