@@ -45,8 +45,8 @@ struct FwdCfg {
   static constexpr int TSK_OFF = TSQ_OFF + 2 * kTsSlot * 8;   // int64 [kTsRing][kTsSlot]
   static constexpr int OCT_OFF = TSK_OFF + kTsRing * kTsSlot * 8;  // OctEntry [32]
   static constexpr int PW_OFF = OCT_OFF + 32 * 16;          // float pw[<=1024] x c1
-  static constexpr int KMAX_OFF = PW_OFF + 1024 * 4;        // int64 [kTsRing][4] per-chunk max ts_k
-  static constexpr int BAR_OFF = KMAX_OFF + kTsRing * 32;  // mbarriers
+  static constexpr int KMAX_OFF = PW_OFF + 1024 * 4;        // int64 [kTsRing][4] per-chunk max ts_k, then min
+  static constexpr int BAR_OFF = KMAX_OFF + 2 * kTsRing * 32;  // mbarriers
   static constexpr int NBARS = 4 + 4 * NS + 3 * kTsRing + 8;
   static constexpr int TMEMPTR_OFF = BAR_OFF + NBARS * 8;
   static constexpr int RING_OFF = TMEMPTR_OFF + 16;  // work-item ring: full[], empty[], slot[]
@@ -285,7 +285,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int64_t m = warp_max_i64(tsk[32 * c + lane]);
-          if (lane == 0) s_kmax[ts * 4 + c] = m;
+          const int64_t mn = warp_min_i64(tsk[32 * c + lane]);
+          if (lane == 0) {
+            s_kmax[ts * 4 + c] = m;
+            s_kmax[kTsRing * 4 + ts * 4 + c] = mn;
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&tsx_full[ts]);
@@ -328,6 +332,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (lane == 0) mbar_arrive(&q_empty[qb]);
       ++q_it;
       const int64_t tq_min = warp_min_i64(tq);
+      const int64_t tq_max = warp_max_i64(row_ok ? tq : (INT64_MIN >> 2));  // over valid rows
+      const int32_t tq32 = (int32_t)(uint32_t)(uint64_t)tq;
       const int64_t row_lo = qp_tile + (r & ~31), row_hi = row_lo + 31;  // warp's q positions
       for (int j = 0; j < n; ++j, ++s_it) {
         if ((int)(s_it & 1) != wg) continue;
@@ -372,20 +378,43 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             // bucket, positional bias and mask, 8 columns per step
             const int relc = (int)(qpos - kv0 - c0);                        // qpos - kpos of column 0
             const int ncol = (int)min(kv_lim - kv0 - c0, (int64_t)32);      // in-range columns
+            // all deltas of the chunk fit in 32 bits (warp-uniform): exact low-word arithmetic
+            const bool fits32 = cap < 0x7FFFFFFFll && tq_max - s_kmax[kTsRing * 4 + ts * 4 + (c0 >> 5)] < 0x7FFFFFFFll &&
+                                tq_min - s_kmax[ts * 4 + (c0 >> 5)] > -0x7FFFFFFFll;
+            const int32_t* tsk32 = reinterpret_cast<const int32_t*>(tsk + c0);
             uint32_t vn[8];
             tmem_ld8(tS + c0, vn);  // the next 8 columns' load stays in flight during each step
 #pragma unroll 1
             for (int g8 = 0; g8 < 32; g8 += 8) {
-              uint32_t v[8], pk[4];
+              uint32_t v[8], pk[4], du[8];
               float bc[8];
+              if (fits32) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                  du[i] = (uint32_t)min(max((int32_t)((uint32_t)tq32 - (uint32_t)tsk32[2 * (g8 + i)]), 0), (int32_t)cap);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) du[i] = clamp_delta(tq - tsk[c0 + g8 + i], cap);
+              }
+              bool unsat = false;
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                int b;
-                oct_lookup(clamp_delta(tq - tsk[c0 + g8 + i], cap), s_oct, b, bc[i]);
+                const int k = g8 + i;
+                unsat |= (k <= relc && k < ncol) && du[i] < (uint32_t)cap;
               }
-              if (has_pos) {
+              if (!has_pos && !__any_sync(0xffffffffu, unsat)) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) bc[i] += s_pwc[min(max(relc - g8 - i, 0), P - 1)];
+                for (int i = 0; i < 8; ++i) bc[i] = cb;  // every visible pair saturated (warp-uniform)
+              } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  int b;
+                  oct_lookup(du[i], s_oct, b, bc[i]);
+                }
+                if (has_pos) {
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) bc[i] += s_pwc[min(max(relc - g8 - i, 0), P - 1)];
+                }
               }
               tmem_ld_wait();
 #pragma unroll
