@@ -303,10 +303,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int st = hc % kQStages;
         mbar_wait(&qd_full[st], (hc / kQStages) & 1);
         const int64_t* tsq = s_tsq + st * kTsSlotH + ((sg.q_row0 + (int64_t)t * kQH) & 1);
-        const int64_t m0 = warp_min_i64(tsq[lane]);
-        const int64_t m1 = warp_min_i64(tsq[32 + lane]);
-        const int64_t x0 = warp_max_i64(tsq[lane]);
-        const int64_t x1 = warp_max_i64(tsq[32 + lane]);
+        const int64_t nqh = sg.lq - (int64_t)t * kQH;  // valid columns of the half (statistics skip the rest)
+        const bool v0 = lane < nqh, v1 = 32 + lane < nqh;
+        const int64_t m0 = warp_min_i64(v0 ? tsq[lane] : (INT64_MAX >> 2));
+        const int64_t m1 = warp_min_i64(v1 ? tsq[32 + lane] : (INT64_MAX >> 2));
+        const int64_t x0 = warp_max_i64(v0 ? tsq[lane] : (INT64_MIN >> 2));
+        const int64_t x1 = warp_max_i64(v1 ? tsq[32 + lane] : (INT64_MIN >> 2));
         if (lane == 0) {  // pad layout: [min0, min1, (TMEM address in slot 0), max0, max1]
           s_tsq[st * kTsSlotH + kTsBoxH] = m0;
           s_tsq[st * kTsSlotH + kTsBoxH + 1] = m1;
@@ -375,9 +377,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           cls[ci] = 0;
           if (!(qc0 + 31 < k_lo || 32 * ci >= nq)) {
             cls[ci] = 2;
-            if ((qc0 >= k_hi) && (32 * ci + 32 <= nq) && warp_k_ok &&
-                (s_tsq[st * kTsSlotH + kTsBoxH + ci] - tk_max >= cap) && (!has_pos || qc0 - k_hi >= P - 1))
-              cls[ci] = 1;
+            if ((qc0 >= k_hi) && (s_tsq[st * kTsSlotH + kTsBoxH + ci] - tk_max >= cap) &&
+                (!has_pos || qc0 - k_hi >= P - 1))
+              cls[ci] = ((32 * ci + 32 <= nq) && warp_k_ok) ? 1 : 3;  // 3: saturated, ragged edge
           }
         }
         // SiLU'(S) (f16 pairs) stays in registers from phase P to phase dS (saturated
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int ci = 0; ci < 2; ++ci) {
           const int c0 = 32 * ci;
           const uint32_t cbase = tmem + 64 * x + c0 + lane_off;  // S^T chunk -> P^T [cbase, +16)
-          if (cls[ci] == 1) {
+          if (cls[ci] == 1 || cls[ci] == 3) {
             uint32_t v[32], pk[16];
             tmem_ld32(cbase, v);
             tmem_ld_wait();
@@ -407,6 +409,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               __half2 hk = __floats2half2_rn((1.f + t0) * (fmaf(-h0f, t0, h0f) + 1.f),
                                              (1.f + t1) * (fmaf(-h1f, t1, h1f) + 1.f));
               kp[ci][i >> 1] = *reinterpret_cast<uint32_t*>(&hk);
+            }
+            if (cls[ci] == 3) {
+              // ragged edge: zero the pairs outside the segment (columns >= nq, rows >= kv_len)
+              const int nv = krow_ok ? min(max(nq - c0, 0), 32) : 0;
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const uint32_t m = (2 * i < nv ? 0x0000FFFFu : 0u) | (2 * i + 1 < nv ? 0xFFFF0000u : 0u);
+                pk[i] &= m;
+                kp[ci][i] &= m;
+              }
             }
             tmem_st16(cbase, pk);
           } else if (cls[ci] == 0) {
@@ -503,7 +515,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const int c0 = 32 * ci;
           const uint32_t cbase = tmem + 64 * x + c0 + lane_off;  // dS^T -> [cbase + 16, +16)
           const uint32_t dpbase = tDP + 64 * x + c0 + lane_off;
-          if (cls[ci] == 1) {
+          if (cls[ci] == 1 || cls[ci] == 3) {
             uint32_t dv[32], dk[16];
             tmem_ld32(dpbase, dv);
             tmem_ld_wait();
