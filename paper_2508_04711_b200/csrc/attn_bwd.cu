@@ -85,6 +85,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                         const __grid_constant__ CUtensorMap tm_tsq, const __grid_constant__ AttnParams p) {
   using C = DkvCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
+  // the dQ kernel may start on SMs this kernel frees (it waits on the dependency counters)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   int64_t* s_tsq = reinterpret_cast<int64_t*>(smem + C::TSQ_OFF);
   OctEntry* s_oct = reinterpret_cast<OctEntry*>(smem + C::OCT_OFF);
   float* s_pwc = reinterpret_cast<float*>(smem + C::PW_OFF);  // pos weights x c1
@@ -341,12 +343,30 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const bool ds_ok = p.wl.hdr->ds_blocks * H <= p.ds_cap_blocks && !(p.dbg & 1);
     if (!ds_ok && et == 0) p.wl.hdr->ds_overflow = 1;
     uint32_t rk = 0;
+    int32_t* dep_item = nullptr;  // completion counter of the previous item (bumped one item late)
     for (int g; (g = ring_consume(ring, rk, true)) >= 0;) {
       const int2 it = p.wl.bwd[g / H];
+      const int h = g % H;
       const Seg sg = load_seg(p.seg, it.x);
       int h0, nh;
       dkv_halves(sg, it.y, h0, nh);
+      // publish the previous item's dS blocks to the dQ kernel
+      if (dep_item != nullptr) {
+        __threadfence();
+        named_bar_sync(2, 32 * kCompWarps);
+        if (et == 0) atomicAdd(dep_item, 1);
+      }
+      dep_item = p.wl.dep + kDepBase + (int64_t)it.x * H + h;
       if (h0 >= nh) continue;
+      if (wg == 0 && (h0 & 1) && ds_ok) {
+        // the dQ kernel reads q halves in pairs: the partner of the first visible
+        // half sees nothing of this kv tile, its dS^T block is zero
+        int4* z = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(p.ds) +
+                                          (p.wl.ds_base[it.x] * H + (int64_t)(h * ds_nkt(sg) + it.y) * nh + h0 - 1) *
+                                              kDsBlockBytes + r * 128);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) z[i] = make_int4(0, 0, 0, 0);
+      }
       const int64_t kv0 = (int64_t)it.y * kBN;
       const int64_t kpos = kv0 + r;
       const bool krow_ok = kpos < sg.kv_len;
@@ -357,7 +377,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int64_t k_lo = kv0 + (r & ~31), k_hi = k_lo + 31;  // this warp's kv positions
       const bool warp_k_ok = k_hi < sg.kv_len;
       // this thread's dS^T row in the scratch block of (segment, head, kv tile, half 0)
-      const int h = g % H;
       uint8_t* ds_row = reinterpret_cast<uint8_t*>(p.ds) +
                         ((p.wl.ds_base[it.x] * H + (int64_t)(h * ds_nkt(sg) + it.y) * nh) * kDsBlockBytes) + r * 128;
       for (int t = h0; t < nh; ++t, ++hc) {
@@ -606,6 +625,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (lane == 0) mbar_arrive(&qd_empty[st]);  // done with this stage's ts_q
       }
     }
+    if (dep_item != nullptr) {
+      __threadfence();
+      named_bar_sync(2, 32 * kCompWarps);
+      if (et == 0) atomicAdd(dep_item, 1);
+    }
     // ---- d_ts_weights / d_pos: last buckets as fp64 partials, the rest from smem bins
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -637,6 +661,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int w2 = 0; w2 < kCompWarps; ++w2) v += s_red[et * kCompWarps + w2];
       p.wl.partials[(size_t)blockIdx.x * 2 + et] = v;
     }
+    __threadfence();
+    named_bar_sync(1, 32 * kCompWarps);
+    if (et == 0) atomicAdd(p.wl.dep, 1);  // this CTA's bins and partials are final
   } else if (warp >= 12) {
     // ================= dK / dV drain (thread = kv row)
     const int r = tid - 384;
@@ -652,15 +679,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int64_t kpos = (int64_t)it.y * kBN + r;
       const bool krow_ok = kpos < sg.kv_len;
       const int64_t krow = sg.kv_row0 + kpos;
-      if ((h0 & 1) && h0 < nh && p.wl.hdr->ds_blocks * H <= p.ds_cap_blocks) {
-        // the dQ kernel reads q halves in pairs: the partner of the first visible
-        // half sees nothing of this kv tile, its dS^T block is zero
-        int4* z = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(p.ds) +
-                                          (p.wl.ds_base[it.x] * H + (int64_t)(h * ds_nkt(sg) + it.y) * nh + h0 - 1) *
-                                              kDsBlockBytes + r * 128);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) z[i] = make_int4(0, 0, 0, 0);
-      }
       if (h0 >= nh) {
         // no query sees this kv tile: its dK/dV rows are zero
         if (krow_ok && !p.dk_accum)
@@ -792,6 +810,12 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         const Seg sg = load_seg(p.seg, it.x);
         const int n = kv_tiles(sg, it.y);
         const int nh = ds_nh(sg), nkt = ds_nkt(sg);
+        if (n > 0) {
+          // wait until the dK/dV kernel finished every kv tile of (segment, head)
+          const int32_t* cnt = p.wl.dep + kDepBase + (int64_t)it.x * H + h;
+          while (ld_acquire_gpu(cnt) < nkt) __nanosleep(256);
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy writes -> TMA reads
+        }
         for (int j = 0; j < n; ++j, ++kc) {
           const int st = kc % kDqStages;
           mbar_wait(&empty[st], ((kc / kDqStages) & 1) ^ 1);
@@ -842,6 +866,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     // (entry e handled by one thread of one CTA: a plain, ordered accumulate)
     const int nb = p.bias.nb, P = p.num_pos;
     const int n_e = 256 + P;
+    if (lane_id() == 0)
+      while (ld_acquire_gpu(p.wl.dep) < (int)gridDim.x) __nanosleep(512);  // all dK/dV CTAs final
+    __syncwarp();
     for (int e = blockIdx.x * 32 + lane_id(); e < n_e; e += gridDim.x * 32) {
       if (e >= nb && e < 256) continue;
       double v = 0.0;
@@ -857,7 +884,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     // ================= dQ drain (thread = q row)
     const int r = tid - 128;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const bool bad = p.wl.hdr->ds_overflow != 0;  // dS scratch overflow: poison dq
+    const bool bad = p.wl.hdr->ds_blocks * H > p.ds_cap_blocks;  // dS scratch overflow: poison dq
     uint32_t o_it = 0;
     uint32_t rk = 0;
     for (int g; (g = ring_consume(ring, rk, true)) >= 0;) {
@@ -927,7 +954,23 @@ int launch_bwd(const TMaps& tm, const AttnParams& p, const jh_attn_args& a, int 
   if (a.prof_event_start) cudaEventRecord((cudaEvent_t)a.prof_event_start, s);
   hstu_bwd_dkv_kernel<D><<<grid, kBwdThreads, C::SMEM, s>>>(tm.q64, tm.k, tm.v, tm.do64, tm.tsq72, p);
   if (cudaError_t e = cudaGetLastError()) return (int)e;
-  hstu_bwd_dq_kernel<D><<<grid, kDqThreads, Q::SMEM, s>>>(tm.ds, tm.k, p, (__nv_bfloat16*)a.dq, a.ld_dq);
+  {
+    // programmatic dependent launch: dQ CTAs start on SMs the dK/dV kernel frees and
+    // wait on its per-(segment, head) completion counters (no kernel-boundary bubble)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kDqThreads);
+    cfg.dynamicSmemBytes = Q::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    __nv_bfloat16* dqp = (__nv_bfloat16*)a.dq;
+    int64_t ldq = a.ld_dq;
+    if (cudaError_t e = cudaLaunchKernelEx(&cfg, hstu_bwd_dq_kernel<D>, tm.ds, tm.k, p, dqp, ldq)) return (int)e;
+  }
   if (a.prof_event_end) cudaEventRecord((cudaEvent_t)a.prof_event_end, s);
   return (int)cudaGetLastError();
 }

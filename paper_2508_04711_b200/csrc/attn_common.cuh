@@ -72,7 +72,12 @@ struct WorkLists {
   int64_t* ds_base;
   float* bins;        // per-CTA fp32 bins (dK/dV kernel, reductions)
   double* partials;   // per-CTA fp64 totals [grid][kBinsPerCta], summed by the dQ kernel
+  // dK/dV -> dQ dependency counters (the dQ kernel starts while dK/dV finishes):
+  // dep[0] = finished dK/dV CTAs, dep[kDepBase + s*H + h] = finished kv tiles of (s, h)
+  int32_t* dep;
+  int32_t dep_heads;
 };
+constexpr int kDepBase = 16;
 
 // Backward dS scratch: per (segment, head) a dense grid of blocks, one per
 // (128-row kv tile j, 64-row q half t), each the bf16 dS^T tile [128 kv][64 q]
@@ -192,6 +197,8 @@ static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, 
       if (s < sa.num_segments) wl.ds_base[s] = carry + ex;
       carry += tot;
     }
+    if (wl.dep != nullptr)
+      for (int64_t i = tid; i < kDepBase + sa.num_segments * wl.dep_heads; i += blockDim.x) wl.dep[i] = 0;
     if (tid == 0) {
       wl.ds_base[sa.num_segments] = carry;
       wl.hdr->ds_blocks = carry;

@@ -40,7 +40,8 @@ static WsLayout ws_layout(int64_t q_rows, int64_t kv_total, int64_t nseg, int32_
   w.items_f = sizeof(WorkHeader);
   w.items_b = w.items_f + ((size_t)max_f * 8 + 255) / 256 * 256;
   w.ds_base = w.items_b + ((size_t)max_b * 8 + 255) / 256 * 256;
-  w.bins = w.ds_base + ((size_t)(nseg + 1) * 8 + 255) / 256 * 256;
+  w.bins = w.ds_base + ((size_t)(nseg + 1) * 8 + 255) / 256 * 256 +
+           ((size_t)(kDepBase + nseg * H) * 4 + 255) / 256 * 256;
   w.total = w.bins + bins_bytes();
   return w;
 }
@@ -144,10 +145,13 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
   // dS block bases and the per-CTA bins are carved from the end of the workspace)
   const size_t bins_off = (a->workspace_bytes - bins_bytes()) & ~size_t(255);
   const size_t dsb_off = (bins_off - (size_t)(a->num_segments + 1) * 8) & ~size_t(255);
+  const size_t dep_off = (dsb_off - (size_t)(kDepBase + a->num_segments * a->num_heads) * 4) & ~size_t(255);
+  p->wl.dep = bwd ? (int32_t*)(ws + dep_off) : nullptr;
+  p->wl.dep_heads = a->num_heads;
   p->wl.bins = bwd ? (float*)(ws + bins_off) : nullptr;
   p->wl.partials = bwd ? (double*)(ws + bins_off + (size_t)sm_count() * kBinsPerCta * 4) : nullptr;
   p->wl.ds_base = bwd ? (int64_t*)(ws + dsb_off) : nullptr;
-  if (bwd && ws + dsb_off < ws + w.items_b + 8)
+  if (bwd && ws + dep_off < ws + w.items_b + 8)
     return set_error(JH_ERR_INVALID, "workspace too small");
   const uint64_t HD = (uint64_t)a->num_heads * a->head_dim;
   if ((uintptr_t)a->ts_q % 16 || (uintptr_t)a->ts_k % 16)

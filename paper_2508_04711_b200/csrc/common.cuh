@@ -233,6 +233,12 @@ JH_DEV void red_add_f32_if(float* addr, float v, bool pred) {
                "r"((int)pred));
 }
 
+JH_DEV int32_t ld_acquire_gpu(const int32_t* ptr) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
+
 JH_DEV float tanh_approx(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
