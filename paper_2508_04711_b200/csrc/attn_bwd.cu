@@ -163,6 +163,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // TMEM: S^T [64x, 64x+64) and dP^T [128+64x, ...) for buffer x, dV, dK
   const uint32_t tDP = tmem + 128, tDV = tmem + 256, tDK = tmem + 256 + D;
 
+  // (programmatic dependent launch: everything above overlapped the work-list build)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int total = p.wl.hdr->n_bwd * H;
 
   if (warp == 0) {
@@ -952,8 +954,20 @@ int launch_bwd(const TMaps& tm, const AttnParams& p, const jh_attn_args& a, int 
     attr = true;
   }
   if (a.prof_event_start) cudaEventRecord((cudaEvent_t)a.prof_event_start, s);
-  hstu_bwd_dkv_kernel<D><<<grid, kBwdThreads, C::SMEM, s>>>(tm.q64, tm.k, tm.v, tm.do64, tm.tsq72, p);
-  if (cudaError_t e = cudaGetLastError()) return (int)e;
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kBwdThreads);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;  // prologue overlaps the work-list build
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaError_t e = cudaLaunchKernelEx(&cfg, hstu_bwd_dkv_kernel<D>, tm.q64, tm.k, tm.v, tm.do64, tm.tsq72, p))
+      return (int)e;
+  }
   {
     // programmatic dependent launch: dQ CTAs start on SMs the dK/dV kernel frees and
     // wait on its per-(segment, head) completion counters (no kernel-boundary bubble)

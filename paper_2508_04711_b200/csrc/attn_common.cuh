@@ -124,6 +124,7 @@ JH_DEV T block_exclusive_scan(T v, T* warp_sum, T* total) {
 // decoded once and kept in registers across the passes.
 static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, WorkLists wl,
                                                                    unsigned long long* stamp = nullptr) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the attention kernel's prologue may start
   if (stamp != nullptr && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -133,6 +133,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
+  // (programmatic dependent launch: everything above overlapped the work-list build)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int n_items = p.wl.hdr->n_fwd;
   const int total = n_items * H;
 
@@ -503,7 +505,17 @@ int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& 
     attr = true;
   }
   if (ev0) cudaEventRecord((cudaEvent_t)ev0, s);
-  hstu_fwd_kernel<D><<<grid, kFwdThreads, C::SMEM, s>>>(tq, tk, tv, ttq, ttk, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kFwdThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = 1;  // prologue overlaps the work-list build
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  if (cudaError_t e = cudaLaunchKernelEx(&cfg, hstu_fwd_kernel<D>, tq, tk, tv, ttq, ttk, p)) return (int)e;
   if (ev1) cudaEventRecord((cudaEvent_t)ev1, s);
   return (int)cudaGetLastError();
 }
