@@ -90,6 +90,7 @@ class Clocks:
                 self.rows.append((float(sm), float(mx), ["Active" if rs & b else "Not Active" for b in bits]))
             except Exception:
                 pass
+            self.ready.set()
             time.sleep(0.001)
 
     def __enter__(self):
@@ -99,8 +100,10 @@ class Clocks:
             import pynvml as nv
             nv.nvmlInit()
             handle = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.ready = threading.Event()
             self.thread = threading.Thread(target=self._nvml_loop, args=(nv, handle), daemon=True)
             self.thread.start()
+            self.ready.wait(2.0)  # the timed region is a few ms: be sampling before it starts
         except Exception:
             self.thread = None
             try:

@@ -12,8 +12,8 @@
 //       warp 1      MMA: S^T = K Q^T, dP^T = V dO^T (128 x 64, two TMEM buffers),
 //                   dV += P^T dO, dK += dS^T Q (A = P^T / dS^T in TMEM)
 //       warp 3      per-chunk min of ts_q (saturation test)
-//       warps 4-11  compute, two warpgroups in ping-pong over the halves (group
-//                   hc % 2 owns TMEM buffer hc % 2), thread = (kv row, half):
+//       warps 4-11  compute, two warpgroups: group g owns q-column chunk g of
+//                   every half, thread = (kv row, 32-column chunk):
 //                   phase P  : S^T -> P^T (TMEM) and SiLU'(S) (f16, TMEM)
 //                   phase dS : dP^T -> dS^T = dP SiLU'(S)/sqrt(d) (TMEM), d_ts_weights
 //       warps 12-15 drain dK / dV (bf16 store, or fp32 accumulate for CP)
@@ -44,7 +44,6 @@ constexpr int kCompWarps = 8;
 constexpr int kQH = 64;     // q rows per half tile
 constexpr int kQStages = 4;  // Q / dO / ts_q ring depth
 constexpr int kTbBuckets = 24;  // >= the fused kernels' num_buckets limit (23)
-static_assert(kQStages % 2 == 0, "a ring stage must always belong to the same compute warpgroup");
 
 template <int D>
 struct DkvCfg {
@@ -134,14 +133,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(kv_empty, 1);
     for (int i = 0; i < kQStages; ++i) {
       mbar_init(&qd_full[i], 1);
-      mbar_init(&qd_empty[i], 1 + kCompWarps / 2);  // MMA + the owning warpgroup
+      mbar_init(&qd_empty[i], 1 + kCompWarps);  // MMA + every compute warp
       mbar_init(&qx_full[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&dp_full[i], 1);
-      mbar_init(&p_full[i], 16 * kCompWarps);  // one warpgroup
-      mbar_init(&ds_full[i], 16 * kCompWarps);
+      mbar_init(&p_full[i], kCompWarps);  // one arrival per compute warp
+      mbar_init(&ds_full[i], kCompWarps);
     }
     mbar_init(dkv_full, 1);
     mbar_init(dkv_empty, 128);
@@ -324,10 +323,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
   } else if (warp >= 4 && warp < 12) {
-    // ================= compute: two warpgroups in ping-pong -- warpgroup wg owns the
-    // halves with hc % 2 == wg (TMEM buffer wg); thread = (kv row r, both 32-q-column
-    // chunks of the half), so one group's TMEM / barrier latency hides behind the
-    // other group's math
+    // ================= compute: warpgroup wg owns q-column chunk wg (columns
+    // [32 wg, 32 wg + 32)) of every half; thread = (kv row r, that chunk).  Splitting
+    // by chunk rather than by half (ping-pong) spreads a diagonal block's general
+    // chunks over both groups: no warp runs more than one of them per half pair
     const int et = tid - 128;
     const int wg = et >> 7;
     const int r = et & 127;
@@ -382,7 +381,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       uint8_t* ds_row = reinterpret_cast<uint8_t*>(p.ds) +
                         ((p.wl.ds_base[it.x] * H + (int64_t)(h * ds_nkt(sg) + it.y) * nh) * kDsBlockBytes) + r * 128;
       for (int t = h0; t < nh; ++t, ++hc) {
-        if ((int)(hc & 1) != wg) continue;
         int4* ds_out = reinterpret_cast<int4*>(ds_row + (int64_t)t * kDsBlockBytes);
         const int st = hc % kQStages;
         const uint32_t x = hc & 1, xp = (hc >> 1) & 1;
@@ -391,33 +389,32 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int nq = (int)min((int64_t)kQH, sg.lq - (int64_t)t * kQH);
         mbar_wait(&qx_full[st], (hc / kQStages) & 1);
         // chunk classes: 0 masked, 1 unmasked with saturated bias, 2 general
-        int cls[2];
-#pragma unroll
-        for (int ci = 0; ci < 2; ++ci) {
+        int cls0 = 0;
+        {
+          const int ci = wg;
           const int64_t qc0 = qp_half + 32 * ci;
-          cls[ci] = 0;
           if (!(qc0 + 31 < k_lo || 32 * ci >= nq)) {
-            cls[ci] = 2;
+            cls0 = 2;
             if ((qc0 >= k_hi) && (s_tsq[st * kTsSlotH + kTsBoxH + ci] - tk_max >= cap) &&
                 (!has_pos || qc0 - k_hi >= P - 1))
-              cls[ci] = ((32 * ci + 32 <= nq) && warp_k_ok) ? 1 : 3;  // 3: saturated, ragged edge
+              cls0 = ((32 * ci + 32 <= nq) && warp_k_ok) ? 1 : 3;  // 3: saturated, ragged edge
           }
         }
         // SiLU'(S) (f16 pairs) stays in registers from phase P to phase dS (saturated
         // chunks) or in a small per-thread local buffer (general chunks: rolled loops
         // keep that rarely-run code small), with the buckets and the mask
-        uint32_t kp[2][16];
-        uint32_t kl[2][16], bl[2][8];
-        uint32_t okm[2] = {0u, 0u};
+        uint32_t kp0[16];
+        uint32_t kl0[16], bl0[8];
+        uint32_t okm0 = 0u;
         // ---------------- phase P: S^T -> P^T, SiLU'
         mbar_wait(&s_full[x], xp);
         if (tr) trace_ev(p, trole, tcnt, 21, t);
         tc_fence_after();
-#pragma unroll
-        for (int ci = 0; ci < 2; ++ci) {
+        {
+          const int ci = wg;
           const int c0 = 32 * ci;
           const uint32_t cbase = tmem + 64 * x + c0 + lane_off;  // S^T chunk -> P^T [cbase, +16)
-          if (cls[ci] == 1 || cls[ci] == 3) {
+          if (cls0 == 1 || cls0 == 3) {
             uint32_t v[32], pk[16];
             tmem_ld32(cbase, v);
             tmem_ld_wait();
@@ -429,20 +426,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               pk[i >> 1] = pack_bf16(fmaf(h0f, t0, h0f), fmaf(h1f, t1, h1f));
               __half2 hk = __floats2half2_rn((1.f + t0) * (fmaf(-h0f, t0, h0f) + 1.f),
                                              (1.f + t1) * (fmaf(-h1f, t1, h1f) + 1.f));
-              kp[ci][i >> 1] = *reinterpret_cast<uint32_t*>(&hk);
+              kp0[i >> 1] = *reinterpret_cast<uint32_t*>(&hk);
             }
-            if (cls[ci] == 3) {
+            if (cls0 == 3) {
               // ragged edge: zero the pairs outside the segment (columns >= nq, rows >= kv_len)
               const int nv = krow_ok ? min(max(nq - c0, 0), 32) : 0;
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
                 const uint32_t m = (2 * i < nv ? 0x0000FFFFu : 0u) | (2 * i + 1 < nv ? 0xFFFF0000u : 0u);
                 pk[i] &= m;
-                kp[ci][i] &= m;
+                kp0[i] &= m;
               }
             }
             tmem_st16(cbase, pk);
-          } else if (cls[ci] == 0) {
+          } else if (cls0 == 0) {
             uint32_t z[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) z[i] = 0u;
@@ -479,7 +476,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 om |= (ok ? 1u : 0u) << j;
                 unsat |= ok && du[j] < (uint32_t)cap;
               }
-              if (!has_pos && !__any_sync(0xffffffffu, unsat)) {
+              if ((p.dbg & 2) || (!has_pos && !__any_sync(0xffffffffu, unsat))) {
                 // every visible pair of these 8 columns is in the last bucket (warp-uniform)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) bc[j] = cb;
@@ -499,9 +496,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                   for (int j = 0; j < 8; ++j) bc[j] += s_pwc[min(max(rel0 + g8 + j, 0), P - 1)];
                 }
               }
-              okm[ci] |= om << g8;
-              bl[ci][g8 >> 2] = bw0;
-              bl[ci][(g8 >> 2) + 1] = bw1;
+              okm0 |= om << g8;
+              bl0[g8 >> 2] = bw0;
+              bl0[(g8 >> 2) + 1] = bw1;
               tmem_ld_wait();
 #pragma unroll
               for (int j = 0; j < 8; j += 2) {
@@ -510,13 +507,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 for (int u = 0; u < 2; ++u) {
                   const bool ok = (om >> (j + u)) & 1u;
                   const float hh = fmaf(__uint_as_float(v[j + u]), c1, bc[j + u]);
-                  const float th = tanh_approx(hh);
+                  const float th = (p.dbg & 4) ? hh : tanh_approx(hh);
                   pp[u] = ok ? fmaf(hh, th, hh) : 0.f;
                   dd[u] = ok ? (1.f + th) * (fmaf(-hh, th, hh) + 1.f) : 0.f;
                 }
                 pk[j >> 1] = pack_bf16(pp[0], pp[1]);
                 __half2 hk = __floats2half2_rn(dd[0], dd[1]);
-                kl[ci][(g8 + j) >> 1] = *reinterpret_cast<uint32_t*>(&hk);
+                kl0[(g8 + j) >> 1] = *reinterpret_cast<uint32_t*>(&hk);
               }
               tmem_st4(cbase + (g8 >> 1), pk);
             }
@@ -524,26 +521,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&p_full[x]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[x]);
         if (tr) trace_ev(p, trole, tcnt, 22, t);
         // ---------------- phase dS: dP^T, SiLU' -> dS^T (TMEM), d_ts_weights
         mbar_wait(&dp_full[x], xp);
         if (tr) trace_ev(p, trole, tcnt, 24, t);
         tc_fence_after();
         float sat_w = 0.f, sat_p = 0.f;
-#pragma unroll
-        for (int ci = 0; ci < 2; ++ci) {
+        {
+          const int ci = wg;
           const int c0 = 32 * ci;
           const uint32_t cbase = tmem + 64 * x + c0 + lane_off;  // dS^T -> [cbase + 16, +16)
           const uint32_t dpbase = tDP + 64 * x + c0 + lane_off;
-          if (cls[ci] == 1 || cls[ci] == 3) {
+          if (cls0 == 1 || cls0 == 3) {
             uint32_t dv[32], dk[16];
             tmem_ld32(dpbase, dv);
             tmem_ld_wait();
             float csum = 0.f;
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
-              const float2 kd = __half22float2(*reinterpret_cast<const __half2*>(&kp[ci][i >> 1]));
+              const float2 kd = __half22float2(*reinterpret_cast<const __half2*>(&kp0[i >> 1]));
               const float d0 = __uint_as_float(dv[i]) * kd.x * c1;
               const float d1 = __uint_as_float(dv[i + 1]) * kd.y * c1;
               dk[i >> 1] = pack_bf16(d0, d1);
@@ -556,7 +554,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
               for (int q4 = 0; q4 < 4; ++q4)
                 ds_out[4 * ci + q4] = make_int4(dk[4 * q4], dk[4 * q4 + 1], dk[4 * q4 + 2], dk[4 * q4 + 3]);
-          } else if (cls[ci] == 0) {
+          } else if (cls0 == 0) {
             uint32_t z[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) z[i] = 0u;
@@ -574,10 +572,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             for (int g8 = 0; g8 < 32; g8 += 8) {
               uint32_t dv[8], dk[4];
               tmem_ld8(dpbase + g8, dv);
-              const uint32_t bw0 = bl[ci][g8 >> 2], bw1 = bl[ci][(g8 >> 2) + 1];
+              const uint32_t bw0 = bl0[g8 >> 2], bw1 = bl0[(g8 >> 2) + 1];
               uint32_t kw[4];
 #pragma unroll
-              for (int j = 0; j < 4; ++j) kw[j] = kl[ci][(g8 >> 1) + j];
+              for (int j = 0; j < 4; ++j) kw[j] = kl0[(g8 >> 1) + j];
               tmem_ld_wait();
               float dd[8];
 #pragma unroll
@@ -592,12 +590,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               uint32_t bj[8], msk = 0;
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const bool ok = (okm[ci] >> (g8 + j)) & 1u;
+                const bool ok = (okm0 >> (g8 + j)) & 1u;
                 bj[j] = ok ? (((j < 4 ? bw0 : bw1) >> (8 * (j & 3))) & 0xFFu) : 31u;
                 msk |= 1u << bj[j];
                 sat_w += bj[j] == (uint32_t)(nb - 1) ? dd[j] : 0.f;
               }
               msk &= ~((1u << (nb - 1)) | 0x80000000u);
+              if (p.dbg & 8) msk = 0;
               for (uint32_t m = __reduce_or_sync(0xffffffffu, msk); m; m &= m - 1) {
                 const uint32_t k = __ffs(m) - 1;
                 float sk = 0.f;
@@ -607,7 +606,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               }
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const bool ok = (okm[ci] >> (g8 + j)) & 1u;
+                const bool ok = (okm0 >> (g8 + j)) & 1u;
                 if (has_pos) {
                   const int rel = min(rel0 + g8 + j, P - 1);
                   red_add_f32_if(g_bins + 256 + max(rel, 0), dd[j], ok && rel != P - 1);
@@ -621,10 +620,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         acc_p += (double)sat_p;
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&ds_full[x]);
-        if (tr) trace_ev(p, trole, tcnt, 25, t);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&qd_empty[st]);  // done with this stage's ts_q
+        if (lane == 0) {
+          mbar_arrive(&ds_full[x]);
+          mbar_arrive(&qd_empty[st]);  // done with this stage's ts_q
+        }
+        if (tr) trace_ev(p, trole, tcnt, 25, t);
       }
     }
     if (dep_item != nullptr) {
