@@ -14,13 +14,14 @@
 //       warp 3      per-chunk min of ts_q (saturation test)
 //       warps 4-11  compute, two warpgroups: group g owns q-column chunk g of
 //                   every half, thread = (kv row, 32-column chunk):
-//                   phase P  : S^T -> P^T (TMEM) and SiLU'(S) (f16, TMEM)
-//                   phase dS : dP^T -> dS^T = dP SiLU'(S)/sqrt(d) (TMEM), d_ts_weights
+//                   phase P  : S^T -> P^T (TMEM) and SiLU'(S) (registers)
+//                   phase dS : dP^T -> dS^T = dP SiLU'(S)/sqrt(d) (TMEM, over dP^T), d_ts_weights
 //       warps 12-15 drain dK / dV (bf16 store, or fp32 accumulate for CP)
 //     TMEM: S^T buffers [0,64) [64,128): per 32-column chunk, P^T (bf16) overwrites
-//           the first 16 columns and dS^T (bf16) the last 16 -- both are the A
-//           operands of the dV / dK MMAs; SiLU'(S) stays in registers | dP^T
-//           buffers [128,256) | dV | dK
+//           the first 16 columns (A operand of dV) | dP^T buffers [128,256): dS^T
+//           (bf16) overwrites the first 16 columns of each chunk (A operand of dK) |
+//           dV | dK.  So S^T of half i+2 only waits for dV_i (issued while the
+//           compute warps run phase dS of half i) and dP^T of half i+2 for dK_i.
 //     The dS^T tile of every half is also written (bf16) to a scratch buffer.
 // (2) hstu_bwd_dq_kernel -- dQ = dS K as a streaming GEMM over that scratch
 //     (q-tile-major, TMA-fed, dQ double-buffered in TMEM), no recomputation.
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       uint32_t it_cnt = 0, hc = 0, tcnt = 0;
       auto q_base = [&](uint32_t hi) { return smem_u32(smem + C::Q_OFF + (hi % kQStages) * C::HTILE); };
       auto do_base = [&](uint32_t hi) { return smem_u32(smem + C::DO_OFF + (hi % kQStages) * C::HTILE); };
-      auto issue_S_dP = [&](uint32_t hi, bool last) {
+      auto issue_S = [&](uint32_t hi) {
         const uint32_t x = hi & 1;
         mbar_wait(&qd_full[hi % kQStages], (hi / kQStages) & 1);
         tc_fence_after();
@@ -237,6 +238,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                   kk > 0 ? 1u : 0u);
         }
         umma_commit(&s_full[x]);
+      };
+      auto issue_dP = [&](uint32_t hi, bool last) {  // after issue_S(hi) (same Q/dO stage)
+        const uint32_t x = hi & 1;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t ka = (kk >> 2) * 16384 + (kk & 3) * 32;
@@ -257,13 +261,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int n = nh - h0;
         mbar_wait(kv_full, it_cnt & 1);
         trace_ev(p, 1, tcnt, 11, g);
-        issue_S_dP(hc, n == 1);
-        if (n > 1) issue_S_dP(hc + 1, n == 2);
+        issue_S(hc);
+        issue_dP(hc, n == 1);
+        if (n > 1) {
+          issue_S(hc + 1);
+          issue_dP(hc + 1, n == 2);
+        }
         for (int i = 0; i < n; ++i) {
           const uint32_t hi = hc + i;
           const uint32_t x = hi & 1, xp = (hi >> 1) & 1;
           // dV += P^T dO.  P^T of chunk c (q columns [32c, 32c+32)) sits at TMEM
-          // columns [32c, 32c+16) of the S^T buffer (SiLU' in the other 16)
+          // columns [32c, 32c+16) of the S^T buffer
           mbar_wait(&p_full[x], xp);
           trace_ev(p, 1, tcnt, 12, hi);
           if (i == 0) mbar_wait(dkv_empty, (it_cnt & 1) ^ 1);  // dK/dV of the previous item drained
@@ -272,19 +280,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int kk = 0; kk < kQH / 16; ++kk)
             umma_ts(tDV, tmem + 64 * x + 32 * (kk >> 1) + 8 * (kk & 1),
                     sdesc_sw128(do_base(hi) + kk * 2048, 8192, 1024), id_kv, (kk > 0 || i > 0) ? 1u : 0u);
+          // S^T of half i+2 into buffer x: P^T (read by dV_i, issued above) is its only
+          // live content, so it overlaps the compute warps' dS phase of half i
+          if (i + 2 < n) issue_S(hi + 2);
           // dK += dS^T Q
           mbar_wait(&ds_full[x], xp);
           trace_ev(p, 1, tcnt, 13, hi);
           tc_fence_after();
-          // A = dS^T from TMEM: chunk c's 32 q columns at [64x + 32c + 16, +16)
+          // A = dS^T from TMEM: chunk c's 32 q columns at [128 + 64x + 32c, +16) (over dP^T)
 #pragma unroll
           for (int kk = 0; kk < kQH / 16; ++kk)
-            umma_ts(tDK, tmem + 64 * x + 32 * (kk >> 1) + 16 + 8 * (kk & 1),
+            umma_ts(tDK, tDP + 64 * x + 32 * (kk >> 1) + 8 * (kk & 1),
                     sdesc_sw128(q_base(hi) + kk * 2048, 8192, 1024), id_kv, (kk > 0 || i > 0) ? 1u : 0u);
           umma_commit(&qd_empty[hi % kQStages]);
-          // S^T / dP^T of half i+2 into buffer x (P^T, dS^T read by dV_i / dK_i in
-          // issue order; dP^T consumed before ds_full)
-          if (i + 2 < n) issue_S_dP(hi + 2, i + 3 == n);
+          // dP^T of half i+2 into buffer x (dS^T read by dK_i in issue order)
+          if (i + 2 < n) issue_dP(hi + 2, i + 3 == n);
         }
         hc += n;
         umma_commit(dkv_full);
@@ -403,7 +413,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // SiLU'(S) (f16 pairs) stays in registers from phase P to phase dS (saturated
         // chunks) or in a small per-thread local buffer (general chunks: rolled loops
         // keep that rarely-run code small), with the buckets and the mask
-        uint32_t kp0[16];
+        float kd0[32];  // c1 * SiLU'(S) of the chunk (saturated / ragged chunks)
         uint32_t kl0[16], bl0[8];
         uint32_t okm0 = 0u;
         // ---------------- phase P: S^T -> P^T, SiLU'
@@ -423,10 +433,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               const float h0f = fmaf(__uint_as_float(v[i]), c1, cb);
               const float h1f = fmaf(__uint_as_float(v[i + 1]), c1, cb);
               const float t0 = tanh_approx(h0f), t1 = tanh_approx(h1f);  // f32: d_ts_weights accuracy
-              pk[i >> 1] = pack_bf16(fmaf(h0f, t0, h0f), fmaf(h1f, t1, h1f));
-              __half2 hk = __floats2half2_rn((1.f + t0) * (fmaf(-h0f, t0, h0f) + 1.f),
-                                             (1.f + t1) * (fmaf(-h1f, t1, h1f) + 1.f));
-              kp0[i >> 1] = *reinterpret_cast<uint32_t*>(&hk);
+              const float p0 = fmaf(h0f, t0, h0f), p1 = fmaf(h1f, t1, h1f);
+              pk[i >> 1] = pack_bf16(p0, p1);
+              // SiLU'(h) = 1 + t + h (1 - t^2) = 1 + t + P (1 - t), times c1 = dh/dS
+              kd0[i] = fmaf(c1, fmaf(-p0, t0, p0) + t0, c1);
+              kd0[i + 1] = fmaf(c1, fmaf(-p1, t1, p1) + t1, c1);
             }
             if (cls0 == 3) {
               // ragged edge: zero the pairs outside the segment (columns >= nq, rows >= kv_len)
@@ -435,7 +446,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               for (int i = 0; i < 16; ++i) {
                 const uint32_t m = (2 * i < nv ? 0x0000FFFFu : 0u) | (2 * i + 1 < nv ? 0xFFFF0000u : 0u);
                 pk[i] &= m;
-                kp0[i] &= m;
+                kd0[2 * i] = 2 * i < nv ? kd0[2 * i] : 0.f;
+                kd0[2 * i + 1] = 2 * i + 1 < nv ? kd0[2 * i + 1] : 0.f;
               }
             }
             tmem_st16(cbase, pk);
@@ -532,8 +544,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         {
           const int ci = wg;
           const int c0 = 32 * ci;
-          const uint32_t cbase = tmem + 64 * x + c0 + lane_off;  // dS^T -> [cbase + 16, +16)
-          const uint32_t dpbase = tDP + 64 * x + c0 + lane_off;
+          const uint32_t dpbase = tDP + 64 * x + c0 + lane_off;  // dP^T chunk -> dS^T [dpbase, +16)
           if (cls0 == 1 || cls0 == 3) {
             uint32_t dv[32], dk[16];
             tmem_ld32(dpbase, dv);
@@ -541,15 +552,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             float csum = 0.f;
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
-              const float2 kd = __half22float2(*reinterpret_cast<const __half2*>(&kp0[i >> 1]));
-              const float d0 = __uint_as_float(dv[i]) * kd.x * c1;
-              const float d1 = __uint_as_float(dv[i + 1]) * kd.y * c1;
+              const float d0 = __uint_as_float(dv[i]) * kd0[i];
+              const float d1 = __uint_as_float(dv[i + 1]) * kd0[i + 1];
               dk[i >> 1] = pack_bf16(d0, d1);
               csum += d0 + d1;
             }
             sat_w += csum;
             if (has_pos) sat_p += csum;  // saturated chunks hit both last buckets
-            tmem_st16(cbase + 16, dk);
+            tmem_st16(dpbase, dk);
             if (ds_ok)
 #pragma unroll
               for (int q4 = 0; q4 < 4; ++q4)
@@ -558,7 +568,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             uint32_t z[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) z[i] = 0u;
-            tmem_st16(cbase + 16, z);
+            tmem_st16(dpbase, z);
             if (ds_ok)
 #pragma unroll
               for (int q4 = 0; q4 < 4; ++q4) ds_out[4 * ci + q4] = make_int4(0, 0, 0, 0);
@@ -585,7 +595,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 dd[j + 1] = __uint_as_float(dv[j + 1]) * kd.y * c1;
                 dk[j >> 1] = pack_bf16(dd[j], dd[j + 1]);
               }
-              tmem_st4(cbase + 16 + (g8 >> 1), dk);
+              tmem_st4(dpbase + (g8 >> 1), dk);
               if (ds_ok) ds_out[4 * ci + (g8 >> 3)] = make_int4(dk[0], dk[1], dk[2], dk[3]);
               uint32_t bj[8], msk = 0;
 #pragma unroll
