@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     if (elect_one()) {
       uint32_t it_cnt = 0, tcnt = 0;
       uint32_t rk = 0;
+      const uint64_t pol_once = l2_policy_evict_first();  // operands nothing re-reads
       for (int g; (g = ring_produce(ring, rk, &p.wl.hdr->next_item[1], total)) >= 0;) {
         const int2 it = p.wl.bwd[g / H];
         const int h = g % H;
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)it.y * kBN);
         for (int pn = 0; pn < C::PANELS; ++pn) {
           tma_load_2d(smem + C::K_OFF + pn * 16384, &tm_k, h * D + pn * 64, krow, kv_full);
-          tma_load_2d(smem + C::V_OFF + pn * 16384, &tm_v, h * D + pn * 64, krow, kv_full);
+          tma_load_2d_hint(smem + C::V_OFF + pn * 16384, &tm_v, h * D + pn * 64, krow, kv_full, pol_once);
         }
         ++it_cnt;
       }
@@ -353,6 +354,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // dS scratch capacity (caller's max_kv_len bound); on overflow dQ becomes NaN
     const bool ds_ok = p.wl.hdr->ds_blocks * H <= p.ds_cap_blocks && !(p.dbg & 1);
     if (!ds_ok && et == 0) p.wl.hdr->ds_overflow = 1;
+    // the dS^T scratch is re-read by the dQ kernel right after: keep it in L2
+    const uint64_t ds_pol = l2_policy_evict_last();
     uint32_t rk = 0;
     int32_t* dep_item = nullptr;  // completion counter of the previous item (bumped one item late)
     for (int g; (g = ring_consume(ring, rk, true)) >= 0;) {
@@ -410,9 +413,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               cls0 = ((32 * ci + 32 <= nq) && warp_k_ok) ? 1 : 3;  // 3: saturated, ragged edge
           }
         }
-        // SiLU'(S) (f16 pairs) stays in registers from phase P to phase dS (saturated
-        // chunks) or in a small per-thread local buffer (general chunks: rolled loops
-        // keep that rarely-run code small), with the buckets and the mask
+        // SiLU'(S) stays in registers from phase P to phase dS (saturated chunks, f32)
+        // or in a small per-thread local buffer (general chunks, f16 pairs: rolled
+        // loops keep that rarely-run code small), with the buckets and the mask
         float kd0[32];  // c1 * SiLU'(S) of the chunk (saturated / ragged chunks)
         uint32_t kl0[16], bl0[8];
         uint32_t okm0 = 0u;
@@ -488,7 +491,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 om |= (ok ? 1u : 0u) << j;
                 unsat |= ok && du[j] < (uint32_t)cap;
               }
-              if ((p.dbg & 2) || (!has_pos && !__any_sync(0xffffffffu, unsat))) {
+              if (!has_pos && !__any_sync(0xffffffffu, unsat)) {
                 // every visible pair of these 8 columns is in the last bucket (warp-uniform)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) bc[j] = cb;
@@ -519,7 +522,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 for (int u = 0; u < 2; ++u) {
                   const bool ok = (om >> (j + u)) & 1u;
                   const float hh = fmaf(__uint_as_float(v[j + u]), c1, bc[j + u]);
-                  const float th = (p.dbg & 4) ? hh : tanh_approx(hh);
+                  const float th = tanh_approx(hh);
                   pp[u] = ok ? fmaf(hh, th, hh) : 0.f;
                   dd[u] = ok ? (1.f + th) * (fmaf(-hh, th, hh) + 1.f) : 0.f;
                 }
@@ -563,7 +566,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             if (ds_ok)
 #pragma unroll
               for (int q4 = 0; q4 < 4; ++q4)
-                ds_out[4 * ci + q4] = make_int4(dk[4 * q4], dk[4 * q4 + 1], dk[4 * q4 + 2], dk[4 * q4 + 3]);
+                st_global_v4_hint(ds_out + 4 * ci + q4, dk[4 * q4], dk[4 * q4 + 1], dk[4 * q4 + 2], dk[4 * q4 + 3], ds_pol);
           } else if (cls0 == 0) {
             uint32_t z[16];
 #pragma unroll
@@ -571,7 +574,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tmem_st16(dpbase, z);
             if (ds_ok)
 #pragma unroll
-              for (int q4 = 0; q4 < 4; ++q4) ds_out[4 * ci + q4] = make_int4(0, 0, 0, 0);
+              for (int q4 = 0; q4 < 4; ++q4) st_global_v4_hint(ds_out + 4 * ci + q4, 0u, 0u, 0u, 0u, ds_pol);
           } else {
             // general chunk: exact bucket scatter.  The last bucket accumulates in a
             // register; the other buckets present in each 8 columns (warp-wide mask)
@@ -596,7 +599,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 dk[j >> 1] = pack_bf16(dd[j], dd[j + 1]);
               }
               tmem_st4(dpbase + (g8 >> 1), dk);
-              if (ds_ok) ds_out[4 * ci + (g8 >> 3)] = make_int4(dk[0], dk[1], dk[2], dk[3]);
+              if (ds_ok) st_global_v4_hint(ds_out + 4 * ci + (g8 >> 3), dk[0], dk[1], dk[2], dk[3], ds_pol);
               uint32_t bj[8], msk = 0;
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
@@ -606,7 +609,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 sat_w += bj[j] == (uint32_t)(nb - 1) ? dd[j] : 0.f;
               }
               msk &= ~((1u << (nb - 1)) | 0x80000000u);
-              if (p.dbg & 8) msk = 0;
               for (uint32_t m = __reduce_or_sync(0xffffffffu, msk); m; m &= m - 1) {
                 const uint32_t k = __ffs(m) - 1;
                 float sk = 0.f;
@@ -817,6 +819,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     if (elect_one()) {
       uint32_t kc = 0;
       uint32_t rk = 0;
+      const uint64_t pol_once = l2_policy_evict_first();  // operands nothing re-reads
       for (int g; (g = ring_produce(ring, rk, &p.wl.hdr->next_item[2], total)) >= 0;) {
         const int2 it = p.wl.fwd[g / H];
         const int h = g % H;
@@ -837,8 +840,8 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           // blocks (j, 2i) and (j, 2i+1); the second one may not exist (odd half
           // count): whatever is loaded only feeds q rows past the segment
           const int64_t blk = p.wl.ds_base[it.x] * H + (int64_t)(h * nkt + j) * nh + 2 * it.y;
-          tma_load_2d(sb, &tm_ds, 0, (int32_t)(blk * 128), &full[st]);
-          tma_load_2d(sb + kDsBlockBytes, &tm_ds, 0, (int32_t)((blk + 1) * 128), &full[st]);
+          tma_load_2d_hint(sb, &tm_ds, 0, (int32_t)(blk * 128), &full[st], pol_once);  // read once
+          tma_load_2d_hint(sb + kDsBlockBytes, &tm_ds, 0, (int32_t)((blk + 1) * 128), &full[st], pol_once);
           const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)j * kBN);
           for (int pn = 0; pn < C::PANELS; ++pn)
             tma_load_2d(sb + C::DSB + pn * 16384, &tm_k, h * D + pn * 64, krow, &full[st]);

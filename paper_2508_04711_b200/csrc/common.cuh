@@ -87,6 +87,16 @@ JH_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* m, int32_t c0, int32_
       : "memory");
 }
 
+// Same with an L2 eviction-priority policy (createpolicy) for the loaded lines.
+JH_DEV void tma_load_2d_hint(void* smem_dst, const CUtensorMap* m, int32_t c0, int32_t c1, uint64_t* bar,
+                             uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 // 1-D tile load (int64 timestamps), completing on an mbarrier.
 JH_DEV void tma_load_1d(void* smem_dst, const CUtensorMap* m, int32_t c0, uint64_t* bar) {
   asm volatile(
@@ -254,6 +264,22 @@ JH_DEV float2 tanh2_approx(float a, float b) {
   uint32_t xi = *reinterpret_cast<uint32_t*>(&x), yi;
   asm("tanh.approx.f16x2 %0, %1;" : "=r"(yi) : "r"(xi));
   return __half22float2(*reinterpret_cast<__half2*>(&yi));
+}
+// L2 eviction-priority policies (createpolicy) and a 16-byte store that carries one
+JH_DEV uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+JH_DEV uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+JH_DEV void st_global_v4_hint(void* ptr, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "r"(a), "r"(b), "r"(c),
+               "r"(d), "l"(pol)
+               : "memory");
 }
 JH_DEV uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
