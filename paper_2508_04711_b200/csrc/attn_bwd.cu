@@ -685,6 +685,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     uint32_t it_cnt = 0;
     uint32_t rk = 0;
+    const uint64_t pol_out = l2_policy_evict_first();  // results nothing in this step re-reads
     for (int g; (g = ring_consume(ring, rk, true)) >= 0;) {
       const int2 it = p.wl.bwd[g / H];
       const int h = g % H;
@@ -731,7 +732,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             for (int i = 0; i < 32; i += 2) pk[i >> 1] = pack_bf16(__uint_as_float(v[i]), __uint_as_float(v[i + 1]));
             int4* d4 = reinterpret_cast<int4*>(dst);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) d4[i] = make_int4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            for (int i = 0; i < 4; ++i) st_global_v4_hint(d4 + i, pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3], pol_out);
           }
         }
       }
@@ -903,6 +904,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     const bool bad = p.wl.hdr->ds_blocks * H > p.ds_cap_blocks;  // dS scratch overflow: poison dq
     uint32_t o_it = 0;
     uint32_t rk = 0;
+    const uint64_t pol_out = l2_policy_evict_first();  // results nothing in this step re-reads
     for (int g; (g = ring_consume(ring, rk, true)) >= 0;) {
       const int2 it = p.wl.fwd[g / H];
       const int h = g % H;
@@ -932,7 +934,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             pk[i >> 1] = bad ? 0x7FC07FC0u : pack_bf16(__uint_as_float(v[i]), __uint_as_float(v[i + 1]));
           int4* d4 = reinterpret_cast<int4*>(dqrow + cc);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) d4[i] = make_int4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          for (int i = 0; i < 4; ++i) st_global_v4_hint(d4 + i, pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3], pol_out);
         }
       }
       tc_fence_before();

@@ -452,6 +452,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     uint32_t o_it = 0;
     uint32_t rk = 0;
+    const uint64_t pol_out = l2_policy_evict_first();  // results nothing in this step re-reads
     for (int g; (g = ring_consume(ring, rk, true)) >= 0;) {
       const int2 it = p.wl.fwd[g / H];
       const int h = g % H;
@@ -483,7 +484,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (row_ok) {
         int4* dst = reinterpret_cast<int4*>(orow);
 #pragma unroll
-        for (int i = 0; i < D / 8; ++i) dst[i] = make_int4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        for (int i = 0; i < D / 8; ++i)
+          st_global_v4_hint(dst + i, pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3], pol_out);
       }
     }
   }
