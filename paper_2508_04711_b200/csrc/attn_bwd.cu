@@ -62,7 +62,7 @@ struct DkvCfg {
   // (the 8 int64 of padding after each ts_q box hold the stage's two chunk
   // minima; slot 0's padding also holds the TMEM base address)
   static constexpr int BAR_OFF = PW_OFF + (D == 64 ? 4096 : 0);
-  static constexpr int NBARS = 26;
+  static constexpr int NBARS = 28;
   static constexpr int RING_OFF = BAR_OFF + NBARS * 8;  // work-item ring: full[], empty[], slot[]
   // thread-private d_ts_weights bins of the general chunks: float [kTbBuckets][256 compute threads]
   static constexpr int TB_OFF = (RING_OFF + 2 * kItemRing * 8 + kItemRing * 4 + 15) & ~15;
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // ================= TMA producer: Q_h, dO_h, ts_q per half tile (runs ahead
     // across item boundaries, independent of the K/V buffer)
     if (elect_one()) {
-      uint32_t hc = 0;
+      uint32_t hc = 0, tcnt = 0;
       uint32_t rk = 0;
       for (int g; (g = ring_consume(ring, rk, false)) >= 0;) {
         const int2 it = p.wl.bwd[g / H];
@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int t = h0; t < nh; ++t, ++hc) {
           const int st = hc % kQStages;
           mbar_wait(&qd_empty[st], ((hc / kQStages) & 1) ^ 1);
+          trace_ev(p, 4, tcnt, 5, hc);
           mbar_expect_tx(&qd_full[st], 2 * C::HTILE + kTsBytesH);
           const int32_t qrow = (int32_t)(sg.q_row0 + (int64_t)t * kQH);
           for (int pn = 0; pn < C::PANELS; ++pn) {
@@ -229,7 +230,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       auto do_base = [&](uint32_t hi) { return smem_u32(smem + C::DO_OFF + (hi % kQStages) * C::HTILE); };
       auto issue_S = [&](uint32_t hi) {
         const uint32_t x = hi & 1;
+        trace_ev(p, 1, tcnt, 16, hi);
         mbar_wait(&qd_full[hi % kQStages], (hi / kQStages) & 1);
+        trace_ev(p, 1, tcnt, 14, hi);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
