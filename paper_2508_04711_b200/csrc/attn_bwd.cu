@@ -44,7 +44,6 @@ constexpr int kCompWarps = 8;
 // the tensor core already computes S^T / dP^T of half i+1.
 constexpr int kQH = 64;     // q rows per half tile
 constexpr int kQStages = 4;  // Q / dO / ts_q ring depth
-constexpr int kTbBuckets = 24;  // >= the fused kernels' num_buckets limit (23)
 
 template <int D>
 struct DkvCfg {
@@ -61,7 +60,8 @@ struct DkvCfg {
   static constexpr int PW_OFF = OCT_OFF + 32 * 16;                   // float [1024] x c1 (D=64 only)
   // (the 8 int64 of padding after each ts_q box hold the stage's two chunk
   // minima; slot 0's padding also holds the TMEM base address)
-  static constexpr int BAR_OFF = PW_OFF + (D == 64 ? 4096 : 0);
+  static constexpr int WT_OFF = PW_OFF + (D == 64 ? 4096 : 0);     // float [32] band weights x c1
+  static constexpr int BAR_OFF = WT_OFF + 128;
   static constexpr int NBARS = 28;
   static constexpr int RING_OFF = BAR_OFF + NBARS * 8;  // work-item ring: full[], empty[], slot[]
   // thread-private d_ts_weights bins of the general chunks: float [kTbBuckets][256 compute threads]
@@ -123,6 +123,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   oct_table_fill(s_oct, p.bias, p.ts_weights, c1, tid, blockDim.x);
   if (D == 64)
     for (int i = tid; i < P; i += blockDim.x) s_pwc[i] = p.pos_weights[i] * c1;
+  float* s_wt = reinterpret_cast<float*>(smem + C::WT_OFF);
+  if (tid < 32) s_wt[tid] = tid < nb ? p.ts_weights[tid] * c1 : (tid == (int)kBandMasked ? -1e30f : 0.f);
   // this CTA's fp32 partial bins (buckets, then positions) in the workspace
   float* g_bins = p.wl.bins + (size_t)blockIdx.x * kBinsPerCta;
   float* s_tb = reinterpret_cast<float*>(smem + C::TB_OFF);
@@ -354,6 +356,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint32_t hc = 0, tcnt = 0;
     const bool tr = (tid == 128 || tid == 256);
     const int trole = tid == 128 ? 2 : 3;
+    // band table chunks: bins of their non-last buckets are thread-private fp32
+    // slots in global memory (fire-and-forget reductions, zeroed here)
+    const bool use_band = p.band != nullptr;
+    float* tbg = use_band ? p.tb_glob + (size_t)blockIdx.x * kTbBuckets * 256 + et : nullptr;
+    if (use_band)
+      for (int b = 0; b < nb; ++b) tbg[b * 256] = 0.f;
     // dS scratch capacity (caller's max_kv_len bound); on overflow dQ becomes NaN
     const bool ds_ok = p.wl.hdr->ds_blocks * H <= p.ds_cap_blocks && !(p.dbg & 1);
     if (!ds_ok && et == 0) p.wl.hdr->ds_overflow = 1;
@@ -393,6 +401,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int32_t tk32 = (int32_t)(uint32_t)(uint64_t)tk;
       const int64_t k_lo = kv0 + (r & ~31), k_hi = k_lo + 31;  // this warp's kv positions
       const bool warp_k_ok = k_hi < sg.kv_len;
+      const int64_t band_q0 = band_group(sg, it.x, 0);
       // this thread's dS^T row in the scratch block of (segment, head, kv tile, half 0)
       uint8_t* ds_row = reinterpret_cast<uint8_t*>(p.ds) +
                         ((p.wl.ds_base[it.x] * H + (int64_t)(h * ds_nkt(sg) + it.y) * nh) * kDsBlockBytes) + r * 128;
@@ -403,8 +412,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int64_t qrow0 = sg.q_row0 + (int64_t)t * kQH;
         const int64_t qp_half = sg.qp0 + (int64_t)t * kQH;
         const int nq = (int)min((int64_t)kQH, sg.lq - (int64_t)t * kQH);
+        // band table chunk of this thread's (kv warp, q chunk): prefetch its
+        // transposed byte row before waiting
+        const int aq = 2 * t + wg;
+        const int64_t bwi = (k_lo >> 5) - ((sg.qp0 >> 5) + aq) + 3;
+        const bool in_band = use_band && bwi >= 0 && bwi < kBandNW && k_lo < sg.kv_len &&
+                             k_lo <= sg.qp0 + 32 * (int64_t)aq + 31 && 32 * aq < sg.lq;
+        uint4 bw0 = make_uint4(0, 0, 0, 0), bw1 = bw0;
+        if (in_band) {
+          const uint4* src = reinterpret_cast<const uint4*>(band_chunk(p.band, band_q0 + aq, (int)bwi) + 1024 + lane * 32);
+          bw0 = __ldg(src);
+          bw1 = __ldg(src + 1);
+        }
         mbar_wait(&qx_full[st], (hc / kQStages) & 1);
-        // chunk classes: 0 masked, 1 unmasked with saturated bias, 2 general
+        // chunk classes: 0 masked, 1 unmasked with saturated bias, 2 general,
+        // 3 saturated ragged edge, 4 band table
         int cls0 = 0;
         {
           const int ci = wg;
@@ -414,8 +436,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             if ((qc0 >= k_hi) && (s_tsq[st * kTsSlotH + kTsBoxH + ci] - tk_max >= cap) &&
                 (!has_pos || qc0 - k_hi >= P - 1))
               cls0 = ((32 * ci + 32 <= nq) && warp_k_ok) ? 1 : 3;  // 3: saturated, ragged edge
+            else if (in_band)
+              cls0 = 4;
           }
         }
+        const uint32_t bwd8[8] = {bw0.x, bw0.y, bw0.z, bw0.w, bw1.x, bw1.y, bw1.z, bw1.w};
         // SiLU'(S) stays in registers from phase P to phase dS (saturated chunks, f32)
         // or in a small per-thread local buffer (general chunks, f16 pairs: rolled
         // loops keep that rarely-run code small), with the buckets and the mask
@@ -430,7 +455,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const int ci = wg;
           const int c0 = 32 * ci;
           const uint32_t cbase = tmem + 64 * x + c0 + lane_off;  // S^T chunk -> P^T [cbase, +16)
-          if (cls0 == 1 || cls0 == 3) {
+          if (cls0 == 4) {
+            // exact bias from the band table; masked pairs (weight -1e30) give
+            // tanh = -1 exactly, so P = 0 and SiLU' = 0 without a select
+            uint32_t v[32], pk[16];
+            tmem_ld32(cbase, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const float w0 = s_wt[__byte_perm(bwd8[i >> 2], 0u, 0x4440u | (i & 3))];
+              const float w1 = s_wt[__byte_perm(bwd8[i >> 2], 0u, 0x4440u | ((i + 1) & 3))];
+              const float h0f = fmaf(__uint_as_float(v[i]), c1, w0);
+              const float h1f = fmaf(__uint_as_float(v[i + 1]), c1, w1);
+              const float t0 = tanh_approx(h0f), t1 = tanh_approx(h1f);
+              const float p0 = fmaf(h0f, t0, h0f), p1 = fmaf(h1f, t1, h1f);
+              pk[i >> 1] = pack_bf16(p0, p1);
+              kd0[i] = fmaf(c1, fmaf(-p0, t0, p0) + t0, c1);
+              kd0[i + 1] = fmaf(c1, fmaf(-p1, t1, p1) + t1, c1);
+            }
+            tmem_st16(cbase, pk);
+          } else if (cls0 == 1 || cls0 == 3) {
             uint32_t v[32], pk[16];
             tmem_ld32(cbase, v);
             tmem_ld_wait();
@@ -551,7 +595,29 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const int ci = wg;
           const int c0 = 32 * ci;
           const uint32_t dpbase = tDP + 64 * x + c0 + lane_off;  // dP^T chunk -> dS^T [dpbase, +16)
-          if (cls0 == 1 || cls0 == 3) {
+          if (cls0 == 4) {
+            uint32_t dv[32], dk[16];
+            tmem_ld32(dpbase, dv);
+            tmem_ld_wait();
+            float csum = 0.f;
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const float d0 = __uint_as_float(dv[i]) * kd0[i];
+              const float d1 = __uint_as_float(dv[i + 1]) * kd0[i + 1];
+              dk[i >> 1] = pack_bf16(d0, d1);
+              const uint32_t b0 = __byte_perm(bwd8[i >> 2], 0u, 0x4440u | (i & 3));
+              const uint32_t b1 = __byte_perm(bwd8[i >> 2], 0u, 0x4440u | ((i + 1) & 3));
+              csum += (b0 == (uint32_t)(nb - 1) ? d0 : 0.f) + (b1 == (uint32_t)(nb - 1) ? d1 : 0.f);
+              red_add_f32_if(tbg + b0 * 256, d0, b0 < (uint32_t)(nb - 1));
+              red_add_f32_if(tbg + b1 * 256, d1, b1 < (uint32_t)(nb - 1));
+            }
+            sat_w += csum;
+            tmem_st16(dpbase, dk);
+            if (ds_ok)
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4)
+                st_global_v4_hint(ds_out + 4 * ci + q4, dk[4 * q4], dk[4 * q4 + 1], dk[4 * q4 + 2], dk[4 * q4 + 3], ds_pol);
+          } else if (cls0 == 1 || cls0 == 3) {
             uint32_t dv[32], dk[16];
             tmem_ld32(dpbase, dv);
             tmem_ld_wait();
@@ -658,6 +724,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // (next on the stream) sums them with every CTA's fp32 bins -- no contended
     // atomics and no memory fence at the end of this kernel
     double* s_red = reinterpret_cast<double*>(smem + C::TSQ_OFF);  // ts_q ring is idle now
+    if (use_band) __threadfence();  // this thread's band-bin reductions before the reads below
     named_bar_sync(1, 32 * kCompWarps);
     if (lane == 0) {
       s_red[(et >> 5)] = acc_w;
@@ -670,6 +737,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       float v = 0.f;
 #pragma unroll
       for (int i = 0; i < 8; ++i) v += s_tb[b * 256 + lane + 32 * i];
+      if (use_band && b < nb - 1) {
+        const float* gb = p.tb_glob + (size_t)blockIdx.x * kTbBuckets * 256 + b * 256;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v += __ldcg(gb + lane + 32 * i);
+      }
 #pragma unroll
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == 0) g_bins[b] = v;

@@ -79,6 +79,27 @@ struct WorkLists {
 };
 constexpr int kDepBase = 16;
 
+// Band table: the exact bucket of every (q, kv) pair near the diagonal,
+// computed once per call for all heads and read by the fused kernels' general
+// chunks instead of per-element bucketization.  The chunk grid is the one both
+// kernels classify on: 32-row q groups a (q rows 32a.. of segment s, stored
+// at index floor(q_row0 / 32) + s + a: collision-free, bounded by
+// q_rows / 32 + nseg, and computable without a prefix sum) x
+// 32-column kv groups b.  For q group a with diagonal kv group
+// bd(a) = floor((qp0 + 32a) / 32), the window holds kv groups
+// b = bd - 3 .. bd + 1 (wi = b - bd + 3).  A chunk is 2 KB: [32 q][32 kv]
+// bytes then the transpose [32 kv][32 q].  Byte = bucket, or kBandMasked for a
+// pair outside the causal / jagged mask (or past the segment's rows).
+constexpr int kTbBuckets = 24;  // >= the fused kernels' num_buckets limit (23)
+constexpr int kBandNW = 5;
+constexpr int kBandChunk = 2048;
+constexpr uint32_t kBandMasked = 31;
+JH_DEV int band_wi(const Seg& g, int64_t a, int64_t b) { return (int)(b - ((g.qp0 >> 5) + a) + 3); }
+JH_DEV int64_t band_group(const Seg& g, int64_t s, int64_t a) { return (g.q_row0 >> 5) + s + a; }
+JH_DEV const uint8_t* band_chunk(const uint8_t* band, int64_t qgroup_global, int wi) {
+  return band + (qgroup_global * kBandNW + wi) * (int64_t)kBandChunk;
+}
+
 // Backward dS scratch: per (segment, head) a dense grid of blocks, one per
 // (128-row kv tile j, 64-row q half t), each the bf16 dS^T tile [128 kv][64 q]
 // (16 KB, row-major); block (s, h, j, t) = ds_base[s] * H + (h * nkt + j) * nh + t.
@@ -214,6 +235,83 @@ static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, 
       stamp[3073] = t;
     }
   }
+  // (launched as a programmatic dependent of the band-table kernel: completing
+  // only after it keeps the attention kernels' single griddepcontrol.wait sufficient)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// Band table builder: one warp per (q group, window chunk); lane = q row for
+// the [q][kv] half, lane = kv column for the transposed half.  Chunks the
+// kernels classify as fully masked (past the kv range or entirely in the
+// future of the q group) are never read and not written.
+static __global__ void __launch_bounds__(256) band_table_kernel(SegArgs sa, const int64_t* __restrict__ ts_q,
+                                                               const int64_t* __restrict__ ts_k, DevBiasTable bt,
+                                                               uint8_t* __restrict__ band) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the work-list build may start
+  __shared__ SmemBias sb;
+  __shared__ uint8_t tr[8][32][36];
+  smem_bias_fill(&sb, bt, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * 8 + warp;
+  const int64_t g = w / kBandNW;
+  const int wi = (int)(w % kBandNW);
+  const int64_t nseg = sa.num_segments;
+  if (nseg <= 0) return;
+  // segment: last s with f(s) = floor(q_row0(s) / 32) + s <= g (f strictly
+  // increasing); 32-ary warp search, one dependent load per level
+  int64_t lo = 0, hi = nseg - 1;
+  while (lo < hi) {
+    const int64_t step = (hi - lo + 32) / 32;
+    const int64_t idx = min(lo + (int64_t)lane * step, hi);
+    const bool le = (sa.q_offsets[idx] >> 5) + idx <= g;
+    const uint32_t m = __ballot_sync(0xffffffffu, le);
+    if (m == 0) return;  // g precedes segment lo (cannot happen for lo = 0)
+    const int64_t best = min(lo + (int64_t)(31 - __clz(m)) * step, hi);
+    lo = best;
+    hi = min(best + step - 1, hi);
+  }
+  const Seg sg = load_seg(sa, lo);
+  const int64_t a = g - ((sg.q_row0 >> 5) + lo);
+  if (a < 0 || 32 * a >= sg.lq) return;  // no q group at this index
+  const int64_t k0 = 32 * ((sg.qp0 >> 5) + a + wi - 3);
+  if (k0 < 0 || k0 >= sg.kv_len || k0 > sg.qp0 + 32 * a + 31) return;
+  const int64_t r = 32 * a + lane;
+  const int64_t qpos = sg.qp0 + r;
+  const bool rok = r < sg.lq;
+  const int64_t tq = rok ? ts_q[sg.q_row0 + r] : 0;
+  const int64_t tk = k0 + lane < sg.kv_len ? ts_k[sg.kv_row0 + k0 + lane] : 0;
+  // chunks the kernels classify as saturated (fully visible, every pair in the
+  // last bucket by the same chunk-level min / max test) are never read either
+  {
+    const int64_t tq_min = warp_min_i64(rok ? tq : (INT64_MAX >> 2));
+    const int64_t tk_max = warp_max_i64(k0 + lane < sg.kv_len ? tk : (INT64_MAX >> 2));
+    if (k0 + 31 < sg.kv_len && k0 + 31 <= sg.qp0 + 32 * a && tq_min - tk_max >= bt.cap) return;
+  }
+  uint32_t wd[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) wd[i] = 0u;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int64_t tki = __shfl_sync(0xffffffffu, tk, i);
+    const int64_t k = k0 + i;
+    const bool ok = rok && k < sg.kv_len && k <= qpos;
+    const uint32_t byte = ok ? (uint32_t)bucket_smem(tq - tki, &sb, bt.cap) : kBandMasked;
+    wd[i >> 2] |= byte << (8 * (i & 3));
+    tr[warp][lane][i] = (uint8_t)byte;
+  }
+  uint8_t* dst = band + (g * kBandNW + wi) * (int64_t)kBandChunk;
+  uint4* d0 = reinterpret_cast<uint4*>(dst + lane * 32);
+  d0[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+  d0[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) wd[i] = 0u;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) wd[i >> 2] |= (uint32_t)tr[warp][i][lane] << (8 * (i & 3));
+  uint4* d1 = reinterpret_cast<uint4*>(dst + 1024 + lane * 32);
+  d1[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+  d1[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
 }
 
 // q, k, v, dout (bf16 2-D, 128-row boxes) and ts_q, ts_k (int64 1-D) tensor maps
@@ -245,6 +343,8 @@ struct AttnParams {
   float* dv_accum;
   double* d_ts_weights;
   double* d_pos_weights;
+  const uint8_t* band;    // band table (NULL: per-element bucketization everywhere)
+  float* tb_glob;         // dK/dV kernel: per-CTA thread-private bins [kTbBuckets][256] of the band chunks
   __nv_bfloat16* ds;      // dS scratch (kDsBlockBytes blocks)
   int64_t ds_cap_blocks;  // its capacity
   WorkLists wl;

@@ -45,7 +45,8 @@ struct FwdCfg {
   static constexpr int TSK_OFF = TSQ_OFF + 2 * kTsSlot * 8;   // int64 [kTsRing][kTsSlot]
   static constexpr int OCT_OFF = TSK_OFF + kTsRing * kTsSlot * 8;  // OctEntry [32]
   static constexpr int PW_OFF = OCT_OFF + 32 * 16;          // float pw[<=1024] x c1
-  static constexpr int KMAX_OFF = PW_OFF + 1024 * 4;        // int64 [kTsRing][4] per-chunk max ts_k, then min
+  static constexpr int WT_OFF = PW_OFF + 1024 * 4;          // float [32] band weights x c1 (31: masked)
+  static constexpr int KMAX_OFF = WT_OFF + 32 * 4;          // int64 [kTsRing][4] per-chunk max ts_k, then min
   static constexpr int BAR_OFF = KMAX_OFF + 2 * kTsRing * 32;  // mbarriers
   static constexpr int NBARS = 4 + 4 * NS + 3 * kTsRing + 8;
   static constexpr int TMEMPTR_OFF = BAR_OFF + NBARS * 8;
@@ -95,6 +96,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const float c1 = 0.5f * rsqrtf((float)D);  // SiLU(s) = h + h*tanh(h), h = s/2 (scaled by 1/sqrt(d))
   oct_table_fill(s_oct, p.bias, p.ts_weights, c1, tid, blockDim.x);
   for (int i = tid; i < p.num_pos; i += blockDim.x) s_pwc[i] = p.pos_weights[i] * c1;
+  float* s_wt = reinterpret_cast<float*>(smem + C::WT_OFF);
+  if (tid < 32) s_wt[tid] = tid < nb ? p.ts_weights[tid] * c1 : (tid == (int)kBandMasked ? -1e30f : 0.f);
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
@@ -309,6 +312,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int64_t cap = p.bias.cap;
     const int P = p.num_pos;
     const bool has_pos = P > 0;
+    const bool use_band = p.band != nullptr;  // (the host turns it off with a positional bias)
     float cb = p.ts_weights[nb - 1];
     if (has_pos) cb += p.pos_weights[P - 1];
     cb *= c1;
@@ -337,8 +341,37 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int64_t tq_max = warp_max_i64(row_ok ? tq : (INT64_MIN >> 2));  // over valid rows
       const int32_t tq32 = (int32_t)(uint32_t)(uint64_t)tq;
       const int64_t row_lo = qp_tile + (r & ~31), row_hi = row_lo + 31;  // warp's q positions
+      // band table: this warp's q group and the byte row of this thread in it
+      const int aq = it.y * 4 + (r >> 5);
+      const int64_t bd = (sg.qp0 >> 5) + aq;
+      const uint8_t* brow = use_band && 32 * aq < sg.lq ? band_chunk(p.band, band_group(sg, it.x, aq), 0) + lane * 32 : nullptr;
       for (int j = 0; j < n; ++j, ++s_it) {
         if ((int)(s_it & 1) != wg) continue;
+        // band chunks of this tile (window and not entirely masked): prefetch the
+        // byte rows of the two right-most ones (the diagonal-most) before any wait
+        uint32_t cand = 0;
+        if (use_band && 32 * aq < sg.lq) {  // (a warp past the segment's rows has no q group)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int64_t b = 4 * (int64_t)j + c;
+            const int64_t wi = b - bd + 3;
+            if (wi >= 0 && wi < kBandNW && 32 * b <= row_hi && 32 * b < kv_lim) cand |= 1u << c;
+          }
+        }
+        const int c_hi = cand ? 31 - __clz(cand) : -1;
+        const uint32_t cand2 = c_hi >= 0 ? cand & ~(1u << c_hi) : 0u;
+        const int c_lo = cand2 ? 31 - __clz(cand2) : -1;
+        uint4 pf_hi0 = make_uint4(0, 0, 0, 0), pf_hi1 = pf_hi0, pf_lo0 = pf_hi0, pf_lo1 = pf_hi0;
+        if (c_hi >= 0) {
+          const uint4* src = reinterpret_cast<const uint4*>(brow + (4 * j + c_hi - bd + 3) * kBandChunk);
+          pf_hi0 = __ldg(src);
+          pf_hi1 = __ldg(src + 1);
+        }
+        if (c_lo >= 0) {
+          const uint4* src = reinterpret_cast<const uint4*>(brow + (4 * j + c_lo - bd + 3) * kBandChunk);
+          pf_lo0 = __ldg(src);
+          pf_lo1 = __ldg(src + 1);
+        }
         const int sb = s_it % 3;
         const int ts = s_it % kTsRing;
         const int64_t kv0 = (int64_t)j * kBN;
@@ -358,8 +391,39 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             if ((kc1 <= row_lo) && (kc1 < kv_lim) && (tq_min - s_kmax[ts * 4 + (c0 >> 5)] >= cap) &&
                 (!has_pos || row_lo - kc1 >= P - 1))
               cls = 1;
+            else if ((cand >> (c0 >> 5)) & 1u)
+              cls = 4;  // band table chunk
           }
-          if (cls == 1) {
+          if (cls == 4) {
+            // exact bias from the band table: per element one byte -> weight
+            const int c = c0 >> 5;
+            uint4 w0, w1;
+            if (c == c_hi) {
+              w0 = pf_hi0;
+              w1 = pf_hi1;
+            } else if (c == c_lo) {
+              w0 = pf_lo0;
+              w1 = pf_lo1;
+            } else {
+              const uint4* src = reinterpret_cast<const uint4*>(brow + (4 * j + c - bd + 3) * kBandChunk);
+              w0 = __ldg(src);
+              w1 = __ldg(src + 1);
+            }
+            const uint32_t wd[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            uint32_t v[32], pk[16];
+            tmem_ld32(tS + c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const float b0 = s_wt[__byte_perm(wd[i >> 2], 0u, 0x4440u | (i & 3))];
+              const float b1 = s_wt[__byte_perm(wd[i >> 2], 0u, 0x4440u | ((i + 1) & 3))];
+              const float h0 = fmaf(__uint_as_float(v[i]), c1, b0);
+              const float h1 = fmaf(__uint_as_float(v[i + 1]), c1, b1);
+              // masked pairs: h = -1e30, tanh = -1 exactly, P = h - h = 0
+              pk[i >> 1] = pack_bf16(fmaf(h0, tanh_approx(h0), h0), fmaf(h1, tanh_approx(h1), h1));
+            }
+            tmem_st16(tS + c0, pk);
+          } else if (cls == 1) {
             uint32_t v[32], pk[16];
             tmem_ld32(tS + c0, v);
             tmem_ld_wait();

@@ -32,6 +32,18 @@ struct WsLayout {
 };
 
 static size_t bins_bytes() { return (size_t)sm_count() * kBinsPerCta * (4 + 8); }  // fp32 bins + fp64 totals
+static size_t band_bytes(int64_t q_rows, int64_t nseg) {
+  return (size_t)(q_rows / 32 + nseg + 1) * kBandNW * kBandChunk;
+}
+static size_t band_groups_bound(int64_t q_rows, int64_t nseg) { return (size_t)(q_rows / 32 + nseg); }
+static size_t tbglob_bytes() { return (size_t)sm_count() * kTbBuckets * 256 * 4; }
+// regions carved from the END of the workspace (the bwd item list in front is
+// bounded by the caller's kv total): band table, per-CTA band bins,
+// dependency counters, dS block bases, per-CTA bins
+static size_t tail_bytes(int64_t q_rows, int64_t nseg, int32_t H) {
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  return band_bytes(q_rows, nseg) + tbglob_bytes() + up((size_t)(kDepBase + nseg * H) * 4) + up((size_t)(nseg + 1) * 8) + bins_bytes() + 1024;
+}
 
 static WsLayout ws_layout(int64_t q_rows, int64_t kv_total, int64_t nseg, int32_t H, int32_t D) {
   WsLayout w;
@@ -40,9 +52,8 @@ static WsLayout ws_layout(int64_t q_rows, int64_t kv_total, int64_t nseg, int32_
   w.items_f = sizeof(WorkHeader);
   w.items_b = w.items_f + ((size_t)max_f * 8 + 255) / 256 * 256;
   w.ds_base = w.items_b + ((size_t)max_b * 8 + 255) / 256 * 256;
-  w.bins = w.ds_base + ((size_t)(nseg + 1) * 8 + 255) / 256 * 256 +
-           ((size_t)(kDepBase + nseg * H) * 4 + 255) / 256 * 256;
-  w.total = w.bins + bins_bytes();
+  w.bins = w.ds_base;
+  w.total = w.ds_base + tail_bytes(q_rows, nseg, H);
   return w;
 }
 
@@ -87,8 +98,8 @@ static int validate(const jh_attn_args* a, bool bwd) {
     }
   }
   WsLayout w = ws_layout(a->q_rows, a->q_rows, a->num_segments, a->num_heads, a->head_dim);
-  if (!a->workspace || a->workspace_bytes < (bwd ? w.total : w.ds_base))
-    return set_error(JH_ERR_INVALID, "workspace too small (need >= %zu bytes)", bwd ? w.total : w.ds_base);
+  if (!a->workspace || a->workspace_bytes < w.total)
+    return set_error(JH_ERR_INVALID, "workspace too small (need >= %zu bytes)", w.total);
   if (bwd && a->q_rows > 0 && (!a->ds_scratch || a->ds_scratch_bytes < (size_t)kDsBlockBytes || !aligned16(a->ds_scratch)))
     return set_error(JH_ERR_INVALID, "ds_scratch missing or too small (see jh_attn_ds_scratch_bytes)");
   return JH_OK;
@@ -151,8 +162,14 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
   p->wl.bins = bwd ? (float*)(ws + bins_off) : nullptr;
   p->wl.partials = bwd ? (double*)(ws + bins_off + (size_t)sm_count() * kBinsPerCta * 4) : nullptr;
   p->wl.ds_base = bwd ? (int64_t*)(ws + dsb_off) : nullptr;
-  if (bwd && ws + dep_off < ws + w.items_b + 8)
-    return set_error(JH_ERR_INVALID, "workspace too small");
+  const size_t tbg_off = (dep_off - tbglob_bytes()) & ~size_t(255);
+  const size_t band_off = (tbg_off - band_bytes(a->q_rows, a->num_segments)) & ~size_t(255);
+  if (band_off < w.items_b + 8 || band_off > a->workspace_bytes) return set_error(JH_ERR_INVALID, "workspace too small");
+  // band table (exact buckets near the diagonal, shared by all heads); off with
+  // a positional bias (its general chunks keep the per-element path) or JH_DBG & 4
+  const bool use_band = a->num_pos == 0 && !(p->dbg & 4);
+  p->band = use_band ? (const uint8_t*)(ws + band_off) : nullptr;
+  p->tb_glob = bwd ? (float*)(ws + tbg_off) : nullptr;
   const uint64_t HD = (uint64_t)a->num_heads * a->head_dim;
   if ((uintptr_t)a->ts_q % 16 || (uintptr_t)a->ts_k % 16)
     return set_error(JH_ERR_INVALID, "ts_q / ts_k must be 16-byte aligned");
@@ -176,9 +193,31 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
     cudaFuncSetAttribute(build_work_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     carve = true;
   }
-  build_work_kernel<<<1, 1024, 0, s>>>(p->seg, p->wl, p->trace_cta == -1 ? p->trace : nullptr);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_error(JH_ERR_CUDA, "build_work: %s", cudaGetErrorString(e));
+  // band table first (it only reads the inputs; a plain launch, so it also
+  // waits for the previous attention kernel, the table's last reader), then the
+  // work-list build as its programmatic dependent (runs concurrently; it waits
+  // for the table at its end, so the attention kernel's wait covers both)
+  cudaError_t e;
+  if (p->band) {
+    const size_t warps = (band_groups_bound(a->q_rows, a->num_segments) + 1) * kBandNW;
+    band_table_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(p->seg, a->ts_q, a->ts_k, p->bias, (uint8_t*)p->band);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(JH_ERR_CUDA, "band_table: %s", cudaGetErrorString(e));
+  }
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(1024);
+    cfg.stream = s;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = p->band ? 1 : 0;
+    e = cudaLaunchKernelEx(&cfg, build_work_kernel, p->seg, p->wl,
+                           (unsigned long long*)(p->trace_cta == -1 ? p->trace : nullptr));
+    if (e != cudaSuccess) return set_error(JH_ERR_CUDA, "build_work: %s", cudaGetErrorString(e));
+  }
   return JH_OK;
 }
 
