@@ -139,6 +139,13 @@ typedef struct jh_attn_args {
    * dQ kernel: at least jh_attn_ds_scratch_bytes(...) bytes (jh_attn_bwd only) */
   void* ds_scratch;
   size_t ds_scratch_bytes;
+  /* forward fp32 output mode (jh_attn_fwd only; CP partial sums, the
+   * reference's additive blockwise partials, attention.py:151-184 and
+   * cp_engine.py:441-450): 0 = write bf16 `out`; 1 = store fp32 into
+   * out_accum; 2 = add into out_accum (rows of q with no visible kv are left
+   * untouched).  Row stride of out_accum = ld_o (elements). */
+  float* out_accum;
+  int32_t out_accum_mode;
 } jh_attn_args;
 
 /* kv_len_total = sum over segments of kv_len[s] (= q_rows when kv_len is NULL). */

@@ -44,6 +44,7 @@ class JhAttnArgs(ctypes.Structure):
         ("prof_event_start", c_vp), ("prof_event_end", c_vp),
         ("trace", c_vp), ("trace_cta", ctypes.c_int32),
         ("ds_scratch", c_vp), ("ds_scratch_bytes", ctypes.c_size_t),
+        ("out_accum", c_vp), ("out_accum_mode", ctypes.c_int32),
     ]
 
 

@@ -13,9 +13,12 @@ restore_outputs), plus the backward pass the reference leaves out
    received buffer is already in plan order (source-major == plan order);
 3. KV exchange = all-gather of the resident K, V, ts slabs (cp_engine.py:
    384-453 rotates them in a ring; summing SiLU partials is order-free, so one
-   gather + one fused attention over the visible prefix gives the same
-   result); the gathered rows are re-ordered into sequence order and each
-   resident chunk attends to its causal prefix [0, chunk end);
+   gather + fused attention over the visible prefix gives the same result),
+   issued on a side (communication) stream and overlapped with the local
+   part: each resident chunk first attends to itself (its causal diagonal
+   block, resident rows only) into an fp32 accumulator; once the gather lands,
+   the gathered rows are re-ordered into sequence order and each chunk adds
+   its remote part, the sequence prefix [0, chunk start) (all visible);
 4. backward: dK/dV partials for the whole group batch are reduced to their
    owners with reduce-scatter, d_ts_weights is all-reduced;
 5. restore = the inverse all-to-all (cp_engine.py:468-525).
@@ -55,6 +58,9 @@ class CPPlan:
     kv_start: np.ndarray
     kv_len: np.ndarray
     group_rows: int
+    local_kv_start: np.ndarray   # overlap split: chunk vs itself (resident rows, q_pos0 = 0)
+    local_kv_len: np.ndarray
+    remote_kv_len: np.ndarray    # ... and vs its sequence prefix [0, start) in the gathered rows
 
 
 def build_cp_plan(lengths_per_rank, cp: int, rank: int, balance_mode: str = "balanced_minichunk") -> CPPlan:
@@ -90,17 +96,19 @@ def build_cp_plan(lengths_per_rank, cp: int, rank: int, balance_mode: str = "bal
             seq_perm[g0 + e.start:g0 + e.end] = np.arange(row, row + e.count, dtype=np.int64)
             row += e.count
     # (4) one attention segment per resident chunk: causal prefix [0, end) of its sequence
-    qo, qp, ks, kl = [0], [], [], []
+    qo, qp, ks, kl, lks, lkl = [0], [], [], [], [], []
     for e in plan.rank_entries[rank]:
         if e.count == 0:
             continue
+        lks.append(qo[-1])
+        lkl.append(e.count)
         qo.append(qo[-1] + e.count)
         qp.append(e.start)
         ks.append(int(goff[e.seq_id]))
         kl.append(e.end)
+    a64 = lambda x: np.asarray(x, np.int64)  # noqa: E731
     return CPPlan(cp, rank, plan, send_perm, send_counts, recv_counts, n_res, max_res, res_counts, seq_perm,
-                  np.asarray(qo, np.int64), np.asarray(qp, np.int64), np.asarray(ks, np.int64),
-                  np.asarray(kl, np.int64), int(goff[-1]))
+                  a64(qo), a64(qp), a64(ks), a64(kl), int(goff[-1]), a64(lks), a64(lkl), a64(qp))
 
 
 class GpuBackend:
@@ -121,6 +129,18 @@ class GpuBackend:
         return self.k.attn_fwd(q, k, v, ts_q, ts_k, qo, H, w, nb, q_pos0=qp, kv_start=ks, kv_len=kl,
                                kv_len_total=kvt)
 
+    def fwd_partial(self, q, k, v, ts_q, ts_k, segs, H, w, nb, acc, accumulate):
+        qo, qp, ks, kl, kvt, _ = segs
+        self.k.attn_fwd(q, k, v, ts_q, ts_k, qo, H, w, nb, q_pos0=qp, kv_start=ks, kv_len=kl, kv_len_total=kvt,
+                        out_accum=acc, accumulate=accumulate)
+
+    def comm_stream(self, device):
+        if device.type != "cuda":
+            return None
+        if getattr(self, "_comm", None) is None:
+            self._comm = torch.cuda.Stream(device=device)
+        return self._comm
+
     def bwd(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb):
         qo, qp, ks, kl, kvt, max_kv = segs
         dq, dk, dv, dw, _ = self.k.attn_bwd(q, k, v, ts_q, ts_k, qo, g, H, w, nb, q_pos0=qp, kv_start=ks,
@@ -132,7 +152,7 @@ class CPAttention:
     """Context-parallel jagged HSTU attention over a process group."""
 
     def __init__(self, group, num_heads: int, num_buckets: int = 16, balance_mode: str = "balanced_minichunk",
-                 backend=None):
+                 backend=None, overlap: bool = True):
         self.group = group
         self.cp = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -140,6 +160,7 @@ class CPAttention:
         self.nb = num_buckets
         self.mode = balance_mode
         self.be = backend if backend is not None else GpuBackend()
+        self.overlap = overlap and hasattr(self.be, "fwd_partial")
         self._plans: dict = {}
 
     # ---------------------------------------------------------------- plan
@@ -154,7 +175,11 @@ class CPAttention:
             t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
             dev = {"send_perm": t(p.send_perm), "seq_perm": t(p.seq_perm),
                    "segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.kv_len), int(p.kv_len.sum()),
-                            int(p.kv_len.max(initial=0)))}
+                            int(p.kv_len.max(initial=0))),
+                   "local_segs": (t(p.q_offsets), t(np.zeros_like(p.q_pos0)), t(p.local_kv_start),
+                                  t(p.local_kv_len), int(p.local_kv_len.sum()), int(p.local_kv_len.max(initial=0))),
+                   "remote_segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.remote_kv_len),
+                                   int(p.remote_kv_len.sum()), int(p.remote_kv_len.max(initial=0)))}
             self._plans[key] = (p, dev)
         return self._plans[key]
 
@@ -197,12 +222,41 @@ class CPAttention:
         p, dev = self.plan_for(local_lengths, q.device)
         q_r, k_r, v_r = (self._redistribute(x, p, dev) for x in (q, k, v))
         ts_r = self._redistribute(ts.view(-1, 1), p, dev).view(-1)
-        k_s, v_s = self._gather_seq(k_r, p, dev), self._gather_seq(v_r, p, dev)
-        ts_s = self._gather_seq(ts_r.view(-1, 1), p, dev).view(-1)
-        o_r = self.be.fwd(q_r, k_s, v_s, ts_r, ts_s, dev["segs"], self.H, w, self.nb)
+        if not self.overlap:
+            k_s, v_s = self._gather_seq(k_r, p, dev), self._gather_seq(v_r, p, dev)
+            ts_s = self._gather_seq(ts_r.view(-1, 1), p, dev).view(-1)
+            o_r = self.be.fwd(q_r, k_s, v_s, ts_r, ts_s, dev["segs"], self.H, w, self.nb)
+        else:
+            k_s, v_s, ts_s, o_r = self._forward_overlapped(q_r, k_r, v_r, ts_r, p, dev, w)
         out = self._restore(o_r, p, dev, q.shape[0])
         ctx = (p, dev, q_r, k_s, v_s, ts_r, ts_s, q.shape[0])
         return out, ctx
+
+    def _forward_overlapped(self, q_r, k_r, v_r, ts_r, p, dev, w):
+        """KV all-gather on the communication stream while each resident chunk
+        attends to itself; then the remote prefix is added (SiLU partials are
+        additive, attention.py:151-184 / cp_engine.py:441-450)."""
+        main = torch.cuda.current_stream(q_r.device) if q_r.is_cuda else None
+        comm = self.be.comm_stream(q_r.device) if hasattr(self.be, "comm_stream") else None
+        if comm is not None:
+            comm.wait_stream(main)
+            for x in (k_r, v_r, ts_r):
+                x.record_stream(comm)
+            with torch.cuda.stream(comm):
+                k_s, v_s = self._gather_seq(k_r, p, dev), self._gather_seq(v_r, p, dev)
+                ts_s = self._gather_seq(ts_r.view(-1, 1), p, dev).view(-1)
+        else:
+            k_s, v_s = self._gather_seq(k_r, p, dev), self._gather_seq(v_r, p, dev)
+            ts_s = self._gather_seq(ts_r.view(-1, 1), p, dev).view(-1)
+        acc_dt = torch.float32 if q_r.dtype in (torch.bfloat16, torch.float16) else q_r.dtype
+        acc = torch.empty(q_r.shape, dtype=acc_dt, device=q_r.device)
+        self.be.fwd_partial(q_r, k_r, v_r, ts_r, ts_r, dev["local_segs"], self.H, w, self.nb, acc, False)
+        if comm is not None:
+            main.wait_stream(comm)
+            for x in (k_s, v_s, ts_s):
+                x.record_stream(main)
+        self.be.fwd_partial(q_r, k_s, v_s, ts_r, ts_s, dev["remote_segs"], self.H, w, self.nb, acc, True)
+        return k_s, v_s, ts_s, acc.to(q_r.dtype)
 
     def backward(self, ctx, g, w):
         """Upstream gradient (local rows) -> (dq, dk, dv local; d_ts_weights summed over CP)."""

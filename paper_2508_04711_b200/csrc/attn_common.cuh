@@ -335,6 +335,8 @@ struct AttnParams {
   // fwd
   __nv_bfloat16* out;
   int64_t ld_o;
+  float* out_acc;      // fp32 output (NULL: bf16 `out`), row stride ld_o
+  int32_t out_acc_add; // 1: add into out_acc, 0: store
   // bwd
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;

@@ -524,15 +524,49 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int n = (int)((fwd_kv_lim(sg, it.y) + kBN - 1) / kBN);
       const int64_t nq = min((int64_t)kBM, sg.lq - (int64_t)it.y * kBM);
       const bool row_ok = r < nq;
-      __nv_bfloat16* orow = p.out + (sg.q_row0 + (int64_t)it.y * kBM + r) * p.ld_o + h * D;
+      const int64_t orow_i = (sg.q_row0 + (int64_t)it.y * kBM + r) * p.ld_o + h * D;
+      __nv_bfloat16* orow = p.out + orow_i;
       if (n == 0) {
-        if (row_ok)
+        if (row_ok && p.out_acc == nullptr)
           for (int c = 0; c < D; c += 8) *reinterpret_cast<int4*>(orow + c) = make_int4(0, 0, 0, 0);
+        else if (row_ok && !p.out_acc_add)
+          for (int c = 0; c < D; c += 4) *reinterpret_cast<float4*>(p.out_acc + orow_i + c) = make_float4(0, 0, 0, 0);
         continue;
       }
       mbar_wait(o_full, o_it & 1);
       ++o_it;
       tc_fence_after();
+      if (p.out_acc != nullptr) {
+        // fp32 partial (CP): store or add, 32 columns at a time; O is released
+        // after the last TMEM load
+        float4* arow = reinterpret_cast<float4*>(p.out_acc + orow_i);
+#pragma unroll 1
+        for (int c0 = 0; c0 < D; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tmem + 384 + lane_off + c0, v);
+          tmem_ld_wait();
+          if (c0 + 32 == D) {
+            tc_fence_before();
+            mbar_arrive(o_empty);
+          }
+          if (row_ok) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              float4 o = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                     __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+              if (p.out_acc_add) {
+                const float4 a = arow[(c0 >> 2) + i];
+                o.x += a.x;
+                o.y += a.y;
+                o.z += a.z;
+                o.w += a.w;
+              }
+              arow[(c0 >> 2) + i] = o;
+            }
+          }
+        }
+        continue;
+      }
       // O -> bf16 registers first, release the accumulator, then store
       uint32_t pk[D / 2];
 #pragma unroll

@@ -84,8 +84,13 @@ static int validate(const jh_attn_args* a, bool bwd) {
       return set_error(JH_ERR_INVALID, "q/k/v must be 16-byte aligned");
   }
   if (!bwd) {
-    if (a->q_rows > 0 && (!a->out || a->ld_o < HD || (a->ld_o * 2) % 16 || !aligned16(a->out)))
+    if (a->out_accum_mode < 0 || a->out_accum_mode > 2) return set_error(JH_ERR_INVALID, "bad out_accum_mode");
+    if (a->out_accum_mode != 0) {
+      if (a->q_rows > 0 && (!a->out_accum || a->ld_o < HD || (a->ld_o * 4) % 16 || !aligned16(a->out_accum)))
+        return set_error(JH_ERR_INVALID, "bad out_accum tensor");
+    } else if (a->q_rows > 0 && (!a->out || a->ld_o < HD || (a->ld_o * 2) % 16 || !aligned16(a->out))) {
       return set_error(JH_ERR_INVALID, "bad out tensor");
+    }
   } else {
     if (!a->d_ts_weights) return set_error(JH_ERR_INVALID, "d_ts_weights is NULL");
     if (a->num_pos > 0 && !a->d_pos_weights) return set_error(JH_ERR_INVALID, "d_pos_weights is NULL");
@@ -122,6 +127,8 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
   p->kv_rows = a->kv_rows;
   p->out = (__nv_bfloat16*)a->out;
   p->ld_o = a->ld_o;
+  p->out_acc = (!bwd && a->out_accum_mode != 0) ? a->out_accum : nullptr;
+  p->out_acc_add = a->out_accum_mode == 2 ? 1 : 0;
   p->dk = (__nv_bfloat16*)a->dk;
   p->dv = (__nv_bfloat16*)a->dv;
   p->ld_dk = a->ld_dk;

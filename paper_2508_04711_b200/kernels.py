@@ -216,20 +216,31 @@ def _prof(a, prof):
 
 
 def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=16, pos_weights=None,
-             q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, out=None, prof=None):
-    """Fused jagged HSTU forward (jh_attn_fwd).  bf16 in/out, fp32 weights."""
+             q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, out=None, prof=None, out_accum=None,
+             accumulate=False):
+    """Fused jagged HSTU forward (jh_attn_fwd).  bf16 in/out, fp32 weights.
+
+    ``out_accum`` (fp32, q's shape): write the fp32 result there instead of a
+    bf16 ``out`` (``accumulate=True``: add it; rows that see no kv are left
+    untouched) -- the additive partials of the CP pipeline (cp_engine.py:441-450)."""
     w = ts_weights.to(device=q.device, dtype=torch.float32).contiguous()
     pw = None if pos_weights is None else pos_weights.to(device=q.device, dtype=torch.float32).contiguous()
     a = _attn_args(q, k, v, ts_q, ts_k, q_offsets, num_heads, w, num_buckets, pw, q_pos0, kv_start, kv_len)
-    if out is None:
-        out = torch.empty_like(q)
-    a.out, a.ld_o = out.data_ptr(), out.stride(0)
+    if out_accum is not None:
+        if out_accum.dtype != torch.float32 or out_accum.shape != q.shape or out_accum.stride(1) != 1:
+            raise ValueError("out_accum must be a float32 tensor shaped like q")
+        a.out_accum, a.ld_o, a.out_accum_mode = out_accum.data_ptr(), out_accum.stride(0), 2 if accumulate else 1
+        out = out_accum
+    else:
+        if out is None:
+            out = torch.empty_like(q)
+        a.out, a.ld_o = out.data_ptr(), out.stride(0)
     ws, nbytes = _workspace(q.shape[0], q.shape[0] if kv_len_total is None else kv_len_total, a.num_segments,
                             num_heads, a.head_dim, q.device)
     a.workspace, a.workspace_bytes = ws.data_ptr(), nbytes
     _prof(a, prof)
     check(_lib.lib().jh_attn_fwd(ctypes.byref(a), _stream(q)), "hstu_attention forward")
-    _bump(2)  # work-list build + fused forward
+    _bump(2 if pw is not None else 3)  # (band table) + work-list build + fused forward
     return out
 
 
@@ -280,7 +291,7 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
     a.ds_scratch, a.ds_scratch_bytes = ds.data_ptr(), ds_bytes
     _prof(a, prof)
     check(_lib.lib().jh_attn_bwd(ctypes.byref(a), _stream(q)), "hstu_attention backward")
-    _bump(4)  # work-list build + dq memset + fused backward + dq convert
+    _bump(3 if pw is not None else 4)  # (band table) + work-list build + dK/dV + dQ kernels
     return dq, dk, dv, d_w, d_pos
 
 

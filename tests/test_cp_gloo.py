@@ -60,6 +60,13 @@ class NumpyBackend:
                 out[a:b, c] = np.where(mask, oracle.silu(sc), 0.0) @ V[kr, c]
         return torch.from_numpy(out)
 
+    def fwd_partial(self, q, k, v, ts_q, ts_k, segs, H, w, nb, acc, accumulate):
+        out = self.fwd(q, k, v, ts_q, ts_k, segs, H, w, nb).to(acc.dtype)
+        if accumulate:
+            acc += out
+        else:
+            acc.copy_(out)
+
     def bwd(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb):
         qo, qp, ks, kl = self._segs(segs)
         Q, K, V, G = q.numpy(), k.numpy(), v.numpy(), g.numpy()
@@ -105,13 +112,13 @@ def _batch(seed, rank, lengths, D):
     return dict(q=q, k=k, v=v, g=g, ts=ts, offsets=offs)
 
 
-def _worker(rank, world, port, lens, H, D, mode, result_dir):
+def _worker(rank, world, port, lens, H, D, mode, result_dir, overlap=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2508_04711_b200.cp_layer import CPAttention
     b = _batch(3, rank, lens[rank], H * D)
     w = torch.from_numpy(oracle.normal_init_ts_weights(16, 11))
-    layer = CPAttention(dist.group.WORLD, H, 16, balance_mode=mode, backend=NumpyBackend())
+    layer = CPAttention(dist.group.WORLD, H, 16, balance_mode=mode, backend=NumpyBackend(), overlap=overlap)
     t = {key: torch.from_numpy(b[key]) for key in ("q", "k", "v", "g", "ts")}
     out, ctx = layer.forward(t["q"], t["k"], t["v"], t["ts"], np.diff(b["offsets"]), w)
     dq, dk, dv, dw = layer.backward(ctx, t["g"], w)
@@ -120,14 +127,16 @@ def _worker(rank, world, port, lens, H, D, mode, result_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,lens,mode", [
-    (2, [[7, 0, 33], [12, 1]], "balanced_minichunk"),
-    (3, [[20, 5], [], [9, 40, 2]], "balanced_minichunk"),
-    (2, [[31, 4], [17]], "naive_contiguous"),
+@pytest.mark.parametrize("world,lens,mode,overlap", [
+    (2, [[7, 0, 33], [12, 1]], "balanced_minichunk", True),
+    (2, [[7, 0, 33], [12, 1]], "balanced_minichunk", False),
+    (3, [[20, 5], [], [9, 40, 2]], "balanced_minichunk", True),
+    (2, [[31, 4], [17]], "naive_contiguous", True),
 ])
-def test_cp_layer_matches_single_device(tmp_path, world, lens, mode):
+def test_cp_layer_matches_single_device(tmp_path, world, lens, mode, overlap):
     H, D = 2, 4
-    mp.spawn(_worker, args=(world, _free_port(), lens, H, D, mode, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), lens, H, D, mode, str(tmp_path), overlap), nprocs=world,
+             join=True)
     batches = [_batch(3, r, lens[r], H * D) for r in range(world)]
     cat = oracle.concat_batches(batches)
     g = np.concatenate([b["g"] for b in batches])

@@ -124,6 +124,41 @@ def test_run_pipeline_matches_oracle(cp, mode, protocol):
         assert row_rel(got, want[r])[1] <= ROW_TOL, r
 
 
+# ------------------------------------- fp32 partial sums (CP overlap split)
+
+def test_fwd_fp32_store_then_add_equals_oracle():
+    # each sequence split into two chunks; (1) every chunk attends to itself
+    # (store), (2) every chunk adds its prefix [0, chunk start) (add): the sum is
+    # the full causal attention (cp_layer's overlapped forward)
+    lens = [300, 17, 129, 1, 0, 64]
+    H = 2
+    case = make_case(lens, H * 128, seed=21)
+    c = to_cuda(case)
+    offs = case["offsets"]
+    qo, lks, lkl, rks, rkl, qp = [0], [], [], [], [], []
+    for b, L in enumerate(lens):
+        m = L // 2
+        for (a0, a1) in ((0, m), (m, L)):
+            if a1 == a0:
+                continue
+            lks.append(int(offs[b]) + a0)
+            lkl.append(a1 - a0)
+            rks.append(int(offs[b]))
+            rkl.append(a0)
+            qp.append(a0)
+            qo.append(qo[-1] + a1 - a0)
+    t = lambda x: torch.tensor(x, dtype=torch.int64, device="cuda")  # noqa: E731
+    from paper_2508_04711_b200 import kernels
+    acc = torch.full(c["q"].shape, float("nan"), dtype=torch.float32, device="cuda")
+    kernels.attn_fwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], t(qo), H, c["w"], 16, q_pos0=t([0] * len(qp)),
+                     kv_start=t(lks), kv_len=t(lkl), out_accum=acc)
+    kernels.attn_fwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], t(qo), H, c["w"], 16, q_pos0=t(qp),
+                     kv_start=t(rks), kv_len=t(rkl), kv_len_total=int(sum(rkl)), out_accum=acc, accumulate=True)
+    torch.cuda.synchronize()
+    want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], offs, case["w"], 16, H)
+    assert row_rel(acc.cpu().numpy(), want)[1] <= ROW_TOL
+
+
 # ------------------------------------------------ SPMD CP layer, one rank
 
 def test_cp_layer_single_rank_matches_single_device():
