@@ -336,11 +336,63 @@ def run_gpu(args):
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(h, g_host, w_host)
+    if world == 1 and not args.no_max_len:
+        del flush
+        torch.cuda.empty_cache()
+        result["max_seq_len"] = max_seq_len_probe(dev, w)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(result))
+
+
+def max_seq_len_probe(dev, w):
+    """Longest single sequence (B=1, H=4, d=128, bf16) whose fwd+bwd runs on
+    this GPU (the metric's "max supported seq len" at CP=1): lengths double
+    from 16K until the first out-of-memory, then a bisection to 4K granularity.
+    Each probe is a real fwd+bwd through the kernels on synthetic data; the
+    binding term is the bf16 dS scratch (2*H*L^2 bytes)."""
+    import torch
+    from paper_2508_04711_b200 import kernels
+
+    def runs(L):
+        try:
+            gen = torch.Generator(device=dev).manual_seed(L)
+            q, k, v, g = (torch.randn(L, H * D, device=dev, generator=gen).bfloat16() for _ in range(4))
+            ts = torch.cumsum(torch.randint(1, 10**6, (L,), device=dev, generator=gen), 0)
+            offs = torch.tensor([0, L], dtype=torch.int64, device=dev)
+            kernels.attn_fwd(q, k, v, ts, ts, offs, H, w, NB)
+            kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, NB, max_kv_len=L)
+            torch.cuda.synchronize()
+            ok = True
+        except torch.OutOfMemoryError:
+            ok = False
+        except RuntimeError as e:  # allocation failures surfaced by the extension
+            if "out of memory" not in str(e).lower():
+                raise
+            ok = False
+        torch.cuda.empty_cache()
+        return ok
+
+    t0 = time.time()
+    lo, hi, L = 0, None, 16384
+    while hi is None and L <= (1 << 21):
+        if runs(L):
+            lo, L = L, 2 * L
+        else:
+            hi = L
+    if hi is not None:
+        while hi - lo > 4096:
+            mid = (lo + hi) // 2 // 4096 * 4096
+            if runs(mid):
+                lo = mid
+            else:
+                hi = mid
+    free, total = torch.cuda.mem_get_info(dev)
+    return {"value": lo, "unit": "tokens", "cp": 1, "batch": 1, "heads": H, "head_dim": D,
+            "first_failure": hi, "gpu_memory_gb": round(total / 1e9, 1), "granularity": 4096,
+            "binding_term": "bf16 dS scratch, 2*H*L^2 bytes (backward)", "probe_s": round(time.time() - t0, 1)}
 
 
 def _traffic(which: str):
@@ -434,6 +486,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a captured CUDA graph")
+    ap.add_argument("--no-max-len", action="store_true", help="skip the max-supported-sequence-length probe")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
