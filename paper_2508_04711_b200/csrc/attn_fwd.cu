@@ -163,22 +163,44 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         ++pend_head;
         --n_pend;
       };
+      // The next item's Q is issued right after this item's second K tile (its
+      // buffer frees when the previous item's last S retires, which the K ring
+      // has just waited for), so the Q load overlaps this item's tiles.
       uint32_t rk = 0;
-      for (int g; (g = ring_produce(ring, rk, &p.wl.hdr->next_item[0], total)) >= 0;) {
-        const int2 it = p.wl.fwd[g / H];
-        const int h = g % H;
-        const Seg sg = load_seg(p.seg, it.x);
-        const int n = (int)((fwd_kv_lim(sg, it.y) + kBN - 1) / kBN);
-        if (n == 0) continue;
+      struct Item {
+        int g, h, n;
+        int2 it;
+        Seg sg;
+      };
+      auto next_item = [&](Item& x) -> bool {
+        while ((x.g = ring_produce(ring, rk, &p.wl.hdr->next_item[0], total)) >= 0) {
+          x.it = p.wl.fwd[x.g / H];
+          x.h = x.g % H;
+          x.sg = load_seg(p.seg, x.it.x);
+          x.n = (int)((fwd_kv_lim(x.sg, x.it.y) + kBN - 1) / kBN);
+          if (x.n > 0) return true;  // (items without visible kv are skipped by every role)
+        }
+        return false;
+      };
+      auto load_q = [&](const Item& x) {
         const int qb = q_it & 1;
         mbar_wait(&q_empty[qb], ((q_it >> 1) & 1) ^ 1);
-        trace_ev(p, 0, tcnt, 1, g);
+        trace_ev(p, 0, tcnt, 1, x.g);
         mbar_expect_tx(&q_full[qb], C::TILE_BYTES + kTsBytes);
-        const int32_t qrow = (int32_t)(sg.q_row0 + (int64_t)it.y * kBM);
+        const int32_t qrow = (int32_t)(x.sg.q_row0 + (int64_t)x.it.y * kBM);
         for (int pn = 0; pn < C::PANELS; ++pn)
-          tma_load_2d(smem + C::Q_OFF + qb * C::TILE_BYTES + pn * 16384, &tm_q, h * D + pn * 64, qrow, &q_full[qb]);
+          tma_load_2d(smem + C::Q_OFF + qb * C::TILE_BYTES + pn * 16384, &tm_q, x.h * D + pn * 64, qrow,
+                      &q_full[qb]);
         tma_load_1d(s_tsq + qb * kTsSlot, &tm_tsq, qrow & ~1, &q_full[qb]);
         ++q_it;
+      };
+      Item cur, nxt;
+      bool have = next_item(cur);
+      if (have) load_q(cur);
+      while (have) {
+        const Seg& sg = cur.sg;
+        const int h = cur.h, n = cur.n;
+        bool have_next = false;
         for (int j = 0; j < n; ++j) {
           const int st = k_it % NS;
           const int ts = k_it % kTsRing;
@@ -197,7 +219,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           pend_col[slot] = h * D;
           ++n_pend;
           if (n_pend > kLag) load_v();
+          if (j == (n > 1 ? 1 : 0)) {
+            have_next = next_item(nxt);
+            if (have_next) load_q(nxt);
+          }
         }
+        have = have_next;
+        cur = nxt;
       }
       while (n_pend) load_v();
     }

@@ -35,11 +35,12 @@ for name in ("fwd", "bwd"):
     bw0, bw1 = raw[3072], raw[3073]
     print(f"{name}: build_work {(bw1 - bw0) / 1e3:.1f} us")
     prev_end = bw1
-    for kern in range(1 if name == "fwd" else 2):
+    for kern in ([2] if name == "fwd" else [0, 1]):
         t = buf.cpu().numpy()[1024 * kern: 1024 * kern + 2 * 148].reshape(148, 2).astype(np.float64)
         t0 = t[:, 0].min()
         busy = (t[:, 1] - t[:, 0]) / 1e3
         end = (t[:, 1] - t0) / 1e3
+        print(np.sort(busy).round(1))
         print(f"{name}[{kern}]: busy us min {busy.min():.1f} mean {busy.mean():.1f} max {busy.max():.1f}; "
               f"end us min {end.min():.1f} max {end.max():.1f}; start spread {(t[:, 0].max() - t0) / 1e3:.1f}; "
               f"gap from previous kernel's end {(t0 - prev_end) / 1e3:.1f}")
