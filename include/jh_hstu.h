@@ -146,6 +146,9 @@ typedef struct jh_attn_args {
    * untouched).  Row stride of out_accum = ld_o (elements). */
   float* out_accum;
   int32_t out_accum_mode;
+  /* backward: add dq (fp32) into dq_accum instead of writing the bf16 `dq`
+   * (row stride ld_dq; rows of q with no visible kv are left untouched), or NULL */
+  float* dq_accum;
 } jh_attn_args;
 
 /* kv_len_total = sum over segments of kv_len[s] (= q_rows when kv_len is NULL). */

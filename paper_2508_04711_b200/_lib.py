@@ -45,6 +45,7 @@ class JhAttnArgs(ctypes.Structure):
         ("trace", c_vp), ("trace_cta", ctypes.c_int32),
         ("ds_scratch", c_vp), ("ds_scratch_bytes", ctypes.c_size_t),
         ("out_accum", c_vp), ("out_accum_mode", ctypes.c_int32),
+        ("dq_accum", c_vp),
     ]
 
 

@@ -19,8 +19,11 @@ restore_outputs), plus the backward pass the reference leaves out
    block, resident rows only) into an fp32 accumulator; once the gather lands,
    the gathered rows are re-ordered into sequence order and each chunk adds
    its remote part, the sequence prefix [0, chunk start) (all visible);
-4. backward: dK/dV partials for the whole group batch are reduced to their
-   owners with reduce-scatter, d_ts_weights is all-reduced;
+4. backward, mirrored: the remote part (chunk vs gathered prefix) first; its
+   dK/dV partials for the whole group batch are reduced to their owners with
+   reduce-scatter on the communication stream while the local part (chunk vs
+   itself, dK/dV on resident rows) runs; dQ accumulates both parts in fp32;
+   d_ts_weights is all-reduced;
 5. restore = the inverse all-to-all (cp_engine.py:468-525).
 
 Gradient semantics for DDP composition: ts_weights gradients are SUMMED over
@@ -147,6 +150,13 @@ class GpuBackend:
                                             kv_len=kl, kv_len_total=kvt, accumulate_dkv=True, max_kv_len=max_kv)
         return dq, dk, dv, dw
 
+    def bwd_partial(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb, dq_acc):
+        qo, qp, ks, kl, kvt, max_kv = segs
+        _, dk, dv, dw, _ = self.k.attn_bwd(q, k, v, ts_q, ts_k, qo, g, H, w, nb, q_pos0=qp, kv_start=ks, kv_len=kl,
+                                           kv_len_total=kvt, accumulate_dkv=True, max_kv_len=max_kv,
+                                           dq_accum=dq_acc)
+        return dk, dv, dw
+
 
 class CPAttention:
     """Context-parallel jagged HSTU attention over a process group."""
@@ -160,7 +170,7 @@ class CPAttention:
         self.nb = num_buckets
         self.mode = balance_mode
         self.be = backend if backend is not None else GpuBackend()
-        self.overlap = overlap and hasattr(self.be, "fwd_partial")
+        self.overlap = overlap and hasattr(self.be, "fwd_partial") and hasattr(self.be, "bwd_partial")
         self._plans: dict = {}
 
     # ---------------------------------------------------------------- plan
@@ -229,7 +239,7 @@ class CPAttention:
         else:
             k_s, v_s, ts_s, o_r = self._forward_overlapped(q_r, k_r, v_r, ts_r, p, dev, w)
         out = self._restore(o_r, p, dev, q.shape[0])
-        ctx = (p, dev, q_r, k_s, v_s, ts_r, ts_s, q.shape[0])
+        ctx = (p, dev, q_r, k_s, v_s, ts_r, ts_s, q.shape[0], k_r, v_r)
         return out, ctx
 
     def _forward_overlapped(self, q_r, k_r, v_r, ts_r, p, dev, w):
@@ -260,16 +270,46 @@ class CPAttention:
 
     def backward(self, ctx, g, w):
         """Upstream gradient (local rows) -> (dq, dk, dv local; d_ts_weights summed over CP)."""
-        p, dev, q_r, k_s, v_s, ts_r, ts_s, n_local = ctx
+        p, dev, q_r, k_s, v_s, ts_r, ts_s, n_local, k_r, v_r = ctx
         g_r = self._redistribute(g, p, dev)
-        dq_r, dk_s, dv_s, dw = self.be.bwd(q_r, k_s, v_s, ts_r, ts_s, dev["segs"], g_r, self.H, w, self.nb)
-        dk_r = self._reduce_to_owner(dk_s, p, dev).to(q_r.dtype)
-        dv_r = self._reduce_to_owner(dv_s, p, dev).to(q_r.dtype)
+        if not self.overlap:
+            dq_r, dk_s, dv_s, dw = self.be.bwd(q_r, k_s, v_s, ts_r, ts_s, dev["segs"], g_r, self.H, w, self.nb)
+            dk_r = self._reduce_to_owner(dk_s, p, dev).to(q_r.dtype)
+            dv_r = self._reduce_to_owner(dv_s, p, dev).to(q_r.dtype)
+        else:
+            dq_r, dk_r, dv_r, dw = self._backward_overlapped(q_r, k_r, v_r, k_s, v_s, ts_r, ts_s, g_r, p, dev, w)
         dist.all_reduce(dw, group=self.group)
         dq = self._restore(dq_r, p, dev, n_local)
         dk = self._restore(dk_r, p, dev, n_local)
         dv = self._restore(dv_r, p, dev, n_local)
         return dq, dk, dv, dw
+
+    def _backward_overlapped(self, q_r, k_r, v_r, k_s, v_s, ts_r, ts_s, g_r, p, dev, w):
+        """Remote part first; its dK/dV reduce-scatter to the owners runs on the
+        communication stream while the local (chunk vs itself) part computes."""
+        acc_dt = torch.float32 if q_r.dtype in (torch.bfloat16, torch.float16) else q_r.dtype
+        dq_acc = torch.zeros(q_r.shape, dtype=acc_dt, device=q_r.device)
+        dk_s, dv_s, dw = self.be.bwd_partial(q_r, k_s, v_s, ts_r, ts_s, dev["remote_segs"], g_r, self.H, w, self.nb,
+                                             dq_acc)
+        main = torch.cuda.current_stream(q_r.device) if q_r.is_cuda else None
+        comm = self.be.comm_stream(q_r.device) if hasattr(self.be, "comm_stream") else None
+        if comm is not None:
+            comm.wait_stream(main)
+            for x in (dk_s, dv_s):
+                x.record_stream(comm)
+            with torch.cuda.stream(comm):
+                dk_red, dv_red = self._reduce_to_owner(dk_s, p, dev), self._reduce_to_owner(dv_s, p, dev)
+        else:
+            dk_red, dv_red = self._reduce_to_owner(dk_s, p, dev), self._reduce_to_owner(dv_s, p, dev)
+        dk_l, dv_l, dw_l = self.be.bwd_partial(q_r, k_r, v_r, ts_r, ts_r, dev["local_segs"], g_r, self.H, w, self.nb,
+                                               dq_acc)
+        if comm is not None:
+            main.wait_stream(comm)
+            for x in (dk_red, dv_red):
+                x.record_stream(main)
+        dk_r = (dk_red + dk_l).to(q_r.dtype)
+        dv_r = (dv_red + dv_l).to(q_r.dtype)
+        return dq_acc.to(q_r.dtype), dk_r, dv_r, dw + dw_l
 
     def bench_step(self, q, k, v, ts, local_offsets, g, w):
         lengths = np.diff(np.asarray(local_offsets))

@@ -987,9 +987,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       const int n = kv_tiles(sg, it.y);
       const int64_t nq = min((int64_t)kBM, sg.lq - (int64_t)it.y * kBM);
       const bool row_ok = r < nq;
-      __nv_bfloat16* dqrow = dq + (sg.q_row0 + (int64_t)it.y * kBM + r) * ld_dq + h * D;
+      const int64_t dq_i = (sg.q_row0 + (int64_t)it.y * kBM + r) * ld_dq + h * D;
+      __nv_bfloat16* dqrow = dq + dq_i;
       if (n == 0) {
-        if (row_ok)
+        if (row_ok && p.dq_acc == nullptr)
           for (int c = 0; c < D; c += 8) *reinterpret_cast<int4*>(dqrow + c) = make_int4(0, 0, 0, 0);
         continue;
       }
@@ -1002,7 +1003,18 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         uint32_t v[32];
         tmem_ld32(tmem + D * y + lane_off + cc, v);
         tmem_ld_wait();
-        if (row_ok) {
+        if (row_ok && p.dq_acc != nullptr) {  // fp32 partial sums (CP): add into dq_acc
+          float4* a4 = reinterpret_cast<float4*>(p.dq_acc + dq_i + cc);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float4 o = a4[i];
+            o.x += bad ? __int_as_float(0x7FC00000) : __uint_as_float(v[4 * i]);
+            o.y += __uint_as_float(v[4 * i + 1]);
+            o.z += __uint_as_float(v[4 * i + 2]);
+            o.w += __uint_as_float(v[4 * i + 3]);
+            a4[i] = o;
+          }
+        } else if (row_ok) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 32; i += 2)

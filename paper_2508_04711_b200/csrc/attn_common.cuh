@@ -343,6 +343,7 @@ struct AttnParams {
   int64_t ld_dk, ld_dv;
   float* dk_accum;
   float* dv_accum;
+  float* dq_acc;          // fp32 dq accumulate (NULL: bf16 dq)
   double* d_ts_weights;
   double* d_pos_weights;
   const uint8_t* band;    // band table (NULL: per-element bucketization everywhere)

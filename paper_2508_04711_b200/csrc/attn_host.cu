@@ -94,9 +94,11 @@ static int validate(const jh_attn_args* a, bool bwd) {
   } else {
     if (!a->d_ts_weights) return set_error(JH_ERR_INVALID, "d_ts_weights is NULL");
     if (a->num_pos > 0 && !a->d_pos_weights) return set_error(JH_ERR_INVALID, "d_pos_weights is NULL");
-    if (a->q_rows > 0 && (!a->dout || !a->dq || a->ld_do < HD || a->ld_dq < HD || (a->ld_do * 2) % 16 ||
-                          !aligned16(a->dout)))
+    if (a->q_rows > 0 && (!a->dout || !(a->dq || a->dq_accum) || a->ld_do < HD || a->ld_dq < HD ||
+                          (a->ld_do * 2) % 16 || !aligned16(a->dout)))
       return set_error(JH_ERR_INVALID, "bad dout/dq tensor");
+    if (a->q_rows > 0 && a->dq_accum && ((a->ld_dq * 4) % 16 || !aligned16(a->dq_accum)))
+      return set_error(JH_ERR_INVALID, "bad dq_accum tensor");
     if (a->kv_rows > 0) {
       if (!a->dk_accum && (!a->dk || a->ld_dk < HD)) return set_error(JH_ERR_INVALID, "bad dk tensor");
       if (!a->dv_accum && (!a->dv || a->ld_dv < HD)) return set_error(JH_ERR_INVALID, "bad dv tensor");
@@ -134,6 +136,7 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
   p->ld_dk = a->ld_dk;
   p->ld_dv = a->ld_dv;
   p->dk_accum = a->dk_accum;
+  p->dq_acc = bwd ? a->dq_accum : nullptr;
   p->dv_accum = a->dv_accum;
   p->d_ts_weights = a->d_ts_weights;
   p->d_pos_weights = a->d_pos_weights;

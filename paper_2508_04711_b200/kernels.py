@@ -246,11 +246,12 @@ def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=
 
 def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_buckets=16, pos_weights=None,
              q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, accumulate_dkv=False, prof=None,
-             max_kv_len=None):
+             max_kv_len=None, dq_accum=None):
     """Fused jagged HSTU backward (jh_attn_bwd).
 
     Returns (dq bf16, dk, dv, d_ts_weights f64, d_pos f64 or None); dk/dv are
-    bf16, or fp32 accumulators when ``accumulate_dkv`` (CP partials).
+    bf16, or fp32 accumulators when ``accumulate_dkv`` (CP partials); with
+    ``dq_accum`` (fp32, q's shape) dq is added there and returned as dq.
     ``max_kv_len`` bounds every segment's kv length (sizes the dS scratch);
     when omitted it is read back from the device (one synchronisation)."""
     w = ts_weights.to(device=q.device, dtype=torch.float32).contiguous()
@@ -258,9 +259,15 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
     a = _attn_args(q, k, v, ts_q, ts_k, q_offsets, num_heads, w, num_buckets, pw, q_pos0, kv_start, kv_len)
     _require_cuda("dout", dout, torch.bfloat16)
     _rowmajor("dout", dout)
-    dq = torch.empty_like(q)
     a.dout, a.ld_do = dout.data_ptr(), dout.stride(0)
-    a.dq, a.ld_dq = dq.data_ptr(), dq.stride(0)
+    if dq_accum is not None:
+        if dq_accum.dtype != torch.float32 or dq_accum.shape != q.shape or dq_accum.stride(1) != 1:
+            raise ValueError("dq_accum must be a float32 tensor shaped like q")
+        dq = dq_accum
+        a.dq_accum, a.ld_dq = dq.data_ptr(), dq.stride(0)
+    else:
+        dq = torch.empty_like(q)
+        a.dq, a.ld_dq = dq.data_ptr(), dq.stride(0)
     if accumulate_dkv:
         dk = torch.zeros(k.shape, dtype=torch.float32, device=k.device)
         dv = torch.zeros(v.shape, dtype=torch.float32, device=v.device)

@@ -67,6 +67,11 @@ class NumpyBackend:
         else:
             acc.copy_(out)
 
+    def bwd_partial(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb, dq_acc):
+        dq, dk, dv, dw = self.bwd(q, k, v, ts_q, ts_k, segs, g, H, w, nb)
+        dq_acc += dq
+        return dk, dv, dw
+
     def bwd(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb):
         qo, qp, ks, kl = self._segs(segs)
         Q, K, V, G = q.numpy(), k.numpy(), v.numpy(), g.numpy()
