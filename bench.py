@@ -352,7 +352,7 @@ def max_seq_len_probe(dev, w):
     this GPU (the metric's "max supported seq len" at CP=1): lengths double
     from 16K until the first out-of-memory, then a bisection to 4K granularity.
     Each probe is a real fwd+bwd through the kernels on synthetic data; the
-    binding term is the bf16 dS scratch (2*H*L^2 bytes)."""
+    binding term is the bf16 dS scratch (causal triangle, ~H*L^2 bytes)."""
     import torch
     from paper_2508_04711_b200 import kernels
 
@@ -392,7 +392,7 @@ def max_seq_len_probe(dev, w):
     free, total = torch.cuda.mem_get_info(dev)
     return {"value": lo, "unit": "tokens", "cp": 1, "batch": 1, "heads": H, "head_dim": D,
             "first_failure": hi, "gpu_memory_gb": round(total / 1e9, 1), "granularity": 4096,
-            "binding_term": "bf16 dS scratch, 2*H*L^2 bytes (backward)", "probe_s": round(time.time() - t0, 1)}
+            "binding_term": "bf16 dS scratch (backward), causal triangle of 16 KB blocks, ~H*L^2 bytes", "probe_s": round(time.time() - t0, 1)}
 
 
 def _traffic(which: str):

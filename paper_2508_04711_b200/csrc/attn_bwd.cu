@@ -387,8 +387,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // the dQ kernel reads q halves in pairs: the partner of the first visible
         // half sees nothing of this kv tile, its dS^T block is zero
         int4* z = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(p.ds) +
-                                          (p.wl.ds_base[it.x] * H + (int64_t)(h * ds_nkt(sg) + it.y) * nh + h0 - 1) *
-                                              kDsBlockBytes + r * 128);
+                                          (ds_block0(p.wl, sg, it.x, h, H, it.y) + h0 - 1) * kDsBlockBytes + r * 128);
 #pragma unroll
         for (int i = 0; i < 8; ++i) z[i] = make_int4(0, 0, 0, 0);
       }
@@ -403,8 +402,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const bool warp_k_ok = k_hi < sg.kv_len;
       const int64_t band_q0 = band_group(sg, it.x, 0);
       // this thread's dS^T row in the scratch block of (segment, head, kv tile, half 0)
-      uint8_t* ds_row = reinterpret_cast<uint8_t*>(p.ds) +
-                        ((p.wl.ds_base[it.x] * H + (int64_t)(h * ds_nkt(sg) + it.y) * nh) * kDsBlockBytes) + r * 128;
+      uint8_t* ds_row = reinterpret_cast<uint8_t*>(p.ds) + ds_block0(p.wl, sg, it.x, h, H, it.y) * kDsBlockBytes +
+                        r * 128;
       for (int t = h0; t < nh; ++t, ++hc) {
         int4* ds_out = reinterpret_cast<int4*>(ds_row + (int64_t)t * kDsBlockBytes);
         const int st = hc % kQStages;
@@ -901,7 +900,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         const int h = g % H;
         const Seg sg = load_seg(p.seg, it.x);
         const int n = kv_tiles(sg, it.y);
-        const int nh = ds_nh(sg), nkt = ds_nkt(sg);
+        const int nkt = ds_nkt(sg);
         if (n > 0) {
           // wait until the dK/dV kernel finished every kv tile of (segment, head)
           const int32_t* cnt = p.wl.dep + kDepBase + (int64_t)it.x * H + h;
@@ -915,7 +914,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           uint8_t* sb = smem + st * C::STAGE;
           // blocks (j, 2i) and (j, 2i+1); the second one may not exist (odd half
           // count): whatever is loaded only feeds q rows past the segment
-          const int64_t blk = p.wl.ds_base[it.x] * H + (int64_t)(h * nkt + j) * nh + 2 * it.y;
+          const int64_t blk = ds_block0(p.wl, sg, it.x, h, H, j) + 2 * it.y;
           tma_load_2d_hint(sb, &tm_ds, 0, (int32_t)(blk * 128), &full[st], pol_once);  // read once
           tma_load_2d_hint(sb + kDsBlockBytes, &tm_ds, 0, (int32_t)((blk + 1) * 128), &full[st], pol_once);
           const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)j * kBN);

@@ -100,12 +100,30 @@ JH_DEV const uint8_t* band_chunk(const uint8_t* band, int64_t qgroup_global, int
   return band + (qgroup_global * kBandNW + wi) * (int64_t)kBandChunk;
 }
 
-// Backward dS scratch: per (segment, head) a dense grid of blocks, one per
-// (128-row kv tile j, 64-row q half t), each the bf16 dS^T tile [128 kv][64 q]
-// (16 KB, row-major); block (s, h, j, t) = ds_base[s] * H + (h * nkt + j) * nh + t.
+// Backward dS scratch: per (segment, head) the causal triangle of blocks, one
+// per (128-row kv tile j, 64-row q half t) with t >= ds_tlo(j) (the first
+// half that sees tile j, rounded down to even so the dQ kernel can read
+// halves in pairs), each the bf16 dS^T tile [128 kv][64 q] (16 KB,
+// row-major).  Block (s, h, j, t) = ds_base[s] * H + h * ds_cnt(s) +
+// ds_off(j) + t - ds_tlo(j), ds_off(j) = sum_{j' < j} (nh - ds_tlo(j')) in
+// closed form (ds_tlo(j) = 2 max(0, j - ceil(qp0 / 128))).
 constexpr int kDsBlockBytes = 128 * 64 * 2;
 JH_DEV int ds_nkt(const Seg& g) { return (int)((seg_kv_vis(g) + kBN - 1) / kBN); }
 JH_DEV int ds_nh(const Seg& g) { return (int)((g.lq + 63) / 64); }
+JH_DEV int ds_tlo(const Seg& g, int j) {
+  const int64_t f = (int64_t)j * kBN - g.qp0;
+  return f <= 0 ? 0 : (int)(f / kBN) * 2;
+}
+JH_DEV int64_t ds_off(const Seg& g, int j) {
+  const int64_t m = (g.qp0 + kBN - 1) / kBN;
+  const int64_t x = (int64_t)j - 1 - m;
+  return (int64_t)j * ds_nh(g) - (x >= 0 ? x * (x + 1) : 0);
+}
+JH_DEV int64_t ds_cnt(const Seg& g) { return ds_off(g, ds_nkt(g)); }
+// first block of (segment s, head h, kv tile j) minus its first half: block of half t = this + t
+JH_DEV int64_t ds_block0(const WorkLists& wl, const Seg& g, int64_t s, int h, int H, int j) {
+  return wl.ds_base[s] * H + (int64_t)h * ds_cnt(g) + ds_off(g, j) - ds_tlo(g, j);
+}
 
 constexpr int kLevels = 1024;  // work-size histogram levels (one per builder thread)
 
@@ -212,7 +230,7 @@ static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, 
       long long v = 0;
       if (s < sa.num_segments) {
         const Seg g = seg(s);
-        v = (long long)ds_nkt(g) * ds_nh(g);
+        v = (long long)ds_cnt(g);
       }
       long long tot;
       const long long ex = block_exclusive_scan(v, lsum, &tot);

@@ -238,10 +238,10 @@ using namespace jh;
 extern "C" {
 
 size_t jh_attn_ds_scratch_bytes(int64_t kv_len_total, int64_t num_segments, int32_t num_heads, int64_t max_kv_len) {
-  // sum_s ceil(kv_s / 128) * ceil(lq_s / 64) <= (ceil(kv_total / 128) + nseg) * ceil(max_kv / 64)
-  // (a segment's q rows never exceed its kv rows)
+  // causal triangle per segment: ds_cnt <= (nkt + 1)(nkt + 2), nkt = ceil(kv_s / 128)
+  // (checked over q_pos0 / length grids), summed <= (sum nkt + nseg)(max nkt + 2)
   if (kv_len_total <= 0 || num_segments <= 0 || num_heads <= 0 || max_kv_len <= 0) return (size_t)kDsBlockBytes;
-  const int64_t blocks = ((kv_len_total + kBN - 1) / kBN + num_segments) * ((max_kv_len + 63) / 64);
+  const int64_t blocks = ((kv_len_total + kBN - 1) / kBN + 2 * num_segments) * ((max_kv_len + kBN - 1) / kBN + 2);
   return (size_t)blocks * num_heads * kDsBlockBytes;
 }
 
