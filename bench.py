@@ -189,10 +189,12 @@ def run_gpu(args):
         tokens_total = sum(sum(x) for x in all_lens)
         flat_lens = [x for r in all_lens for x in r]
     else:
+        band = kernels.new_band_table(T, len(lens), dev)  # computed by the forward, reused by the backward
+
         def step_fn(prof=None):
-            kernels.attn_fwd(q, k, v, ts, ts, offs, H, w, NB, prof=None if prof is None else prof[0])
+            kernels.attn_fwd(q, k, v, ts, ts, offs, H, w, NB, prof=None if prof is None else prof[0], band_table=band)
             return kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, NB, prof=None if prof is None else prof[1],
-                                    max_kv_len=MAXLEN)
+                                    max_kv_len=MAXLEN, band_table=band)
         tokens_total = T
         flat_lens = [int(x) for x in lens]
 

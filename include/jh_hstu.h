@@ -149,6 +149,14 @@ typedef struct jh_attn_args {
   /* backward: add dq (fp32) into dq_accum instead of writing the bf16 `dq`
    * (row stride ld_dq; rows of q with no visible kv are left untouched), or NULL */
   float* dq_accum;
+  /* optional caller-owned band table (jh_attn_band_table_bytes bytes): the
+   * exact near-diagonal buckets, a function of ts_q, ts_k and the segment
+   * description only.  ready == 0: computed into it; ready == 1: it already
+   * holds the table for these same inputs (e.g. from the forward call of the
+   * same step) and is reused.  NULL: a private copy in the workspace. */
+  void* band_table;
+  size_t band_table_bytes;
+  int32_t band_table_ready;
 } jh_attn_args;
 
 /* kv_len_total = sum over segments of kv_len[s] (= q_rows when kv_len is NULL). */
@@ -158,6 +166,8 @@ JH_API size_t jh_attn_workspace_bytes(int64_t q_rows, int64_t kv_len_total, int6
 /* Backward dS scratch bound.  max_kv_len >= every segment's kv_len (= its
  * length when kv_len is NULL).  If the bound is violated at run time the
  * backward writes NaN into dq instead of overrunning the scratch. */
+JH_API size_t jh_attn_band_table_bytes(int64_t q_rows, int64_t num_segments);
+
 JH_API size_t jh_attn_ds_scratch_bytes(int64_t kv_len_total, int64_t num_segments, int32_t num_heads,
                                        int64_t max_kv_len);
 

@@ -46,6 +46,7 @@ class JhAttnArgs(ctypes.Structure):
         ("ds_scratch", c_vp), ("ds_scratch_bytes", ctypes.c_size_t),
         ("out_accum", c_vp), ("out_accum_mode", ctypes.c_int32),
         ("dq_accum", c_vp),
+        ("band_table", c_vp), ("band_table_bytes", ctypes.c_size_t), ("band_table_ready", ctypes.c_int32),
     ]
 
 
@@ -59,6 +60,7 @@ SIGNATURES = {
     "jh_dbias_scatter": (ctypes.c_int, [c_vp, ctypes.c_int64, c_vp, ctypes.c_int64, c_vp, ctypes.c_int, c_vp, c_vp]),
     "jh_attn_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
                                                   ctypes.c_int32]),
+    "jh_attn_band_table_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64]),
     "jh_attn_ds_scratch_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64]),
     "jh_attn_fwd": (ctypes.c_int, [ctypes.POINTER(JhAttnArgs), c_vp]),
     "jh_attn_bwd": (ctypes.c_int, [ctypes.POINTER(JhAttnArgs), c_vp]),

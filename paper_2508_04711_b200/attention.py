@@ -165,16 +165,18 @@ def hstu_attention_backward(inputs: AttentionInputs, upstream: JaggedTensor) -> 
 class _HSTUAttentionFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, q, k, v, ts_weights, ts, offsets, num_heads, num_buckets, pos_weights):
-        out = kernels.attn_fwd(q, k, v, ts, ts, offsets, num_heads, ts_weights, num_buckets, pos_weights)
+        band = kernels.new_band_table(q.shape[0], offsets.numel() - 1, q.device) if pos_weights is None else None
+        out = kernels.attn_fwd(q, k, v, ts, ts, offsets, num_heads, ts_weights, num_buckets, pos_weights,
+                               band_table=band)
         ctx.save_for_backward(q, k, v, ts_weights, ts, offsets, pos_weights)
-        ctx.num_heads, ctx.num_buckets = num_heads, num_buckets
+        ctx.num_heads, ctx.num_buckets, ctx.band = num_heads, num_buckets, band
         return out
 
     @staticmethod
     def backward(ctx, g):
         q, k, v, w, ts, offsets, pw = ctx.saved_tensors
         dq, dk, dv, dw, dpos = kernels.attn_bwd(q, k, v, ts, ts, offsets, g.to(torch.bfloat16).contiguous(),
-                                                ctx.num_heads, w, ctx.num_buckets, pw)
+                                                ctx.num_heads, w, ctx.num_buckets, pw, band_table=ctx.band)
         return (dq, dk, dv, dw.to(w.dtype), None, None, None, None,
                 None if dpos is None else dpos.to(pw.dtype))
 

@@ -179,6 +179,13 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
   // a positional bias (its general chunks keep the per-element path) or JH_DBG & 4
   const bool use_band = a->num_pos == 0 && !(p->dbg & 4);
   p->band = use_band ? (const uint8_t*)(ws + band_off) : nullptr;
+  bool band_ready = false;
+  if (use_band && a->band_table != nullptr) {
+    if (a->band_table_bytes < band_bytes(a->q_rows, a->num_segments) || (uintptr_t)a->band_table % 16)
+      return set_error(JH_ERR_INVALID, "band_table smaller than jh_attn_band_table_bytes() or misaligned");
+    p->band = (const uint8_t*)a->band_table;
+    band_ready = a->band_table_ready != 0;
+  }
   p->tb_glob = bwd ? (float*)(ws + tbg_off) : nullptr;
   const uint64_t HD = (uint64_t)a->num_heads * a->head_dim;
   if ((uintptr_t)a->ts_q % 16 || (uintptr_t)a->ts_k % 16)
@@ -208,7 +215,7 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
   // work-list build as its programmatic dependent (runs concurrently; it waits
   // for the table at its end, so the attention kernel's wait covers both)
   cudaError_t e;
-  if (p->band) {
+  if (p->band && !band_ready) {
     const size_t warps = (band_groups_bound(a->q_rows, a->num_segments) + 1) * kBandNW;
     band_table_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(p->seg, a->ts_q, a->ts_k, p->bias, (uint8_t*)p->band);
     e = cudaGetLastError();
@@ -223,7 +230,7 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
     la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     la[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = la;
-    cfg.numAttrs = p->band ? 1 : 0;
+    cfg.numAttrs = (p->band && !band_ready) ? 1 : 0;
     e = cudaLaunchKernelEx(&cfg, build_work_kernel, p->seg, p->wl,
                            (unsigned long long*)(p->trace_cta == -1 ? p->trace : nullptr));
     if (e != cudaSuccess) return set_error(JH_ERR_CUDA, "build_work: %s", cudaGetErrorString(e));
@@ -236,6 +243,10 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
 using namespace jh;
 
 extern "C" {
+
+size_t jh_attn_band_table_bytes(int64_t q_rows, int64_t num_segments) {
+  return band_bytes(std::max<int64_t>(q_rows, 0), std::max<int64_t>(num_segments, 0));
+}
 
 size_t jh_attn_ds_scratch_bytes(int64_t kv_len_total, int64_t num_segments, int32_t num_heads, int64_t max_kv_len) {
   // causal triangle per segment: ds_cnt <= (nkt + 1)(nkt + 2), nkt = ceil(kv_s / 128)

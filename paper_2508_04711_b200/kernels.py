@@ -190,6 +190,22 @@ def _attn_args(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_bucket
     return a
 
 
+def band_table_bytes(q_rows: int, num_segments: int) -> int:
+    return int(_lib.lib().jh_attn_band_table_bytes(int(q_rows), int(num_segments)))
+
+
+def new_band_table(q_rows: int, num_segments: int, device) -> torch.Tensor:
+    """Caller-owned band table shared by a forward and a backward call."""
+    return torch.empty(band_table_bytes(q_rows, num_segments), dtype=torch.uint8, device=device)
+
+
+def _band(a, band_table, ready: bool) -> None:
+    if band_table is not None:
+        if band_table.dtype != torch.uint8 or not band_table.is_cuda:
+            raise ValueError("band_table must be a uint8 CUDA tensor (see new_band_table)")
+        a.band_table, a.band_table_bytes, a.band_table_ready = band_table.data_ptr(), band_table.numel(), int(ready)
+
+
 def _workspace(q_rows, kv_total, nseg, H, d, device):
     nbytes = _lib.lib().jh_attn_workspace_bytes(q_rows, kv_total, nseg, H, d)
     return torch.empty(nbytes, dtype=torch.uint8, device=device), nbytes
@@ -217,12 +233,14 @@ def _prof(a, prof):
 
 def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=16, pos_weights=None,
              q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, out=None, prof=None, out_accum=None,
-             accumulate=False):
+             accumulate=False, band_table=None):
     """Fused jagged HSTU forward (jh_attn_fwd).  bf16 in/out, fp32 weights.
 
     ``out_accum`` (fp32, q's shape): write the fp32 result there instead of a
     bf16 ``out`` (``accumulate=True``: add it; rows that see no kv are left
-    untouched) -- the additive partials of the CP pipeline (cp_engine.py:441-450)."""
+    untouched) -- the additive partials of the CP pipeline (cp_engine.py:441-450).
+    ``band_table`` (uint8, ``band_table_bytes``): the near-diagonal bucket table
+    is computed into it, for a backward call on the same inputs to reuse."""
     w = ts_weights.to(device=q.device, dtype=torch.float32).contiguous()
     pw = None if pos_weights is None else pos_weights.to(device=q.device, dtype=torch.float32).contiguous()
     a = _attn_args(q, k, v, ts_q, ts_k, q_offsets, num_heads, w, num_buckets, pw, q_pos0, kv_start, kv_len)
@@ -238,6 +256,7 @@ def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=
     ws, nbytes = _workspace(q.shape[0], q.shape[0] if kv_len_total is None else kv_len_total, a.num_segments,
                             num_heads, a.head_dim, q.device)
     a.workspace, a.workspace_bytes = ws.data_ptr(), nbytes
+    _band(a, band_table, ready=False)
     _prof(a, prof)
     check(_lib.lib().jh_attn_fwd(ctypes.byref(a), _stream(q)), "hstu_attention forward")
     _bump(2 if pw is not None else 3)  # (band table) + work-list build + fused forward
@@ -246,12 +265,14 @@ def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=
 
 def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_buckets=16, pos_weights=None,
              q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, accumulate_dkv=False, prof=None,
-             max_kv_len=None, dq_accum=None):
+             max_kv_len=None, dq_accum=None, band_table=None):
     """Fused jagged HSTU backward (jh_attn_bwd).
 
     Returns (dq bf16, dk, dv, d_ts_weights f64, d_pos f64 or None); dk/dv are
     bf16, or fp32 accumulators when ``accumulate_dkv`` (CP partials); with
-    ``dq_accum`` (fp32, q's shape) dq is added there and returned as dq.
+    ``dq_accum`` (fp32, q's shape) dq is added there and returned as dq;
+    ``band_table`` filled by the forward call on the same inputs is reused
+    (no recomputation).
     ``max_kv_len`` bounds every segment's kv length (sizes the dS scratch);
     when omitted it is read back from the device (one synchronisation)."""
     w = ts_weights.to(device=q.device, dtype=torch.float32).contiguous()
@@ -296,9 +317,10 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
     ds_bytes = _lib.lib().jh_attn_ds_scratch_bytes(kvt, a.num_segments, num_heads, int(max_kv_len))
     ds = torch.empty(ds_bytes, dtype=torch.uint8, device=q.device)
     a.ds_scratch, a.ds_scratch_bytes = ds.data_ptr(), ds_bytes
+    _band(a, band_table, ready=True)
     _prof(a, prof)
     check(_lib.lib().jh_attn_bwd(ctypes.byref(a), _stream(q)), "hstu_attention backward")
-    _bump(3 if pw is not None else 4)  # (band table) + work-list build + dK/dV + dQ kernels
+    _bump(3 if (pw is not None or band_table is not None) else 4)  # (band table) + build + dK/dV + dQ
     return dq, dk, dv, d_w, d_pos
 
 
