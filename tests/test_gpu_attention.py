@@ -111,3 +111,54 @@ def test_bwd_matches_reference_golden(name):
     for a, b in ((dq, c["dq"]), (dk, c["dk"]), (dv, c["dv"])):
         assert row_rel(a, b)[1] <= ROW_TOL
     assert np.abs(dw - c["dw"]).max() / np.abs(c["dw"]).max() <= DW_TOL
+
+
+# ------------------------------------------------ timestamp regimes (band table)
+
+def _ts_case(lens, D, gap_max, seed, equal=False):
+    case = make_case(lens, D, seed=seed, ts_gap_max=max(gap_max, 1))
+    if equal:  # every delta 0 -> bucket 0 for every pair: nothing saturates anywhere
+        offs = case["offsets"]
+        for b in range(len(lens)):
+            case["ts"][offs[b]:offs[b + 1]] = 12345 + b
+    return case
+
+
+@pytest.mark.parametrize("gap_max,equal", [(1000, False), (1, True), (10**9, False), (30_000, False)])
+def test_fwd_bwd_timestamp_regimes(gap_max, equal):
+    # gaps << cap: unsaturated far beyond the band-table window (general path
+    # outside it); equal timestamps: bucket 0 everywhere; huge gaps: saturated
+    # right next to the diagonal; 30K: the band spans ~100 columns (window edge)
+    H = 2
+    case = _ts_case([700, 129, 1, 64, 333], H * 128, gap_max, seed=gap_max % 97 + int(equal), equal=equal)
+    got = _fwd(case, H)
+    want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], case["offsets"], case["w"], 16, H)
+    assert row_rel(got, want)[1] <= ROW_TOL
+    _check_bwd(case, H, _bwd(case, H))
+
+
+# ------------------------------------------------ full-size configs (sampled)
+
+def test_c2_full_batch_matches_oracle():
+    # the bench workload itself (BASELINE configs[1]): B=32, L<=1024, H=4, d=128,
+    # bf16; every output row checked against the oracle, d_ts_weights over the batch
+    b = synthetic(7, 0, 32, 1024, 4, 128)
+    rng = np.random.default_rng(99)
+    g = rng.standard_normal(b["q"].shape).astype(np.float32)
+    from _cases import bf16_round
+    case = dict(q=b["q"], k=b["k"], v=b["v"], g=bf16_round(g), ts=b["ts"], offsets=b["offsets"],
+                w=oracle.normal_init_ts_weights(16, 7 + 0x5EED), nb=16)
+    got = _fwd(case, 4)
+    want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], case["offsets"], case["w"], 16, 4)
+    assert row_rel(got, want)[1] <= ROW_TOL
+    _check_bwd(case, 4, _bwd(case, 4))
+
+
+def test_long_sequences_c3_lengths():
+    # C3-like lengths (up to 4096) with the reference generator's timestamps
+    H = 2
+    case = make_case([4096, 2500, 1], H * 128, seed=41)
+    got = _fwd(case, H)
+    want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], case["offsets"], case["w"], 16, H)
+    assert row_rel(got, want)[1] <= ROW_TOL
+    _check_bwd(case, H, _bwd(case, H))
