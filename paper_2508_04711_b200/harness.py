@@ -1,5 +1,5 @@
-"""Synthetic jagged batches and the error metric (mirror of
-``jaggedcp/harness.py``: harness.py:52-206).
+"""Synthetic jagged batches, the error metric and the experiment / sweep
+reports (mirror of ``jaggedcp/harness.py``: harness.py:52-368).
 
 ``gen_synthetic_batch`` draws from the same numpy RNG stream as the
 reference (``default_rng([seed, rank])``: lengths, q, k, v, starts, gaps in
@@ -19,7 +19,16 @@ from .jagged import new_int_series, new_jagged
 
 PROTOCOLS = ("allgather_split", "alltoall")
 LENGTH_DISTS = ("uniform", "lognormal")
+SCHEDULINGS = ("sequential", "threaded")
 MAX_TS_GAP_SECONDS = 1_000_000
+DTYPE_SIZES = {"bf16": 2, "f32": 4, "f64": 8}
+
+# harness.py:45-49 (same text: the report's accounting is the reference's)
+ACCOUNTING_NOTE = (
+    "residency counts value payloads (q/k/v/ts and outputs) in bytes; headers are "
+    "tallied separately; gathers retain sent data while all-to-all relinquishes it; "
+    "memory_reduction_ratio compares worst-rank redistribution peaks of the two protocols"
+)
 
 
 @dataclass(frozen=True)
@@ -59,6 +68,18 @@ class ExperimentConfig:
             raise ValueError(f"protocol must be one of {PROTOCOLS}")
         if self.balance_mode not in ("balanced_minichunk", "naive_contiguous"):
             raise ValueError("unknown balance_mode")
+        if self.dtype not in DTYPE_SIZES:
+            raise ValueError(f"dtype must be one of {sorted(DTYPE_SIZES)}")
+
+    def to_json_dict(self) -> dict:
+        """harness.py:97-113 (+ num_heads)."""
+        return {
+            "cp_size": self.cp_size, "batch_size": self.batch_size, "length_dist": self.length_dist,
+            "min_len": self.min_len, "max_len": self.max_len, "lognorm_mu": self.lognorm_mu,
+            "lognorm_sigma": self.lognorm_sigma, "max_length": self.max_length, "embed_dim": self.embed_dim,
+            "num_buckets": self.num_buckets, "dtype": self.dtype, "protocol": self.protocol,
+            "balance_mode": self.balance_mode, "seed": self.seed, "num_heads": self.num_heads,
+        }
 
 
 def draw_lengths(cfg: ExperimentConfig, rng: np.random.Generator) -> np.ndarray:
@@ -120,3 +141,174 @@ def output_errors(got, want) -> tuple[float, float]:
         max_abs = max(max_abs, float(diff.max()))
         max_rel = max(max_rel, float((diff.max(axis=1) / np.maximum(1.0, ref.max(axis=1))).max()))
     return max_abs, max_rel
+
+
+# --------------------------------------------------------------- experiment
+
+def concat_batches(batches):
+    """harness.py:155-170: the CP group's combined batch, sequences in rank order."""
+    from .cp_engine import QKVBatch
+    offs = [0]
+    for b in batches:
+        base = offs[-1]
+        offs.extend(int(base + o) for o in b.q.host_offsets[1:])
+    offs = np.asarray(offs, dtype=np.int64)
+    ml = max(b.q.max_length for b in batches)
+    cat = lambda f: torch.cat([getattr(b, f).values for b in batches])  # noqa: E731
+    return QKVBatch(q=new_jagged(cat("q"), offs, ml, copy=False), k=new_jagged(cat("k"), offs, ml, copy=False),
+                    v=new_jagged(cat("v"), offs, ml, copy=False), ts=new_int_series(cat("ts"), offs))
+
+
+def reference_outputs(batches, params, bias_cfg, num_heads: int = 1):
+    """harness.py:173-186: single-device forward over the combined batch (the
+    fused kernel), split back per rank."""
+    from .attention import AttentionInputs, hstu_attention_reference
+    from .jagged import JaggedTensor
+    c = concat_batches(batches)
+    out = hstu_attention_reference(AttentionInputs(c.q, c.k, c.v, c.ts, params, bias_cfg, num_heads=num_heads))
+    res, row = [], 0
+    for b in batches:
+        n = int(b.q.host_offsets[-1])
+        res.append(JaggedTensor(out.values[row:row + n], b.q.offsets, b.q.max_length, b.q.host_offsets))
+        row += n
+    return res
+
+
+def redistribution_peaks(batches, cp_size: int, balance_mode: str, protocol: str) -> list:
+    """harness.py:256-267: per-rank peak resident bytes of one redistribution protocol."""
+    from .comm import RankGroup
+    from .cp_engine import build_shard_plan, redistribute_allgather_split, redistribute_alltoall
+    from .jagged import lengths
+    plan = build_shard_plan([lengths(b.q).tolist() for b in batches], cp_size, balance_mode)
+    fn = redistribute_allgather_split if protocol == "allgather_split" else redistribute_alltoall
+    _, stats = fn(RankGroup(cp_size), batches, plan)
+    return [s.peak_resident_bytes for s in stats]
+
+
+@dataclass
+class ExperimentReport:
+    """harness.py:213-253 (same JSON schema; the GPU timing of the pipeline is
+    reported under ``metadata.gpu``)."""
+
+    config: ExperimentConfig
+    max_abs_error: float
+    max_rel_error: float
+    redistribute_stats: list
+    ring_stats: list
+    restore_stats: list
+    flops_per_rank: list
+    flops_total: int
+    flops_max_mean_ratio: float
+    resident_tokens_per_rank: list
+    per_rank_peak_resident_bytes: list
+    redistribute_peak_allgather: list
+    redistribute_peak_alltoall: list
+    memory_reduction_ratio: float
+    gpu: dict
+
+    def to_json_dict(self) -> dict:
+        st = lambda xs: [x.to_json_dict() for x in xs]  # noqa: E731
+        return {
+            "config": self.config.to_json_dict(),
+            "max_abs_error": self.max_abs_error,
+            "max_rel_error": self.max_rel_error,
+            "comm": {"redistribute": st(self.redistribute_stats), "ring": st(self.ring_stats),
+                     "restore": st(self.restore_stats)},
+            "flops": {"per_rank": self.flops_per_rank, "total": self.flops_total,
+                      "max_mean_ratio": self.flops_max_mean_ratio},
+            "resident_tokens_per_rank": self.resident_tokens_per_rank,
+            "per_rank_peak_resident_bytes": self.per_rank_peak_resident_bytes,
+            "redistribute_peak_bytes": {"allgather_split": self.redistribute_peak_allgather,
+                                        "alltoall": self.redistribute_peak_alltoall},
+            "memory_reduction_ratio": self.memory_reduction_ratio,
+            "metadata": {"accounting": ACCOUNTING_NOTE, "gpu": self.gpu},
+        }
+
+
+def run_experiment(cfg: ExperimentConfig, scheduling: str = "sequential", device=None) -> ExperimentReport:
+    """harness.py:270-316 on the GPU path: the CP pipeline (cp_engine.run_pipeline,
+    fused kernels) against the single-device fused forward, plus both
+    protocols' redistribution peaks; ``metadata.gpu`` carries the pipeline's
+    device time (CUDA events)."""
+    from .cp_engine import run_pipeline
+    if scheduling not in SCHEDULINGS:
+        raise ValueError(f"unknown scheduling {scheduling!r}")
+    batches = [gen_synthetic_batch(cfg, r, device) for r in range(cfg.cp_size)]
+    params, bias_cfg = bias_for_config(cfg)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    result = run_pipeline(batches, cfg.cp_size, cfg.protocol, cfg.balance_mode, params, bias_cfg, scheduling,
+                          num_heads=cfg.num_heads)
+    ev[1].record()
+    want = reference_outputs(batches, params, bias_cfg, cfg.num_heads)
+    max_abs, max_rel = output_errors(result.outputs, want)
+    if not (np.isfinite(max_abs) and np.isfinite(max_rel)):
+        raise RuntimeError(f"non-finite equivalence error: abs={max_abs} rel={max_rel}")
+    ag = redistribution_peaks(batches, cfg.cp_size, cfg.balance_mode, "allgather_split")
+    a2a = redistribution_peaks(batches, cfg.cp_size, cfg.balance_mode, "alltoall")
+    reduction = 1.0 - (max(a2a) / max(ag)) if max(ag) else 0.0
+    torch.cuda.synchronize()
+    gpu = {"pipeline_ms": float(ev[0].elapsed_time(ev[1])), "device": torch.cuda.get_device_name(),
+           "note": "global-view pipeline on one device (simulated collectives, fused sm_100a kernels)"}
+    return ExperimentReport(cfg, max_abs, max_rel, result.redistribute_stats, result.ring_stats,
+                            result.restore_stats, list(result.flops.per_rank), result.flops.total,
+                            result.flops.max_mean_ratio, list(result.resident_tokens),
+                            list(result.peak_resident_bytes), ag, a2a, reduction, gpu)
+
+
+# ------------------------------------------------------- memory-budget sweep
+
+def modeled_rank_bytes(seq_length: int, cp_size: int, embed_dim: int, dtype_size: int) -> int:
+    """harness.py:321-341: modelled per-rank peak for one sequence under the
+    balanced shard (q/k/v/ts slabs + output slab + the largest score block)."""
+    from .jagged import chunk_assignment, make_minichunks
+    sizes = make_minichunks([seq_length], cp_size).chunk_lengths[0]
+    t = max(sizes[a] + sizes[b] for a, b in chunk_assignment(cp_size).values())
+    largest = max(sizes)
+    return t * (3 * embed_dim * dtype_size + 8) + t * embed_dim * dtype_size + t * largest * dtype_size
+
+
+@dataclass
+class SweepReport:
+    """harness.py:344-366."""
+
+    budget_bytes: int
+    embed_dim: int
+    dtype: str
+    seed: int
+    rows: list
+
+    def to_json_dict(self) -> dict:
+        return {"budget_bytes": self.budget_bytes, "embed_dim": self.embed_dim, "dtype": self.dtype,
+                "seed": self.seed, "rows": self.rows,
+                "metadata": {"model": "per-rank token slabs (q/k/v/ts + output) plus largest score block; "
+                             "balanced mini-chunk shard of a single sequence"}}
+
+
+def sweep_max_tokens(budget_bytes: int, cp_sizes, embed_dim: int = 8, dtype: str = "f32", seed: int = 0) -> SweepReport:
+    """harness.py:369-394: largest single-sequence length whose modelled per-rank
+    footprint fits the budget, per CP size (the model is monotone: doubling,
+    then bisection).  ``bench.py`` reports the measured counterpart on the GPU
+    (max_seq_len)."""
+    if dtype not in DTYPE_SIZES:
+        raise ValueError(f"dtype must be one of {sorted(DTYPE_SIZES)}")
+    ds = DTYPE_SIZES[dtype]
+    rows = []
+    for cp in cp_sizes:
+        if cp < 1:
+            raise ValueError("cp sizes must be >= 1")
+        if modeled_rank_bytes(1, cp, embed_dim, ds) > budget_bytes:
+            raise ValueError(f"budget {budget_bytes} too small for a single token at cp={cp}")
+        lo, hi = 1, 2
+        while modeled_rank_bytes(hi, cp, embed_dim, ds) <= budget_bytes:
+            lo, hi = hi, hi * 2
+            if hi > 1 << 31:
+                break
+        while lo + 1 < hi:
+            mid = (lo + hi) // 2
+            if modeled_rank_bytes(mid, cp, embed_dim, ds) <= budget_bytes:
+                lo = mid
+            else:
+                hi = mid
+        rows.append({"cp_size": int(cp), "max_supported_length": int(lo)})
+    return SweepReport(int(budget_bytes), embed_dim, dtype, seed, rows)
