@@ -104,7 +104,6 @@ def gather_rows(src: torch.Tensor, perm: torch.Tensor, out: torch.Tensor | None 
     _require_cuda("perm", perm, torch.int64)
     s = src.contiguous()
     rows = perm.numel()
-    row_bytes = s[0].numel() * s.element_size() if s.shape[0] else (s.numel() and 0)
     if out is None:
         out = torch.empty((rows,) + tuple(s.shape[1:]), dtype=s.dtype, device=s.device)
     if rows:
@@ -162,8 +161,15 @@ def _attn_args(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_bucket
     for name, t in (("q", q), ("k", k), ("v", v)):
         _require_cuda(name, t, torch.bfloat16)
         _rowmajor(name, t)
-    for name, t in (("ts_q", ts_q), ("ts_k", ts_k), ("q_offsets", q_offsets)):
+    for name, t in (("ts_q", ts_q), ("ts_k", ts_k), ("q_offsets", q_offsets), ("q_pos0", q_pos0),
+                    ("kv_start", kv_start), ("kv_len", kv_len)):
+        if t is None and name not in ("ts_q", "ts_k", "q_offsets"):
+            continue
         _require_cuda(name, t, torch.int64)
+        if t.dim() != 1 or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous 1-D tensor")
+    if not ts_weights.is_contiguous() or (pos_weights is not None and not pos_weights.is_contiguous()):
+        raise ValueError("ts_weights / pos_weights must be contiguous")
     D = q.shape[1]
     if D % num_heads:
         raise ValueError(f"embed_dim {D} not divisible by num_heads {num_heads}")
