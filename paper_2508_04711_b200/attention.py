@@ -164,31 +164,36 @@ def hstu_attention_backward(inputs: AttentionInputs, upstream: JaggedTensor) -> 
 
 class _HSTUAttentionFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, ts_weights, ts, offsets, num_heads, num_buckets, pos_weights):
+    def forward(ctx, q, k, v, ts_weights, ts, offsets, num_heads, num_buckets, pos_weights, max_len):
         band = kernels.new_band_table(q.shape[0], offsets.numel() - 1, q.device) if pos_weights is None else None
         out = kernels.attn_fwd(q, k, v, ts, ts, offsets, num_heads, ts_weights, num_buckets, pos_weights,
                                band_table=band)
         ctx.save_for_backward(q, k, v, ts_weights, ts, offsets, pos_weights)
-        ctx.num_heads, ctx.num_buckets, ctx.band = num_heads, num_buckets, band
+        ctx.num_heads, ctx.num_buckets, ctx.band, ctx.max_len = num_heads, num_buckets, band, max_len
         return out
 
     @staticmethod
     def backward(ctx, g):
         q, k, v, w, ts, offsets, pw = ctx.saved_tensors
         dq, dk, dv, dw, dpos = kernels.attn_bwd(q, k, v, ts, ts, offsets, g.to(torch.bfloat16).contiguous(),
-                                                ctx.num_heads, w, ctx.num_buckets, pw, band_table=ctx.band)
+                                                ctx.num_heads, w, ctx.num_buckets, pw, band_table=ctx.band,
+                                                max_kv_len=ctx.max_len)
         return (dq, dk, dv, dw.to(w.dtype), None, None, None, None,
-                None if dpos is None else dpos.to(pw.dtype))
+                None if dpos is None else dpos.to(pw.dtype), None)
 
 
-def hstu_attention(q, k, v, ts, offsets, ts_weights, num_heads=1, num_buckets=None, pos_weights=None):
+def hstu_attention(q, k, v, ts, offsets, ts_weights, num_heads=1, num_buckets=None, pos_weights=None,
+                   max_len=None):
     """Differentiable jagged HSTU attention on device tensors.
 
     q, k, v: (T, H*d) bf16; ts: (T,) int64; offsets: (B+1,) int64 (device);
     ts_weights: (nb,) parameter.  Gradients flow to q, k, v, ts_weights (and
-    pos_weights)."""
+    pos_weights).  ``max_len`` (an upper bound of the sequence lengths, e.g.
+    the JaggedTensor's max_length) keeps the step free of host synchronisation;
+    without it the backward reads the longest length back from the device once."""
     nb = ts_weights.numel() if num_buckets is None else int(num_buckets)
-    return _HSTUAttentionFn.apply(q, k, v, ts_weights, ts, offsets, int(num_heads), nb, pos_weights)
+    return _HSTUAttentionFn.apply(q, k, v, ts_weights, ts, offsets, int(num_heads), nb, pos_weights,
+                                  None if max_len is None else int(max_len))
 
 
 class JaggedHSTUAttention(torch.nn.Module):
@@ -204,6 +209,6 @@ class JaggedHSTUAttention(torch.nn.Module):
         self.num_heads = num_heads
         self.num_buckets = num_buckets
 
-    def forward(self, q, k, v, ts, offsets):
+    def forward(self, q, k, v, ts, offsets, max_len=None):
         return hstu_attention(q, k, v, ts, offsets, self.ts_weights, self.num_heads, self.num_buckets,
-                              self.pos_weights)
+                              self.pos_weights, max_len)

@@ -188,13 +188,16 @@ def test_cp_layer_single_rank_matches_single_device():
 
 # ------------------------------------------------------------------ autograd
 
-def test_autograd_matches_kernels():
+@pytest.mark.parametrize("max_len", [None, 100])
+def test_autograd_matches_kernels(max_len):
+    # (max_len given: no host synchronisation in the step; the shared band table
+    # of the forward is reused by the backward either way)
     from paper_2508_04711_b200.attention import hstu_attention
     case = make_case([100, 40], 2 * 64, seed=9)
     c = to_cuda(case)
     q, k, v = (c[x].clone().requires_grad_(True) for x in ("q", "k", "v"))
     w = c["w"].clone().requires_grad_(True)
-    out = hstu_attention(q, k, v, c["ts"], c["offsets"], w, num_heads=2)
+    out = hstu_attention(q, k, v, c["ts"], c["offsets"], w, num_heads=2, max_len=max_len)
     out.backward(c["g"])
     dq, dk, dv, dw, _ = _k().attn_bwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], c["g"], 2, c["w"], 16)
     torch.cuda.synchronize()
