@@ -57,10 +57,10 @@ struct DkvCfg {
   static constexpr int TSQ_OFF = DO_OFF + kQStages * HTILE;       // int64 [kQStages][kTsSlotH]
   static constexpr int MAX_NB = (D == 64) ? 256 : 32;
   static constexpr int OCT_OFF = TSQ_OFF + kQStages * kTsSlotH * 8;  // OctEntry [32]
-  static constexpr int PW_OFF = OCT_OFF + 32 * 16;                   // float [1024] x c1 (D=64 only)
+  static constexpr int PW_OFF = OCT_OFF + 32 * 16;                   // float [1024] pos weights x c1
   // (the 8 int64 of padding after each ts_q box hold the stage's two chunk
   // minima; slot 0's padding also holds the TMEM base address)
-  static constexpr int WT_OFF = PW_OFF + (D == 64 ? 4096 : 0);     // float [32] band weights x c1
+  static constexpr int WT_OFF = PW_OFF + 4096;                     // float [32] band weights x c1
   static constexpr int BAR_OFF = WT_OFF + 128;
   static constexpr int NBARS = 28;
   static constexpr int RING_OFF = BAR_OFF + NBARS * 8;  // work-item ring: full[], empty[], slot[]
@@ -121,8 +121,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   cta_stamp(p, 0);
   if (smem_u32(smem) & 1023) __trap();
   oct_table_fill(s_oct, p.bias, p.ts_weights, c1, tid, blockDim.x);
-  if (D == 64)
-    for (int i = tid; i < P; i += blockDim.x) s_pwc[i] = p.pos_weights[i] * c1;
+  for (int i = tid; i < P; i += blockDim.x) s_pwc[i] = p.pos_weights[i] * c1;
   float* s_wt = reinterpret_cast<float*>(smem + C::WT_OFF);
   if (tid < 32) s_wt[tid] = tid < nb ? p.ts_weights[tid] * c1 : (tid == (int)kBandMasked ? -1e30f : 0.f);
   // this CTA's fp32 partial bins (buckets, then positions) in the workspace
@@ -1040,10 +1039,6 @@ int launch_bwd(const TMaps& tm, const AttnParams& p, const jh_attn_args& a, int 
   static_assert(C::SMEM <= 232448 && Q::SMEM <= 232448, "bwd smem budget");
   if (a.num_buckets > C::MAX_NB) {
     set_error(JH_ERR_UNSUPPORTED, "backward supports num_buckets <= %d at head_dim %d", C::MAX_NB, D);
-    return -1;
-  }
-  if (D == 128 && a.num_pos > 0) {
-    set_error(JH_ERR_UNSUPPORTED, "pos_weights backward is implemented for head_dim 64 only");
     return -1;
   }
   static bool attr = false;

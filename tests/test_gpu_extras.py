@@ -57,10 +57,10 @@ def test_num_buckets_beyond_fused_limit_is_unsupported():
 
 # --------------------------------------------------------- positional bias
 
-@pytest.mark.parametrize("P", [1, 40])
-def test_pos_bias_fwd_bwd_d64(P):
-    lens = [150, 3, 70]
-    case = make_case(lens, 64, seed=11 + P)
+@pytest.mark.parametrize("P,d", [(1, 64), (40, 64), (40, 128), (300, 128)])
+def test_pos_bias_fwd_bwd(P, d):
+    lens = [150, 3, 70, 400]
+    case = make_case(lens, d, seed=11 + P)
     pos = (np.random.default_rng(P).standard_normal(P) * 0.05).astype(np.float32)
     c = to_cuda(case)
     k = _k()
@@ -79,14 +79,6 @@ def test_pos_bias_fwd_bwd_d64(P):
     assert np.abs(dw.cpu().numpy() - ww).max() / np.abs(ww).max() <= DW_TOL
     dp = dpos.cpu().numpy()
     assert np.abs(dp - wp).max() / max(np.abs(wp).max(), 1e-30) <= DW_TOL
-
-
-def test_pos_bias_backward_d128_is_unsupported():
-    case = make_case([16], 128, seed=2)
-    c = to_cuda(case)
-    with pytest.raises(NotImplementedError):
-        _k().attn_bwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], c["g"], 1, c["w"], 16,
-                      pos_weights=torch.zeros(8, device="cuda"))
 
 
 # ------------------------------------------- segment form: global-view CP ring
