@@ -52,7 +52,9 @@ __global__ void bucketize_kernel(const int64_t* __restrict__ d, int64_t n, const
 }
 
 // ------------------------------------------------------------ compute_bias
-// out[i, j] = w[bucket(tq[i] - tk[j])]; 4 outputs per thread, row-wise.
+// out[i, j] = w[bucket(tq[i] - tk[j])].  Rows are strided over the grid, a
+// block's threads sweep the row's columns 4 at a time (one float4 store per
+// thread, no per-element index division).
 __global__ void compute_bias_kernel(const int64_t* __restrict__ tq, int64_t nq, const int64_t* __restrict__ tk,
                                     int64_t nk, const float* __restrict__ w, const __grid_constant__ DevBiasTable t,
                                     float* __restrict__ out) {
@@ -65,57 +67,74 @@ __global__ void compute_bias_kernel(const int64_t* __restrict__ tq, int64_t nq, 
   }
   for (int i = threadIdx.x; i < t.nb && i < 256; i += blockDim.x) ws[i] = w[i];
   __syncthreads();
-  const int64_t groups_per_row = (nk + 3) / 4;
-  const int64_t total = nq * groups_per_row;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = g / groups_per_row, j0 = (g - i * groups_per_row) * 4;
-    int64_t q = tq[i];
-    float v[4];
+  const bool vec = (nk & 3) == 0;
+  for (int64_t i = blockIdx.x; i < nq; i += gridDim.x) {
+    const int64_t q = tq[i];
+    float* orow = out + i * nk;
+    for (int64_t j0 = 4 * (int64_t)threadIdx.x; j0 < nk; j0 += 4 * (int64_t)blockDim.x) {
+      float v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      int64_t j = j0 + u;
-      v[u] = j < nk ? ws[bucket_of(q - tk[j], thr, base, t.cap)] : 0.f;
-    }
-    float* o = out + i * nk + j0;
-    if ((nk & 3) == 0) {
-      *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
-    } else {
-      for (int u = 0; u < 4 && j0 + u < nk; ++u) o[u] = v[u];
+      for (int u = 0; u < 4; ++u) v[u] = j0 + u < nk ? ws[bucket_of(q - tk[j0 + u], thr, base, t.cap)] : 0.f;
+      if (vec)
+        __stcs(reinterpret_cast<float4*>(orow + j0), make_float4(v[0], v[1], v[2], v[3]));  // streamed, not re-read
+      else
+        for (int u = 0; u < 4 && j0 + u < nk; ++u) orow[j0 + u] = v[u];
     }
   }
 }
 
 // ------------------------------------------------------------ dbias scatter
-// d_w[b] += sum dbias[i, j] over bucket(tq[i]-tk[j]) == b.  Per-thread fp32
-// partial for the saturated (last) bucket, fp64 smem bins for the rest.
+// d_w[b] += sum dbias[i, j] over bucket(tq[i]-tk[j]) == b.  The last bucket
+// accumulates in a register; the others in thread-private fp32 shared bins
+// (no contended atomics); each block folds its bins into fp64 and adds them
+// to d_w once.
+constexpr int kScatterBins = 32;  // thread-private bins (num_buckets <= 32); larger nb: shared fp64 atomics
 __global__ void dbias_scatter_kernel(const int64_t* __restrict__ tq, int64_t nq, const int64_t* __restrict__ tk,
                                      int64_t nk, const float* __restrict__ db, const __grid_constant__ DevBiasTable t,
                                      double* __restrict__ d_w) {
   __shared__ int64_t thr[64];
   __shared__ int32_t base[64];
   __shared__ double bins[256];
+  __shared__ float tb[kScatterBins * 256];  // [bucket][thread]
   if (threadIdx.x < 64) {
     thr[threadIdx.x] = t.thr[threadIdx.x];
     base[threadIdx.x] = t.base[threadIdx.x];
   }
+  const bool priv = t.nb <= kScatterBins;
   for (int i = threadIdx.x; i < t.nb; i += blockDim.x) bins[i] = 0.0;
+  if (priv)
+    for (int b = 0; b < t.nb; ++b) tb[b * 256 + threadIdx.x] = 0.f;
   __syncthreads();
   const int last = t.nb - 1;
   float sat = 0.f;
-  const int64_t total = nq * nk;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = g / nk, j = g - i * nk;
-    int b = bucket_of(tq[i] - tk[j], thr, base, t.cap);
-    float x = db[g];
-    if (b == last)
-      sat += x;
-    else
-      atomicAdd(&bins[b], (double)x);
+  float* my = tb + threadIdx.x;
+  for (int64_t i = blockIdx.x; i < nq; i += gridDim.x) {
+    const int64_t q = tq[i];
+    const float* drow = db + i * nk;
+    for (int64_t j = threadIdx.x; j < nk; j += blockDim.x) {
+      const int b = bucket_of(q - tk[j], thr, base, t.cap);
+      const float x = __ldcs(drow + j);  // read once
+      if (b == last)
+        sat += x;
+      else if (priv)
+        my[b * 256] += x;
+      else
+        atomicAdd(&bins[b], (double)x);
+    }
   }
-  // warp-reduce the saturated partial
   for (int o = 16; o; o >>= 1) sat += __shfl_xor_sync(0xffffffffu, sat, o);
   if ((threadIdx.x & 31) == 0) atomicAdd(&bins[last], (double)sat);
   __syncthreads();
+  if (priv) {  // warp w folds buckets w, w + 8, ...
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int b = wid; b < last; b += blockDim.x >> 5) {
+      double v = 0.0;
+      for (int k = lane; k < 256; k += 32) v += (double)tb[b * 256 + k];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) bins[b] += v;
+    }
+    __syncthreads();
+  }
   for (int i = threadIdx.x; i < t.nb; i += blockDim.x)
     if (bins[i] != 0.0) atomicAdd(&d_w[i], bins[i]);
 }
@@ -135,26 +154,34 @@ __global__ void gather_rows_kernel(const uint8_t* __restrict__ src, uint8_t* __r
   }
 }
 
-// padded[b, pos, :] <-> values[offsets[b] + pos, :]
+// padded[b, pos, :] <-> values[offsets[b] + pos, :]: one warp per padded row
+// (lanes over the row's vectors), so the index arithmetic is per row, not per
+// vector; padded_to_jagged skips padding rows entirely.
 template <typename V>
 __global__ void pad_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                            const int64_t* __restrict__ offsets, int64_t num_seqs, int64_t max_len, int64_t row_bytes,
                            int to_padded) {
-  const int64_t vec_per_row = row_bytes / sizeof(V);
-  const int64_t total = num_seqs * max_len * vec_per_row;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-    int64_t pr = g / vec_per_row, c = g - pr * vec_per_row;
-    int64_t b = pr / max_len, pos = pr - b * max_len;
-    int64_t lo = offsets[b], L = offsets[b + 1] - lo;
+  const int vpr = (int)(row_bytes / sizeof(V));
+  const int lane = threadIdx.x & 31;
+  const int64_t nrows = num_seqs * max_len;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t pr = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); pr < nrows; pr += warps) {
+    const int64_t b = pr / max_len, pos = pr - b * max_len;
+    const int64_t lo = offsets[b], L = offsets[b + 1] - lo;
     if (to_padded) {
-      V v;
-      if (pos < L)
-        v = __ldg(reinterpret_cast<const V*>(src + (lo + pos) * row_bytes) + c);
-      else
-        memset(&v, 0, sizeof(V));
-      reinterpret_cast<V*>(dst + pr * row_bytes)[c] = v;
+      V* d = reinterpret_cast<V*>(dst + pr * row_bytes);
+      if (pos < L) {
+        const V* sr = reinterpret_cast<const V*>(src + (lo + pos) * row_bytes);
+        for (int c = lane; c < vpr; c += 32) d[c] = __ldg(sr + c);
+      } else {
+        V z;
+        memset(&z, 0, sizeof(V));
+        for (int c = lane; c < vpr; c += 32) d[c] = z;
+      }
     } else if (pos < L) {
-      reinterpret_cast<V*>(dst + (lo + pos) * row_bytes)[c] = __ldg(reinterpret_cast<const V*>(src + pr * row_bytes) + c);
+      const V* sr = reinterpret_cast<const V*>(src + pr * row_bytes);
+      V* d = reinterpret_cast<V*>(dst + (lo + pos) * row_bytes);
+      for (int c = lane; c < vpr; c += 32) d[c] = __ldg(sr + c);
     }
   }
 }
@@ -187,8 +214,8 @@ int jh_compute_bias(const int64_t* ts_q, int64_t nq, const int64_t* ts_k, int64_
   DevBiasTable t;
   if (!fill_dev_table(num_buckets, &t)) return set_error(JH_ERR_INVALID, "num_buckets must be >= 1");
   if (nq == 0 || nk == 0) return JH_OK;
-  int64_t work = nq * ((nk + 3) / 4);
-  compute_bias_kernel<<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(ts_q, nq, ts_k, nk, ts_weights, t, out);
+  const int grid = (int)std::min<int64_t>(nq, (int64_t)num_sms() * 8);
+  compute_bias_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(ts_q, nq, ts_k, nk, ts_weights, t, out);
   return launch_check("compute_bias");
 }
 
@@ -199,7 +226,8 @@ int jh_dbias_scatter(const int64_t* ts_q, int64_t nq, const int64_t* ts_k, int64
   DevBiasTable t;
   if (!fill_dev_table(num_buckets, &t)) return set_error(JH_ERR_INVALID, "num_buckets must be >= 1");
   if (nq == 0 || nk == 0) return JH_OK;
-  dbias_scatter_kernel<<<grid_for(nq * nk, 256), 256, 0, (cudaStream_t)stream>>>(ts_q, nq, ts_k, nk, dbias, t, d_w);
+  const int grid = (int)std::min<int64_t>(nq, (int64_t)num_sms() * 4);
+  dbias_scatter_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(ts_q, nq, ts_k, nk, dbias, t, d_w);
   return launch_check("dbias_scatter");
 }
 
@@ -235,10 +263,10 @@ static int pad_common(const void* src, void* dst, const int64_t* offsets, int64_
   cudaStream_t s = (cudaStream_t)stream;
   bool v16 = (row_bytes % 16 == 0) && ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0);
   if (v16)
-    pad_kernel<int4><<<grid_for(work * row_bytes / 16, 256), 256, 0, s>>>(
+    pad_kernel<int4><<<grid_for(work * 32, 256), 256, 0, s>>>(
         (const uint8_t*)src, (uint8_t*)dst, offsets, num_seqs, max_len, row_bytes, to_padded);
   else
-    pad_kernel<int2><<<grid_for(work * row_bytes / 8, 256), 256, 0, s>>>(
+    pad_kernel<int2><<<grid_for(work * 32, 256), 256, 0, s>>>(
         (const uint8_t*)src, (uint8_t*)dst, offsets, num_seqs, max_len, row_bytes, to_padded);
   return launch_check(to_padded ? "jagged_to_padded" : "padded_to_jagged");
 }
