@@ -46,12 +46,21 @@ JH_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-// try_wait with a suspend-time hint: the waiting thread sleeps in hardware
-// until the phase completes instead of spinning through issue slots.
-// A watchdog turns a pipeline deadlock (a protocol bug) into a trap after
-// ~2^36 cycles instead of a hung GPU.
+// try_wait (the hardware holds the thread for a bounded window before
+// returning false; build with -DJH_SUSPEND_HINT for the suspend-time-hint form,
+// measured ~1.5 % slower on the C2 step).  A watchdog turns a pipeline
+// deadlock (a protocol bug) into a trap after ~2^36 cycles instead of a hung GPU.
 JH_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
+#ifndef JH_SUSPEND_HINT  // (the suspend-time hint measured ~1.5 % slower on C2)
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
@@ -59,6 +68,7 @@ JH_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680)
       : "memory");
+#endif
   return ok != 0;
 }
 JH_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
