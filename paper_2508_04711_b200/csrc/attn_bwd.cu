@@ -828,6 +828,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 //          MN-major), dQ double-buffered in TMEM
 //   warp 2 TMEM allocator;  warps 4-7 drain dQ (bf16) while the next item runs
 constexpr int kDqStages = 3;
+#ifndef JH_DQ_SLEEP_NS
+#define JH_DQ_SLEEP_NS 256  // back-off while a (segment, head) is still in the dK/dV kernel
+#endif
 constexpr int kDqThreads = 256;
 
 template <int D>
@@ -903,7 +906,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         if (n > 0) {
           // wait until the dK/dV kernel finished every kv tile of (segment, head)
           const int32_t* cnt = p.wl.dep + kDepBase + (int64_t)it.x * H + h;
-          while (ld_acquire_gpu(cnt) < nkt) __nanosleep(256);
+          while (ld_acquire_gpu(cnt) < nkt) __nanosleep(JH_DQ_SLEEP_NS);
           asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy writes -> TMA reads
         }
         for (int j = 0; j < n; ++j, ++kc) {
