@@ -394,7 +394,10 @@ JH_DEV void cta_stamp(const AttnParams& p, int which, int kernel = 0) {
 // global counter and publishes it in a small shared-memory ring that every
 // other role of the CTA consumes in the same order (longest-processing-time-
 // first scheduling without any static imbalance).
-constexpr int kItemRing = 2;
+#ifndef JH_ITEM_RING
+#define JH_ITEM_RING 2
+#endif
+constexpr int kItemRing = JH_ITEM_RING;
 struct ItemRing {
   int32_t* slot;    // [kItemRing]
   uint64_t* full;   // [kItemRing], count 1
