@@ -364,8 +364,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // dS scratch capacity (caller's max_kv_len bound); on overflow dQ becomes NaN
     const bool ds_ok = p.wl.hdr->ds_blocks * H <= p.ds_cap_blocks && !(p.dbg & 1);
     if (!ds_ok && et == 0) p.wl.hdr->ds_overflow = 1;
-    // the dS^T scratch is re-read by the dQ kernel right after: keep it in L2
+    // the dS^T scratch is re-read by the dQ kernel right after
+    // (evict_last measured ~0.5 % slower on C2: the scratch outgrows L2 anyway
+    // and pushed the forward's inputs out; build with -DJH_DS_EVICT_LAST for it)
+#ifdef JH_DS_EVICT_LAST
     const uint64_t ds_pol = l2_policy_evict_last();
+#else
+    const uint64_t ds_pol = l2_policy_evict_normal();
+#endif
     uint32_t rk = 0;
     int32_t* dep_item = nullptr;  // completion counter of the previous item (bumped one item late)
     for (int g; (g = ring_consume(ring, rk, true)) >= 0;) {

@@ -143,7 +143,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   // The K/S stream runs two kv tiles ahead of the V/PV stream, continuously
   // across work items (a small ring carries the deferred tiles' coordinates).
-  constexpr int kLag = 2;
+#ifndef JH_FWD_LAG
+#define JH_FWD_LAG 2
+#endif
+  constexpr int kLag = JH_FWD_LAG;
   if (warp == 0) {
     // ================= TMA producer: Q + ts_q per item, K + ts_k per tile, V two tiles later
     if (elect_one()) {
