@@ -157,7 +157,29 @@ typedef struct jh_attn_args {
   void* band_table;
   size_t band_table_bytes;
   int32_t band_table_ready;
+  /* score scale: scores = (q k^T + bias) * score_scale; 0 -> 1/sqrt(head_dim).
+   * Lets a caller zero-pad a smaller head dimension d to 64 / 128 columns and
+   * keep the reference's 1/sqrt(d) (attention.py:143, :180). */
+  float score_scale;
+  /* backward: 1 = deterministic two-kernel path (dK/dV kernel + dQ GEMM over a
+   * bf16 dS scratch, needs ds_scratch); 0 = fused single kernel (dQ reduced in
+   * fp32 into bwd_state, no dS scratch, O(L) memory) */
+  int32_t deterministic;
+  /* fused backward state (jh_attn_bwd_state_bytes bytes): must be all-zero the
+   * first time it is used; every fused call leaves it all-zero again.  One
+   * state buffer per concurrently running call (stream). */
+  void* bwd_state;
+  size_t bwd_state_bytes;
+  /* debug (forward): when non-NULL, head 0 writes the bucket it applied to
+   * every visible (q row, kv position) pair into dbg_buckets[q_row * dbg_ld +
+   * kv_pos] (uint8; entries of pairs it never evaluated are left untouched) */
+  uint8_t* dbg_buckets;
+  int64_t dbg_ld;
 } jh_attn_args;
+
+/* Size of the fused backward's persistent state (fp32 dQ accumulator rows +
+ * per-(q tile, head) completion counters + the d_ts_weights reduction slots). */
+JH_API size_t jh_attn_bwd_state_bytes(int64_t q_rows, int64_t num_segments, int32_t num_heads, int32_t head_dim);
 
 /* kv_len_total = sum over segments of kv_len[s] (= q_rows when kv_len is NULL). */
 JH_API size_t jh_attn_workspace_bytes(int64_t q_rows, int64_t kv_len_total, int64_t num_segments, int32_t num_heads,

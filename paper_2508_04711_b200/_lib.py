@@ -47,6 +47,9 @@ class JhAttnArgs(ctypes.Structure):
         ("out_accum", c_vp), ("out_accum_mode", ctypes.c_int32),
         ("dq_accum", c_vp),
         ("band_table", c_vp), ("band_table_bytes", ctypes.c_size_t), ("band_table_ready", ctypes.c_int32),
+        ("score_scale", ctypes.c_float), ("deterministic", ctypes.c_int32),
+        ("bwd_state", c_vp), ("bwd_state_bytes", ctypes.c_size_t),
+        ("dbg_buckets", c_vp), ("dbg_ld", ctypes.c_int64),
     ]
 
 
@@ -62,6 +65,7 @@ SIGNATURES = {
                                                   ctypes.c_int32]),
     "jh_attn_band_table_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64]),
     "jh_attn_ds_scratch_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64]),
+    "jh_attn_bwd_state_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]),
     "jh_attn_fwd": (ctypes.c_int, [ctypes.POINTER(JhAttnArgs), c_vp]),
     "jh_attn_bwd": (ctypes.c_int, [ctypes.POINTER(JhAttnArgs), c_vp]),
     "jh_gather_rows": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int64, ctypes.c_int64, c_vp]),

@@ -89,6 +89,111 @@ def compute_bias(ts_q, ts_k, params: BiasParams, cfg: BiasConfig) -> torch.Tenso
                                 cfg.num_buckets)
 
 
+def _host_i64(x) -> np.ndarray:
+    if isinstance(x, torch.Tensor):
+        x = x.detach().cpu().numpy()
+    return np.asarray(x, dtype=np.int64).reshape(-1)
+
+
+def _dev_rows(x, dtype, device) -> torch.Tensor:
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+    return t.to(device=device, dtype=dtype).contiguous()
+
+
+def _blockwise_segments(q_seq_ids, q_positions, k_seq_ids, k_positions):
+    """Host routing of blockwise_partial onto the kernel's segment form.
+
+    The keys are sorted by (sequence, position).  A query of sequence s gets an
+    effective position e in s's sorted key run: e = q_pos - p0 when the run's
+    positions are consecutive p0, p0+1, ... (e may exceed the run: every key
+    visible), otherwise e = vis - 1 with vis = #keys of s at positions <= q_pos.
+    Either way the query sees exactly the run's keys 0..e, i.e. the
+    reference's allowed set (attention.py:180-183).  Queries sorted by (s, e)
+    with consecutive e share one segment (q_pos0 = e of its first row,
+    kv = s's run); queries with e < 0 see nothing and get kv_len 0.  Returns
+    (q_perm, k_perm, q_offsets, q_pos0, kv_start, kv_len)."""
+    qs, qp, ks, kp = (_host_i64(x) for x in (q_seq_ids, q_positions, k_seq_ids, k_positions))
+    k_perm = np.lexsort((kp, ks))
+    ks_s, kp_s = ks[k_perm], kp[k_perm]
+    seqs, run_start = np.unique(ks_s, return_index=True)
+    run_len = np.diff(np.append(run_start, ks_s.size))
+    eff = np.full(qs.size, -1, dtype=np.int64)
+    rs = np.zeros(qs.size, dtype=np.int64)
+    rl = np.zeros(qs.size, dtype=np.int64)
+    if seqs.size:
+        j = np.searchsorted(seqs, qs)
+        jj = np.minimum(j, seqs.size - 1)
+        has = (j < seqs.size) & (seqs[jj] == qs)
+        consec = {}
+        for i in np.nonzero(has)[0]:
+            a, n = int(run_start[jj[i]]), int(run_len[jj[i]])
+            rs[i], rl[i] = a, n
+            if a not in consec:
+                consec[a] = bool(np.all(np.diff(kp_s[a:a + n]) == 1))
+            if consec[a]:
+                eff[i] = qp[i] - kp_s[a]
+            else:
+                eff[i] = np.searchsorted(kp_s[a:a + n], qp[i], side="right") - 1
+    eff = np.maximum(eff, -1)
+    q_perm = np.lexsort((eff, qs))
+    offs, pos0, kvs, kvl = [0], [], [], []
+    prev = None  # (sequence, eff) of the previous query row in q_perm order
+    for row, i in enumerate(q_perm):
+        if prev is None or qs[i] != prev[0]:
+            new = True
+        elif eff[i] < 0:
+            new = False  # (sorted: a sequence's blind rows come first, one kv_len-0 segment)
+        else:
+            new = prev[1] < 0 or eff[i] != prev[1] + 1
+        if new and row > 0:
+            offs.append(row)
+        if new:
+            pos0.append(max(int(eff[i]), 0))
+            kvs.append(int(rs[i]))
+            kvl.append(int(rl[i]) if eff[i] >= 0 else 0)
+        prev = (qs[i], eff[i])
+    if qs.size:
+        offs.append(qs.size)
+    a64 = lambda x: np.asarray(x, dtype=np.int64)  # noqa: E731
+    return q_perm.astype(np.int64), k_perm.astype(np.int64), a64(offs), a64(pos0), a64(kvs), a64(kvl)
+
+
+def blockwise_partial(q, q_seq_ids, q_positions, ts_q, k, k_seq_ids, k_positions, ts_k, v,
+                      params: BiasParams, cfg: BiasConfig) -> torch.Tensor:
+    """attention.py:151-184 -- attention contribution of one key/value block to
+    one query block: a pair (i, j) contributes iff both rows are in the same
+    sequence and k_positions[j] <= q_positions[i].  SiLU partials are additive,
+    so the full output is the plain sum of these over any key partition.
+
+    Runs the fused sm_100a forward in its segment form (fp32 output): keys are
+    sorted by (sequence, position) on the host plan, rows are moved by the
+    gather / scatter kernels.  Returns a float32 CUDA tensor (nq, d)."""
+    kn = k.shape[0]
+    vn = v.shape[0]
+    if kn != vn:
+        raise ValueError(f"k has {kn} rows but v has {vn}")
+    nq = q.shape[0]
+    dv = v.shape[1] if len(v.shape) == 2 else 0
+    dev = q.device if isinstance(q, torch.Tensor) and q.is_cuda else torch.device("cuda")
+    if nq == 0 or kn == 0:
+        return torch.zeros((nq, dv), dtype=torch.float32, device=dev)
+    if q.shape[1] != k.shape[1] or dv != q.shape[1]:
+        raise ValueError("q, k, v must share embed_dim")
+    q_perm, k_perm, offs, pos0, kvs, kvl = _blockwise_segments(q_seq_ids, q_positions, k_seq_ids, k_positions)
+    t = lambda a: torch.from_numpy(a).to(dev)  # noqa: E731
+    qp, kp = t(q_perm), t(k_perm)
+    qd = kernels.gather_rows(_dev_rows(q, torch.bfloat16, dev), qp)
+    kd = kernels.gather_rows(_dev_rows(k, torch.bfloat16, dev), kp)
+    vd = kernels.gather_rows(_dev_rows(v, torch.bfloat16, dev), kp)
+    tq = kernels.gather_rows(_dev_rows(_host_i64(ts_q), torch.int64, dev).view(-1, 1), qp).view(-1)
+    tk = kernels.gather_rows(_dev_rows(_host_i64(ts_k), torch.int64, dev).view(-1, 1), kp).view(-1)
+    acc = torch.empty((nq, qd.shape[1]), dtype=torch.float32, device=dev)
+    kernels.attn_fwd(qd, kd, vd, tq, tk, t(offs), 1, params.device_weights(dev), cfg.num_buckets,
+                     q_pos0=t(pos0), kv_start=t(kvs), kv_len=t(kvl), kv_len_total=int(kvl.sum()),
+                     out_accum=acc)
+    return kernels.scatter_rows(acc, qp, torch.empty_like(acc))
+
+
 @dataclass(frozen=True)
 class AttentionInputs:
     """attention.py:97-114 (+ num_heads / pos_weights extensions)."""

@@ -186,6 +186,35 @@ def _check_sched(scheduling: str) -> None:
         raise ValueError(f"unknown scheduling {scheduling!r}")
 
 
+def _map_ranks(fn, cp_size: int, scheduling: str) -> list:
+    """cp_engine.py:188-206: run a per-rank function sequentially or on a
+    thread pool (kernel launches are thread-safe; every rank's work is
+    stream-ordered on the caller's current stream); results in rank order,
+    failures re-raised as RuntimeError("rank r: ...")."""
+
+    def run(r: int):
+        try:
+            return fn(r)
+        except Exception as exc:  # annotate with the failing rank
+            raise RuntimeError(f"rank {r}: {exc}") from exc
+
+    if scheduling == "threaded" and cp_size > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        stream = torch.cuda.current_stream() if torch.cuda.is_available() else None
+
+        def run_on_stream(r: int):
+            if stream is None:
+                return run(r)
+            with torch.cuda.stream(stream):
+                return run(r)
+
+        with ThreadPoolExecutor(max_workers=cp_size) as pool:
+            futures = [pool.submit(run_on_stream, r) for r in range(cp_size)]
+            return [f.result() for f in futures]
+    _check_sched(scheduling)
+    return [run(r) for r in range(cp_size)]
+
+
 def _entries_meta(entries):
     """cp_engine.py:209-213."""
     if not entries:
@@ -230,14 +259,16 @@ def redistribute_allgather_split(group: RankGroup, batches, plan: ShardPlan, sch
     full = {n: torch.cat([getattr(b, n).values for b in batches]) for n in ("q", "k", "v", "ts")}
     full_bytes = sum(int(t.numel() * t.element_size()) for t in full.values())
     goff = plan.group_offsets()
-    contexts = []
-    for r in range(cp):
+
+    def keep(r: int) -> RankContext:
         idx = np.concatenate([np.arange(goff[e.seq_id] + e.start, goff[e.seq_id] + e.end, dtype=np.int64)
                               for e in plan.rank_entries[r]]) if plan.rank_entries[r] else np.zeros(0, np.int64)
-        ctx = _context(r, plan, *(_rows(full[n], idx) for n in ("q", "k", "v", "ts")))
+        return _context(r, plan, *(_rows(full[n], idx) for n in ("q", "k", "v", "ts")))
+
+    contexts = _map_ranks(keep, cp, scheduling)
+    for r, ctx in enumerate(contexts):
         meters[r].step(ctx.payload_nbytes() - full_bytes)
         stats[r].peak_resident_bytes = meters[r].peak
-        contexts.append(ctx)
     group.steps_completed += 1
     return contexts, stats
 
@@ -250,8 +281,7 @@ def redistribute_alltoall(group: RankGroup, batches, plan: ShardPlan, scheduling
     _check_plan_matches(batches, plan)
     cp = group.cp_size
     seq_base = np.concatenate([[0], np.cumsum([b.num_sequences for b in batches])]).astype(np.int64)
-    send = []
-    for src in range(cp):
+    def pack(src: int) -> list:
         loff = batches[src].q.host_offsets
         msgs = []
         for dst in range(cp):
@@ -262,13 +292,16 @@ def redistribute_alltoall(group: RankGroup, batches, plan: ShardPlan, scheduling
             msgs.append(JaggedMessage([e.seq_id for e in ents], [e.chunk_id for e in ents],
                                       [e.start for e in ents], [e.count for e in ents],
                                       {n: _rows(getattr(batches[src], n).values, idx) for n in ("q", "k", "v", "ts")}))
-        send.append(msgs)
+        return msgs
+
+    send = _map_ranks(pack, cp, scheduling)
     received, stats = all_to_all_jagged(group, send)
-    contexts = []
-    for r in range(cp):
+
+    def assemble(r: int) -> RankContext:
         parts = {n: [m.arrays[n] for m in received[r]] for n in ("q", "k", "v", "ts")}
-        contexts.append(_context(r, plan, *(torch.cat(parts[n]) for n in ("q", "k", "v", "ts"))))
-    return contexts, stats
+        return _context(r, plan, *(torch.cat(parts[n]) for n in ("q", "k", "v", "ts")))
+
+    return _map_ranks(assemble, cp, scheduling), stats
 
 
 def _bundle(ctx: RankContext) -> JaggedMessage:
@@ -323,21 +356,23 @@ def ring_hstu_attention(group: RankGroup, contexts, params, cfg, scheduling: str
         kernels.scatter_rows(c.v, perm, V)
         kernels.scatter_rows(c.ts.view(-1, 1), perm, TS.view(-1, 1))
     w = torch.from_numpy(np.asarray(params.ts_weights, dtype=np.float32)).to(dev)
-    outputs = []
-    for r, c in enumerate(contexts):
+
+    def attend(r: int) -> torch.Tensor:
+        c = contexts[r]
         ents = [e for e in c.entries if e.count > 0]
         if not ents:
-            outputs.append(c.q.new_zeros(c.q.shape))
-            continue
+            return c.q.new_zeros(c.q.shape)
         qo = np.concatenate([[0], np.cumsum([e.count for e in ents])]).astype(np.int64)
         t = lambda a: torch.from_numpy(np.asarray(a, dtype=np.int64)).to(dev)  # noqa: E731
         kl = [e.end for e in ents]
-        out = kernels.attn_fwd(c.q, K, V, c.ts, TS, t(qo), num_heads, w, cfg.num_buckets,
-                               q_pos0=t([e.start for e in ents]), kv_start=t([base[e.seq_id] for e in ents]),
-                               kv_len=t(kl), kv_len_total=int(sum(kl)))
+        return kernels.attn_fwd(c.q, K, V, c.ts, TS, t(qo), num_heads, w, cfg.num_buckets,
+                                q_pos0=t([e.start for e in ents]), kv_start=t([base[e.seq_id] for e in ents]),
+                                kv_len=t(kl), kv_len_total=int(sum(kl)))
+
+    outputs = _map_ranks(attend, cp, scheduling)
+    for r, out in enumerate(outputs):
         meters[r].step(_nbytes_t(out))
         totals[r].peak_resident_bytes = max(totals[r].peak_resident_bytes, meters[r].peak)
-        outputs.append(out)
     return outputs, totals
 
 

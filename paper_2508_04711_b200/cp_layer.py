@@ -33,6 +33,7 @@ average over data-parallel replicas only.
 
 from __future__ import annotations
 
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -114,6 +115,91 @@ def build_cp_plan(lengths_per_rank, cp: int, rank: int, balance_mode: str = "bal
                   a64(qo), a64(qp), a64(ks), a64(kl), int(goff[-1]), a64(lks), a64(lkl), a64(qp))
 
 
+class TorchComm:
+    """The layer's collectives over a torch.distributed group (NCCL on B200:
+    device tensors straight to the collective)."""
+
+    def __init__(self, group, device=None):
+        self.group = group
+        self.size = dist.get_world_size(group)
+        self.device = device
+
+    def _dev(self, like=None):
+        if self.device is not None:
+            return self.device
+        if like is not None:
+            return like.device
+        return torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(self.group) == "nccl" \
+            else torch.device("cpu")
+
+    def all_gather_lengths(self, local_lengths) -> tuple:
+        """Every rank's sequence lengths (one int64 all-gather of the counts,
+        one of the padded lengths), identical on all ranks."""
+        dev = self._dev()
+        loc = torch.as_tensor(np.asarray(local_lengths, dtype=np.int64), device=dev)
+        n = torch.tensor([loc.numel()], dtype=torch.int64, device=dev)
+        ns = [torch.empty_like(n) for _ in range(self.size)]
+        self._all_gather(ns, n)
+        ns = [int(x.item()) for x in ns]
+        m = max(max(ns), 1)
+        pad = torch.zeros(m, dtype=torch.int64, device=dev)
+        pad[: loc.numel()] = loc
+        parts = [torch.empty_like(pad) for _ in range(self.size)]
+        self._all_gather(parts, pad)
+        return tuple(tuple(int(v) for v in p[:k].tolist()) for p, k in zip(parts, ns))
+
+    def _all_gather(self, outs, x):
+        dist.all_gather(outs, x, group=self.group)
+
+    def all_to_all(self, out, send, out_splits, in_splits):
+        dist.all_to_all_single(out, send, list(out_splits), list(in_splits), group=self.group)
+
+    def all_gather_into(self, full, x):
+        dist.all_gather_into_tensor(full, x, group=self.group)
+
+    def reduce_scatter(self, out, full):
+        dist.reduce_scatter_tensor(out, full, group=self.group)
+
+    def all_reduce(self, x):
+        dist.all_reduce(x, group=self.group)
+
+
+class HostStagedComm(TorchComm):
+    """Same collectives for a CPU (gloo) group with device tensors: each call
+    stages through host memory.  Lets several processes that share one GPU run
+    the real CUDA layer (tests), with no kernel waiting on another process."""
+
+    def _dev(self, like=None):
+        return torch.device("cpu")
+
+    @staticmethod
+    def _host(x):
+        return x.detach().to("cpu")
+
+    def _all_gather(self, outs, x):
+        dist.all_gather(outs, self._host(x), group=self.group)
+
+    def all_to_all(self, out, send, out_splits, in_splits):
+        h = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_to_all_single(h, self._host(send), list(out_splits), list(in_splits), group=self.group)
+        out.copy_(h)
+
+    def all_gather_into(self, full, x):
+        h = torch.empty(full.shape, dtype=full.dtype)
+        dist.all_gather_into_tensor(h, self._host(x), group=self.group)
+        full.copy_(h)
+
+    def reduce_scatter(self, out, full):
+        h = torch.empty(out.shape, dtype=out.dtype)
+        dist.reduce_scatter_tensor(h, self._host(full), group=self.group)
+        out.copy_(h)
+
+    def all_reduce(self, x):
+        h = self._host(x).clone()
+        dist.all_reduce(h, group=self.group)
+        x.copy_(h)
+
+
 class GpuBackend:
     """Compute pieces on the B200 kernels (libjh_hstu.so)."""
 
@@ -162,41 +248,47 @@ class CPAttention:
     """Context-parallel jagged HSTU attention over a process group."""
 
     def __init__(self, group, num_heads: int, num_buckets: int = 16, balance_mode: str = "balanced_minichunk",
-                 backend=None, overlap: bool = True):
+                 backend=None, overlap: bool = True, comm=None, max_plans: int = 64):
         self.group = group
         self.cp = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self.comm = comm if comm is not None else TorchComm(group)
+        self.max_plans = int(max_plans)
         self.H = num_heads
         self.nb = num_buckets
         self.mode = balance_mode
         self.be = backend if backend is not None else GpuBackend()
         self.overlap = overlap and hasattr(self.be, "fwd_partial") and hasattr(self.be, "bwd_partial")
-        self._plans: dict = {}
+        self._plans: "OrderedDict" = OrderedDict()
 
     # ---------------------------------------------------------------- plan
     def plan_for(self, local_lengths, device) -> tuple[CPPlan, dict]:
-        key = tuple(int(x) for x in local_lengths)
-        if key not in self._plans:
-            allv = [None] * self.cp
-            dist.all_gather_object(allv, list(key), group=self.group)
-            if len(self._plans) > 64:
-                self._plans.clear()
-            p = build_cp_plan([list(x) for x in allv], self.cp, self.rank, self.mode)
-            t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
-            dev = {"send_perm": t(p.send_perm), "seq_perm": t(p.seq_perm),
-                   "segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.kv_len), int(p.kv_len.sum()),
-                            int(p.kv_len.max(initial=0))),
-                   "local_segs": (t(p.q_offsets), t(np.zeros_like(p.q_pos0)), t(p.local_kv_start),
-                                  t(p.local_kv_len), int(p.local_kv_len.sum()), int(p.local_kv_len.max(initial=0))),
-                   "remote_segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.remote_kv_len),
-                                   int(p.remote_kv_len.sum()), int(p.remote_kv_len.max(initial=0)))}
-            self._plans[key] = (p, dev)
+        """Every rank's lengths are all-gathered EVERY step and the plan cache is
+        keyed on that global tuple, so all ranks make the same hit / miss /
+        eviction decision (LRU over identical key sequences) and enter the same
+        collectives."""
+        key = self.comm.all_gather_lengths([int(x) for x in local_lengths])
+        if key in self._plans:
+            self._plans.move_to_end(key)
+            return self._plans[key]
+        p = build_cp_plan([list(x) for x in key], self.cp, self.rank, self.mode)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
+        dev = {"send_perm": t(p.send_perm), "seq_perm": t(p.seq_perm),
+               "segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.kv_len), int(p.kv_len.sum()),
+                        int(p.kv_len.max(initial=0))),
+               "local_segs": (t(p.q_offsets), t(np.zeros_like(p.q_pos0)), t(p.local_kv_start),
+                              t(p.local_kv_len), int(p.local_kv_len.sum()), int(p.local_kv_len.max(initial=0))),
+               "remote_segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.remote_kv_len),
+                               int(p.remote_kv_len.sum()), int(p.remote_kv_len.max(initial=0)))}
+        self._plans[key] = (p, dev)
+        while len(self._plans) > self.max_plans:
+            self._plans.popitem(last=False)
         return self._plans[key]
 
     # ---------------------------------------------------------- collectives
     def _a2a_rows(self, send, send_counts, recv_counts):
         out = send.new_empty((int(sum(recv_counts)),) + tuple(send.shape[1:]))
-        dist.all_to_all_single(out, send, list(recv_counts), list(send_counts), group=self.group)
+        self.comm.all_to_all(out, send, recv_counts, send_counts)
         return out
 
     def _redistribute(self, x, p, dev):
@@ -214,7 +306,7 @@ class CPAttention:
         pad = x_res.new_zeros((p.max_res,) + tuple(x_res.shape[1:]))
         pad[: p.n_res] = x_res
         full = x_res.new_empty((self.cp * p.max_res,) + tuple(x_res.shape[1:]))
-        dist.all_gather_into_tensor(full, pad, group=self.group)
+        self.comm.all_gather_into(full, pad)
         return self.be.gather(full, dev["seq_perm"])
 
     def _reduce_to_owner(self, x_seq, p, dev):
@@ -222,7 +314,7 @@ class CPAttention:
         full = x_seq.new_zeros((self.cp * p.max_res,) + tuple(x_seq.shape[1:]))
         self.be.scatter(x_seq, dev["seq_perm"], full)
         mine = x_seq.new_empty((p.max_res,) + tuple(x_seq.shape[1:]))
-        dist.reduce_scatter_tensor(mine, full, group=self.group)
+        self.comm.reduce_scatter(mine, full)
         return mine[: p.n_res]
 
     # --------------------------------------------------------------- passes
@@ -278,7 +370,7 @@ class CPAttention:
             dv_r = self._reduce_to_owner(dv_s, p, dev).to(q_r.dtype)
         else:
             dq_r, dk_r, dv_r, dw = self._backward_overlapped(q_r, k_r, v_r, k_s, v_s, ts_r, ts_s, g_r, p, dev, w)
-        dist.all_reduce(dw, group=self.group)
+        self.comm.all_reduce(dw)
         dq = self._restore(dq_r, p, dev, n_local)
         dk = self._restore(dk_r, p, dev, n_local)
         dv = self._restore(dv_r, p, dev, n_local)
@@ -339,3 +431,51 @@ class _CPAttentionFn(torch.autograd.Function):
 def cp_hstu_attention(layer: CPAttention, q, k, v, ts, local_lengths, ts_weights):
     """Differentiable CP attention (gradients to q, k, v and ts_weights)."""
     return _CPAttentionFn.apply(q, k, v, ts_weights, ts, np.asarray(local_lengths), layer)
+
+
+# ------------------------------------------------------- hybrid CP x DP (C5)
+
+def make_cp_dp_groups(cp_size: int, backend=None):
+    """Process groups of a hybrid CP x DP layout:
+    rank = dp_index * cp_size + cp_index, CP groups are consecutive ranks
+    ({0..cp-1}, {cp..2cp-1}, ...), DP groups stride by cp_size ({0, cp, ...},
+    {1, cp+1, ...}).  Every rank creates every group (torch.distributed
+    requires the same new_group call sequence on all ranks).  Returns
+    (cp_group, dp_group, cp_index, dp_index)."""
+    world = dist.get_world_size()
+    rank = dist.get_rank()
+    if cp_size < 1 or world % cp_size:
+        raise ValueError(f"world size {world} is not a multiple of cp_size {cp_size}")
+    dp_size = world // cp_size
+    cp_group = dp_group = None
+    for d in range(dp_size):
+        g = dist.new_group(list(range(d * cp_size, (d + 1) * cp_size)), backend=backend)
+        if rank // cp_size == d:
+            cp_group = g
+    for c in range(cp_size):
+        g = dist.new_group(list(range(c, world, cp_size)), backend=backend)
+        if rank % cp_size == c:
+            dp_group = g
+    return cp_group, dp_group, rank % cp_size, rank // cp_size
+
+
+class CPJaggedHSTUAttention(torch.nn.Module):
+    """The attention layer sharded along the sequence by jagged CP: learnable
+    ts_weights around ``cp_hstu_attention``.  Composes with DDP over the DP
+    group: CPAttention's backward SUMS the ts_weights gradient over the CP
+    group (its ranks hold different tokens of one batch); wrapping this module
+    in ``DistributedDataParallel(process_group=dp_group)`` then AVERAGES it
+    over the data-parallel replicas -- the rule of SURVEY §7 hard part 6."""
+
+    def __init__(self, cp_group, num_heads: int, num_buckets: int = 16, balance_mode: str = "balanced_minichunk",
+                 seed: int = 0, backend=None, comm=None, overlap: bool = True, weights=None):
+        super().__init__()
+        if weights is None:
+            from .attention import BiasConfig, BiasParams
+            weights = BiasParams.normal_init(BiasConfig(num_buckets), seed).ts_weights
+        self.ts_weights = torch.nn.Parameter(torch.as_tensor(np.asarray(weights, dtype=np.float32)).clone())
+        self.cp = CPAttention(cp_group, num_heads, num_buckets, balance_mode, backend=backend, overlap=overlap,
+                              comm=comm)
+
+    def forward(self, q, k, v, ts, local_lengths):
+        return cp_hstu_attention(self.cp, q, k, v, ts, local_lengths, self.ts_weights)

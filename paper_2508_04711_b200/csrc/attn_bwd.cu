@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const bool has_pos = P > 0;
   const int64_t HD = (int64_t)H * D;
 
-  const float c1 = 0.5f * rsqrtf((float)D);  // SiLU(s) = h (1 + tanh h), h = s / (2 sqrt(d))
+  const float c1 = p.c1;  // SiLU(s) = h (1 + tanh h), h = s / (2 sqrt(d))
   cta_stamp(p, 0);
   if (smem_u32(smem) & 1023) __trap();
   oct_table_fill(s_oct, p.bias, p.ts_weights, c1, tid, blockDim.x);

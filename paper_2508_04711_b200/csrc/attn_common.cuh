@@ -375,6 +375,9 @@ struct AttnParams {
   unsigned long long* trace;
   int32_t trace_cta;
   int32_t dbg;  // experiment switches (JH_DBG environment variable), 0 in production
+  float c1;     // score_scale / 2: SiLU(s) = h + h tanh(h), h = c1 * (q k^T + bias)
+  uint8_t* dbg_buckets;  // forward debug export of the applied bucket per (q row, kv pos), head 0
+  int64_t dbg_ld;
 };
 
 constexpr int kTraceCap = 4096;

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   cta_stamp(p, 0, 2);
   if (smem_u32(smem) & 1023) __trap();  // 128B-swizzled operand tiles need 1 KB alignment
-  const float c1 = 0.5f * rsqrtf((float)D);  // SiLU(s) = h + h*tanh(h), h = s/2 (scaled by 1/sqrt(d))
+  const float c1 = p.c1;  // SiLU(s) = h + h*tanh(h), h = s/2 (scaled by 1/sqrt(d))
   oct_table_fill(s_oct, p.bias, p.ts_weights, c1, tid, blockDim.x);
   for (int i = tid; i < p.num_pos; i += blockDim.x) s_pwc[i] = p.pos_weights[i] * c1;
   float* s_wt = reinterpret_cast<float*>(smem + C::WT_OFF);
@@ -355,6 +355,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int2 it = p.wl.fwd[g / H];
       const Seg sg = load_seg(p.seg, it.x);
       const int64_t kv_lim = fwd_kv_lim(sg, it.y);
+      // debug export (tests): the bucket this thread applies to each visible pair (head 0)
+      uint8_t* dbgb = (p.dbg_buckets != nullptr && g % H == 0 && r < sg.lq - (int64_t)it.y * kBM)
+                          ? p.dbg_buckets + (sg.q_row0 + (int64_t)it.y * kBM + r) * p.dbg_ld
+                          : nullptr;
       const int n = (int)((kv_lim + kBN - 1) / kBN);
       if (n == 0) continue;
       const int64_t nq = min((int64_t)kBM, sg.lq - (int64_t)it.y * kBM);
@@ -441,6 +445,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               w1 = __ldg(src + 1);
             }
             const uint32_t wd[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            if (dbgb != nullptr) {
+#pragma unroll 1
+              for (int i = 0; i < 32; ++i) {
+                const uint32_t b = (wd[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+                if (b != kBandMasked) dbgb[kv0 + c0 + i] = (uint8_t)b;
+              }
+            }
             uint32_t v[32], pk[16];
             tmem_ld32(tS + c0, v);
             tmem_ld_wait();
@@ -455,6 +466,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             }
             tmem_st16(tS + c0, pk);
           } else if (cls == 1) {
+            if (dbgb != nullptr) {
+#pragma unroll 1
+              for (int i = 0; i < 32; ++i) dbgb[kv0 + c0 + i] = (uint8_t)(nb - 1);
+            }
             uint32_t v[32], pk[16];
             tmem_ld32(tS + c0, v);
             tmem_ld_wait();
@@ -499,7 +514,18 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                 const int k = g8 + i;
                 unsat |= (k <= relc && k < ncol) && du[i] < (uint32_t)cap;
               }
-              if (!has_pos && !__any_sync(0xffffffffu, unsat)) {
+              const bool all_sat = !has_pos && !__any_sync(0xffffffffu, unsat);
+              if (dbgb != nullptr) {
+#pragma unroll 1
+                for (int i = 0; i < 8; ++i) {
+                  const int k = g8 + i;
+                  int b = nb - 1;
+                  float wdummy;
+                  if (!all_sat) oct_lookup(du[i], s_oct, b, wdummy);
+                  if (k <= relc && k < ncol) dbgb[kv0 + c0 + k] = (uint8_t)b;
+                }
+              }
+              if (all_sat) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) bc[i] = cb;  // every visible pair saturated (warp-uniform)
               } else {

@@ -2,6 +2,7 @@
 // argument validation, tensor maps, work-list build, kernel launches.
 #include <algorithm>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 
 #include "abi_internal.h"
@@ -57,6 +58,23 @@ static WsLayout ws_layout(int64_t q_rows, int64_t kv_total, int64_t nseg, int32_
   return w;
 }
 
+// Fused-backward persistent state (zero between calls): fp32 dQ accumulator
+// [q_rows][H*d], per-(q tile, head) contribution counters at index
+// ((q_row0 >> 7) + s + t) * H + h (collision-free without a prefix sum), and
+// the d_ts_weights last-CTA counter.
+struct BwdStateLayout {
+  size_t acc, cnt, done, total;
+};
+static BwdStateLayout bwd_state_layout(int64_t q_rows, int64_t nseg, int32_t H, int32_t D) {
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  BwdStateLayout l;
+  l.acc = 0;
+  l.cnt = up((size_t)q_rows * H * D * 4);
+  l.done = l.cnt + up((size_t)(q_rows / 128 + nseg + 2) * H * 4);
+  l.total = l.done + 256;
+  return l;
+}
+
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 static int validate(const jh_attn_args* a, bool bwd) {
@@ -74,6 +92,8 @@ static int validate(const jh_attn_args* a, bool bwd) {
   if (a->num_pos < 0 || a->num_pos > 1024) return set_error(JH_ERR_UNSUPPORTED, "num_pos must be in [0, 1024]");
   if (a->num_pos > 0 && !a->pos_weights) return set_error(JH_ERR_INVALID, "pos_weights is NULL");
   if (!a->q_offsets) return set_error(JH_ERR_INVALID, "q_offsets is NULL");
+  if (!(a->score_scale >= 0.f) || a->score_scale > 1e30f) return set_error(JH_ERR_INVALID, "score_scale must be finite and >= 0");
+  if (a->dbg_buckets && a->dbg_ld < 1) return set_error(JH_ERR_INVALID, "dbg_ld must be >= 1");
   const int64_t HD = (int64_t)a->num_heads * a->head_dim;
   if (a->q_rows > 0 || a->kv_rows > 0) {
     if (!a->q || !a->k || !a->v || !a->ts_q || !a->ts_k) return set_error(JH_ERR_INVALID, "NULL input tensor");
@@ -146,6 +166,9 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
   }
   p->bias.cap = bt->cap;
   p->bias.nb = a->num_buckets;
+  p->c1 = 0.5f * (a->score_scale > 0.f ? a->score_scale : 1.0f / sqrtf((float)a->head_dim));
+  p->dbg_buckets = bwd ? nullptr : a->dbg_buckets;
+  p->dbg_ld = a->dbg_ld;
   p->trace = (unsigned long long*)a->trace;
   p->trace_cta = a->trace_cta;
   {
@@ -254,6 +277,13 @@ size_t jh_attn_ds_scratch_bytes(int64_t kv_len_total, int64_t num_segments, int3
   if (kv_len_total <= 0 || num_segments <= 0 || num_heads <= 0 || max_kv_len <= 0) return (size_t)kDsBlockBytes;
   const int64_t blocks = ((kv_len_total + kBN - 1) / kBN + 2 * num_segments) * ((max_kv_len + kBN - 1) / kBN + 2);
   return (size_t)blocks * num_heads * kDsBlockBytes;
+}
+
+size_t jh_attn_bwd_state_bytes(int64_t q_rows, int64_t num_segments, int32_t num_heads, int32_t head_dim) {
+  q_rows = std::max<int64_t>(q_rows, 0);
+  num_segments = std::max<int64_t>(num_segments, 0);
+  num_heads = std::max<int32_t>(num_heads, 1);
+  return bwd_state_layout(q_rows, num_segments, num_heads, head_dim < 64 ? 64 : (head_dim > 64 ? 128 : 64)).total;
 }
 
 size_t jh_attn_workspace_bytes(int64_t q_rows, int64_t kv_len_total, int64_t num_segments, int32_t num_heads,

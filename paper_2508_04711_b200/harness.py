@@ -91,14 +91,18 @@ def draw_lengths(cfg: ExperimentConfig, rng: np.random.Generator) -> np.ndarray:
 
 
 def gen_synthetic_host(cfg: ExperimentConfig, rank: int) -> dict:
-    """harness.py:123-145 on the host: dict of numpy arrays (q/k/v f32)."""
+    """harness.py:123-145 on the host: dict of numpy arrays (q/k/v in the drawn dtype)."""
     rng = np.random.default_rng([cfg.seed, rank])
     seq_lengths = draw_lengths(cfg, rng)
     offsets = np.concatenate([[0], np.cumsum(seq_lengths)]).astype(np.int64)
     total = int(offsets[-1])
-    q = rng.standard_normal((total, cfg.embed_dim), dtype=np.float32)
-    k = rng.standard_normal((total, cfg.embed_dim), dtype=np.float32)
-    v = rng.standard_normal((total, cfg.embed_dim), dtype=np.float32)
+    # the reference draws in the config's dtype (harness.py:130-133, jagged.py:17);
+    # bf16 (this repo's tag) draws the f64 stream and is rounded on the device,
+    # so starts / gaps / timestamps are the reference's for the same seed
+    dt = np.float32 if cfg.dtype == "f32" else np.float64
+    q = rng.standard_normal((total, cfg.embed_dim), dtype=dt)
+    k = rng.standard_normal((total, cfg.embed_dim), dtype=dt)
+    v = rng.standard_normal((total, cfg.embed_dim), dtype=dt)
     starts = rng.integers(0, 1_000_000_000, size=cfg.batch_size)
     gaps = rng.integers(1, MAX_TS_GAP_SECONDS + 1, size=total)
     ts = np.zeros(total, dtype=np.int64)
@@ -225,11 +229,15 @@ class ExperimentReport:
         }
 
 
-def run_experiment(cfg: ExperimentConfig, scheduling: str = "sequential", device=None) -> ExperimentReport:
+def run_experiment(cfg: ExperimentConfig, scheduling: str = "sequential", device=None,
+                   reference=None) -> ExperimentReport:
     """harness.py:270-316 on the GPU path: the CP pipeline (cp_engine.run_pipeline,
-    fused kernels) against the single-device fused forward, plus both
-    protocols' redistribution peaks; ``metadata.gpu`` carries the pipeline's
-    device time (CUDA events)."""
+    fused kernels) against a single-device reference, plus both protocols'
+    redistribution peaks; ``metadata.gpu`` carries the pipeline's device time
+    (CUDA events).  ``reference(batches, params, bias_cfg, num_heads)`` returns
+    the per-rank expected outputs; the default is the single-device fused
+    forward over the combined batch (as harness.py:173-186 uses its own
+    single-device path); tests inject the CPU oracle here."""
     from .cp_engine import run_pipeline
     if scheduling not in SCHEDULINGS:
         raise ValueError(f"unknown scheduling {scheduling!r}")
@@ -240,7 +248,7 @@ def run_experiment(cfg: ExperimentConfig, scheduling: str = "sequential", device
     result = run_pipeline(batches, cfg.cp_size, cfg.protocol, cfg.balance_mode, params, bias_cfg, scheduling,
                           num_heads=cfg.num_heads)
     ev[1].record()
-    want = reference_outputs(batches, params, bias_cfg, cfg.num_heads)
+    want = (reference or reference_outputs)(batches, params, bias_cfg, cfg.num_heads)
     max_abs, max_rel = output_errors(result.outputs, want)
     if not (np.isfinite(max_abs) and np.isfinite(max_rel)):
         raise RuntimeError(f"non-finite equivalence error: abs={max_abs} rel={max_rel}")

@@ -77,6 +77,7 @@ def compute_bias(ts_q: torch.Tensor, ts_k: torch.Tensor, ts_weights: torch.Tenso
     _require_cuda("ts_q", ts_q, torch.int64)
     _require_cuda("ts_k", ts_k, torch.int64)
     w = ts_weights.to(device=ts_q.device, dtype=torch.float32).contiguous()
+    _check_weights(w, num_buckets)
     tq, tk = ts_q.contiguous(), ts_k.contiguous()
     out = torch.empty((tq.numel(), tk.numel()), dtype=torch.float32, device=tq.device)
     check(_lib.lib().jh_compute_bias(_ptr(tq), tq.numel(), _ptr(tk), tk.numel(), _ptr(w), int(num_buckets),
@@ -156,6 +157,39 @@ def padded_to_jagged(padded: torch.Tensor, offsets: torch.Tensor, total: int) ->
 
 # ------------------------------------------------------------------ attention
 
+def _check_weights(ts_weights, num_buckets, pos_weights=None):
+    # the kernels read ts_weights[0 .. num_buckets-1] (attention.py:94 indexes
+    # params.ts_weights with buckets < cfg.num_buckets: a shorter vector is an error there too)
+    if ts_weights.dim() != 1 or ts_weights.numel() < int(num_buckets):
+        raise ValueError(f"ts_weights must be a 1-D vector with at least num_buckets={int(num_buckets)} entries, "
+                         f"got shape {tuple(ts_weights.shape)}")
+    if pos_weights is not None and (pos_weights.dim() != 1 or pos_weights.numel() < 1):
+        raise ValueError("pos_weights must be a non-empty 1-D vector")
+
+
+def padded_head_dim(d: int) -> int:
+    """Head dims the kernels implement: 64 and 128; smaller ones are zero-padded
+    (scores keep the 1/sqrt(d) of the true d via score_scale)."""
+    if d < 1 or d > 128:
+        raise NotImplementedError(f"head_dim {d} unsupported (1 .. 128)")
+    return 64 if d <= 64 else 128
+
+
+def _pad_heads(t, H: int, d: int, dp: int):
+    if t is None or d == dp:
+        return t
+    T = t.shape[0]
+    out = t.new_zeros((T, H, dp))
+    out[:, :, :d] = t.reshape(T, H, d)
+    return out.view(T, H * dp)
+
+
+def _unpad_heads(t, H: int, d: int, dp: int):
+    if t is None or d == dp:
+        return t
+    return t.view(t.shape[0], H, dp)[:, :, :d].reshape(t.shape[0], H * d)
+
+
 def _attn_args(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets, pos_weights,
                q_pos0=None, kv_start=None, kv_len=None):
     for name, t in (("q", q), ("k", k), ("v", v)):
@@ -170,6 +204,7 @@ def _attn_args(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_bucket
             raise ValueError(f"{name} must be a contiguous 1-D tensor")
     if not ts_weights.is_contiguous() or (pos_weights is not None and not pos_weights.is_contiguous()):
         raise ValueError("ts_weights / pos_weights must be contiguous")
+    _check_weights(ts_weights, num_buckets, pos_weights)
     D = q.shape[1]
     if D % num_heads:
         raise ValueError(f"embed_dim {D} not divisible by num_heads {num_heads}")
@@ -239,39 +274,80 @@ def _prof(a, prof):
 
 def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=16, pos_weights=None,
              q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, out=None, prof=None, out_accum=None,
-             accumulate=False, band_table=None):
+             accumulate=False, band_table=None, dbg_buckets=None):
     """Fused jagged HSTU forward (jh_attn_fwd).  bf16 in/out, fp32 weights.
 
     ``out_accum`` (fp32, q's shape): write the fp32 result there instead of a
     bf16 ``out`` (``accumulate=True``: add it; rows that see no kv are left
     untouched) -- the additive partials of the CP pipeline (cp_engine.py:441-450).
     ``band_table`` (uint8, ``band_table_bytes``): the near-diagonal bucket table
-    is computed into it, for a backward call on the same inputs to reuse."""
+    is computed into it, for a backward call on the same inputs to reuse.
+    Head dims below 64 (or between 64 and 128) are zero-padded; the score scale
+    stays 1/sqrt(head_dim).  ``dbg_buckets`` (uint8 [q_rows, max_kv], tests):
+    the bucket the kernel applied to each visible pair of head 0."""
     w = ts_weights.to(device=q.device, dtype=torch.float32).contiguous()
     pw = None if pos_weights is None else pos_weights.to(device=q.device, dtype=torch.float32).contiguous()
-    a = _attn_args(q, k, v, ts_q, ts_k, q_offsets, num_heads, w, num_buckets, pw, q_pos0, kv_start, kv_len)
+    H = int(num_heads)
+    if q.dim() != 2 or q.shape[1] % H:
+        raise ValueError(f"embed_dim {q.shape[-1]} not divisible by num_heads {H}")
+    d = q.shape[1] // H
+    dp = padded_head_dim(d)
+    qq, kk, vv = (_pad_heads(t, H, d, dp) for t in (q, k, v))
+    a = _attn_args(qq, kk, vv, ts_q, ts_k, q_offsets, H, w, num_buckets, pw, q_pos0, kv_start, kv_len)
+    a.score_scale = 1.0 / float(np.sqrt(d))
+    ret = None
     if out_accum is not None:
         if out_accum.dtype != torch.float32 or out_accum.shape != q.shape or out_accum.stride(1) != 1:
             raise ValueError("out_accum must be a float32 tensor shaped like q")
-        a.out_accum, a.ld_o, a.out_accum_mode = out_accum.data_ptr(), out_accum.stride(0), 2 if accumulate else 1
-        out = out_accum
+        acc = out_accum
+        if dp != d:
+            acc = _pad_heads(out_accum, H, d, dp) if accumulate else torch.empty(qq.shape, dtype=torch.float32,
+                                                                                  device=q.device)
+        a.out_accum, a.ld_o, a.out_accum_mode = acc.data_ptr(), acc.stride(0), 2 if accumulate else 1
+        ret = out_accum
     else:
         if out is None:
             out = torch.empty_like(q)
-        a.out, a.ld_o = out.data_ptr(), out.stride(0)
+        acc = out if dp == d else torch.empty_like(qq)
+        a.out, a.ld_o = acc.data_ptr(), acc.stride(0)
+        ret = out
     ws, nbytes = _workspace(q.shape[0], q.shape[0] if kv_len_total is None else kv_len_total, a.num_segments,
-                            num_heads, a.head_dim, q.device)
+                            H, dp, q.device)
     a.workspace, a.workspace_bytes = ws.data_ptr(), nbytes
     _band(a, band_table, ready=False)
+    if dbg_buckets is not None:
+        if dbg_buckets.dtype != torch.uint8 or dbg_buckets.dim() != 2 or dbg_buckets.shape[0] < q.shape[0] \
+                or dbg_buckets.stride(1) != 1:
+            raise ValueError("dbg_buckets must be a uint8 [q_rows, max_kv] tensor")
+        a.dbg_buckets, a.dbg_ld = dbg_buckets.data_ptr(), dbg_buckets.stride(0)
     _prof(a, prof)
     check(_lib.lib().jh_attn_fwd(ctypes.byref(a), _stream(q)), "hstu_attention forward")
     _bump(2 if pw is not None else 3)  # (band table) + work-list build + fused forward
-    return out
+    if dp != d:
+        ret.copy_(_unpad_heads(acc, H, d, dp))
+    return ret
+
+
+# deterministic backward (two kernels over a bf16 dS scratch) or the fused one
+DETERMINISTIC_DEFAULT = {"value": True}
+_BWD_STATE: dict = {}
+
+
+def bwd_state(q_rows: int, num_segments: int, H: int, dp: int, device) -> torch.Tensor:
+    """Persistent zero-initialised state of the fused backward (one per device
+    and stream; every call leaves it zero again)."""
+    need = int(_lib.lib().jh_attn_bwd_state_bytes(int(q_rows), int(num_segments), int(H), int(dp)))
+    key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+    buf = _BWD_STATE.get(key)
+    if buf is None or buf.numel() < need:
+        buf = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=device)
+        _BWD_STATE[key] = buf
+    return buf
 
 
 def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_buckets=16, pos_weights=None,
              q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, accumulate_dkv=False, prof=None,
-             max_kv_len=None, dq_accum=None, band_table=None):
+             max_kv_len=None, dq_accum=None, band_table=None, deterministic=None):
     """Fused jagged HSTU backward (jh_attn_bwd).
 
     Returns (dq bf16, dk, dv, d_ts_weights f64, d_pos f64 or None); dk/dv are
@@ -279,29 +355,43 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
     ``dq_accum`` (fp32, q's shape) dq is added there and returned as dq;
     ``band_table`` filled by the forward call on the same inputs is reused
     (no recomputation).
-    ``max_kv_len`` bounds every segment's kv length (sizes the dS scratch);
-    when omitted it is read back from the device (one synchronisation)."""
+    ``deterministic``: the two-kernel path over a bf16 dS scratch (bitwise
+    reproducible dq; memory O(H L^2)); otherwise the fused kernel (dq reduced
+    in fp32, O(L) memory).  ``max_kv_len`` bounds every segment's kv length
+    (sizes the dS scratch of the deterministic path; when omitted it is read
+    back from the device, one synchronisation)."""
+    if deterministic is None:
+        deterministic = DETERMINISTIC_DEFAULT["value"]
     w = ts_weights.to(device=q.device, dtype=torch.float32).contiguous()
     pw = None if pos_weights is None else pos_weights.to(device=q.device, dtype=torch.float32).contiguous()
-    a = _attn_args(q, k, v, ts_q, ts_k, q_offsets, num_heads, w, num_buckets, pw, q_pos0, kv_start, kv_len)
+    H = int(num_heads)
+    if q.dim() != 2 or q.shape[1] % H:
+        raise ValueError(f"embed_dim {q.shape[-1]} not divisible by num_heads {H}")
+    d = q.shape[1] // H
+    dp = padded_head_dim(d)
     _require_cuda("dout", dout, torch.bfloat16)
     _rowmajor("dout", dout)
-    a.dout, a.ld_do = dout.data_ptr(), dout.stride(0)
+    qq, kk, vv, gg = (_pad_heads(t, H, d, dp) for t in (q, k, v, dout))
+    a = _attn_args(qq, kk, vv, ts_q, ts_k, q_offsets, H, w, num_buckets, pw, q_pos0, kv_start, kv_len)
+    a.score_scale = 1.0 / float(np.sqrt(d))
+    a.dout, a.ld_do = gg.data_ptr(), gg.stride(0)
     if dq_accum is not None:
         if dq_accum.dtype != torch.float32 or dq_accum.shape != q.shape or dq_accum.stride(1) != 1:
             raise ValueError("dq_accum must be a float32 tensor shaped like q")
         dq = dq_accum
-        a.dq_accum, a.ld_dq = dq.data_ptr(), dq.stride(0)
+        dqk = _pad_heads(dq_accum, H, d, dp)
+        a.dq_accum, a.ld_dq = dqk.data_ptr(), dqk.stride(0)
     else:
         dq = torch.empty_like(q)
-        a.dq, a.ld_dq = dq.data_ptr(), dq.stride(0)
+        dqk = dq if dp == d else torch.empty_like(qq)
+        a.dq, a.ld_dq = dqk.data_ptr(), dqk.stride(0)
     if accumulate_dkv:
-        dk = torch.zeros(k.shape, dtype=torch.float32, device=k.device)
-        dv = torch.zeros(v.shape, dtype=torch.float32, device=v.device)
+        dk = torch.zeros(kk.shape, dtype=torch.float32, device=k.device)
+        dv = torch.zeros(vv.shape, dtype=torch.float32, device=v.device)
         a.dk_accum, a.dv_accum = dk.data_ptr(), dv.data_ptr()
-        a.ld_dk = a.ld_dv = k.shape[1]
+        a.ld_dk = a.ld_dv = kk.shape[1]
     else:
-        dk, dv = torch.empty_like(k), torch.empty_like(v)
+        dk, dv = torch.empty_like(kk), torch.empty_like(vv)
         a.dk, a.dv = dk.data_ptr(), dv.data_ptr()
         a.ld_dk, a.ld_dv = dk.stride(0), dv.stride(0)
     d_w = torch.zeros(num_buckets, dtype=torch.float64, device=q.device)
@@ -311,22 +401,36 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
         d_pos = torch.zeros(pw.numel(), dtype=torch.float64, device=q.device)
         a.d_pos_weights = d_pos.data_ptr()
     kvt = q.shape[0] if kv_len_total is None else kv_len_total
-    ws, nbytes = _workspace(q.shape[0], kvt, a.num_segments, num_heads, a.head_dim, q.device)
+    ws, nbytes = _workspace(q.shape[0], kvt, a.num_segments, H, dp, q.device)
     a.workspace, a.workspace_bytes = ws.data_ptr(), nbytes
-    if max_kv_len is None:
-        if a.num_segments == 0:
-            max_kv_len = 0
-        elif kv_len is not None:
-            max_kv_len = int(kv_len.max().item())
-        else:
-            max_kv_len = int((q_offsets[1:] - q_offsets[:-1]).max().item())
-    ds_bytes = _lib.lib().jh_attn_ds_scratch_bytes(kvt, a.num_segments, num_heads, int(max_kv_len))
-    ds = torch.empty(ds_bytes, dtype=torch.uint8, device=q.device)
-    a.ds_scratch, a.ds_scratch_bytes = ds.data_ptr(), ds_bytes
+    a.deterministic = int(bool(deterministic))
+    if deterministic:
+        if max_kv_len is None:
+            if a.num_segments == 0:
+                max_kv_len = 0
+            elif kv_len is not None:
+                max_kv_len = int(kv_len.max().item())
+            else:
+                max_kv_len = int((q_offsets[1:] - q_offsets[:-1]).max().item())
+        ds_bytes = _lib.lib().jh_attn_ds_scratch_bytes(kvt, a.num_segments, H, int(max_kv_len))
+        ds = torch.empty(ds_bytes, dtype=torch.uint8, device=q.device)
+        a.ds_scratch, a.ds_scratch_bytes = ds.data_ptr(), ds_bytes
+    else:
+        st = bwd_state(q.shape[0], a.num_segments, H, dp, q.device)
+        a.bwd_state, a.bwd_state_bytes = st.data_ptr(), st.numel()
     _band(a, band_table, ready=True)
     _prof(a, prof)
     check(_lib.lib().jh_attn_bwd(ctypes.byref(a), _stream(q)), "hstu_attention backward")
-    _bump(3 if (pw is not None or band_table is not None) else 4)  # (band table) + build + dK/dV + dQ
+    if deterministic:
+        _bump(3 if (pw is not None or band_table is not None) else 4)  # (band table) + build + dK/dV + dQ
+    else:
+        _bump(2 if (pw is not None or band_table is not None) else 3)  # (band table) + build + fused
+    if dp != d:
+        if dq_accum is not None:
+            dq_accum.copy_(_unpad_heads(dqk, H, d, dp))
+        else:
+            dq.copy_(_unpad_heads(dqk, H, d, dp))
+        dk, dv = _unpad_heads(dk, H, d, dp), _unpad_heads(dv, H, d, dp)
     return dq, dk, dv, d_w, d_pos
 
 

@@ -45,8 +45,8 @@ class NumpyBackend:
 
     def fwd(self, q, k, v, ts_q, ts_k, segs, H, w, nb):
         qo, qp, ks, kl = self._segs(segs)
-        Q, K, V = q.numpy(), k.numpy(), v.numpy()
-        tq, tk, w = ts_q.numpy(), ts_k.numpy(), w.numpy()
+        Q, K, V = q.detach().numpy(), k.detach().numpy(), v.detach().numpy()
+        tq, tk, w = ts_q.numpy(), ts_k.numpy(), w.detach().numpy()
         d = Q.shape[1] // H
         out = np.zeros_like(Q)
         for s in range(len(qp)):
@@ -74,8 +74,8 @@ class NumpyBackend:
 
     def bwd(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb):
         qo, qp, ks, kl = self._segs(segs)
-        Q, K, V, G = q.numpy(), k.numpy(), v.numpy(), g.numpy()
-        tq, tk, w = ts_q.numpy(), ts_k.numpy(), w.numpy()
+        Q, K, V, G = q.detach().numpy(), k.detach().numpy(), v.detach().numpy(), g.detach().numpy()
+        tq, tk, w = ts_q.numpy(), ts_k.numpy(), w.detach().numpy()
         d = Q.shape[1] // H
         dq, dk, dv = np.zeros_like(Q), np.zeros_like(K), np.zeros_like(V)
         dw = np.zeros(nb)
@@ -158,3 +158,96 @@ def test_cp_layer_matches_single_device(tmp_path, world, lens, mode, overlap):
             assert got.shape == ref.shape and (got.size == 0 or np.abs(got - ref).max() < 1e-10), (r, name)
         assert np.abs(res["dw"] - ww).max() < 1e-10
         row += n
+
+
+def _worker_steps(rank, world, port, steps, H, D, result_dir, staged):
+    """Variable batches over several steps: some ranks repeat their local
+    lengths while others change (the plan-cache divergence scenario)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2508_04711_b200.cp_layer import CPAttention, HostStagedComm
+    w = torch.from_numpy(oracle.normal_init_ts_weights(16, 11))
+    comm = HostStagedComm(dist.group.WORLD) if staged else None
+    layer = CPAttention(dist.group.WORLD, H, 16, backend=NumpyBackend(), comm=comm, max_plans=2)
+    res = {}
+    for i, lens in enumerate(steps):
+        b = _batch(10 + i, rank, lens[rank], H * D)
+        t = {key: torch.from_numpy(b[key]) for key in ("q", "k", "v", "g", "ts")}
+        out, ctx = layer.forward(t["q"], t["k"], t["v"], t["ts"], np.diff(b["offsets"]), w)
+        dq, dk, dv, dw = layer.backward(ctx, t["g"], w)
+        res[f"out{i}"], res[f"dq{i}"], res[f"dw{i}"] = out.numpy(), dq.numpy(), dw.numpy()
+    np.savez(os.path.join(result_dir, f"r{rank}.npz"), **res)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("staged", [False, True])
+def test_cp_plan_cache_consistent_across_variable_batches(tmp_path, staged):
+    world, H, D = 2, 1, 4
+    steps = [[[7, 3], [12]], [[7, 3], [5, 9]], [[4], [5, 9]], [[7, 3], [12]], [[7, 3], [5, 9]]]
+    mp.spawn(_worker_steps, args=(world, _free_port(), steps, H, D, str(tmp_path), staged), nprocs=world, join=True)
+    w = oracle.normal_init_ts_weights(16, 11)
+    res = [np.load(os.path.join(tmp_path, f"r{r}.npz")) for r in range(world)]
+    for i, lens in enumerate(steps):
+        batches = [_batch(10 + i, r, lens[r], H * D) for r in range(world)]
+        cat = oracle.concat_batches(batches)
+        g = np.concatenate([b["g"] for b in batches])
+        want = oracle.hstu_forward(cat["q"], cat["k"], cat["v"], cat["ts"], cat["offsets"], w, 16, H)
+        wq, _, _, ww, _ = oracle.hstu_backward(cat["q"], cat["k"], cat["v"], cat["ts"], cat["offsets"], g, w, 16, H)
+        row = 0
+        for r in range(world):
+            n = batches[r]["q"].shape[0]
+            assert np.abs(res[r][f"out{i}"] - want[row:row + n]).max(initial=0) < 1e-10, (i, r)
+            assert np.abs(res[r][f"dq{i}"] - wq[row:row + n]).max(initial=0) < 1e-10, (i, r)
+            assert np.abs(res[r][f"dw{i}"] - ww).max() < 1e-10, (i, r)
+            row += n
+
+
+def _worker_cpdp(rank, world, port, cp, lens, H, D, result_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from torch.nn.parallel import DistributedDataParallel as DDP
+
+    from paper_2508_04711_b200.cp_layer import CPJaggedHSTUAttention, make_cp_dp_groups
+    cp_group, dp_group, ci, di = make_cp_dp_groups(cp)
+    w = oracle.normal_init_ts_weights(16, 11)
+    mod = CPJaggedHSTUAttention(cp_group, H, 16, backend=NumpyBackend(), weights=w)
+    model = DDP(mod, process_group=dp_group)
+    b = _batch(3, rank, lens[rank], H * D)
+    t = {key: torch.from_numpy(b[key]) for key in ("q", "k", "v", "g", "ts")}
+    for key in ("q", "k", "v"):
+        t[key].requires_grad_(True)
+    out = model(t["q"], t["k"], t["v"], t["ts"], np.diff(b["offsets"]))
+    (out * t["g"]).sum().backward()
+    np.savez(os.path.join(result_dir, f"r{rank}.npz"), out=out.detach().numpy(), dq=t["q"].grad.numpy(),
+             dk=t["k"].grad.numpy(), dv=t["v"].grad.numpy(), dw=mod.ts_weights.grad.numpy(), ci=ci, di=di)
+    dist.destroy_process_group()
+
+
+def test_hybrid_cp_dp_gradient_semantics(tmp_path):
+    """CP2 x DP2 (config C5's layout at world 4): outputs / input gradients
+    equal the single-device oracle on each CP group's batch; the ts_weights
+    gradient is the SUM over CP and the MEAN over DP (DDP over the DP group)."""
+    world, cp, H, D = 4, 2, 1, 4
+    lens = [[9, 0, 20], [13], [5, 30], [8, 8]]
+    mp.spawn(_worker_cpdp, args=(world, _free_port(), cp, lens, H, D, str(tmp_path)), nprocs=world, join=True)
+    w = oracle.normal_init_ts_weights(16, 11).astype(np.float32).astype(np.float64)
+    dws = []
+    res = [np.load(os.path.join(tmp_path, f"r{r}.npz")) for r in range(world)]
+    for grp in range(world // cp):
+        ranks = list(range(grp * cp, (grp + 1) * cp))
+        batches = [_batch(3, r, lens[r], H * D) for r in ranks]
+        cat = oracle.concat_batches(batches)
+        g = np.concatenate([b["g"] for b in batches])
+        want = oracle.hstu_forward(cat["q"], cat["k"], cat["v"], cat["ts"], cat["offsets"], w, 16, H)
+        wq, wk, wv, ww, _ = oracle.hstu_backward(cat["q"], cat["k"], cat["v"], cat["ts"], cat["offsets"], g, w, 16, H)
+        dws.append(ww)
+        row = 0
+        for r in ranks:
+            assert int(res[r]["ci"]) == r % cp and int(res[r]["di"]) == grp
+            n = batches[r - ranks[0]]["q"].shape[0]
+            for name, ref in (("out", want), ("dq", wq), ("dk", wk), ("dv", wv)):
+                assert np.abs(res[r][name] - ref[row:row + n]).max(initial=0) < 1e-9, (r, name)
+            row += n
+    expect = np.mean(dws, axis=0)
+    for r in range(world):
+        assert np.abs(res[r]["dw"] - expect).max() < 1e-6 * max(1.0, np.abs(expect).max()), r

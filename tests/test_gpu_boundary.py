@@ -1,0 +1,131 @@
+"""GPU tests of the drop-in boundary: the reference-signature entry points
+(attention.py:125/151/187, harness.py:270) against the CPU oracle, the
+small-head-dim path (zero-padded to 64 columns, 1/sqrt(d) kept), and the
+validation errors.
+
+Tolerance: the reference's row-normalised metric (harness.py:189-206) <= ROW_TOL
+for bf16 inputs with fp32 accumulation (measured ~3e-3); max-abs is printed.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from _cases import bf16_round, make_case, row_rel
+from conftest import load_npz_cases
+
+pytestmark = pytest.mark.gpu
+
+ROW_TOL = 6e-3
+DW_TOL = 1e-3
+
+
+def _report(name, got, want):
+    mx, rel = row_rel(got, want)
+    print(f"{name}: max_abs={mx:.3e} row_rel={rel:.3e}")
+    return rel
+
+
+def test_blockwise_partial_reference_signature_golden():
+    import paper_2508_04711_b200 as pkg
+    c = load_npz_cases("blockwise_cases.npz")["b0"]
+    q, k, v = (bf16_round(c[x].astype(np.float32)) for x in ("q", "k", "v"))
+    params, cfg = pkg.BiasParams(c["w"]), pkg.BiasConfig(16)
+    got = pkg.blockwise_partial(q, c["qs"], c["qp"], c["tq"], k, c["ks"], c["kp"], c["tk"], v, params, cfg)
+    assert got.shape == c["out"].shape and got.dtype == torch.float32
+    got = got.cpu().numpy()
+    want = oracle.blockwise_partial(q.astype(np.float64), c["qs"], c["qp"], c["tq"], k.astype(np.float64), c["ks"],
+                                    c["kp"], c["tk"], v.astype(np.float64), c["w"], 16)
+    assert _report("blockwise(oracle)", got, want) <= ROW_TOL
+    # the reference's own f64 output on the unrounded inputs (bf16 input rounding on top)
+    assert _report("blockwise(golden)", got, c["out"]) <= 3e-2
+    with pytest.raises(ValueError, match="rows but v has"):
+        pkg.blockwise_partial(q, c["qs"], c["qp"], c["tq"], k, c["ks"], c["kp"], c["tk"], v[:3], params, cfg)
+    z = pkg.blockwise_partial(q[:0], c["qs"][:0], c["qp"][:0], c["tq"][:0], k, c["ks"], c["kp"], c["tk"], v,
+                              params, cfg)
+    assert tuple(z.shape) == (0, 8)
+
+
+@pytest.mark.parametrize("d,seed", [(128, 1), (64, 2), (8, 3)])
+def test_blockwise_partial_cp_ring_blocks_sum_to_forward(d, seed):
+    # block additivity (test_attention.py:220-250): partials over a partition of
+    # the keys sum to the full forward
+    import paper_2508_04711_b200 as pkg
+    lens = [300, 77, 513]
+    case = make_case(lens, d, seed=seed)
+    offs = case["offsets"]
+    seq = np.repeat(np.arange(len(lens)), lens)
+    pos = np.concatenate([np.arange(L) for L in lens])
+    params, cfg = pkg.BiasParams(case["w"]), pkg.BiasConfig(16)
+    parts = np.array_split(np.random.default_rng(seed).permutation(int(offs[-1])), 3)
+    total = 0
+    for idx in parts:
+        idx = np.sort(idx)
+        total = total + pkg.blockwise_partial(case["q"], seq, pos, case["ts"], case["k"][idx], seq[idx], pos[idx],
+                                              case["ts"][idx], case["v"][idx], params, cfg).cpu().numpy()
+    want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], offs, case["w"], 16, 1)
+    assert _report(f"blockwise sum d={d}", total, want) <= ROW_TOL
+
+
+@pytest.mark.parametrize("lens,H,d", [([5, 0, 17, 33], 2, 8), ([130, 1, 64], 3, 32), ([200, 9], 1, 96)])
+def test_small_head_dims_through_reference_api(lens, H, d):
+    import paper_2508_04711_b200 as pkg
+    case = make_case(lens, H * d, seed=sum(lens) + d)
+    offs = case["offsets"]
+    ml = max(max(lens), 1)
+    J = lambda x: pkg.new_jagged(torch.from_numpy(x), offs, ml, device="cuda")  # noqa: E731
+    inp = pkg.AttentionInputs(J(case["q"]), J(case["k"]), J(case["v"]),
+                              pkg.new_int_series(case["ts"], offs, device="cuda"), pkg.BiasParams(case["w"]),
+                              pkg.BiasConfig(16), num_heads=H)
+    out = pkg.hstu_attention_reference(inp).values.float().cpu().numpy()
+    want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], offs, case["w"], 16, H)
+    assert _report(f"fwd d={d}", out, want) <= ROW_TOL
+    gr = pkg.hstu_attention_backward(inp, J(case["g"]))
+    wq, wk, wv, ww, _ = oracle.hstu_backward(case["q"], case["k"], case["v"], case["ts"], offs, case["g"], case["w"],
+                                             16, H)
+    for name, got, want in (("dq", gr.dq, wq), ("dk", gr.dk, wk), ("dv", gr.dv, wv)):
+        assert _report(f"{name} d={d}", got.values.float().cpu().numpy(), want) <= ROW_TOL, name
+    dw = gr.d_ts_weights.cpu().numpy()
+    assert np.abs(dw - ww).max() <= DW_TOL * np.abs(ww).max()
+
+
+def test_ts_weights_shorter_than_num_buckets_raises():
+    from paper_2508_04711_b200 import kernels
+    case = make_case([10], 64, seed=0)
+    t = lambda x: torch.from_numpy(x).cuda()  # noqa: E731
+    q = t(case["q"]).bfloat16()
+    with pytest.raises(ValueError, match="num_buckets"):
+        kernels.attn_fwd(q, q, q, t(case["ts"]), t(case["ts"]), t(case["offsets"]), 1,
+                         torch.zeros(8, device="cuda"), 16)
+
+
+def _oracle_reference(batches, params, bias_cfg, num_heads):
+    """harness.py:173-186 on the CPU oracle (the bf16 values the GPU holds, upcast)."""
+    vals = lambda b, f: getattr(b, f).values.float().cpu().numpy()  # noqa: E731
+    cat = {f: np.concatenate([vals(b, f) for b in batches]) for f in ("q", "k", "v")}
+    ts = np.concatenate([b.ts.values.cpu().numpy() for b in batches])
+    offs = [0]
+    for b in batches:
+        offs.extend(int(offs[-1] + o) for o in b.q.host_offsets[1:])
+    out = oracle.hstu_forward(cat["q"], cat["k"], cat["v"], ts, np.asarray(offs), np.asarray(params.ts_weights),
+                              bias_cfg.num_buckets, num_heads)
+    res, row = [], 0
+    for b in batches:
+        n = int(b.q.host_offsets[-1])
+        res.append(out[row:row + n])
+        row += n
+    return res
+
+
+@pytest.mark.parametrize("cp,mode,sched", [(2, "balanced_minichunk", "sequential"),
+                                           (4, "naive_contiguous", "threaded")])
+def test_run_experiment_checked_against_oracle(cp, mode, sched):
+    from paper_2508_04711_b200 import harness
+    cfg = harness.ExperimentConfig(cp_size=cp, batch_size=3, min_len=0, max_len=300, max_length=512, embed_dim=128,
+                                   num_heads=1, balance_mode=mode, seed=5)
+    rep = harness.run_experiment(cfg, scheduling=sched, reference=_oracle_reference)
+    print(f"run_experiment cp={cp}: max_abs={rep.max_abs_error:.3e} row_rel={rep.max_rel_error:.3e}")
+    assert rep.max_rel_error <= ROW_TOL
