@@ -379,7 +379,7 @@ def max_seq_len_probe(dev, w):
 
     t0 = time.time()
     lo, hi, L = 0, None, 16384
-    while hi is None and L <= (1 << 21):
+    while hi is None and L <= (1 << 20) and time.time() - t0 < 60:
         if runs(L):
             lo, L = L, 2 * L
         else:

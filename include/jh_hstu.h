@@ -175,6 +175,10 @@ typedef struct jh_attn_args {
    * kv_pos] (uint8; entries of pairs it never evaluated are left untouched) */
   uint8_t* dbg_buckets;
   int64_t dbg_ld;
+  /* debug (fused backward): 1 = d_ts_weights receives the exact number of
+   * visible (q, kv) pairs per bucket (summed over heads) instead of dS sums --
+   * the backward's bucket placement as integers */
+  int32_t dbg_count_buckets;
 } jh_attn_args;
 
 /* Size of the fused backward's persistent state (fp32 dQ accumulator rows +

@@ -49,7 +49,7 @@ class JhAttnArgs(ctypes.Structure):
         ("band_table", c_vp), ("band_table_bytes", ctypes.c_size_t), ("band_table_ready", ctypes.c_int32),
         ("score_scale", ctypes.c_float), ("deterministic", ctypes.c_int32),
         ("bwd_state", c_vp), ("bwd_state_bytes", ctypes.c_size_t),
-        ("dbg_buckets", c_vp), ("dbg_ld", ctypes.c_int64),
+        ("dbg_buckets", c_vp), ("dbg_ld", ctypes.c_int64), ("dbg_count_buckets", ctypes.c_int32),
     ]
 
 

@@ -76,6 +76,7 @@ struct WorkLists {
   // dep[0] = finished dK/dV CTAs, dep[kDepBase + s*H + h] = finished kv tiles of (s, h)
   int32_t* dep;
   int32_t dep_heads;
+  int32_t fwd_pairs;  // 1: fwd items are pairs of q tiles (s, u) = tiles 2u, 2u+1 (two-tile forward)
 };
 constexpr int kDepBase = 16;
 
@@ -159,7 +160,10 @@ JH_DEV T block_exclusive_scan(T v, T* warp_sum, T* total) {
 
 // One block of 1024 threads.  fwd items (s, q_tile) ordered by #kv tiles
 // descending; bwd items (s, kv_tile) ordered by #q tiles descending (counting
-// sort over a 1024-level histogram).  The segment each thread owns first is
+// sort over a 1024-level histogram).  q tiles that see no kv at all (a
+// segment with kv_len 0) are not items: a run of such items could otherwise
+// stall the persistent kernels' 2-deep item ring (their output rows are zeroed
+// by the host in the segment form, the only form where they occur).  The segment each thread owns first is
 // decoded once and kept in registers across the passes.
 static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, WorkLists wl,
                                                                    unsigned long long* stamp = nullptr) {
@@ -185,12 +189,13 @@ static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, 
     first = first < 0 ? 0 : first;
     return (int)((g.lq - first + kBM - 1) / kBM);
   };
+  const int fstep = wl.fwd_pairs ? 2 : 1;
   for (int64_t s = tid; s < sa.num_segments; s += blockDim.x) {
     const Seg g = seg(s);
     const int nt = (int)((g.lq + kBM - 1) / kBM);
-    for (int t = 0; t < nt; ++t) {
-      const int w = (int)((fwd_kv_lim(g, t) + kBN - 1) / kBN);
-      atomicAdd(&hist_f[min(w, kLevels - 1)], 1);
+    for (int t = 0; t < nt; t += fstep) {
+      const int w = (int)((fwd_kv_lim(g, min(t + fstep - 1, nt - 1)) + kBN - 1) / kBN);
+      if (w > 0) atomicAdd(&hist_f[min(w, kLevels - 1)], 1);  // (tiles that see no kv are not items)
     }
     const int nj = (int)((seg_kv_vis(g) + kBN - 1) / kBN);
     for (int j = 0; j < nj; ++j) atomicAdd(&hist_b[min(bwd_w(g, j), kLevels - 1)], 1);
@@ -215,9 +220,9 @@ static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, 
   for (int64_t s = tid; s < sa.num_segments; s += blockDim.x) {
     const Seg g = seg(s);
     const int nt = (int)((g.lq + kBM - 1) / kBM);
-    for (int t = 0; t < nt; ++t) {
-      const int w = (int)((fwd_kv_lim(g, t) + kBN - 1) / kBN);
-      wl.fwd[atomicAdd(&hist_f[min(w, kLevels - 1)], 1)] = make_int2((int)s, t);
+    for (int t = 0; t < nt; t += fstep) {
+      const int w = (int)((fwd_kv_lim(g, min(t + fstep - 1, nt - 1)) + kBN - 1) / kBN);
+      if (w > 0) wl.fwd[atomicAdd(&hist_f[min(w, kLevels - 1)], 1)] = make_int2((int)s, t / fstep);
     }
     const int nj = (int)((seg_kv_vis(g) + kBN - 1) / kBN);
     for (int j = 0; j < nj; ++j) wl.bwd[atomicAdd(&hist_b[min(bwd_w(g, j), kLevels - 1)], 1)] = make_int2((int)s, j);
@@ -375,6 +380,11 @@ struct AttnParams {
   unsigned long long* trace;
   int32_t trace_cta;
   int32_t dbg;  // experiment switches (JH_DBG environment variable), 0 in production
+  // fused backward (hstu_bwd_fused_kernel): persistent zero state
+  float* dq_state;      // fp32 dQ accumulator [q_rows][H*D] (bf16-dq mode)
+  int32_t* dq_cnt;      // per-(q tile, head) contribution counters
+  int32_t* dw_done;     // last-CTA counter of the d_ts_weights reduction
+  int32_t dbg_count;    // debug: d_ts_weights = exact pair count per bucket
   float c1;     // score_scale / 2: SiLU(s) = h + h tanh(h), h = c1 * (q k^T + bias)
   uint8_t* dbg_buckets;  // forward debug export of the applied bucket per (q row, kv pos), head 0
   int64_t dbg_ld;

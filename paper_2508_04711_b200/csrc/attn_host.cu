@@ -15,7 +15,12 @@ template <int D>
 int launch_fwd(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                const AttnParams&, int, cudaStream_t, void*, void*);
 template <int D>
+int launch_fwd2(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                const AttnParams&, int, cudaStream_t, void*, void*);
+template <int D>
 int launch_bwd(const TMaps&, const AttnParams&, const jh_attn_args&, int, cudaStream_t);
+template <int D>
+int launch_bwd_fused(const TMaps&, const AttnParams&, const jh_attn_args&, int, cudaStream_t);
 
 static int sm_count() {
   static int n = 0;
@@ -75,6 +80,17 @@ static BwdStateLayout bwd_state_layout(int64_t q_rows, int64_t nseg, int32_t H, 
   return l;
 }
 
+// Forward kernel: the two-q-tile kernel (attn_fwd2.cu) unless JH_FWD1=1 selects
+// the one-tile kernel (attn_fwd.cu) for A/B measurements.
+static bool fwd_two_tile() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("JH_FWD1");
+    v = (e && atoi(e) == 1) ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 static int validate(const jh_attn_args* a, bool bwd) {
@@ -127,8 +143,16 @@ static int validate(const jh_attn_args* a, bool bwd) {
   WsLayout w = ws_layout(a->q_rows, a->q_rows, a->num_segments, a->num_heads, a->head_dim);
   if (!a->workspace || a->workspace_bytes < w.total)
     return set_error(JH_ERR_INVALID, "workspace too small (need >= %zu bytes)", w.total);
-  if (bwd && a->q_rows > 0 && (!a->ds_scratch || a->ds_scratch_bytes < (size_t)kDsBlockBytes || !aligned16(a->ds_scratch)))
+  if (bwd && a->q_rows > 0 && a->deterministic &&
+      (!a->ds_scratch || a->ds_scratch_bytes < (size_t)kDsBlockBytes || !aligned16(a->ds_scratch)))
     return set_error(JH_ERR_INVALID, "ds_scratch missing or too small (see jh_attn_ds_scratch_bytes)");
+  if (bwd && a->q_rows > 0 && !a->deterministic) {
+    const int D = a->head_dim;
+    if (!a->bwd_state || (uintptr_t)a->bwd_state % 256 ||
+        a->bwd_state_bytes < bwd_state_layout(a->q_rows, a->num_segments, a->num_heads, D).total)
+      return set_error(JH_ERR_INVALID, "bwd_state missing, misaligned or too small (see jh_attn_bwd_state_bytes)");
+    if (!a->dq_accum && (a->ld_dq * 2) % 16) return set_error(JH_ERR_INVALID, "dq row stride must be 16-byte aligned");
+  }
   return JH_OK;
 }
 
@@ -182,19 +206,29 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
   p->wl.hdr = (WorkHeader*)ws;
   p->wl.fwd = (int2*)(ws + w.items_f);
   p->wl.bwd = (int2*)(ws + w.items_b);
-  p->ds = bwd ? (__nv_bfloat16*)a->ds_scratch : nullptr;
-  p->ds_cap_blocks = bwd ? (int64_t)(a->ds_scratch_bytes / kDsBlockBytes) : 0;
+  const bool det = bwd && a->deterministic;
+  p->ds = det ? (__nv_bfloat16*)a->ds_scratch : nullptr;
+  p->ds_cap_blocks = det ? (int64_t)(a->ds_scratch_bytes / kDsBlockBytes) : 0;
+  if (bwd && !det) {
+    const BwdStateLayout sl = bwd_state_layout(a->q_rows, a->num_segments, a->num_heads, a->head_dim);
+    uint8_t* st = (uint8_t*)a->bwd_state;
+    p->dq_state = (float*)(st + sl.acc);
+    p->dq_cnt = (int32_t*)(st + sl.cnt);
+    p->dw_done = (int32_t*)(st + sl.done);
+  }
+  p->dbg_count = bwd ? a->dbg_count_buckets : 0;
   // per-CTA gradient bins at the end of the caller's workspace
   // (the bwd item list is bounded by the caller's kv total, unknown here: the
   // dS block bases and the per-CTA bins are carved from the end of the workspace)
   const size_t bins_off = (a->workspace_bytes - bins_bytes()) & ~size_t(255);
   const size_t dsb_off = (bins_off - (size_t)(a->num_segments + 1) * 8) & ~size_t(255);
   const size_t dep_off = (dsb_off - (size_t)(kDepBase + a->num_segments * a->num_heads) * 4) & ~size_t(255);
-  p->wl.dep = bwd ? (int32_t*)(ws + dep_off) : nullptr;
+  p->wl.dep = det ? (int32_t*)(ws + dep_off) : nullptr;
   p->wl.dep_heads = a->num_heads;
+  p->wl.fwd_pairs = (!bwd && fwd_two_tile()) ? 1 : 0;
   p->wl.bins = bwd ? (float*)(ws + bins_off) : nullptr;
   p->wl.partials = bwd ? (double*)(ws + bins_off + (size_t)sm_count() * kBinsPerCta * 4) : nullptr;
-  p->wl.ds_base = bwd ? (int64_t*)(ws + dsb_off) : nullptr;
+  p->wl.ds_base = det ? (int64_t*)(ws + dsb_off) : nullptr;
   const size_t tbg_off = (dep_off - tbglob_bytes()) & ~size_t(255);
   const size_t band_off = (tbg_off - band_bytes(a->q_rows, a->num_segments)) & ~size_t(255);
   if (band_off < w.items_b + 8 || band_off > a->workspace_bytes) return set_error(JH_ERR_INVALID, "workspace too small");
@@ -219,8 +253,9 @@ static int prepare(const jh_attn_args* a, bool bwd, AttnParams* p, TMaps* tm, cu
       make_tmap_i64_1d(&tm->tsq, a->ts_q, a->q_rows, kTsBox) ||
       make_tmap_i64_1d(&tm->tsk, a->ts_k, a->kv_rows, kTsBox))
     return set_error(JH_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  if (bwd && (make_tmap_bf16_2d(&tm->dout, a->dout, a->q_rows, HD, a->ld_do, 128) ||
-              make_tmap_bf16_2d(&tm->q64, a->q, a->q_rows, HD, a->ld_q, 64) ||
+  if (bwd && make_tmap_bf16_2d(&tm->dout, a->dout, a->q_rows, HD, a->ld_do, 128))
+    return set_error(JH_ERR_CUDA, "cuTensorMapEncodeTiled failed (dout)");
+  if (det && (make_tmap_bf16_2d(&tm->q64, a->q, a->q_rows, HD, a->ld_q, 64) ||
               make_tmap_bf16_2d(&tm->do64, a->dout, a->q_rows, HD, a->ld_do, 64) ||
               make_tmap_i64_1d(&tm->tsq72, a->ts_q, a->q_rows, kTsBoxH) ||
               make_tmap_bf16_2d(&tm->k64, a->k, a->kv_rows, HD, a->ld_k, 64) ||
@@ -305,10 +340,27 @@ int jh_attn_fwd(const jh_attn_args* a, void* stream) {
   TMaps tm;
   rc = prepare(a, false, &p, &tm, s);
   if (rc) return rc;
+  if (a->q_pos0 || a->kv_len) {
+    // segment form: q tiles of kv_len-0 segments are not work items -> zero rows
+    // (store modes; the add mode leaves them untouched, as documented)
+    cudaError_t e = cudaSuccess;
+    const size_t HDe = (size_t)a->num_heads * a->head_dim;
+    if (a->out_accum_mode == 1)
+      e = cudaMemset2DAsync(a->out_accum, (size_t)a->ld_o * 4, 0, HDe * 4, (size_t)a->q_rows, s);
+    else if (a->out_accum_mode == 0)
+      e = cudaMemset2DAsync(a->out, (size_t)a->ld_o * 2, 0, HDe * 2, (size_t)a->q_rows, s);
+    if (e != cudaSuccess) return set_error(JH_ERR_CUDA, "out memset: %s", cudaGetErrorString(e));
+  }
   int grid = sm_count();
-  int lr = a->head_dim == 64
-               ? launch_fwd<64>(tm.q, tm.k, tm.v, tm.tsq, tm.tsk, p, grid, s, a->prof_event_start, a->prof_event_end)
-               : launch_fwd<128>(tm.q, tm.k, tm.v, tm.tsq, tm.tsk, p, grid, s, a->prof_event_start, a->prof_event_end);
+  int lr;
+  if (p.wl.fwd_pairs)
+    lr = a->head_dim == 64
+             ? launch_fwd2<64>(tm.q, tm.k, tm.v, tm.tsq, tm.tsk, p, grid, s, a->prof_event_start, a->prof_event_end)
+             : launch_fwd2<128>(tm.q, tm.k, tm.v, tm.tsq, tm.tsk, p, grid, s, a->prof_event_start, a->prof_event_end);
+  else
+    lr = a->head_dim == 64
+             ? launch_fwd<64>(tm.q, tm.k, tm.v, tm.tsq, tm.tsk, p, grid, s, a->prof_event_start, a->prof_event_end)
+             : launch_fwd<128>(tm.q, tm.k, tm.v, tm.tsq, tm.tsk, p, grid, s, a->prof_event_start, a->prof_event_end);
   if (lr > 0) return set_error(JH_ERR_CUDA, "hstu_fwd launch: %s", cudaGetErrorString((cudaError_t)lr));
   if (lr) return JH_ERR_UNSUPPORTED;
   return JH_OK;
@@ -324,7 +376,25 @@ int jh_attn_bwd(const jh_attn_args* a, void* stream) {
   rc = prepare(a, true, &p, &tm, s);
   if (rc) return rc;
   int grid = sm_count();
-  int lr = a->head_dim == 64 ? launch_bwd<64>(tm, p, *a, grid, s) : launch_bwd<128>(tm, p, *a, grid, s);
+  if (!a->dq_accum && (a->q_pos0 || a->kv_len)) {
+    // segment form: q tiles that see no kv get no dQ contribution -> zero rows
+    const size_t HDb = (size_t)a->num_heads * a->head_dim * 2;
+    cudaError_t e = cudaMemset2DAsync(a->dq, (size_t)a->ld_dq * 2, 0, HDb, (size_t)a->q_rows, s);
+    if (e != cudaSuccess) return set_error(JH_ERR_CUDA, "dq memset: %s", cudaGetErrorString(e));
+  }
+  if ((a->q_pos0 || a->kv_len) && a->kv_rows > 0) {
+    // kv rows past every segment's visible range get no dK / dV: zero them (bf16 modes)
+    const size_t HDb = (size_t)a->num_heads * a->head_dim * 2;
+    cudaError_t e = cudaSuccess;
+    if (!a->dk_accum) e = cudaMemset2DAsync(a->dk, (size_t)a->ld_dk * 2, 0, HDb, (size_t)a->kv_rows, s);
+    if (e == cudaSuccess && !a->dv_accum) e = cudaMemset2DAsync(a->dv, (size_t)a->ld_dv * 2, 0, HDb, (size_t)a->kv_rows, s);
+    if (e != cudaSuccess) return set_error(JH_ERR_CUDA, "dk/dv memset: %s", cudaGetErrorString(e));
+  }
+  int lr;
+  if (a->deterministic)
+    lr = a->head_dim == 64 ? launch_bwd<64>(tm, p, *a, grid, s) : launch_bwd<128>(tm, p, *a, grid, s);
+  else
+    lr = a->head_dim == 64 ? launch_bwd_fused<64>(tm, p, *a, grid, s) : launch_bwd_fused<128>(tm, p, *a, grid, s);
   if (lr > 0) return set_error(JH_ERR_CUDA, "hstu_bwd launch: %s", cudaGetErrorString((cudaError_t)lr));
   if (lr) return JH_ERR_UNSUPPORTED;
   return JH_OK;

@@ -329,7 +329,7 @@ def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=
 
 
 # deterministic backward (two kernels over a bf16 dS scratch) or the fused one
-DETERMINISTIC_DEFAULT = {"value": True}
+DETERMINISTIC_DEFAULT = {"value": False}
 _BWD_STATE: dict = {}
 
 
@@ -347,7 +347,7 @@ def bwd_state(q_rows: int, num_segments: int, H: int, dp: int, device) -> torch.
 
 def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_buckets=16, pos_weights=None,
              q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, accumulate_dkv=False, prof=None,
-             max_kv_len=None, dq_accum=None, band_table=None, deterministic=None):
+             max_kv_len=None, dq_accum=None, band_table=None, deterministic=None, dbg_count_buckets=False):
     """Fused jagged HSTU backward (jh_attn_bwd).
 
     Returns (dq bf16, dk, dv, d_ts_weights f64, d_pos f64 or None); dk/dv are
@@ -404,6 +404,9 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
     ws, nbytes = _workspace(q.shape[0], kvt, a.num_segments, H, dp, q.device)
     a.workspace, a.workspace_bytes = ws.data_ptr(), nbytes
     a.deterministic = int(bool(deterministic))
+    a.dbg_count_buckets = int(bool(dbg_count_buckets))
+    if dbg_count_buckets and deterministic:
+        raise ValueError("dbg_count_buckets is a fused-backward debug mode")
     if deterministic:
         if max_kv_len is None:
             if a.num_segments == 0:

@@ -17,7 +17,8 @@ from conftest import load_npz_cases
 
 pytestmark = pytest.mark.gpu
 
-ROW_TOL = 2e-2
+ROW_TOL = 1e-2  # measured 3-7e-3 (bf16 P / dS / outputs, L <= 1024); 2e-2 before round 2
+ROW_TOL_LONG = 1e-2  # L up to 4096 (error grows slowly with L: 3-6e-3 measured)
 DW_TOL = 1e-3
 
 
@@ -68,23 +69,25 @@ def test_fwd_synthetic_c2_subset():
     assert row_rel(got, want)[1] <= ROW_TOL
 
 
-def _bwd(case, H, pos=None):
+def _bwd(case, H, pos=None, det=False):
     from paper_2508_04711_b200 import kernels
     c = to_cuda(case)
     dq, dk, dv, dw, dpos = kernels.attn_bwd(
         c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], c["g"], H, c["w"], case["nb"],
-        pos_weights=None if pos is None else torch.from_numpy(pos).float().cuda())
+        pos_weights=None if pos is None else torch.from_numpy(pos).float().cuda(), deterministic=det)
     torch.cuda.synchronize()
     f = lambda t: t.float().cpu().numpy()  # noqa: E731
     return f(dq), f(dk), f(dv), dw.cpu().numpy(), None if dpos is None else dpos.cpu().numpy()
 
 
-def _check_bwd(case, H, got):
+def _check_bwd(case, H, got, tol=ROW_TOL):
     dq, dk, dv, dw, _ = got
     wq, wk, wv, ww, _ = oracle.hstu_backward(case["q"], case["k"], case["v"], case["ts"], case["offsets"],
                                               case["g"], case["w"], case["nb"], H)
     for name, a, b in (("dq", dq, wq), ("dk", dk, wk), ("dv", dv, wv)):
-        assert row_rel(a, b)[1] <= ROW_TOL, (name, row_rel(a, b))
+        mx, rel = row_rel(a, b)
+        print(f"{name}: max_abs={mx:.3e} row_rel={rel:.3e}")
+        assert rel <= tol, (name, mx, rel)
     assert np.abs(dw - ww).max() / max(np.abs(ww).max(), 1e-30) <= DW_TOL, (dw, ww)
 
 
@@ -92,14 +95,16 @@ def _check_bwd(case, H, got):
     ([1], 1, 128), ([5, 0, 17, 1, 32], 1, 64), ([128], 1, 128), ([129, 255, 256, 257], 2, 64),
     ([300, 77, 1000], 4, 128), ([513, 1, 2, 3], 2, 128),
 ])
-def test_bwd_matches_oracle(lens, H, d):
+@pytest.mark.parametrize("det", [False, True], ids=["fused", "deterministic"])
+def test_bwd_matches_oracle(lens, H, d, det):
     case = make_case(lens, H * d, seed=sum(lens) + 7 * H)
-    _check_bwd(case, H, _bwd(case, H))
+    _check_bwd(case, H, _bwd(case, H, det=det))
 
 
-def test_bwd_unsorted_timestamps():
+@pytest.mark.parametrize("det", [False, True], ids=["fused", "deterministic"])
+def test_bwd_unsorted_timestamps(det):
     case = make_case([400, 200], 128, seed=5, unsorted_ts=True)
-    _check_bwd(case, 1, _bwd(case, 1))
+    _check_bwd(case, 1, _bwd(case, 1, det=det))
 
 
 @pytest.mark.parametrize("name", ["f32_c1_bf16", "f32_d64_bf16_long"])
@@ -135,6 +140,7 @@ def test_fwd_bwd_timestamp_regimes(gap_max, equal):
     want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], case["offsets"], case["w"], 16, H)
     assert row_rel(got, want)[1] <= ROW_TOL
     _check_bwd(case, H, _bwd(case, H))
+    _check_bwd(case, H, _bwd(case, H, det=True))
 
 
 # ------------------------------------------------ full-size configs (sampled)
@@ -152,6 +158,7 @@ def test_c2_full_batch_matches_oracle():
     want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], case["offsets"], case["w"], 16, 4)
     assert row_rel(got, want)[1] <= ROW_TOL
     _check_bwd(case, 4, _bwd(case, 4))
+    _check_bwd(case, 4, _bwd(case, 4, det=True))
 
 
 def test_long_sequences_c3_lengths():
@@ -160,5 +167,6 @@ def test_long_sequences_c3_lengths():
     case = make_case([4096, 2500, 1], H * 128, seed=41)
     got = _fwd(case, H)
     want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], case["offsets"], case["w"], 16, H)
-    assert row_rel(got, want)[1] <= ROW_TOL
-    _check_bwd(case, H, _bwd(case, H))
+    assert row_rel(got, want)[1] <= ROW_TOL_LONG
+    _check_bwd(case, H, _bwd(case, H), tol=ROW_TOL_LONG)
+    _check_bwd(case, H, _bwd(case, H, det=True), tol=ROW_TOL_LONG)

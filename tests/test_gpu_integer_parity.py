@@ -134,3 +134,29 @@ def test_backward_d_ts_weights_per_bucket(deterministic):
     assert (err[~present] == 0).all()
     # each bucket within 2e-2 of its own magnitude (+ 1e-3 of the largest)
     assert (err <= 2e-2 * np.abs(want) + 1e-3 * np.abs(want).max()).all()
+
+
+@pytest.mark.parametrize("name,case", _cases(), ids=[n for n, _ in _cases()])
+def test_backward_bucket_placement_counts_bit_exact(name, case):
+    """Fused backward in count mode: d_ts_weights[b] = the number of visible
+    (q, kv) pairs the backward's epilogue placed in bucket b (x heads) -- every
+    chunk class (saturated, band table, per-element) -- equals the oracle's
+    bincount of bucketize_array over the causal pairs, exactly."""
+    from paper_2508_04711_b200 import kernels
+    offs = case["offsets"]
+    nb, H = 16, 2 if case["q"].shape[1] == 128 and name == "ragged" else 1
+    c = {x: _t(case[x]).bfloat16() for x in ("q", "k", "v")}
+    g = c["q"].clone()
+    w = _t(np.asarray(case["w"], np.float32))
+    _, _, _, dw, _ = kernels.attn_bwd(c["q"], c["k"], c["v"], _t(case["ts"]), _t(case["ts"]), _t(offs), g, H, w,
+                                      nb, dbg_count_buckets=True)
+    got = dw.cpu().numpy()
+    want = np.zeros(nb, dtype=np.int64)
+    for b in range(len(offs) - 1):
+        lo, hi = int(offs[b]), int(offs[b + 1])
+        L = hi - lo
+        if L == 0:
+            continue
+        bk = oracle.bucketize_array(case["ts"][lo:hi, None] - case["ts"][None, lo:hi], nb)
+        want += np.bincount(bk[np.tril(np.ones((L, L), bool))], minlength=nb)
+    np.testing.assert_array_equal(got, (want * H).astype(np.float64))
