@@ -12,9 +12,10 @@ N > 1  -> jagged context parallelism over N ranks (one process per GPU,
 A step is one forward + backward of the attention over the whole batch.
 ``value`` = tokens of all ranks / device step time (inputs resident, L2
 flushed between timed steps); ``e2e`` = the same through the public API with
-host (pinned) inputs copied H2D and d_ts_weights read D2H inside the timed
-region.  ``--impl reference`` times the CPU reference (the oracle port of
-jaggedcp's numpy path) on host cores.
+host (pinned) inputs copied H2D and every result (out, dq, dk, dv,
+d_ts_weights) read back D2H inside the timed region.  ``--impl reference``
+times the reference's own CPU path (jaggedcp installed in baseline/_ref,
+through its public API) on host cores.
 """
 
 from __future__ import annotations
@@ -190,11 +191,13 @@ def run_gpu(args):
         flat_lens = [x for r in all_lens for x in r]
     else:
         band = kernels.new_band_table(T, len(lens), dev)  # computed by the forward, reused by the backward
+        seg_host = (h["offsets"], None, None)
+        bwd_two_kernel = kernels.ds_scratch_bytes(H, h["offsets"]) <= kernels.ds_scratch_budget(dev)
 
         def step_fn(prof=None):
             kernels.attn_fwd(q, k, v, ts, ts, offs, H, w, NB, prof=None if prof is None else prof[0], band_table=band)
             return kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, NB, prof=None if prof is None else prof[1],
-                                    max_kv_len=MAXLEN, band_table=band)
+                                    seg_host=seg_host, band_table=band)
         tokens_total = T
         flat_lens = [int(x) for x in lens]
 
@@ -286,11 +289,13 @@ def run_gpu(args):
         ach_b = Fb / (bwd_ms / 1e3) / 1e12
         ach_f = Ff / (fwd_ms / 1e3) / 1e12
         result["roofline"] = {
-            "bound": "tensor", "kernel": "jh_attn_bwd: hstu_bwd_dkv_kernel<128> + hstu_bwd_dq_kernel<128>", "achieved": ach_b, "peak": peak,
+            "bound": "tensor",
+            "kernel": ("jh_attn_bwd: hstu_bwd_dkv_kernel<128> + hstu_bwd_dq_kernel<128>" if bwd_two_kernel
+                       else "jh_attn_bwd: hstu_bwd_fused_kernel<128>"), "achieved": ach_b, "peak": peak,
             "unit": "TFLOP/s", "frac": ach_b / peak, "traffic": _traffic("bwd"),
             "peak_kind": f"{peak_kind} burst bf16 (MEASURED_PEAKS.json)",
             "algorithmic_flops_per_launch": Fb, "ms_per_launch": bwd_ms,
-            "fwd": {"kernel": "hstu_fwd_kernel<128>", "achieved": ach_f, "frac": ach_f / peak,
+            "fwd": {"kernel": "hstu_fwd2_kernel<128>" if os.environ.get("JH_FWD2") == "1" else "hstu_fwd_kernel<128>", "achieved": ach_f, "frac": ach_f / peak,
                     "algorithmic_flops_per_launch": Ff, "ms_per_launch": fwd_ms, "traffic": _traffic("fwd")},
         }
     result["clocks"] = clk.summary()
@@ -303,36 +308,50 @@ def run_gpu(args):
     tsh, offh = pin(h["ts"]), h["offsets"]
     params, bcfg = BiasParams(w_host), BiasConfig(NB)
     h2d = sum(x.numel() * x.element_size() for x in (qh, kh, vh, gh, tsh)) + 5 * offh.nbytes + 2 * NB * 4
-    d2h = NB * 8
+    # results back to pinned host buffers: out, dq, dk, dv (bf16) and d_ts_weights (f64),
+    # i.e. everything the reference's numpy API returns
+    outs_h = [torch.empty((T, H * D), dtype=torch.bfloat16).pin_memory() for _ in range(4)]
+    dw_h = torch.empty(NB, dtype=torch.float64).pin_memory()
+    d2h_full = sum(x.numel() * x.element_size() for x in outs_h) + dw_h.numel() * 8
+    d2h_dw = NB * 8
 
-    def e2e_step():
+    def e2e_step(full: bool):
         qj = new_jagged(qh.to(dev, non_blocking=True), offh, MAXLEN, copy=False)
         kj = new_jagged(kh.to(dev, non_blocking=True), offh, MAXLEN, copy=False)
         vj = new_jagged(vh.to(dev, non_blocking=True), offh, MAXLEN, copy=False)
         tj = new_int_series(tsh.to(dev, non_blocking=True), offh)
         inp = AttentionInputs(qj, kj, vj, tj, params, bcfg, num_heads=H)
-        hstu_attention_reference(inp)
+        out = hstu_attention_reference(inp)
         gr = hstu_attention_backward(inp, new_jagged(gh.to(dev, non_blocking=True), offh, MAXLEN, copy=False))
-        return gr.d_ts_weights.cpu()
+        if full:
+            for dst, src in zip(outs_h, (out.values, gr.dq.values, gr.dk.values, gr.dv.values)):
+                dst.copy_(src, non_blocking=True)
+        dw_h.copy_(gr.d_ts_weights, non_blocking=True)
 
-    if world == 1:
+    def e2e_time(full: bool):
         for _ in range(max(args.warmup, 3)):
-            e2e_step()
+            e2e_step(full)
         torch.cuda.synchronize()
-        Ke = K
         tot = 0.0
-        for i in range(Ke):
+        for i in range(K):
             flush.fill_(float(i))
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            e2e_step()
+            e2e_step(full)
             e1.record(stream)
             e1.synchronize()
             tot += e0.elapsed_time(e1)
-        e2e_ms = tot / Ke
+        return tot / K
+
+    if world == 1:
+        e2e_ms = e2e_time(True)
+        e2e_dw_ms = e2e_time(False)
         result["e2e"] = {"value": T / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                         "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
-                         "api": "paper_2508_04711_b200.attention.hstu_attention_reference + hstu_attention_backward"}
+                         "d2h_bytes_per_step": int(d2h_full), "ms_per_step": e2e_ms,
+                         "returns": "out, dq, dk, dv (bf16) + d_ts_weights (f64) to pinned host memory",
+                         "api": "paper_2508_04711_b200.attention.hstu_attention_reference + hstu_attention_backward",
+                         "d_ts_weights_only": {"value": T / (e2e_dw_ms / 1e3), "d2h_bytes_per_step": int(d2h_dw),
+                                               "ms_per_step": e2e_dw_ms}}
     else:
         result["e2e"] = None
 
@@ -419,8 +438,26 @@ def _cpu_threads():
         return os.cpu_count() or 1, []
 
 
-def _oracle_fwd_bwd(h, g, w, seq_ids):
-    import oracle
+def _load_reference():
+    """The unmodified reference package installed in baseline/_ref (pip --target,
+    DESIGN.md (d)); None when it is absent (then the oracle port stands in)."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "jaggedcp")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import jaggedcp
+        return jaggedcp
+    except Exception:
+        return None
+
+
+def _cpu_fwd_bwd(h, g, w, seq_ids, ref):
+    """fwd+bwd of the given sequences, all heads, f32, on the host: through the
+    reference's own public API (jaggedcp.hstu_attention_reference /
+    hstu_attention_backward, one call per head: the reference is single-head)
+    or the oracle port.  Returns (seconds, tokens)."""
     offs = h["offsets"]
     rows = np.concatenate([np.arange(offs[b], offs[b + 1]) for b in seq_ids]) if len(seq_ids) else np.zeros(0, int)
     sub_offs = np.concatenate([[0], np.cumsum([offs[b + 1] - offs[b] for b in seq_ids])]).astype(np.int64)
@@ -428,46 +465,66 @@ def _oracle_fwd_bwd(h, g, w, seq_ids):
     q, k, v, gg = bf(h["q"]), bf(h["k"]), bf(h["v"]), bf(g)
     ts = h["ts"][rows]
     t0 = time.perf_counter()
-    oracle.hstu_forward(q, k, v, ts, sub_offs, w, NB, H)
-    oracle.hstu_backward(q, k, v, ts, sub_offs, gg, w, NB, H)
+    if ref is None:
+        import oracle
+        oracle.hstu_forward(q, k, v, ts, sub_offs, w, NB, H)
+        oracle.hstu_backward(q, k, v, ts, sub_offs, gg, w, NB, H)
+    else:
+        params, cfg = ref.BiasParams(np.asarray(w, dtype=np.float64)), ref.BiasConfig(NB)
+        tsj = ref.new_int_series(ts, sub_offs)
+        for hh in range(H):
+            sl = slice(hh * D, (hh + 1) * D)
+            inp = ref.AttentionInputs(ref.new_jagged(q[:, sl], sub_offs, MAXLEN), ref.new_jagged(k[:, sl], sub_offs, MAXLEN),
+                                      ref.new_jagged(v[:, sl], sub_offs, MAXLEN), tsj, params, cfg)
+            ref.hstu_attention_reference(inp)
+            ref.hstu_attention_backward(inp, ref.new_jagged(gg[:, sl], sub_offs, MAXLEN))
     return time.perf_counter() - t0, int(sub_offs[-1])
 
 
 def cpu_baseline(h, g, w):
-    """Oracle port (numpy restatement of jaggedcp attention.py) on the host's
-    cores: the full C2 batch, fwd+bwd, f32 (a reported baseline only)."""
+    """The reference (baseline/_ref jaggedcp, else the oracle port) on the
+    host's cores: the full C2 batch, fwd+bwd, f32, one pass (reported only)."""
+    ref = _load_reference()
     cores, info = _cpu_threads()
-    secs, toks = _oracle_fwd_bwd(h, g, w, list(range(len(h["offsets"]) - 1)))
-    return {"value": toks / secs, "unit": UNIT, "cores": cores, "kind": "port",
+    secs, toks = _cpu_fwd_bwd(h, g, w, list(range(len(h["offsets"]) - 1)), ref)
+    return {"value": toks / secs, "unit": UNIT, "cores": cores, "kind": "port" if ref is None else "reference",
             "sample": f"full C2 batch ({toks} tokens, 32 sequences, 4 heads), fwd+bwd f32, one pass, "
-                      f"{secs:.2f} s", "host_cpus": os.cpu_count(), "blas": info}
+                      f"{secs:.2f} s" + ("" if ref is None else ", jaggedcp from baseline/_ref"),
+            "host_cpus": os.cpu_count(), "blas": info}
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path (oracle port) on host cores."""
+    """--impl reference: the reference's own CPU path (jaggedcp from
+    baseline/_ref through its public API; the oracle port if it is absent) on
+    the host cores.  Each step is a bounded sample of the C2 batch: 4
+    sequences, taken round-robin so that consecutive steps cycle through the
+    whole batch (every 8 steps cover all 32 sequences once)."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
+    ref = _load_reference()
     h = _host_batch(0)
     T = int(h["offsets"][-1])
     rng = np.random.default_rng([SEED, 99, 0])
     g = rng.standard_normal((T, H * D), dtype=np.float32)
     w = _ts_weights()
-    lens = np.diff(h["offsets"])
-    # bounded per-step sample: the 3 sequences closest to the median length (~0.6 s / step)
-    order = np.argsort(np.abs(lens - np.median(lens)))[:3]
-    sample = sorted(int(x) for x in order)
-    for _ in range(args.warmup):
-        _oracle_fwd_bwd(h, g, w, sample)
+    nseq = len(h["offsets"]) - 1
+    per = 4
+    for i in range(args.warmup):
+        _cpu_fwd_bwd(h, g, w, [(per * i + j) % nseq for j in range(per)], ref)
     tot_s, tot_tok = 0.0, 0
-    for _ in range(args.steps):
-        s, t = _oracle_fwd_bwd(h, g, w, sample)
+    for i in range(args.steps):
+        s, t = _cpu_fwd_bwd(h, g, w, [(per * i + j) % nseq for j in range(per)], ref)
         tot_s += s
         tot_tok += t
     value = tot_tok / tot_s
     cores, info = _cpu_threads()
-    desc = f"3 of the 32 C2 sequences per step (lengths {[int(lens[i]) for i in sample]}), 4 heads, fwd+bwd f32"
+    kind = "port" if ref is None else "reference"
+    desc = (f"{per} of the 32 C2 sequences per step, round-robin over the batch ({args.steps} steps, "
+            f"{tot_tok} tokens), 4 heads, fwd+bwd f32, "
+            + ("oracle port (baseline/_ref absent)" if ref is None else
+               "unmodified jaggedcp (baseline/_ref) hstu_attention_reference + hstu_attention_backward per head"))
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
@@ -475,7 +532,7 @@ def run_reference(args):
         "data": "synthetic (reference generator harness.py:123, seed 7)",
         "config": {"workload": "C2: jagged HSTU attention fwd+bwd, B=32, lengths uniform[1,1024], H=4, d=128",
                    "sample": desc},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc, "blas": info},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 

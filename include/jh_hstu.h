@@ -189,13 +189,17 @@ JH_API size_t jh_attn_bwd_state_bytes(int64_t q_rows, int64_t num_segments, int3
 JH_API size_t jh_attn_workspace_bytes(int64_t q_rows, int64_t kv_len_total, int64_t num_segments, int32_t num_heads,
                                       int32_t head_dim);
 
-/* Backward dS scratch bound.  max_kv_len >= every segment's kv_len (= its
- * length when kv_len is NULL).  If the bound is violated at run time the
- * backward writes NaN into dq instead of overrunning the scratch. */
 JH_API size_t jh_attn_band_table_bytes(int64_t q_rows, int64_t num_segments);
 
+/* Deterministic-backward dS scratch (jh_attn_args.deterministic = 1).
+ * Bound: max_len >= every segment's kv_len AND q length (= the sequence
+ * length for self-attention).  Exact: the segment arrays on the HOST
+ * (q_pos0 / kv_len may be NULL).  If the scratch is too small at run time the
+ * backward writes NaN into dq instead of overrunning it. */
 JH_API size_t jh_attn_ds_scratch_bytes(int64_t kv_len_total, int64_t num_segments, int32_t num_heads,
-                                       int64_t max_kv_len);
+                                       int64_t max_len);
+JH_API size_t jh_attn_ds_scratch_bytes_segs(const int64_t* q_offsets, const int64_t* q_pos0, const int64_t* kv_len,
+                                            int64_t num_segments, int32_t num_heads);
 
 /* Forward: attention.py:125 hstu_attention_reference / :151 blockwise_partial. */
 JH_API int jh_attn_fwd(const jh_attn_args* a, void* stream);
@@ -215,6 +219,27 @@ JH_API int jh_jagged_to_padded(const void* values, const int64_t* offsets, int64
                         int64_t row_bytes, void* padded, void* stream);
 JH_API int jh_padded_to_jagged(const void* padded, const int64_t* offsets, int64_t num_seqs, int64_t max_len,
                         int64_t row_bytes, void* values, void* stream);
+
+/* ---------------------------------------------------------- HSTU layer --
+ * Row-wise pieces of the HSTU layer around the attention (
+ * no reference counterpart: the reference stops at the attention).
+ * All bf16, 16-byte aligned, row strides in elements (multiples of 8).
+ *   silu:      y = x sigmoid(x);  dx = dy s (1 + x (1 - s)).  n % 8 == 0.
+ *   norm_gate: y = (LN(x) * gamma + beta) * u   (u / gamma / beta may be NULL),
+ *              LN over n <= 2048 columns with eps, fp32 statistics saved in
+ *              mean / rstd [rows].  The backward ADDS the gamma / beta
+ *              gradients into dgamma / dbeta (fp32, deterministic; workspace
+ *              of jh_norm_gate_bwd_workspace_bytes) and writes dx, du. */
+JH_API int jh_silu_fwd(const void* x, void* y, int64_t n, void* stream);
+JH_API int jh_silu_bwd(const void* x, const void* dy, void* dx, int64_t n, void* stream);
+JH_API int jh_norm_gate_fwd(const void* x, int64_t ld_x, const void* u, int64_t ld_u, const float* gamma,
+                            const float* beta, float eps, int64_t rows, int32_t n, void* y, int64_t ld_y, float* mean,
+                            float* rstd, void* stream);
+JH_API size_t jh_norm_gate_bwd_workspace_bytes(int64_t rows, int32_t n);
+JH_API int jh_norm_gate_bwd(const void* dy, int64_t ld_dy, const void* x, int64_t ld_x, const void* u, int64_t ld_u,
+                            const float* gamma, const float* beta, const float* mean, const float* rstd, int64_t rows,
+                            int32_t n, void* dx, int64_t ld_dx, void* du, int64_t ld_du, float* dgamma, float* dbeta,
+                            void* workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------ plan --
  * cp_engine.py:105 build_shard_plan (+ jagged.py:162 make_minichunks,

@@ -260,7 +260,7 @@ def hstu_attention_backward(inputs: AttentionInputs, upstream: JaggedTensor) -> 
     dq, dk, dv, dw, dpos = kernels.attn_bwd(q.values, k.values, v.values, ts.values, ts.values, q.offsets,
                                             g.contiguous(), inputs.num_heads, inputs.params.device_weights(dev),
                                             inputs.cfg.num_buckets, _pw(inputs, dev),
-                                            max_kv_len=int(np.diff(q.host_offsets).max(initial=0)))
+                                            seg_host=(q.host_offsets, None, None))
     mk = lambda t, like: JaggedTensor(t, like.offsets, like.max_length, like.host_offsets)  # noqa: E731
     return AttentionGradients(mk(dq, q), mk(dk, k), mk(dv, v), dw, dpos)
 

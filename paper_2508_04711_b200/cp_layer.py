@@ -214,12 +214,12 @@ class GpuBackend:
         return self.k.scatter_rows(src, perm, out)
 
     def fwd(self, q, k, v, ts_q, ts_k, segs, H, w, nb):
-        qo, qp, ks, kl, kvt, _ = segs
+        qo, qp, ks, kl, kvt = segs[:5]
         return self.k.attn_fwd(q, k, v, ts_q, ts_k, qo, H, w, nb, q_pos0=qp, kv_start=ks, kv_len=kl,
                                kv_len_total=kvt)
 
     def fwd_partial(self, q, k, v, ts_q, ts_k, segs, H, w, nb, acc, accumulate):
-        qo, qp, ks, kl, kvt, _ = segs
+        qo, qp, ks, kl, kvt = segs[:5]
         self.k.attn_fwd(q, k, v, ts_q, ts_k, qo, H, w, nb, q_pos0=qp, kv_start=ks, kv_len=kl, kv_len_total=kvt,
                         out_accum=acc, accumulate=accumulate)
 
@@ -231,15 +231,15 @@ class GpuBackend:
         return self._comm
 
     def bwd(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb):
-        qo, qp, ks, kl, kvt, max_kv = segs
+        qo, qp, ks, kl, kvt = segs[:5]
         dq, dk, dv, dw, _ = self.k.attn_bwd(q, k, v, ts_q, ts_k, qo, g, H, w, nb, q_pos0=qp, kv_start=ks,
-                                            kv_len=kl, kv_len_total=kvt, accumulate_dkv=True, max_kv_len=max_kv)
+                                            kv_len=kl, kv_len_total=kvt, accumulate_dkv=True, seg_host=segs[6])
         return dq, dk, dv, dw
 
     def bwd_partial(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb, dq_acc):
-        qo, qp, ks, kl, kvt, max_kv = segs
+        qo, qp, ks, kl, kvt = segs[:5]
         _, dk, dv, dw, _ = self.k.attn_bwd(q, k, v, ts_q, ts_k, qo, g, H, w, nb, q_pos0=qp, kv_start=ks, kv_len=kl,
-                                           kv_len_total=kvt, accumulate_dkv=True, max_kv_len=max_kv,
+                                           kv_len_total=kvt, accumulate_dkv=True, seg_host=segs[6],
                                            dq_accum=dq_acc)
         return dk, dv, dw
 
@@ -274,12 +274,15 @@ class CPAttention:
         p = build_cp_plan([list(x) for x in key], self.cp, self.rank, self.mode)
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
         dev = {"send_perm": t(p.send_perm), "seq_perm": t(p.seq_perm),
+               # (q_offsets, q_pos0, kv_start, kv_len, kv total, max kv, host (q_offsets, q_pos0, kv_len))
                "segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.kv_len), int(p.kv_len.sum()),
-                        int(p.kv_len.max(initial=0))),
+                        int(p.kv_len.max(initial=0)), (p.q_offsets, p.q_pos0, p.kv_len)),
                "local_segs": (t(p.q_offsets), t(np.zeros_like(p.q_pos0)), t(p.local_kv_start),
-                              t(p.local_kv_len), int(p.local_kv_len.sum()), int(p.local_kv_len.max(initial=0))),
+                              t(p.local_kv_len), int(p.local_kv_len.sum()), int(p.local_kv_len.max(initial=0)),
+                              (p.q_offsets, np.zeros_like(p.q_pos0), p.local_kv_len)),
                "remote_segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.remote_kv_len),
-                               int(p.remote_kv_len.sum()), int(p.remote_kv_len.max(initial=0)))}
+                               int(p.remote_kv_len.sum()), int(p.remote_kv_len.max(initial=0)),
+                               (p.q_offsets, p.q_pos0, p.remote_kv_len))}
         self._plans[key] = (p, dev)
         while len(self._plans) > self.max_plans:
             self._plans.popitem(last=False)

@@ -80,13 +80,15 @@ static BwdStateLayout bwd_state_layout(int64_t q_rows, int64_t nseg, int32_t H, 
   return l;
 }
 
-// Forward kernel: the two-q-tile kernel (attn_fwd2.cu) unless JH_FWD1=1 selects
-// the one-tile kernel (attn_fwd.cu) for A/B measurements.
+// Forward kernel: the one-tile kernel (attn_fwd.cu); JH_FWD2=1 selects the
+// two-q-tile kernel (attn_fwd2.cu) for A/B measurements (C2: 45 vs 38 us per
+// launch under ncu, r2 launch list -- the pair items halve L2 bytes per flop
+// but double the per-item latency chain and coarsen the tail).
 static bool fwd_two_tile() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("JH_FWD1");
-    v = (e && atoi(e) == 1) ? 0 : 1;
+    const char* e = getenv("JH_FWD2");
+    v = (e && atoi(e) == 1) ? 1 : 0;
   }
   return v == 1;
 }
@@ -306,12 +308,36 @@ size_t jh_attn_band_table_bytes(int64_t q_rows, int64_t num_segments) {
   return band_bytes(std::max<int64_t>(q_rows, 0), std::max<int64_t>(num_segments, 0));
 }
 
-size_t jh_attn_ds_scratch_bytes(int64_t kv_len_total, int64_t num_segments, int32_t num_heads, int64_t max_kv_len) {
-  // causal triangle per segment: ds_cnt <= (nkt + 1)(nkt + 2), nkt = ceil(kv_s / 128)
-  // (checked over q_pos0 / length grids), summed <= (sum nkt + nseg)(max nkt + 2)
-  if (kv_len_total <= 0 || num_segments <= 0 || num_heads <= 0 || max_kv_len <= 0) return (size_t)kDsBlockBytes;
-  const int64_t blocks = ((kv_len_total + kBN - 1) / kBN + 2 * num_segments) * ((max_kv_len + kBN - 1) / kBN + 2);
+size_t jh_attn_ds_scratch_bytes(int64_t kv_len_total, int64_t num_segments, int32_t num_heads, int64_t max_len) {
+  // per segment ds_cnt <= nkt * nh with nkt = ceil(kv_s / 128) and
+  // nh = ceil(q_s / 64): summed <= (sum nkt) * max nh <= (ceil(kv_total / 128)
+  // + nseg) * ceil(max_len / 64), max_len >= every segment's kv AND q length
+  // (a CP "remote" segment can have q_s > kv_s).  About twice the exact size
+  // for self-attention: callers that know the segments use the _segs form.
+  if (kv_len_total <= 0 || num_segments <= 0 || num_heads <= 0 || max_len <= 0) return (size_t)kDsBlockBytes;
+  const int64_t blocks = ((kv_len_total + kBN - 1) / kBN + num_segments) * ((max_len + 63) / 64);
   return (size_t)blocks * num_heads * kDsBlockBytes;
+}
+
+size_t jh_attn_ds_scratch_bytes_segs(const int64_t* q_offsets, const int64_t* q_pos0, const int64_t* kv_len,
+                                     int64_t num_segments, int32_t num_heads) {
+  // host mirror of ds_cnt (attn_common.cuh), summed: the exact block count the
+  // work-list builder's scan produces
+  if (!q_offsets || num_segments <= 0 || num_heads <= 0) return (size_t)kDsBlockBytes;
+  int64_t blocks = 0;
+  for (int64_t s = 0; s < num_segments; ++s) {
+    const int64_t lq = q_offsets[s + 1] - q_offsets[s];
+    const int64_t qp0 = q_pos0 ? q_pos0[s] : 0;
+    const int64_t kvl = kv_len ? kv_len[s] : lq;
+    if (lq <= 0) continue;
+    const int64_t vis = std::min(qp0 + lq, kvl);
+    const int64_t nkt = vis > 0 ? (vis + kBN - 1) / kBN : 0;
+    const int64_t nh = (lq + 63) / 64;
+    const int64_t m = (qp0 + kBN - 1) / kBN;
+    const int64_t x = nkt - 1 - m;
+    blocks += nkt * nh - (x >= 0 ? x * (x + 1) : 0);
+  }
+  return (size_t)std::max<int64_t>(blocks, 1) * num_heads * kDsBlockBytes;
 }
 
 size_t jh_attn_bwd_state_bytes(int64_t q_rows, int64_t num_segments, int32_t num_heads, int32_t head_dim) {

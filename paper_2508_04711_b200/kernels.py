@@ -328,9 +328,31 @@ def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=
     return ret
 
 
-# deterministic backward (two kernels over a bf16 dS scratch) or the fused one
-DETERMINISTIC_DEFAULT = {"value": False}
+# Backward variant.  None = auto: the two-kernel path (dK/dV kernel writes bf16
+# dS tiles, the dQ GEMM reads them; fastest at C2) whenever its exact dS
+# scratch fits DS_SCRATCH_BUDGET, else the fused one-kernel path (dq reduced
+# in fp32, O(L) memory: the long-sequence regime).  True / False force one.
+DETERMINISTIC_DEFAULT = {"value": None}
 _BWD_STATE: dict = {}
+
+
+def ds_scratch_budget(device) -> int:
+    """Bytes the auto policy lets the dS scratch take (JH_DS_SCRATCH_BUDGET,
+    default 1/8 of the device's memory)."""
+    import os
+    env = os.environ.get("JH_DS_SCRATCH_BUDGET")
+    if env:
+        return int(float(env))
+    return int(torch.cuda.get_device_properties(device).total_memory // 8)
+
+
+def ds_scratch_bytes(num_heads: int, q_offsets_host, q_pos0_host=None, kv_len_host=None) -> int:
+    """Exact dS scratch of the deterministic backward for host segment arrays."""
+    qo = np.ascontiguousarray(q_offsets_host, dtype=np.int64)
+    qp = None if q_pos0_host is None else np.ascontiguousarray(q_pos0_host, dtype=np.int64)
+    kl = None if kv_len_host is None else np.ascontiguousarray(kv_len_host, dtype=np.int64)
+    vp = lambda a: None if a is None else a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    return int(_lib.lib().jh_attn_ds_scratch_bytes_segs(vp(qo), vp(qp), vp(kl), int(qo.size - 1), int(num_heads)))
 
 
 def bwd_state(q_rows: int, num_segments: int, H: int, dp: int, device) -> torch.Tensor:
@@ -347,7 +369,8 @@ def bwd_state(q_rows: int, num_segments: int, H: int, dp: int, device) -> torch.
 
 def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_buckets=16, pos_weights=None,
              q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, accumulate_dkv=False, prof=None,
-             max_kv_len=None, dq_accum=None, band_table=None, deterministic=None, dbg_count_buckets=False):
+             max_kv_len=None, dq_accum=None, band_table=None, deterministic=None, dbg_count_buckets=False,
+             seg_host=None):
     """Fused jagged HSTU backward (jh_attn_bwd).
 
     Returns (dq bf16, dk, dv, d_ts_weights f64, d_pos f64 or None); dk/dv are
@@ -355,11 +378,14 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
     ``dq_accum`` (fp32, q's shape) dq is added there and returned as dq;
     ``band_table`` filled by the forward call on the same inputs is reused
     (no recomputation).
-    ``deterministic``: the two-kernel path over a bf16 dS scratch (bitwise
-    reproducible dq; memory O(H L^2)); otherwise the fused kernel (dq reduced
-    in fp32, O(L) memory).  ``max_kv_len`` bounds every segment's kv length
-    (sizes the dS scratch of the deterministic path; when omitted it is read
-    back from the device, one synchronisation)."""
+    ``deterministic``: True = the two-kernel path over a bf16 dS scratch
+    (bitwise reproducible dq; scratch ~H L^2 bytes per sequence), False = the
+    fused kernel (dq reduced in fp32, O(L) memory), None = auto (the two-kernel
+    path when its scratch fits ``ds_scratch_budget``).  ``seg_host`` =
+    (q_offsets, q_pos0 or None, kv_len or None) as host arrays sizes the
+    scratch exactly; without it ``max_kv_len`` (>= every segment's q and kv
+    length) gives a bound, and without either the lengths are read back from
+    the device (one synchronisation)."""
     if deterministic is None:
         deterministic = DETERMINISTIC_DEFAULT["value"]
     w = ts_weights.to(device=q.device, dtype=torch.float32).contiguous()
@@ -403,19 +429,27 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
     kvt = q.shape[0] if kv_len_total is None else kv_len_total
     ws, nbytes = _workspace(q.shape[0], kvt, a.num_segments, H, dp, q.device)
     a.workspace, a.workspace_bytes = ws.data_ptr(), nbytes
+    if dbg_count_buckets:
+        if deterministic:
+            raise ValueError("dbg_count_buckets is a fused-backward debug mode")
+        deterministic = False
+    ds_bytes = None
+    if deterministic is not False:
+        if seg_host is not None:
+            ds_bytes = ds_scratch_bytes(H, *seg_host)
+        else:
+            if max_kv_len is None:
+                if a.num_segments == 0:
+                    max_kv_len = 0
+                else:
+                    ql = int((q_offsets[1:] - q_offsets[:-1]).max().item())
+                    max_kv_len = max(ql, int(kv_len.max().item())) if kv_len is not None else ql
+            ds_bytes = int(_lib.lib().jh_attn_ds_scratch_bytes(kvt, a.num_segments, H, int(max_kv_len)))
+        if deterministic is None:
+            deterministic = ds_bytes <= ds_scratch_budget(q.device)
     a.deterministic = int(bool(deterministic))
     a.dbg_count_buckets = int(bool(dbg_count_buckets))
-    if dbg_count_buckets and deterministic:
-        raise ValueError("dbg_count_buckets is a fused-backward debug mode")
     if deterministic:
-        if max_kv_len is None:
-            if a.num_segments == 0:
-                max_kv_len = 0
-            elif kv_len is not None:
-                max_kv_len = int(kv_len.max().item())
-            else:
-                max_kv_len = int((q_offsets[1:] - q_offsets[:-1]).max().item())
-        ds_bytes = _lib.lib().jh_attn_ds_scratch_bytes(kvt, a.num_segments, H, int(max_kv_len))
         ds = torch.empty(ds_bytes, dtype=torch.uint8, device=q.device)
         a.ds_scratch, a.ds_scratch_bytes = ds.data_ptr(), ds_bytes
     else:

@@ -109,3 +109,45 @@ def test_plan_rejects_bad_args(L):
     assert b"cp_size" in L.jh_last_error()
     assert L.jh_plan_build(ln, 1, 2, 7, cl, cs, co) == 1
     assert b"balance_mode" in L.jh_last_error()
+
+
+def _ds_cnt_py(lq, qp0, kvl):
+    # attn_common.cuh ds_cnt, restated: causal triangle of (128-row kv tile, 64-row q half) blocks
+    if lq <= 0:
+        return 0
+    vis = min(qp0 + lq, kvl)
+    nkt = -(-vis // 128) if vis > 0 else 0
+    nh = -(-lq // 64)
+    m = -(-qp0 // 128)
+    x = nkt - 1 - m
+    cnt = nkt * nh - (x * (x + 1) if x >= 0 else 0)
+    # brute force: blocks (j, t) with t >= tlo(j) = 2 * max(0, floor((128 j - qp0) / 128))
+    brute = 0
+    for j in range(nkt):
+        f = 128 * j - qp0
+        tlo = 0 if f <= 0 else (f // 128) * 2
+        brute += max(nh - tlo, 0)
+    assert cnt == brute
+    return cnt
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_ds_scratch_exact_and_bound(L, seed):
+    # exact size = sum of the per-segment block counts; the bound (max_len >= q and
+    # kv lengths) covers it, including CP "remote" segments with q longer than kv
+    from paper_2508_04711_b200 import kernels
+    rng = np.random.default_rng(seed)
+    n = 12
+    lq = rng.integers(0, 5000, n)
+    qp0 = np.where(rng.random(n) < 0.5, 0, rng.integers(0, 6000, n))
+    kvl = np.where(qp0 == 0, lq, rng.integers(1, 6000, n))
+    qo = np.concatenate([[0], np.cumsum(lq)]).astype(np.int64)
+    H = 3
+    want = max(sum(_ds_cnt_py(int(a), int(b), int(c)) for a, b, c in zip(lq, qp0, kvl)), 1) * H * 16384
+    assert kernels.ds_scratch_bytes(H, qo, qp0, kvl) == want
+    bound = L.jh_attn_ds_scratch_bytes(int(kvl.sum()), n, H, int(max(lq.max(), kvl.max())))
+    assert bound >= want
+    # the ADVICE case: one 4096-token sequence at CP=1 in the remote form (q [2048, 4096) vs kv [0, 2048))
+    one = kernels.ds_scratch_bytes(4, np.array([0, 2048]), np.array([2048]), np.array([2048]))
+    assert one == 4 * 16 * 32 * 16384
+    assert L.jh_attn_ds_scratch_bytes(2048, 1, 4, 2048) >= one

@@ -245,3 +245,34 @@ def test_row_moves_and_padding_are_bitwise():
         assert not pad[b, L:].any()
     back = k.padded_to_jagged(pad, to, T)
     assert torch.equal(back, x)
+
+
+# ------------------------- deterministic backward on long CP "remote" segments
+
+@pytest.mark.parametrize("split", [2048, 1000])
+def test_bwd_remote_segment_long_q_both_paths(split):
+    # a CP-1 / naive-mode remote segment (q rows [split, L) vs kv [0, split))
+    # needs ceil(split/128) * ceil((L-split)/64) dS blocks; the exact host sizing
+    # (seg_host) must cover it: deterministic and fused paths agree, no NaN
+    L, H = 4096, 2
+    case = make_case([L], H * 128, seed=5)
+    c = to_cuda(case)
+    t = lambda x: torch.tensor(x, dtype=torch.int64, device="cuda")  # noqa: E731
+    qo, qp, ks, kl = [0, L - split], [split], [0], [split]
+    q_r = c["q"][split:].contiguous()
+    g_r = c["g"][split:].contiguous()
+    ts_r = c["ts"][split:].contiguous()
+    from paper_2508_04711_b200 import kernels
+    res = {}
+    for det in (True, False):
+        acc = torch.zeros(q_r.shape, dtype=torch.float32, device="cuda")
+        _, dk, dv, dw, _ = kernels.attn_bwd(q_r, c["k"], c["v"], ts_r, c["ts"], t(qo), g_r, H, c["w"], 16,
+                                            q_pos0=t(qp), kv_start=t(ks), kv_len=t(kl), kv_len_total=split,
+                                            accumulate_dkv=True, dq_accum=acc, deterministic=det,
+                                            seg_host=(np.array(qo), np.array(qp), np.array(kl)))
+        torch.cuda.synchronize()
+        res[det] = [x.float().cpu().numpy() for x in (acc, dk[:split], dv[:split])] + [dw.cpu().numpy()]
+    for name, a, b in zip(("dq", "dk", "dv"), res[True][:3], res[False][:3]):
+        assert np.isfinite(a).all() and np.isfinite(b).all(), name
+        assert row_rel(a, b)[1] <= 5e-3, name
+    assert np.abs(res[True][3] - res[False][3]).max() / np.abs(res[False][3]).max() <= DW_TOL
