@@ -248,7 +248,7 @@ class CPAttention:
     """Context-parallel jagged HSTU attention over a process group."""
 
     def __init__(self, group, num_heads: int, num_buckets: int = 16, balance_mode: str = "balanced_minichunk",
-                 backend=None, overlap: bool = True, comm=None, max_plans: int = 64):
+                 backend=None, overlap: bool = True, comm=None, max_plans: int = 64, retain_kv: bool = False):
         self.group = group
         self.cp = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -260,6 +260,9 @@ class CPAttention:
         self.be = backend if backend is not None else GpuBackend()
         self.overlap = overlap and hasattr(self.be, "fwd_partial") and hasattr(self.be, "bwd_partial")
         self._plans: "OrderedDict" = OrderedDict()
+        # keep the gathered group K/V/ts between forward and backward (one fewer
+        # all-gather per layer, O(group rows) memory) or re-gather them
+        self.retain_kv = bool(retain_kv)
 
     # ---------------------------------------------------------------- plan
     def plan_for(self, local_lengths, device) -> tuple[CPPlan, dict]:
@@ -321,21 +324,36 @@ class CPAttention:
         return mine[: p.n_res]
 
     # --------------------------------------------------------------- passes
+    def redistribute(self, x, p, dev):
+        """Public form of the batch -> sequence sharding (any trailing shape)."""
+        return self._redistribute(x, p, dev)
+
+    def restore(self, x_r, p, dev, n_local):
+        return self._restore(x_r, p, dev, n_local)
+
     def forward(self, q, k, v, ts, local_lengths, w):
         """Local (batch-sharded) q, k, v, ts -> local attention output.
         Returns (out_local, ctx) where ctx feeds ``backward``."""
         p, dev = self.plan_for(local_lengths, q.device)
         q_r, k_r, v_r = (self._redistribute(x, p, dev) for x in (q, k, v))
         ts_r = self._redistribute(ts.view(-1, 1), p, dev).view(-1)
+        o_r, rctx = self.attend(q_r, k_r, v_r, ts_r, p, dev, w)
+        out = self._restore(o_r, p, dev, q.shape[0])
+        return out, (rctx, q.shape[0])
+
+    def attend(self, q_r, k_r, v_r, ts_r, p, dev, w):
+        """Attention on RESIDENT rows (plan order; the sharded activations of a
+        CP stack stay in this layout across layers): KV exchange + fused
+        kernels.  Returns (o_r, ctx) for ``attend_backward``."""
         if not self.overlap:
             k_s, v_s = self._gather_seq(k_r, p, dev), self._gather_seq(v_r, p, dev)
             ts_s = self._gather_seq(ts_r.view(-1, 1), p, dev).view(-1)
             o_r = self.be.fwd(q_r, k_s, v_s, ts_r, ts_s, dev["segs"], self.H, w, self.nb)
         else:
             k_s, v_s, ts_s, o_r = self._forward_overlapped(q_r, k_r, v_r, ts_r, p, dev, w)
-        out = self._restore(o_r, p, dev, q.shape[0])
-        ctx = (p, dev, q_r, k_s, v_s, ts_r, ts_s, q.shape[0], k_r, v_r)
-        return out, ctx
+        if not self.retain_kv:  # re-gathered by the backward: O(resident) memory between the passes
+            k_s = v_s = ts_s = None
+        return o_r, (p, dev, q_r, k_s, v_s, ts_r, ts_s, k_r, v_r)
 
     def _forward_overlapped(self, q_r, k_r, v_r, ts_r, p, dev, w):
         """KV all-gather on the communication stream while each resident chunk
@@ -343,6 +361,15 @@ class CPAttention:
         additive, attention.py:151-184 / cp_engine.py:441-450)."""
         main = torch.cuda.current_stream(q_r.device) if q_r.is_cuda else None
         comm = self.be.comm_stream(q_r.device) if hasattr(self.be, "comm_stream") else None
+        k_s, v_s, ts_s = self._gather_kv_async(k_r, v_r, ts_r, p, dev, main, comm)
+        acc_dt = torch.float32 if q_r.dtype in (torch.bfloat16, torch.float16) else q_r.dtype
+        acc = torch.empty(q_r.shape, dtype=acc_dt, device=q_r.device)
+        self.be.fwd_partial(q_r, k_r, v_r, ts_r, ts_r, dev["local_segs"], self.H, w, self.nb, acc, False)
+        self._join(main, comm, (k_s, v_s, ts_s))
+        self.be.fwd_partial(q_r, k_s, v_s, ts_r, ts_s, dev["remote_segs"], self.H, w, self.nb, acc, True)
+        return k_s, v_s, ts_s, acc.to(q_r.dtype)
+
+    def _gather_kv_async(self, k_r, v_r, ts_r, p, dev, main, comm):
         if comm is not None:
             comm.wait_stream(main)
             for x in (k_r, v_r, ts_r):
@@ -353,31 +380,59 @@ class CPAttention:
         else:
             k_s, v_s = self._gather_seq(k_r, p, dev), self._gather_seq(v_r, p, dev)
             ts_s = self._gather_seq(ts_r.view(-1, 1), p, dev).view(-1)
-        acc_dt = torch.float32 if q_r.dtype in (torch.bfloat16, torch.float16) else q_r.dtype
-        acc = torch.empty(q_r.shape, dtype=acc_dt, device=q_r.device)
-        self.be.fwd_partial(q_r, k_r, v_r, ts_r, ts_r, dev["local_segs"], self.H, w, self.nb, acc, False)
+        return k_s, v_s, ts_s
+
+    @staticmethod
+    def _join(main, comm, tensors):
         if comm is not None:
             main.wait_stream(comm)
-            for x in (k_s, v_s, ts_s):
+            for x in tensors:
                 x.record_stream(main)
-        self.be.fwd_partial(q_r, k_s, v_s, ts_r, ts_s, dev["remote_segs"], self.H, w, self.nb, acc, True)
-        return k_s, v_s, ts_s, acc.to(q_r.dtype)
 
     def backward(self, ctx, g, w):
         """Upstream gradient (local rows) -> (dq, dk, dv local; d_ts_weights summed over CP)."""
-        p, dev, q_r, k_s, v_s, ts_r, ts_s, n_local, k_r, v_r = ctx
+        rctx, n_local = ctx
+        p, dev = rctx[0], rctx[1]
         g_r = self._redistribute(g, p, dev)
-        if not self.overlap:
-            dq_r, dk_s, dv_s, dw = self.be.bwd(q_r, k_s, v_s, ts_r, ts_s, dev["segs"], g_r, self.H, w, self.nb)
-            dk_r = self._reduce_to_owner(dk_s, p, dev).to(q_r.dtype)
-            dv_r = self._reduce_to_owner(dv_s, p, dev).to(q_r.dtype)
-        else:
-            dq_r, dk_r, dv_r, dw = self._backward_overlapped(q_r, k_r, v_r, k_s, v_s, ts_r, ts_s, g_r, p, dev, w)
-        self.comm.all_reduce(dw)
+        dq_r, dk_r, dv_r, dw = self.attend_backward(rctx, g_r, w)
         dq = self._restore(dq_r, p, dev, n_local)
         dk = self._restore(dk_r, p, dev, n_local)
         dv = self._restore(dv_r, p, dev, n_local)
         return dq, dk, dv, dw
+
+    def attend_backward(self, rctx, g_r, w):
+        """Resident-row backward: (dq_r, dk_r, dv_r, d_ts_weights summed over CP)."""
+        p, dev, q_r, k_s, v_s, ts_r, ts_s, k_r, v_r = rctx
+        if not self.overlap:
+            if k_s is None:
+                k_s, v_s = self._gather_seq(k_r, p, dev), self._gather_seq(v_r, p, dev)
+                ts_s = self._gather_seq(ts_r.view(-1, 1), p, dev).view(-1)
+            dq_r, dk_s, dv_s, dw = self.be.bwd(q_r, k_s, v_s, ts_r, ts_s, dev["segs"], g_r, self.H, w, self.nb)
+            dk_r = self._reduce_to_owner(dk_s, p, dev).to(q_r.dtype)
+            dv_r = self._reduce_to_owner(dv_s, p, dev).to(q_r.dtype)
+        elif k_s is None:
+            dq_r, dk_r, dv_r, dw = self._backward_regather(q_r, k_r, v_r, ts_r, g_r, p, dev, w)
+        else:
+            dq_r, dk_r, dv_r, dw = self._backward_overlapped(q_r, k_r, v_r, k_s, v_s, ts_r, ts_s, g_r, p, dev, w)
+        self.comm.all_reduce(dw)
+        return dq_r, dk_r, dv_r, dw
+
+    def _backward_regather(self, q_r, k_r, v_r, ts_r, g_r, p, dev, w):
+        """K/V were not kept: re-gather them on the communication stream while
+        the local part (chunk vs itself) computes, then the remote part; its
+        dK/dV partials are reduced to the owners afterwards."""
+        acc_dt = torch.float32 if q_r.dtype in (torch.bfloat16, torch.float16) else q_r.dtype
+        main = torch.cuda.current_stream(q_r.device) if q_r.is_cuda else None
+        comm = self.be.comm_stream(q_r.device) if hasattr(self.be, "comm_stream") else None
+        k_s, v_s, ts_s = self._gather_kv_async(k_r, v_r, ts_r, p, dev, main, comm)
+        dq_acc = torch.zeros(q_r.shape, dtype=acc_dt, device=q_r.device)
+        dk_l, dv_l, dw_l = self.be.bwd_partial(q_r, k_r, v_r, ts_r, ts_r, dev["local_segs"], g_r, self.H, w, self.nb,
+                                               dq_acc)
+        self._join(main, comm, (k_s, v_s, ts_s))
+        dk_s, dv_s, dw = self.be.bwd_partial(q_r, k_s, v_s, ts_r, ts_s, dev["remote_segs"], g_r, self.H, w, self.nb,
+                                             dq_acc)
+        dk_red, dv_red = self._reduce_to_owner(dk_s, p, dev), self._reduce_to_owner(dv_s, p, dev)
+        return dq_acc.to(q_r.dtype), (dk_red + dk_l).to(q_r.dtype), (dv_red + dv_l).to(q_r.dtype), dw + dw_l
 
     def _backward_overlapped(self, q_r, k_r, v_r, k_s, v_s, ts_r, ts_s, g_r, p, dev, w):
         """Remote part first; its dK/dV reduce-scatter to the owners runs on the
@@ -398,10 +453,7 @@ class CPAttention:
             dk_red, dv_red = self._reduce_to_owner(dk_s, p, dev), self._reduce_to_owner(dv_s, p, dev)
         dk_l, dv_l, dw_l = self.be.bwd_partial(q_r, k_r, v_r, ts_r, ts_r, dev["local_segs"], g_r, self.H, w, self.nb,
                                                dq_acc)
-        if comm is not None:
-            main.wait_stream(comm)
-            for x in (dk_red, dv_red):
-                x.record_stream(main)
+        self._join(main, comm, (dk_red, dv_red))
         dk_r = (dk_red + dk_l).to(q_r.dtype)
         dv_r = (dv_red + dv_l).to(q_r.dtype)
         return dq_acc.to(q_r.dtype), dk_r, dv_r, dw + dw_l
@@ -427,8 +479,66 @@ class _CPAttentionFn(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g):
         (w,) = ctx.saved_tensors
-        dq, dk, dv, dw = ctx.layer.backward(ctx.c, g.to(ctx.c[2].dtype).contiguous(), w)
+        dq, dk, dv, dw = ctx.layer.backward(ctx.c, g.to(ctx.c[0][2].dtype).contiguous(), w)
         return dq, dk, dv, dw.to(w.dtype), None, None, None
+
+
+class _CPResidentAttentionFn(torch.autograd.Function):
+    """Attention over resident rows (plan order) -- the per-layer op of a CP
+    stack whose activations stay sequence-sharded between layers."""
+
+    @staticmethod
+    def forward(ctx, q_r, k_r, v_r, ts_weights, ts_r, layer, plan):
+        p, dev = plan
+        o_r, rctx = layer.attend(q_r, k_r, v_r, ts_r, p, dev, ts_weights)
+        ctx.rctx, ctx.layer = rctx, layer
+        ctx.save_for_backward(ts_weights)
+        return o_r
+
+    @staticmethod
+    def backward(ctx, g_r):
+        (w,) = ctx.saved_tensors
+        dq, dk, dv, dw = ctx.layer.attend_backward(ctx.rctx, g_r.to(ctx.rctx[2].dtype).contiguous(), w)
+        ctx.rctx = None
+        return dq, dk, dv, dw.to(w.dtype), None, None, None
+
+
+class _ShardFn(torch.autograd.Function):
+    """local rows -> resident rows (the all-to-all); its gradient is the inverse."""
+
+    @staticmethod
+    def forward(ctx, x, layer, plan, n_local):
+        ctx.layer, ctx.plan, ctx.n_local = layer, plan, n_local
+        return layer.redistribute(x, *plan)
+
+    @staticmethod
+    def backward(ctx, g):
+        return ctx.layer.restore(g.contiguous(), *ctx.plan, ctx.n_local), None, None, None
+
+
+class _UnshardFn(torch.autograd.Function):
+    """resident rows -> local rows (restore_outputs); its gradient is the forward a2a."""
+
+    @staticmethod
+    def forward(ctx, x_r, layer, plan, n_local):
+        ctx.layer, ctx.plan = layer, plan
+        return layer.restore(x_r, *plan, n_local)
+
+    @staticmethod
+    def backward(ctx, g):
+        return ctx.layer.redistribute(g.contiguous(), *ctx.plan), None, None, None
+
+
+def cp_resident_attention(layer: CPAttention, plan, q_r, k_r, v_r, ts_r, ts_weights):
+    return _CPResidentAttentionFn.apply(q_r, k_r, v_r, ts_weights, ts_r, layer, plan)
+
+
+def cp_shard(layer: CPAttention, plan, x, n_local: int):
+    return _ShardFn.apply(x, layer, plan, n_local)
+
+
+def cp_unshard(layer: CPAttention, plan, x_r, n_local: int):
+    return _UnshardFn.apply(x_r, layer, plan, n_local)
 
 
 def cp_hstu_attention(layer: CPAttention, q, k, v, ts, local_lengths, ts_weights):

@@ -477,3 +477,77 @@ def debug_umma(a: torch.Tensor, b: torch.Tensor, a_mode: int, b_mode: int) -> to
     check(_lib.lib().jh_debug_umma(_ptr(a.contiguous()), _ptr(b.contiguous()), _ptr(d), a_mode, b_mode, _stream(a)),
           "debug_umma")
     return d
+
+
+# ------------------------------------------------------- HSTU layer row work
+
+def _ld(name, t, n):
+    if t.dim() != 2 or t.stride(1) != 1 or t.shape[1] != n:
+        raise ValueError(f"{name} must be 2-D [rows, {n}] with unit column stride")
+    return t.stride(0)
+
+
+def silu(x: torch.Tensor) -> torch.Tensor:
+    """y = x sigmoid(x) (bf16, jh_silu_fwd)."""
+    _require_cuda("x", x, torch.bfloat16)
+    x = x.contiguous()
+    y = torch.empty_like(x)
+    check(_lib.lib().jh_silu_fwd(_ptr(x), _ptr(y), x.numel(), _stream(x)), "silu")
+    _bump()
+    return y
+
+
+def silu_bwd(x: torch.Tensor, dy: torch.Tensor) -> torch.Tensor:
+    _require_cuda("x", x, torch.bfloat16)
+    _require_cuda("dy", dy, torch.bfloat16)
+    x, dy = x.contiguous(), dy.contiguous()
+    dx = torch.empty_like(x)
+    check(_lib.lib().jh_silu_bwd(_ptr(x), _ptr(dy), _ptr(dx), x.numel(), _stream(x)), "silu_bwd")
+    _bump()
+    return dx
+
+
+def norm_gate_fwd(x, u=None, gamma=None, beta=None, eps: float = 1e-6):
+    """y = (LayerNorm(x) * gamma + beta) * u per row (jh_norm_gate_fwd).
+    x: [rows, n] bf16; u: [rows, n] bf16 view (any 16-B row stride) or None;
+    gamma / beta: fp32 [n] or None.  Returns (y bf16, mean fp32, rstd fp32)."""
+    _require_cuda("x", x, torch.bfloat16)
+    rows, n = x.shape
+    ldx = _ld("x", x, n)
+    ldu = 0
+    if u is not None:
+        _require_cuda("u", u, torch.bfloat16)
+        ldu = _ld("u", u, n)
+    y = torch.empty((rows, n), dtype=torch.bfloat16, device=x.device)
+    mean = torch.empty(rows, dtype=torch.float32, device=x.device)
+    rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+    g = None if gamma is None else gamma.to(device=x.device, dtype=torch.float32).contiguous()
+    b = None if beta is None else beta.to(device=x.device, dtype=torch.float32).contiguous()
+    check(_lib.lib().jh_norm_gate_fwd(_ptr(x), ldx, _ptr(u), ldu, _ptr(g), _ptr(b), float(eps), rows, n, _ptr(y), n,
+                                      _ptr(mean), _ptr(rstd), _stream(x)), "norm_gate_fwd")
+    _bump()
+    return y, mean, rstd
+
+
+def norm_gate_bwd(dy, x, u, gamma, beta, mean, rstd, need_affine: bool = True):
+    """Gradients of norm_gate_fwd: (dx, du or None, dgamma or None, dbeta or None)."""
+    _require_cuda("dy", dy, torch.bfloat16)
+    rows, n = x.shape
+    dy = dy.contiguous()
+    ldx = _ld("x", x, n)
+    ldu = 0 if u is None else _ld("u", u, n)
+    dx = torch.empty((rows, n), dtype=torch.bfloat16, device=x.device)
+    du = None if u is None else torch.empty((rows, n), dtype=torch.bfloat16, device=x.device)
+    g = None if gamma is None else gamma.to(device=x.device, dtype=torch.float32).contiguous()
+    b = None if beta is None else beta.to(device=x.device, dtype=torch.float32).contiguous()
+    dg = torch.zeros(n, dtype=torch.float32, device=x.device) if (need_affine and gamma is not None) else None
+    db = torch.zeros(n, dtype=torch.float32, device=x.device) if (need_affine and beta is not None) else None
+    ws, wsb = None, 0
+    if dg is not None or db is not None:
+        wsb = int(_lib.lib().jh_norm_gate_bwd_workspace_bytes(rows, n))
+        ws = torch.empty(wsb, dtype=torch.uint8, device=x.device)
+    check(_lib.lib().jh_norm_gate_bwd(_ptr(dy), n, _ptr(x), ldx, _ptr(u), ldu, _ptr(g), _ptr(b), _ptr(mean),
+                                      _ptr(rstd), rows, n, _ptr(dx), n, _ptr(du), n, _ptr(dg), _ptr(db), _ptr(ws), wsb,
+                                      _stream(x)), "norm_gate_bwd")
+    _bump(2 if ws is not None else 1)
+    return dx, du, dg, db

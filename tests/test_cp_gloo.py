@@ -117,13 +117,14 @@ def _batch(seed, rank, lengths, D):
     return dict(q=q, k=k, v=v, g=g, ts=ts, offsets=offs)
 
 
-def _worker(rank, world, port, lens, H, D, mode, result_dir, overlap=True):
+def _worker(rank, world, port, lens, H, D, mode, result_dir, overlap=True, retain=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2508_04711_b200.cp_layer import CPAttention
     b = _batch(3, rank, lens[rank], H * D)
     w = torch.from_numpy(oracle.normal_init_ts_weights(16, 11))
-    layer = CPAttention(dist.group.WORLD, H, 16, balance_mode=mode, backend=NumpyBackend(), overlap=overlap)
+    layer = CPAttention(dist.group.WORLD, H, 16, balance_mode=mode, backend=NumpyBackend(), overlap=overlap,
+                        retain_kv=retain)
     t = {key: torch.from_numpy(b[key]) for key in ("q", "k", "v", "g", "ts")}
     out, ctx = layer.forward(t["q"], t["k"], t["v"], t["ts"], np.diff(b["offsets"]), w)
     dq, dk, dv, dw = layer.backward(ctx, t["g"], w)
@@ -132,15 +133,16 @@ def _worker(rank, world, port, lens, H, D, mode, result_dir, overlap=True):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,lens,mode,overlap", [
-    (2, [[7, 0, 33], [12, 1]], "balanced_minichunk", True),
-    (2, [[7, 0, 33], [12, 1]], "balanced_minichunk", False),
-    (3, [[20, 5], [], [9, 40, 2]], "balanced_minichunk", True),
-    (2, [[31, 4], [17]], "naive_contiguous", True),
+@pytest.mark.parametrize("world,lens,mode,overlap,retain", [
+    (2, [[7, 0, 33], [12, 1]], "balanced_minichunk", True, False),
+    (2, [[7, 0, 33], [12, 1]], "balanced_minichunk", True, True),
+    (2, [[7, 0, 33], [12, 1]], "balanced_minichunk", False, False),
+    (3, [[20, 5], [], [9, 40, 2]], "balanced_minichunk", True, False),
+    (2, [[31, 4], [17]], "naive_contiguous", True, True),
 ])
-def test_cp_layer_matches_single_device(tmp_path, world, lens, mode, overlap):
+def test_cp_layer_matches_single_device(tmp_path, world, lens, mode, overlap, retain):
     H, D = 2, 4
-    mp.spawn(_worker, args=(world, _free_port(), lens, H, D, mode, str(tmp_path), overlap), nprocs=world,
+    mp.spawn(_worker, args=(world, _free_port(), lens, H, D, mode, str(tmp_path), overlap, retain), nprocs=world,
              join=True)
     batches = [_batch(3, r, lens[r], H * D) for r in range(world)]
     cat = oracle.concat_batches(batches)
