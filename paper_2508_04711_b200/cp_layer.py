@@ -244,14 +244,53 @@ class GpuBackend:
         return dk, dv, dw
 
 
+class LoopbackComm:
+    """One process standing in for rank ``rank`` of a CP group of ``size``
+    ranks, communication EXCLUDED: every collective returns a correctly sized
+    buffer filled from local data (the other ranks' K/V are replicas of this
+    rank's, so values are meaningless but shapes, memory and kernel work are
+    exactly one rank's).  Used by the bench's per-rank max-length probe
+    (bench.py --cp-probe), the measured analogue of the reference's modeled
+    per-rank footprint (harness.py:308-374)."""
+
+    def __init__(self, size: int, rank: int = 0, peer_lengths=None):
+        self.size, self.rank = int(size), int(rank)
+        self.peer_lengths = peer_lengths  # callable rank -> lengths of that rank's local batch
+
+    def all_gather_lengths(self, local_lengths) -> tuple:
+        loc = tuple(int(x) for x in local_lengths)
+        if self.peer_lengths is None:
+            return tuple(loc for _ in range(self.size))
+        return tuple(loc if r == self.rank else tuple(int(x) for x in self.peer_lengths(r))
+                     for r in range(self.size))
+
+    def all_to_all(self, out, send, out_splits, in_splits):
+        out.zero_()
+
+    def all_gather_into(self, full, x):
+        full.view((self.size,) + tuple(x.shape)).copy_(x.unsqueeze(0).expand((self.size,) + tuple(x.shape)))
+
+    def reduce_scatter(self, out, full):
+        out.copy_(full.view((self.size,) + tuple(out.shape))[self.rank])
+
+    def all_reduce(self, x):
+        pass
+
+
 class CPAttention:
-    """Context-parallel jagged HSTU attention over a process group."""
+    """Context-parallel jagged HSTU attention over a process group (or, with
+    ``group=None``, over the topology of ``comm``: a LoopbackComm probe)."""
 
     def __init__(self, group, num_heads: int, num_buckets: int = 16, balance_mode: str = "balanced_minichunk",
                  backend=None, overlap: bool = True, comm=None, max_plans: int = 64, retain_kv: bool = False):
         self.group = group
-        self.cp = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
+        if group is None:
+            if comm is None or not hasattr(comm, "size"):
+                raise ValueError("group=None needs a comm that carries its topology (LoopbackComm)")
+            self.cp, self.rank = comm.size, comm.rank
+        else:
+            self.cp = dist.get_world_size(group)
+            self.rank = dist.get_rank(group)
         self.comm = comm if comm is not None else TorchComm(group)
         self.max_plans = int(max_plans)
         self.H = num_heads

@@ -337,13 +337,17 @@ _BWD_STATE: dict = {}
 
 
 def ds_scratch_budget(device) -> int:
-    """Bytes the auto policy lets the dS scratch take (JH_DS_SCRATCH_BUDGET,
-    default 1/8 of the device's memory)."""
+    """Bytes the auto policy lets the dS scratch take: JH_DS_SCRATCH_BUDGET, or
+    min(1/8 of the device, 1/4 of what this process may still allocate under
+    its per-process memory fraction)."""
     import os
     env = os.environ.get("JH_DS_SCRATCH_BUDGET")
     if env:
         return int(float(env))
-    return int(torch.cuda.get_device_properties(device).total_memory // 8)
+    total = torch.cuda.get_device_properties(device).total_memory
+    allowed = total * torch.cuda.get_per_process_memory_fraction(device)
+    avail = max(allowed - torch.cuda.memory_allocated(device), 0)
+    return int(min(total // 8, avail // 4))
 
 
 def ds_scratch_bytes(num_heads: int, q_offsets_host, q_pos0_host=None, kv_len_host=None) -> int:

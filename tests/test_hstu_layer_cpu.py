@@ -121,3 +121,23 @@ def test_copy_params_roundtrip():
     copy_params(a, b)
     for p1, p2 in zip(a.parameters(), b.parameters()):
         assert torch.equal(p1, p2)
+
+
+@pytest.mark.parametrize("k", [1, 2, 4])
+def test_loopback_probe_runs_one_rank_share(k):
+    # bench.py's CP max-length probe: one process = rank 0 of a CP group of k,
+    # communication excluded; shapes / resident rows are exactly one rank's
+    from paper_2508_04711_b200.cp_layer import CPAttention, LoopbackComm
+    L = 64 * k
+    cp = CPAttention(None, H, 16, backend=NumpyBackend(), comm=LoopbackComm(k, 0, peer_lengths=lambda r: []))
+    st = _stack(cp)
+    plan = cp.plan_for([L], torch.device("cpu"))
+    n = plan[0].n_res
+    assert n == L // k  # two balanced mini-chunks of L / (2k)
+    x = torch.randn(n, E, dtype=torch.float64, requires_grad=True)
+    ts = torch.cumsum(torch.randint(1, 1000, (n,)), 0)
+    y = x
+    for layer in st.layers:
+        y = layer(y, ts, cp=(cp, plan))
+    y.sum().backward()
+    assert torch.isfinite(y).all() and torch.isfinite(x.grad).all()
