@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         int h0, nh;
         dkv_halves(sg, it.y, h0, nh);
         if (h0 >= nh) continue;
-        mbar_wait(kv_empty, (it_cnt & 1) ^ 1);  // last S^T / dP^T of the previous item done
+        mbar_wait_idle(kv_empty, (it_cnt & 1) ^ 1);  // last S^T / dP^T of the previous item done
         trace_ev(p, 0, tcnt, 1, g);
         mbar_expect_tx(kv_full, 2 * C::TILE);
         const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)it.y * kBN);
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         dkv_halves(sg, it.y, h0, nh);
         for (int t = h0; t < nh; ++t, ++hc) {
           const int st = hc % kQStages;
-          mbar_wait(&qd_empty[st], ((hc / kQStages) & 1) ^ 1);
+          mbar_wait_idle(&qd_empty[st], ((hc / kQStages) & 1) ^ 1);
           trace_ev(p, 4, tcnt, 5, hc);
           mbar_expect_tx(&qd_full[st], 2 * C::HTILE + kTsBytesH);
           const int32_t qrow = (int32_t)(sg.q_row0 + (int64_t)t * kQH);
@@ -783,7 +783,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
         continue;
       }
-      mbar_wait(dkv_full, it_cnt & 1);
+      mbar_wait_idle(dkv_full, it_cnt & 1);
       ++it_cnt;
       tc_fence_after();
 #pragma unroll 1
@@ -917,7 +917,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         }
         for (int j = 0; j < n; ++j, ++kc) {
           const int st = kc % kDqStages;
-          mbar_wait(&empty[st], ((kc / kDqStages) & 1) ^ 1);
+          mbar_wait_idle(&empty[st], ((kc / kDqStages) & 1) ^ 1);
           mbar_expect_tx(&full[st], C::STAGE);
           uint8_t* sb = smem + st * C::STAGE;
           // blocks (j, 2i) and (j, 2i+1); the second one may not exist (odd half
@@ -1002,7 +1002,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         continue;
       }
       const uint32_t y = o_it & 1;
-      mbar_wait(&dq_full[y], (o_it >> 1) & 1);
+      mbar_wait_idle(&dq_full[y], (o_it >> 1) & 1);
       ++o_it;
       tc_fence_after();
 #pragma unroll 1

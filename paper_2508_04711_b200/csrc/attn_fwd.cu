@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       auto load_v = [&]() {
         const int slot = pend_head & 3;
         const int st = v_it % NS;
-        mbar_wait(&v_empty[st], ((v_it / NS) & 1) ^ 1);
+        mbar_wait_idle(&v_empty[st], ((v_it / NS) & 1) ^ 1);
         trace_ev(p, 0, tcnt, 3, v_it);
         mbar_expect_tx(&v_full[st], C::TILE_BYTES);
         for (int pn = 0; pn < C::PANELS; ++pn)
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       };
       auto load_q = [&](const Item& x) {
         const int qb = q_it & 1;
-        mbar_wait(&q_empty[qb], ((q_it >> 1) & 1) ^ 1);
+        mbar_wait_idle(&q_empty[qb], ((q_it >> 1) & 1) ^ 1);
         trace_ev(p, 0, tcnt, 1, x.g);
         mbar_expect_tx(&q_full[qb], C::TILE_BYTES + kTsBytes);
         const int32_t qrow = (int32_t)(x.sg.q_row0 + (int64_t)x.it.y * kBM);
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const int st = k_it % NS;
           const int ts = k_it % kTsRing;
           const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)j * kBN);
-          mbar_wait(&k_empty[st], ((k_it / NS) & 1) ^ 1);
+          mbar_wait_idle(&k_empty[st], ((k_it / NS) & 1) ^ 1);
           trace_ev(p, 0, tcnt, 2, j);
           mbar_expect_tx(&k_full[st], C::TILE_BYTES);
           for (int pn = 0; pn < C::PANELS; ++pn)
@@ -462,7 +462,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               const float h0 = fmaf(__uint_as_float(v[i]), c1, b0);
               const float h1 = fmaf(__uint_as_float(v[i + 1]), c1, b1);
               // masked pairs: h = -1e30, tanh = -1 exactly, P = h - h = 0
-              pk[i >> 1] = pack_bf16(fmaf(h0, tanh_approx(h0), h0), fmaf(h1, tanh_approx(h1), h1));
+              float p0, p1;
+              silu_pair(h0, h1, p0, p1);
+              pk[i >> 1] = pack_bf16(p0, p1);
             }
             tmem_st16(tS + c0, pk);
           } else if (cls == 1) {
@@ -477,7 +479,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             for (int i = 0; i < 32; i += 2) {
               const float h0 = fmaf(__uint_as_float(v[i]), c1, cb);
               const float h1 = fmaf(__uint_as_float(v[i + 1]), c1, cb);
-              pk[i >> 1] = pack_bf16(fmaf(h0, tanh_approx(h0), h0), fmaf(h1, tanh_approx(h1), h1));
+              float p0, p1;
+              silu_pair(h0, h1, p0, p1);
+              pk[i >> 1] = pack_bf16(p0, p1);
             }
             tmem_st16(tS + c0, pk);  // P over the chunk's (consumed) S columns
           } else if (cls == 0) {
@@ -590,7 +594,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int c = 0; c < D; c += 4) *reinterpret_cast<float4*>(p.out_acc + orow_i + c) = make_float4(0, 0, 0, 0);
         continue;
       }
-      mbar_wait(o_full, o_it & 1);
+      mbar_wait_idle(o_full, o_it & 1);
       ++o_it;
       tc_fence_after();
       if (p.out_acc != nullptr) {

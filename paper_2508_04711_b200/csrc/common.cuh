@@ -79,6 +79,44 @@ JH_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Wait for a role that is NOT on the critical path (drain warps waiting for a
+// whole item, TMA producers waiting for a free stage): a plain try_wait loop
+// there issues ~9 instructions per ~80 cycles on every SMSP it shares with the
+// compute warps (r2 ncu: spin loops were ~39 % of the dK/dV kernel's executed
+// instructions).  JH_IDLE: 1 (default) = try_wait with a suspend-time hint (the
+// warp sleeps until the phase completes), 2 = nanosleep back-off, 0 = spin.
+#ifndef JH_IDLE
+#define JH_IDLE 1
+#endif
+JH_DEV void mbar_wait_idle(uint64_t* bar, uint32_t parity) {
+#if JH_IDLE == 0
+  mbar_wait(bar, parity);
+#elif JH_IDLE == 1
+  const long long t0 = clock64();
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+    if (ok) return;
+    if (clock64() - t0 > (1ll << 36)) __trap();
+  }
+#else
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
+  uint32_t ns = 32;
+  while (!mbar_try_wait(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < 256 ? 2 * ns : 256;
+    if (clock64() - t0 > (1ll << 36)) __trap();
+  }
+#endif
+}
+
 // Named barrier over a subset of warps (id 0 is __syncthreads).
 JH_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -274,6 +312,24 @@ JH_DEV float2 tanh2_approx(float a, float b) {
   uint32_t xi = *reinterpret_cast<uint32_t*>(&x), yi;
   asm("tanh.approx.f16x2 %0, %1;" : "=r"(yi) : "r"(xi));
   return __half22float2(*reinterpret_cast<__half2*>(&yi));
+}
+// SiLU of two pre-scaled scores h = s / 2: P = h + h tanh(h).  JH_TANH2=1 takes
+// both tanh from one packed f16x2 MUFU op (half the MUFU issue of the forward
+// epilogue, which is MUFU-bound while both epilogue warpgroups run); the f16
+// tanh error (<= 2^-11 near |t| = 1) moves P by <= |h| 2^-11, below the bf16
+// rounding of P for the rows' large entries.
+#ifndef JH_TANH2
+#define JH_TANH2 0
+#endif
+JH_DEV void silu_pair(float h0, float h1, float& p0, float& p1) {
+#if JH_TANH2
+  const float2 t = tanh2_approx(h0, h1);
+  p0 = fmaf(h0, t.x, h0);
+  p1 = fmaf(h1, t.y, h1);
+#else
+  p0 = fmaf(h0, tanh_approx(h0), h0);
+  p1 = fmaf(h1, tanh_approx(h1), h1);
+#endif
 }
 // L2 eviction-priority policies (createpolicy) and a 16-byte store that carries one
 JH_DEV uint64_t l2_policy_evict_last() {

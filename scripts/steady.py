@@ -21,7 +21,7 @@ offs = torch.arange(0, T + 1, L, device=dev, dtype=torch.int64)
 w = torch.randn(16, device=dev) * 0.02
 for _ in range(3):
     kernels.attn_fwd(q, k, v, ts, ts, offs, H, w, 16)
-    kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, 16, max_kv_len=L)
+    kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, 16, seg_host=(offs.cpu().numpy(), None, None))
 torch.cuda.synchronize()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 ev[0].record()
@@ -29,7 +29,7 @@ for _ in range(5):
     kernels.attn_fwd(q, k, v, ts, ts, offs, H, w, 16)
 ev[1].record()
 for _ in range(5):
-    kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, 16, max_kv_len=L)
+    kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, 16, seg_host=(offs.cpu().numpy(), None, None))
 ev[2].record()
 torch.cuda.synchronize()
 tf, tb = ev[0].elapsed_time(ev[1]) / 5, ev[1].elapsed_time(ev[2]) / 5
@@ -37,5 +37,7 @@ nq = (L + 127) // 128
 tiles = B * H * nq * (nq + 1) // 2
 halves = B * H * sum(2 * nq - 2 * j for j in range(nq))
 clk = 1.965e6  # cycles per ms
-print(f"L={L} B={B}: fwd {tf * 1e3:.1f} us  ({tf * clk * 148 / tiles:.0f} cycles/tile/SM)   "
+F = 2.0 * D * H * B * L * (L + 1)
+print(f"[{'fwd2' if os.environ.get('JH_FWD2') == '1' else 'fwd1'}] L={L} B={B}: fwd {tf * 1e3:.1f} us "
+      f"({F / tf / 1e9:.0f} TF/s)  ({tf * clk * 148 / tiles:.0f} cycles/tile/SM)   "
       f"bwd {tb * 1e3:.1f} us  ({tb * clk * 148 / halves:.0f} cycles/half/SM incl. dQ)")

@@ -50,7 +50,7 @@ ms = timeit(lambda: kernels.attn_fwd(q, k, v, ts, ts, offs, H, w, 16, band_table
 print(f"fwd ({'fwd2' if os.environ.get('JH_FWD2') == '1' else 'fwd1'}): {ms * 1e3:.1f} us  "
       f"{F_fwd / ms / 1e9:.1f} TF/s  frac {F_fwd / ms / 1e9 / 1650.2:.3f}", flush=True)
 if os.environ.get("JH_FWD2") != "1":
-    for det, dbg in ((True, 0), (False, 0), (False, 8), (False, 16), (False, 24)):
+    for det, dbg in ((True, 0),) if os.environ.get("JH_ALL") != "1" else ((True, 0), (False, 0), (False, 8), (False, 16), (False, 24)):
         os.environ["JH_DBG"] = str(dbg)
         ms = timeit(lambda: kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, 16, band_table=band,
                                              deterministic=det, max_kv_len=int(L.max())))
