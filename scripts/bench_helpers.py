@@ -73,6 +73,23 @@ def main():
     dw = torch.zeros(16, dtype=torch.float64, device=dev)
     rec("dbias_scatter", timed(lambda: kernels.dbias_scatter(ts, ts, bias, 16, dw), flush), Lb * Lb * 4 + 2 * Lb * 8,
         [Lb, Lb])
+    # HSTU layer row kernels at the C4 batch scale x4 (180K rows): silu over uvqk
+    # (4 H d = 2048 columns, read + write), norm_gate over the attention output
+    # (512 columns, gate = strided u view): fwd reads x, u, writes y (+ 8 B stats),
+    # bwd reads dy, x, u, writes dx, du
+    R, N = 180_420, 512
+    uvqk = torch.randn(R, 4 * N, device=dev).bfloat16()
+    rec("silu_fwd", timed(lambda: kernels.silu(uvqk), flush), 2 * R * 4 * N * 2, [R, 4 * N])
+    dyu = torch.randn(R, 4 * N, device=dev).bfloat16()
+    rec("silu_bwd", timed(lambda: kernels.silu_bwd(uvqk, dyu), flush), 3 * R * 4 * N * 2, [R, 4 * N])
+    xa = torch.randn(R, N, device=dev).bfloat16()
+    u = uvqk[:, :N]
+    g_, b_ = torch.ones(N, device=dev), torch.zeros(N, device=dev)
+    y, mean, rstd = kernels.norm_gate_fwd(xa, u, g_, b_)
+    rec("norm_gate_fwd", timed(lambda: kernels.norm_gate_fwd(xa, u, g_, b_), flush), 3 * R * N * 2 + 8 * R, [R, N])
+    dy = torch.randn(R, N, device=dev).bfloat16()
+    rec("norm_gate_bwd", timed(lambda: kernels.norm_gate_bwd(dy, xa, u, g_, b_, mean, rstd), flush),
+        5 * R * N * 2 + 8 * R, [R, N])
     res = {"peak_hbm_gbs": peak, "peak_kind": "MEASURED_PEAKS.json copy bandwidth", "rows": rows,
            "device": torch.cuda.get_device_name()}
     for r in rows:

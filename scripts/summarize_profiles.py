@@ -8,7 +8,9 @@ import subprocess
 import sys
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
-rows = [r for r in csv.reader(open("gpurun_out/launches_all.csv")) if len(r) > 10]
+launches = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/launches_all.csv"
+suffix = sys.argv[3] if len(sys.argv) > 3 else ""  # full_<kernel><suffix>.ncu-rep
+rows = [r for r in csv.reader(open(launches)) if len(r) > 10]
 hdr = rows[0]
 ki, vi, ii = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("ID")
 out = [["launch_id", "kernel", "gpu__time_duration_ns"]]
@@ -25,7 +27,7 @@ for k, v in agg.items():
 
 
 def raw(k):
-    txt = subprocess.run(["ncu", "-i", f"gpurun_out/full_{k}.ncu-rep", "--page", "raw", "--csv"],
+    txt = subprocess.run(["ncu", "-i", f"gpurun_out/full_{k}{suffix}.ncu-rep", "--page", "raw", "--csv"],
                          capture_output=True, text=True).stdout
     rr = list(csv.reader(txt.splitlines()))
     return {h: (v, u) for h, v, u in zip(rr[0], rr[2], rr[1])}
