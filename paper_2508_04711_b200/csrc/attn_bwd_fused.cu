@@ -729,6 +729,16 @@ __global__ void __launch_bounds__(kFThreads, 1)
         mbar_wait(dq_full, tc & 1);
         if (trd) trace_ev(p, 2, tcnt, 20, tc);
         tc_fence_after();
+        // coalesced reduction: an 8x8 transpose of 16-byte blocks inside each
+        // group of 8 lanes turns "thread = row, 32 columns" into "8 lanes = one
+        // row's 128 contiguous bytes", so each red.global.add.v4 instruction
+        // covers 4 full lines instead of 32 rows x 16 bytes (r2: the per-row
+        // form made the reductions the fused kernel's bottleneck)
+        const int lane = r & 31, gi = lane & 7, rbase = (r & ~31) + (lane & ~7);
+        float* drow = p.dq_acc != nullptr ? p.dq_acc + (sg.q_row0 + t * kBM + rbase) * ld_dq + h * D
+                                          : p.dq_state + (sg.q_row0 + t * kBM + rbase) * HD + h * D;
+        const int64_t dld = p.dq_acc != nullptr ? ld_dq : HD;
+        const int nrow = (int)min((int64_t)8, max((int64_t)0, sg.lq - t * kBM - rbase));
 #pragma unroll 1
         for (int cc = 0; cc < D; cc += 32) {
           uint32_t v[32];
@@ -738,9 +748,28 @@ __global__ void __launch_bounds__(kFThreads, 1)
             tc_fence_before();
             mbar_arrive(dq_empty);
           }
-          if (row_ok && !(p.dbg & 8)) {
+          if (!(p.dbg & 8)) {
 #pragma unroll
-            for (int q4 = 0; q4 < 8; ++q4) red_add_v4(dst + cc + 4 * q4, v + 4 * q4);
+            for (int m = 4; m >= 1; m >>= 1) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                if (j & m) continue;
+                const bool up = (gi & m) != 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const uint32_t send = up ? v[4 * j + e] : v[4 * (j | m) + e];
+                  const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, m);
+                  if (up)
+                    v[4 * j + e] = recv;
+                  else
+                    v[4 * (j | m) + e] = recv;
+                }
+              }
+            }
+            // v[4 j ..] = row rbase + j, columns cc + 4 gi .. + 3
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (j < nrow) red_add_v4(drow + j * dld + cc + 4 * gi, v + 4 * j);
           }
         }
         if (trd) trace_ev(p, 2, tcnt, 21, tc);
