@@ -181,10 +181,22 @@ def run_gpu(args):
     offs = torch.from_numpy(h["offsets"]).to(dev)
     w = torch.from_numpy(w_host.astype(np.float32)).to(dev)
 
+    cp_size = world if args.cp <= 0 else args.cp
     if world > 1:
-        from paper_2508_04711_b200.cp_layer import CPAttention
-        cp = CPAttention(dist.group.WORLD, H, NB)
-        step_fn = cp.bench_step(q, k, v, ts, h["offsets"], g, w)
+        from paper_2508_04711_b200.cp_layer import CPAttention, make_cp_dp_groups
+        if cp_size == world:
+            cp_group, dp_group = dist.group.WORLD, None
+        else:  # hybrid CP x DP (config C5): CP groups of consecutive ranks, DP across them
+            cp_group, dp_group, _, _ = make_cp_dp_groups(cp_size)
+        cp = CPAttention(cp_group, H, NB, protocol=args.protocol)
+        cp_step = cp.bench_step(q, k, v, ts, h["offsets"], g, w)
+
+        def step_fn(prof=None):
+            dq_, dk_, dv_, dw_ = cp_step()
+            if dp_group is not None:  # DDP rule: summed over CP (inside), averaged over DP
+                dist.all_reduce(dw_, group=dp_group)
+                dw_ /= world // cp_size
+            return dq_, dk_, dv_, dw_
         all_lens = [None] * world
         dist.all_gather_object(all_lens, [int(x) for x in lens])
         tokens_total = sum(sum(x) for x in all_lens)
@@ -276,7 +288,9 @@ def run_gpu(args):
         "config": {"workload": "C2: jagged HSTU attention fwd+bwd, B=32/rank, lengths uniform[1,1024], "
                                "H=4, d=128, nb=16" + ("" if world == 1 else f", jagged CP={world} (balanced)"),
                    "batch_per_rank": B, "max_seq_len": MAXLEN, "heads": H, "head_dim": D, "tokens": tokens_total,
-                   "parallelism": "single" if world == 1 else f"cp{world}",
+                   "parallelism": "single" if world == 1 else (f"cp{world}" if cp_size == world
+                                                                else f"cp{cp_size}xdp{world // cp_size}"),
+                   "cp_protocol": None if world == 1 else args.protocol,
                    "l2": "flushed between timed steps (512 MiB write, outside the timed events)",
                    "cuda_graph": graph is not None},
         "tflops": F / (ms_per_step / 1e3) / 1e12,
@@ -355,6 +369,16 @@ def run_gpu(args):
     else:
         result["e2e"] = None
 
+    if world > 1:
+        # one extra, untimed step with CUDA events around every collective: bytes,
+        # GB/s against NVLink 5 and the exposed (non-overlapped) exchange time
+        cp.meter = {"coll": [], "join": []}
+        step_fn()
+        rep = cp.exchange_report()
+        t = torch.tensor([rep.get("exposed_ms", 0.0)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        rep["exposed_ms_max_over_ranks"] = float(t.item())
+        result["cp_exchange"] = rep
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(h, g_host, w_host)
     if world == 1 and not args.no_stack:
@@ -690,6 +714,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a captured CUDA graph")
     ap.add_argument("--no-max-len", action="store_true", help="skip the max-supported-sequence-length probe")
+    ap.add_argument("--cp", type=int, default=0, help="CP group size for N > 1 (default: all ranks; "
+                    "smaller = hybrid CP x DP)")
+    ap.add_argument("--protocol", choices=["alltoall", "allgather_split"], default="alltoall",
+                    help="batch -> sequence redistribution protocol for N > 1")
     ap.add_argument("--no-stack", action="store_true", help="skip the 8-layer HSTU stack (C4 batch) measurement")
     ap.add_argument("--cp-sweep-gb", type=float, default=24.0,
                     help="per-GPU memory cap of the CP max-length sweep (0 = skip)")

@@ -65,6 +65,8 @@ class CPPlan:
     local_kv_start: np.ndarray   # overlap split: chunk vs itself (resident rows, q_pos0 = 0)
     local_kv_len: np.ndarray
     remote_kv_len: np.ndarray    # ... and vs its sequence prefix [0, start) in the gathered rows
+    max_local: int = 0           # allgather_split: padded local rows per rank in the gathered batch
+    split_perm: np.ndarray = None  # allgather_split: resident row -> index in the padded gathered batch
 
 
 def build_cp_plan(lengths_per_rank, cp: int, rank: int, balance_mode: str = "balanced_minichunk") -> CPPlan:
@@ -110,9 +112,22 @@ def build_cp_plan(lengths_per_rank, cp: int, rank: int, balance_mode: str = "bal
         qp.append(e.start)
         ks.append(int(goff[e.seq_id]))
         kl.append(e.end)
+    # (5) allgather_split (cp_engine.py:246-283): every rank gathers all local
+    # batches (rank-major, each padded to max_local rows) and keeps its plan rows
+    local_tot = [int(sum(x)) for x in lengths_per_rank]
+    max_local = max(local_tot) if local_tot else 0
+    seq_local0 = np.zeros(len(plan.seq_owner), dtype=np.int64)  # first local row of each sequence
+    nxt = [0] * cp
+    for sid, (L, own) in enumerate(zip(plan.seq_lengths, plan.seq_owner)):
+        seq_local0[sid] = nxt[own]
+        nxt[own] += int(L)
+    split_rows = [np.arange(e.start, e.end, dtype=np.int64) + plan.seq_owner[e.seq_id] * max_local +
+                  seq_local0[e.seq_id] for e in plan.rank_entries[rank]]
+    split_perm = np.concatenate(split_rows) if split_rows else np.zeros(0, np.int64)
     a64 = lambda x: np.asarray(x, np.int64)  # noqa: E731
     return CPPlan(cp, rank, plan, send_perm, send_counts, recv_counts, n_res, max_res, res_counts, seq_perm,
-                  a64(qo), a64(qp), a64(ks), a64(kl), int(goff[-1]), a64(lks), a64(lkl), a64(qp))
+                  a64(qo), a64(qp), a64(ks), a64(kl), int(goff[-1]), a64(lks), a64(lkl), a64(qp), max_local,
+                  split_perm)
 
 
 class TorchComm:
@@ -132,21 +147,45 @@ class TorchComm:
         return torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(self.group) == "nccl" \
             else torch.device("cpu")
 
-    def all_gather_lengths(self, local_lengths) -> tuple:
-        """Every rank's sequence lengths (one int64 all-gather of the counts,
-        one of the padded lengths), identical on all ranks."""
+    MAX_SEQS = 16384  # per-rank sequence capacity of the length exchange
+
+    def lengths_start(self, local_lengths):
+        """Start the length exchange: ONE all-gather of a fixed-capacity
+        [count, lengths...] int64 row per rank (no count round, no .item()),
+        then an asynchronous copy into pinned host memory; returns a handle for
+        ``lengths_finish``.  The host waits only when the plan is needed
+        (asynchronous offsets, sync delayed), so a training loop
+        can start the next batch's exchange before this step's compute ends
+        (CPAttention.prefetch_plan)."""
+        loc = np.asarray(local_lengths, dtype=np.int64)
+        if loc.size > self.MAX_SEQS:
+            raise ValueError(f"{loc.size} sequences exceed the length-exchange capacity {self.MAX_SEQS}")
         dev = self._dev()
-        loc = torch.as_tensor(np.asarray(local_lengths, dtype=np.int64), device=dev)
-        n = torch.tensor([loc.numel()], dtype=torch.int64, device=dev)
-        ns = [torch.empty_like(n) for _ in range(self.size)]
-        self._all_gather(ns, n)
-        ns = [int(x.item()) for x in ns]
-        m = max(max(ns), 1)
-        pad = torch.zeros(m, dtype=torch.int64, device=dev)
-        pad[: loc.numel()] = loc
-        parts = [torch.empty_like(pad) for _ in range(self.size)]
-        self._all_gather(parts, pad)
-        return tuple(tuple(int(v) for v in p[:k].tolist()) for p, k in zip(parts, ns))
+        row = np.zeros(self.MAX_SEQS + 1, dtype=np.int64)
+        row[0] = loc.size
+        row[1:1 + loc.size] = loc
+        send = torch.from_numpy(row).to(dev, non_blocking=dev.type == "cuda")
+        full = torch.empty((self.size, self.MAX_SEQS + 1), dtype=torch.int64, device=dev)
+        self._all_gather(list(full.unbind(0)), send)
+        if dev.type == "cuda":
+            host = torch.empty(full.shape, dtype=torch.int64, pin_memory=True)
+            host.copy_(full, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            return host, ev
+        return full, None
+
+    @staticmethod
+    def lengths_finish(handle) -> tuple:
+        host, ev = handle
+        if ev is not None:
+            ev.synchronize()
+        h = host.numpy()
+        return tuple(tuple(int(v) for v in r[1:1 + int(r[0])]) for r in h)
+
+    def all_gather_lengths(self, local_lengths) -> tuple:
+        """Every rank's sequence lengths, identical on all ranks."""
+        return self.lengths_finish(self.lengths_start(local_lengths))
 
     def _all_gather(self, outs, x):
         dist.all_gather(outs, x, group=self.group)
@@ -282,7 +321,8 @@ class CPAttention:
     ``group=None``, over the topology of ``comm``: a LoopbackComm probe)."""
 
     def __init__(self, group, num_heads: int, num_buckets: int = 16, balance_mode: str = "balanced_minichunk",
-                 backend=None, overlap: bool = True, comm=None, max_plans: int = 64, retain_kv: bool = False):
+                 backend=None, overlap: bool = True, comm=None, max_plans: int = 64, retain_kv: bool = False,
+                 protocol: str = "alltoall", measure: bool = False):
         self.group = group
         if group is None:
             if comm is None or not hasattr(comm, "size"):
@@ -299,23 +339,45 @@ class CPAttention:
         self.be = backend if backend is not None else GpuBackend()
         self.overlap = overlap and hasattr(self.be, "fwd_partial") and hasattr(self.be, "bwd_partial")
         self._plans: "OrderedDict" = OrderedDict()
+        self._pending = None
+        # exchange timing (CUDA events; exchange_report) -- off by default
+        self.meter = {"coll": [], "join": []} if measure else None
+        self._on_cuda = isinstance(self.be, GpuBackend)
+        if protocol not in ("alltoall", "allgather_split"):
+            raise ValueError(f"unknown protocol {protocol!r}")
+        self.protocol = protocol
         # keep the gathered group K/V/ts between forward and backward (one fewer
         # all-gather per layer, O(group rows) memory) or re-gather them
         self.retain_kv = bool(retain_kv)
 
     # ---------------------------------------------------------------- plan
+    def prefetch_plan(self, local_lengths) -> None:
+        """Start the length exchange of a FUTURE step (e.g. the next batch,
+        right after this step's forward is enqueued); the matching
+        ``plan_for`` then only waits for a copy that finished long ago.  Every
+        rank must prefetch at the same point (it is a collective)."""
+        if hasattr(self.comm, "lengths_start"):
+            loc = tuple(int(x) for x in local_lengths)
+            self._pending = (loc, self.comm.lengths_start(list(loc)))
+
     def plan_for(self, local_lengths, device) -> tuple[CPPlan, dict]:
         """Every rank's lengths are all-gathered EVERY step and the plan cache is
         keyed on that global tuple, so all ranks make the same hit / miss /
         eviction decision (LRU over identical key sequences) and enter the same
         collectives."""
-        key = self.comm.all_gather_lengths([int(x) for x in local_lengths])
+        loc = tuple(int(x) for x in local_lengths)
+        pend = self._pending
+        self._pending = None
+        if pend is not None and pend[0] == loc:
+            key = self.comm.lengths_finish(pend[1])
+        else:
+            key = self.comm.all_gather_lengths(list(loc))
         if key in self._plans:
             self._plans.move_to_end(key)
             return self._plans[key]
         p = build_cp_plan([list(x) for x in key], self.cp, self.rank, self.mode)
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
-        dev = {"send_perm": t(p.send_perm), "seq_perm": t(p.seq_perm),
+        dev = {"send_perm": t(p.send_perm), "seq_perm": t(p.seq_perm), "split_perm": t(p.split_perm),
                # (q_offsets, q_pos0, kv_start, kv_len, kv total, max kv, host (q_offsets, q_pos0, kv_len))
                "segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.kv_len), int(p.kv_len.sum()),
                         int(p.kv_len.max(initial=0)), (p.q_offsets, p.q_pos0, p.kv_len)),
@@ -331,13 +393,61 @@ class CPAttention:
         return self._plans[key]
 
     # ---------------------------------------------------------- collectives
+    def _timed(self, name, nbytes, fn):
+        """Run one collective; with ``measure`` on a CUDA stream, CUDA events
+        bracket it on the stream it is issued on (exchange_report)."""
+        if self.meter is None or not torch.cuda.is_available() or not self._on_cuda:
+            return fn()
+        s = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        r = fn()
+        e1.record(s)
+        self.meter["coll"].append((name, int(nbytes), e0, e1))
+        return r
+
+    def exchange_report(self, reset: bool = True) -> dict:
+        """Per-collective totals since the last report: bytes (the collective's
+        output buffer on this rank), device ms, GB/s against NVLink 5 (900 GB/s
+        per direction), and the EXPOSED time -- how long the main stream waited
+        for the communication stream (the part the overlap did not hide)."""
+        if self.meter is None:
+            return {}
+        torch.cuda.synchronize()
+        out = {}
+        for name, nb, e0, e1 in self.meter["coll"]:
+            d = out.setdefault(name, {"calls": 0, "bytes": 0, "ms": 0.0})
+            d["calls"] += 1
+            d["bytes"] += nb
+            d["ms"] += e0.elapsed_time(e1)
+        for d in out.values():
+            d["GB_s"] = d["bytes"] / max(d["ms"], 1e-9) / 1e6
+            d["frac_nvlink_900"] = d["GB_s"] / 900.0
+        exposed = sum(max(0.0, a.elapsed_time(b)) for a, b in self.meter["join"])
+        rep = {"collectives": out, "exposed_ms": exposed, "joins": len(self.meter["join"])}
+        if reset:
+            self.meter = {"coll": [], "join": []}
+        return rep
+
     def _a2a_rows(self, send, send_counts, recv_counts):
         out = send.new_empty((int(sum(recv_counts)),) + tuple(send.shape[1:]))
-        self.comm.all_to_all(out, send, recv_counts, send_counts)
+        self._timed("all_to_all", out.numel() * out.element_size(),
+                    lambda: self.comm.all_to_all(out, send, recv_counts, send_counts))
         return out
 
     def _redistribute(self, x, p, dev):
-        """local rows -> resident rows in plan order (cp_engine.py:330-371)."""
+        """local rows -> resident rows in plan order: one all-to-all of the
+        destination-packed rows (cp_engine.py:330-371), or with
+        protocol="allgather_split" the reference's baseline -- gather every
+        rank's whole local batch, keep the plan rows (cp_engine.py:246-283;
+        peak = the full group batch on every rank)."""
+        if self.protocol == "allgather_split":
+            pad = x.new_zeros((p.max_local,) + tuple(x.shape[1:]))
+            pad[: x.shape[0]] = x
+            full = x.new_empty((self.cp * p.max_local,) + tuple(x.shape[1:]))
+            self._timed("allgather_split", full.numel() * full.element_size(),
+                        lambda: self.comm.all_gather_into(full, pad))
+            return self.be.gather(full, dev["split_perm"])
         return self._a2a_rows(self.be.gather(x, dev["send_perm"]), p.send_counts, p.recv_counts)
 
     def _restore(self, x_res, p, dev, n_local):
@@ -351,7 +461,7 @@ class CPAttention:
         pad = x_res.new_zeros((p.max_res,) + tuple(x_res.shape[1:]))
         pad[: p.n_res] = x_res
         full = x_res.new_empty((self.cp * p.max_res,) + tuple(x_res.shape[1:]))
-        self.comm.all_gather_into(full, pad)
+        self._timed("kv_all_gather", full.numel() * full.element_size(), lambda: self.comm.all_gather_into(full, pad))
         return self.be.gather(full, dev["seq_perm"])
 
     def _reduce_to_owner(self, x_seq, p, dev):
@@ -359,7 +469,8 @@ class CPAttention:
         full = x_seq.new_zeros((self.cp * p.max_res,) + tuple(x_seq.shape[1:]))
         self.be.scatter(x_seq, dev["seq_perm"], full)
         mine = x_seq.new_empty((p.max_res,) + tuple(x_seq.shape[1:]))
-        self.comm.reduce_scatter(mine, full)
+        self._timed("dkv_reduce_scatter", full.numel() * full.element_size(),
+                    lambda: self.comm.reduce_scatter(mine, full))
         return mine[: p.n_res]
 
     # --------------------------------------------------------------- passes
@@ -421,9 +532,13 @@ class CPAttention:
             ts_s = self._gather_seq(ts_r.view(-1, 1), p, dev).view(-1)
         return k_s, v_s, ts_s
 
-    @staticmethod
-    def _join(main, comm, tensors):
+    def _join(self, main, comm, tensors):
         if comm is not None:
+            if self.meter is not None:
+                need, done = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                need.record(main)
+                done.record(comm)
+                self.meter["join"].append((need, done))
             main.wait_stream(comm)
             for x in tensors:
                 x.record_stream(main)
@@ -453,7 +568,7 @@ class CPAttention:
             dq_r, dk_r, dv_r, dw = self._backward_regather(q_r, k_r, v_r, ts_r, g_r, p, dev, w)
         else:
             dq_r, dk_r, dv_r, dw = self._backward_overlapped(q_r, k_r, v_r, k_s, v_s, ts_r, ts_s, g_r, p, dev, w)
-        self.comm.all_reduce(dw)
+        self._timed("d_w_all_reduce", dw.numel() * dw.element_size(), lambda: self.comm.all_reduce(dw))
         return dq_r, dk_r, dv_r, dw
 
     def _backward_regather(self, q_r, k_r, v_r, ts_r, g_r, p, dev, w):

@@ -1074,9 +1074,29 @@ int launch_bwd(const TMaps& tm, const AttnParams& p, const jh_attn_args& a, int 
     if (cudaError_t e = cudaLaunchKernelEx(&cfg, hstu_bwd_dkv_kernel<D>, tm.q64, tm.k, tm.v, tm.do64, tm.tsq72, p))
       return (int)e;
   }
+  // programmatic dependent launch of the dQ kernel: its CTAs start on SMs the dK/dV
+  // kernel frees and wait on the per-(segment, head) completion counters (no
+  // kernel-boundary bubble).  The dQ kernel reads the work lists of the build
+  // kernel without a griddepcontrol.wait (that would wait for the whole dK/dV
+  // grid and remove the overlap); this is safe only because a dQ CTA cannot
+  // start before some dK/dV CTA -- which did wait for the build -- has exited:
+  // the dK/dV grid covers every SM and fills it (one CTA per SM whose registers
+  // take the whole register file).  Checked once here; otherwise the launch is
+  // plain stream-ordered.
+  static int pdl_ok = -1;
+  if (pdl_ok < 0) {
+    int nblk = 0, dev = 0, rf = 0;
+    cudaFuncAttributes fa{};
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&rf, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nblk, hstu_bwd_dkv_kernel<D>, kBwdThreads, C::SMEM);
+    cudaFuncGetAttributes(&fa, hstu_bwd_dkv_kernel<D>);
+    pdl_ok = (nblk == 1 && fa.numRegs * kBwdThreads >= rf) ? 1 : 0;
+  }
   {
-    // programmatic dependent launch: dQ CTAs start on SMs the dK/dV kernel frees and
-    // wait on its per-(segment, head) completion counters (no kernel-boundary bubble)
+    int nsm = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kDqThreads);
@@ -1084,7 +1104,7 @@ int launch_bwd(const TMaps& tm, const AttnParams& p, const jh_attn_args& a, int 
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[0].val.programmaticStreamSerializationAllowed = (pdl_ok == 1 && grid >= nsm) ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     __nv_bfloat16* dqp = (__nv_bfloat16*)a.dq;

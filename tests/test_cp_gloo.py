@@ -117,14 +117,14 @@ def _batch(seed, rank, lengths, D):
     return dict(q=q, k=k, v=v, g=g, ts=ts, offsets=offs)
 
 
-def _worker(rank, world, port, lens, H, D, mode, result_dir, overlap=True, retain=False):
+def _worker(rank, world, port, lens, H, D, mode, result_dir, overlap=True, retain=False, protocol="alltoall"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2508_04711_b200.cp_layer import CPAttention
     b = _batch(3, rank, lens[rank], H * D)
     w = torch.from_numpy(oracle.normal_init_ts_weights(16, 11))
     layer = CPAttention(dist.group.WORLD, H, 16, balance_mode=mode, backend=NumpyBackend(), overlap=overlap,
-                        retain_kv=retain)
+                        retain_kv=retain, protocol=protocol)
     t = {key: torch.from_numpy(b[key]) for key in ("q", "k", "v", "g", "ts")}
     out, ctx = layer.forward(t["q"], t["k"], t["v"], t["ts"], np.diff(b["offsets"]), w)
     dq, dk, dv, dw = layer.backward(ctx, t["g"], w)
@@ -133,17 +133,18 @@ def _worker(rank, world, port, lens, H, D, mode, result_dir, overlap=True, retai
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,lens,mode,overlap,retain", [
-    (2, [[7, 0, 33], [12, 1]], "balanced_minichunk", True, False),
-    (2, [[7, 0, 33], [12, 1]], "balanced_minichunk", True, True),
-    (2, [[7, 0, 33], [12, 1]], "balanced_minichunk", False, False),
-    (3, [[20, 5], [], [9, 40, 2]], "balanced_minichunk", True, False),
-    (2, [[31, 4], [17]], "naive_contiguous", True, True),
+@pytest.mark.parametrize("world,lens,mode,overlap,retain,protocol", [
+    (2, [[7, 0, 33], [12, 1]], "balanced_minichunk", True, False, "alltoall"),
+    (2, [[7, 0, 33], [12, 1]], "balanced_minichunk", True, True, "allgather_split"),
+    (2, [[7, 0, 33], [12, 1]], "balanced_minichunk", False, False, "alltoall"),
+    (3, [[20, 5], [], [9, 40, 2]], "balanced_minichunk", True, False, "alltoall"),
+    (3, [[20, 5], [], [9, 40, 2]], "balanced_minichunk", True, False, "allgather_split"),
+    (2, [[31, 4], [17]], "naive_contiguous", True, True, "alltoall"),
 ])
-def test_cp_layer_matches_single_device(tmp_path, world, lens, mode, overlap, retain):
+def test_cp_layer_matches_single_device(tmp_path, world, lens, mode, overlap, retain, protocol):
     H, D = 2, 4
-    mp.spawn(_worker, args=(world, _free_port(), lens, H, D, mode, str(tmp_path), overlap, retain), nprocs=world,
-             join=True)
+    mp.spawn(_worker, args=(world, _free_port(), lens, H, D, mode, str(tmp_path), overlap, retain, protocol),
+             nprocs=world, join=True)
     batches = [_batch(3, r, lens[r], H * D) for r in range(world)]
     cat = oracle.concat_batches(batches)
     g = np.concatenate([b["g"] for b in batches])
@@ -162,7 +163,7 @@ def test_cp_layer_matches_single_device(tmp_path, world, lens, mode, overlap, re
         row += n
 
 
-def _worker_steps(rank, world, port, steps, H, D, result_dir, staged):
+def _worker_steps(rank, world, port, steps, H, D, result_dir, staged, prefetch=False):
     """Variable batches over several steps: some ranks repeat their local
     lengths while others change (the plan-cache divergence scenario)."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -176,17 +177,20 @@ def _worker_steps(rank, world, port, steps, H, D, result_dir, staged):
         b = _batch(10 + i, rank, lens[rank], H * D)
         t = {key: torch.from_numpy(b[key]) for key in ("q", "k", "v", "g", "ts")}
         out, ctx = layer.forward(t["q"], t["k"], t["v"], t["ts"], np.diff(b["offsets"]), w)
+        if prefetch and i + 1 < len(steps):  # next step's length exchange, started before this backward
+            layer.prefetch_plan(steps[i + 1][rank])
         dq, dk, dv, dw = layer.backward(ctx, t["g"], w)
         res[f"out{i}"], res[f"dq{i}"], res[f"dw{i}"] = out.numpy(), dq.numpy(), dw.numpy()
     np.savez(os.path.join(result_dir, f"r{rank}.npz"), **res)
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("staged", [False, True])
-def test_cp_plan_cache_consistent_across_variable_batches(tmp_path, staged):
+@pytest.mark.parametrize("staged,prefetch", [(False, False), (True, False), (False, True)])
+def test_cp_plan_cache_consistent_across_variable_batches(tmp_path, staged, prefetch):
     world, H, D = 2, 1, 4
     steps = [[[7, 3], [12]], [[7, 3], [5, 9]], [[4], [5, 9]], [[7, 3], [12]], [[7, 3], [5, 9]]]
-    mp.spawn(_worker_steps, args=(world, _free_port(), steps, H, D, str(tmp_path), staged), nprocs=world, join=True)
+    mp.spawn(_worker_steps, args=(world, _free_port(), steps, H, D, str(tmp_path), staged, prefetch), nprocs=world,
+             join=True)
     w = oracle.normal_init_ts_weights(16, 11)
     res = [np.load(os.path.join(tmp_path, f"r{r}.npz")) for r in range(world)]
     for i, lens in enumerate(steps):

@@ -51,7 +51,7 @@ def _batch(seed, rank, dist_kind, B):
     return dict(q=q, k=k, v=v, g=g, ts=ts, offsets=offs)
 
 
-def _worker(rank, world, port, dist_kind, B, mode, overlap, out_dir):
+def _worker(rank, world, port, dist_kind, B, mode, overlap, out_dir, protocol="alltoall", retain=False):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
@@ -60,7 +60,7 @@ def _worker(rank, world, port, dist_kind, B, mode, overlap, out_dir):
     b = _batch(17, rank, dist_kind, B)
     w = torch.from_numpy(oracle.normal_init_ts_weights(16, 23).astype(np.float32)).cuda()
     layer = CPAttention(dist.group.WORLD, H, 16, balance_mode=mode, overlap=overlap,
-                        comm=HostStagedComm(dist.group.WORLD))
+                        comm=HostStagedComm(dist.group.WORLD), protocol=protocol, retain_kv=retain)
     t = {x: torch.from_numpy(b[x]).cuda().bfloat16() for x in ("q", "k", "v", "g")}
     ts = torch.from_numpy(b["ts"]).cuda()
     lens = np.diff(b["offsets"])
@@ -74,15 +74,16 @@ def _worker(rank, world, port, dist_kind, B, mode, overlap, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,dist_kind,B,mode,overlap", [
-    (2, "uniform", 3, "balanced_minichunk", True),
-    (2, "uniform", 3, "naive_contiguous", False),
-    (4, "lognormal", 3, "balanced_minichunk", True),
-    (4, "lognormal", 2, "naive_contiguous", True),
+@pytest.mark.parametrize("world,dist_kind,B,mode,overlap,protocol,retain", [
+    (2, "uniform", 3, "balanced_minichunk", True, "alltoall", False),
+    (2, "uniform", 3, "naive_contiguous", False, "alltoall", False),
+    (2, "uniform", 3, "balanced_minichunk", True, "allgather_split", True),
+    (4, "lognormal", 3, "balanced_minichunk", True, "alltoall", False),
+    (4, "lognormal", 2, "naive_contiguous", True, "allgather_split", False),
 ])
-def test_cuda_cp_layer_matches_oracle(tmp_path, world, dist_kind, B, mode, overlap):
-    mp.spawn(_worker, args=(world, _free_port(), dist_kind, B, mode, overlap, str(tmp_path)), nprocs=world,
-             join=True)
+def test_cuda_cp_layer_matches_oracle(tmp_path, world, dist_kind, B, mode, overlap, protocol, retain):
+    mp.spawn(_worker, args=(world, _free_port(), dist_kind, B, mode, overlap, str(tmp_path), protocol, retain),
+             nprocs=world, join=True)
     batches = [_batch(17, r, dist_kind, B) for r in range(world)]
     cat = oracle.concat_batches(batches)
     g = np.concatenate([b["g"] for b in batches])

@@ -163,10 +163,13 @@ def test_cp_layer_single_rank_matches_single_device():
     try:
         case = make_case([300, 17, 129], 2 * 128, seed=3)
         c = to_cuda(case)
-        layer = CPAttention(dist.group.WORLD, 2, 16)
+        layer = CPAttention(dist.group.WORLD, 2, 16, measure=True)
         out, ctx = layer.forward(c["q"], c["k"], c["v"], c["ts"], np.diff(case["offsets"]), c["w"])
         dq, dk, dv, dw = layer.backward(ctx, c["g"], c["w"])
         torch.cuda.synchronize()
+        rep = layer.exchange_report()
+        assert {"all_to_all", "kv_all_gather", "dkv_reduce_scatter", "d_w_all_reduce"} <= set(rep["collectives"])
+        assert rep["joins"] >= 2 and rep["exposed_ms"] >= 0
         want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], case["offsets"], case["w"], 16, 2)
         assert row_rel(out.float().cpu().numpy(), want)[1] <= ROW_TOL
         wq, wk, wv, ww, _ = oracle.hstu_backward(case["q"], case["k"], case["v"], case["ts"], case["offsets"],
