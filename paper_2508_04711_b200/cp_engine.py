@@ -186,26 +186,33 @@ def _check_sched(scheduling: str) -> None:
         raise ValueError(f"unknown scheduling {scheduling!r}")
 
 
-def _map_ranks(fn, cp_size: int, scheduling: str) -> list:
+def _map_ranks(fn, cp_size: int, scheduling: str, devices=None) -> list:
     """cp_engine.py:188-206: run a per-rank function sequentially or on a
     thread pool (kernel launches are thread-safe; every rank's work is
-    stream-ordered on the caller's current stream); results in rank order,
-    failures re-raised as RuntimeError("rank r: ...")."""
+    stream-ordered on the current stream of ITS device -- ``devices[r]`` in
+    the single-process multi-device mode); results in rank order, failures
+    re-raised as RuntimeError("rank r: ...")."""
 
     def run(r: int):
         try:
+            dev = None if devices is None else devices[r]
+            if dev is not None and dev.type == "cuda":
+                with torch.cuda.device(dev):
+                    return fn(r)
             return fn(r)
         except Exception as exc:  # annotate with the failing rank
             raise RuntimeError(f"rank {r}: {exc}") from exc
 
     if scheduling == "threaded" and cp_size > 1:
         from concurrent.futures import ThreadPoolExecutor
-        stream = torch.cuda.current_stream() if torch.cuda.is_available() else None
+        cuda = torch.cuda.is_available()
+        streams = [torch.cuda.current_stream(None if devices is None else devices[r]) if cuda else None
+                   for r in range(cp_size)]
 
         def run_on_stream(r: int):
-            if stream is None:
+            if streams[r] is None:
                 return run(r)
-            with torch.cuda.stream(stream):
+            with torch.cuda.stream(streams[r]):
                 return run(r)
 
         with ThreadPoolExecutor(max_workers=cp_size) as pool:
@@ -243,6 +250,12 @@ def _rows(values: torch.Tensor, idx: np.ndarray) -> torch.Tensor:
     return out if values.dim() == 2 else out.view(-1)
 
 
+def _devices(batches) -> list:
+    """Single-process multi-device mode: rank r works on the device its batch
+    lives on (all ranks on one device is the common single-GPU case)."""
+    return [b.q.values.device for b in batches]
+
+
 def _context(rank: int, plan: ShardPlan, q, k, v, ts) -> RankContext:
     seq, pos, chk = _entries_meta(plan.rank_entries[rank])
     return RankContext(rank, q, k, v, ts, seq, pos, chk, plan.rank_entries[rank])
@@ -256,16 +269,19 @@ def redistribute_allgather_split(group: RankGroup, batches, plan: ShardPlan, sch
     cp = group.cp_size
     payload = [b.payload_nbytes() for b in batches]
     stats, meters = gather_traffic(cp, payload, batches[0].q.values.element_size())
-    full = {n: torch.cat([getattr(b, n).values for b in batches]) for n in ("q", "k", "v", "ts")}
-    full_bytes = sum(int(t.numel() * t.element_size()) for t in full.values())
+    devs = _devices(batches)
+    full_bytes = sum(int(getattr(b, n).values.numel() * getattr(b, n).values.element_size())
+                     for b in batches for n in ("q", "k", "v", "ts"))
     goff = plan.group_offsets()
 
     def keep(r: int) -> RankContext:
+        # every rank materialises the whole group batch on its own device (the peak)
+        full = {n: torch.cat([getattr(b, n).values.to(devs[r]) for b in batches]) for n in ("q", "k", "v", "ts")}
         idx = np.concatenate([np.arange(goff[e.seq_id] + e.start, goff[e.seq_id] + e.end, dtype=np.int64)
                               for e in plan.rank_entries[r]]) if plan.rank_entries[r] else np.zeros(0, np.int64)
         return _context(r, plan, *(_rows(full[n], idx) for n in ("q", "k", "v", "ts")))
 
-    contexts = _map_ranks(keep, cp, scheduling)
+    contexts = _map_ranks(keep, cp, scheduling, devs)
     for r, ctx in enumerate(contexts):
         meters[r].step(ctx.payload_nbytes() - full_bytes)
         stats[r].peak_resident_bytes = meters[r].peak
@@ -294,14 +310,16 @@ def redistribute_alltoall(group: RankGroup, batches, plan: ShardPlan, scheduling
                                       {n: _rows(getattr(batches[src], n).values, idx) for n in ("q", "k", "v", "ts")}))
         return msgs
 
-    send = _map_ranks(pack, cp, scheduling)
+    devs = _devices(batches)
+    send = _map_ranks(pack, cp, scheduling, devs)
     received, stats = all_to_all_jagged(group, send)
 
     def assemble(r: int) -> RankContext:
-        parts = {n: [m.arrays[n] for m in received[r]] for n in ("q", "k", "v", "ts")}
+        # messages from other devices are copied peer-to-peer to the receiver's device
+        parts = {n: [m.arrays[n].to(devs[r]) for m in received[r]] for n in ("q", "k", "v", "ts")}
         return _context(r, plan, *(torch.cat(parts[n]) for n in ("q", "k", "v", "ts")))
 
-    return _map_ranks(assemble, cp, scheduling), stats
+    return _map_ranks(assemble, cp, scheduling, devs), stats
 
 
 def _bundle(ctx: RankContext) -> JaggedMessage:
@@ -341,7 +359,8 @@ def ring_hstu_attention(group: RankGroup, contexts, params, cfg, scheduling: str
     for s in order:
         base[s] = run
         run += seq_len[s]
-    dev = contexts[0].q.device
+    devs = [c.q.device for c in contexts]
+    dev = devs[0]
     D = contexts[0].q.shape[1]
     K = contexts[0].k.new_empty((run, D))
     V = contexts[0].v.new_empty((run, D))
@@ -352,24 +371,31 @@ def ring_hstu_attention(group: RankGroup, contexts, params, cfg, scheduling: str
         dst = np.concatenate([np.arange(base[e.seq_id] + e.start, base[e.seq_id] + e.end, dtype=np.int64)
                               for e in c.entries])
         perm = torch.from_numpy(dst).to(dev)
-        kernels.scatter_rows(c.k, perm, K)
-        kernels.scatter_rows(c.v, perm, V)
-        kernels.scatter_rows(c.ts.view(-1, 1), perm, TS.view(-1, 1))
-    w = torch.from_numpy(np.asarray(params.ts_weights, dtype=np.float32)).to(dev)
+        kernels.scatter_rows(c.k.to(dev), perm, K)
+        kernels.scatter_rows(c.v.to(dev), perm, V)
+        kernels.scatter_rows(c.ts.view(-1, 1).to(dev), perm, TS.view(-1, 1))
+    # the gathered group K/V/ts on every device that hosts a rank (peer copies)
+    kv = {dev: (K, V, TS)}
+    for d in devs:
+        if d not in kv:
+            kv[d] = (K.to(d), V.to(d), TS.to(d))
+    w_np = np.asarray(params.ts_weights, dtype=np.float32)
 
     def attend(r: int) -> torch.Tensor:
         c = contexts[r]
+        d = devs[r]
         ents = [e for e in c.entries if e.count > 0]
         if not ents:
             return c.q.new_zeros(c.q.shape)
         qo = np.concatenate([[0], np.cumsum([e.count for e in ents])]).astype(np.int64)
-        t = lambda a: torch.from_numpy(np.asarray(a, dtype=np.int64)).to(dev)  # noqa: E731
+        t = lambda a: torch.from_numpy(np.asarray(a, dtype=np.int64)).to(d)  # noqa: E731
         kl = [e.end for e in ents]
-        return kernels.attn_fwd(c.q, K, V, c.ts, TS, t(qo), num_heads, w, cfg.num_buckets,
-                                q_pos0=t([e.start for e in ents]), kv_start=t([base[e.seq_id] for e in ents]),
-                                kv_len=t(kl), kv_len_total=int(sum(kl)))
+        Kd, Vd, TSd = kv[d]
+        return kernels.attn_fwd(c.q, Kd, Vd, c.ts, TSd, t(qo), num_heads, torch.from_numpy(w_np).to(d),
+                                cfg.num_buckets, q_pos0=t([e.start for e in ents]),
+                                kv_start=t([base[e.seq_id] for e in ents]), kv_len=t(kl), kv_len_total=int(sum(kl)))
 
-    outputs = _map_ranks(attend, cp, scheduling)
+    outputs = _map_ranks(attend, cp, scheduling, devs)
     for r, out in enumerate(outputs):
         meters[r].step(_nbytes_t(out))
         totals[r].peak_resident_bytes = max(totals[r].peak_resident_bytes, meters[r].peak)
@@ -415,10 +441,10 @@ def restore_outputs(group: RankGroup, slabs, plan: ShardPlan, max_lengths=None, 
         for b in own:
             for c in range(plan.layout.chunks_per_seq):
                 src, a, z = index[plan.chunk_owner[c]][(b, c)]
-                parts.append(received[r][src].arrays["out"][a:z])
+                parts.append(received[r][src].arrays["out"][a:z].to(slabs[r].device))
             offs.append(offs[-1] + plan.seq_lengths[b])
         d = slabs[0].shape[1]
-        vals = torch.cat(parts) if parts else slabs[0].new_zeros((0, d))
+        vals = torch.cat(parts) if parts else slabs[r].new_zeros((0, d))
         h = np.asarray(offs, dtype=np.int64)
         ml = max_lengths[r] if max_lengths is not None else max((plan.seq_lengths[b] for b in own), default=0)
         outputs.append(JaggedTensor(vals, torch.from_numpy(h).to(vals.device), int(ml), h))

@@ -116,6 +116,31 @@ def test_run_pipeline_matches_oracle(cp, mode, protocol):
         assert row_rel(got, want[r])[1] <= ROW_TOL, r
 
 
+@pytest.mark.parametrize("scheduling", ["sequential", "threaded"])
+def test_run_pipeline_multi_device(scheduling):
+    # single-process multi-device mode: rank r's batch on cuda:(r % n); on a
+    # one-GPU box every rank shares cuda:0 (the cross-device copies are no-ops)
+    from paper_2508_04711_b200.attention import BiasConfig, BiasParams
+    from paper_2508_04711_b200.cp_engine import QKVBatch, run_pipeline
+    from paper_2508_04711_b200.jagged import new_int_series, new_jagged
+    cp, H, d = 4, 2, 64
+    host, _ = _batches(cp, 77, H, d, 300)
+    n = torch.cuda.device_count()
+    batches = []
+    for r, b in enumerate(host):
+        dv = torch.device("cuda", r % n)
+        mk = lambda a: new_jagged(torch.from_numpy(a).to(dv).bfloat16(), b["offsets"], 300)  # noqa: E731
+        batches.append(QKVBatch(mk(b["q"]), mk(b["k"]), mk(b["v"]),
+                                new_int_series(torch.from_numpy(b["ts"]).to(dv), b["offsets"])))
+    w = oracle.normal_init_ts_weights(16, 5)
+    res = run_pipeline(batches, cp, "alltoall", "balanced_minichunk", BiasParams(w), BiasConfig(16),
+                       scheduling=scheduling, num_heads=H)
+    want, _ = oracle.cp_forward_sim(host, cp, "balanced_minichunk", w, 16, H)
+    for r in range(cp):
+        assert res.outputs[r].values.device == batches[r].q.values.device
+        assert row_rel(res.outputs[r].values.float().cpu().numpy(), want[r])[1] <= ROW_TOL, r
+
+
 # ------------------------------------- fp32 partial sums (CP overlap split)
 
 def test_fwd_fp32_store_then_add_equals_oracle():
