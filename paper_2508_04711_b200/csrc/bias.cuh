@@ -74,8 +74,8 @@ JH_DEV void oct_table_fill(OctEntry* t, const DevBiasTable& bt, const float* w, 
     OctEntry e;
     e.thr = bt.thr[o] > 0xFFFFFFFFll ? 0xFFFFFFFFu : static_cast<uint32_t>(bt.thr[o]);
     e.base = b;
-    e.wlo = w[b] * scale;
-    e.whi = w[b1] * scale;
+    e.wlo = w != nullptr ? w[b] * scale : 0.f;  // (w = nullptr: bucket-only lookups)
+    e.whi = w != nullptr ? w[b1] * scale : 0.f;
     t[o] = e;
   }
 }

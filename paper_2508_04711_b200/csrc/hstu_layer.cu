@@ -106,17 +106,21 @@ __global__ void __launch_bounds__(32 * kNgWarps) norm_gate_fwd_kernel(
   const int64_t warps = (int64_t)gridDim.x * kNgWarps;
   const float inv_n = 1.f / (float)n;
   for (int64_t r = blockIdx.x * (int64_t)kNgWarps + (threadIdx.x >> 5); r < rows; r += warps) {
-    float v[CH][8];
+    float v[CH][8], gt[CH][8];
     float s = 0.f;
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
+    for (int c = 0; c < CH; ++c) {  // x and the gate in flight together
       const int col = (c * 32 + lane) * 8;
       if (col < n) {
         load8(x + r * ld_x + col, v[c]);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) s += v[c][e];
+        if (u != nullptr) load8(u + r * ld_u + col, gt[c]);
       }
     }
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if ((c * 32 + lane) * 8 < n)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s += v[c][e];
     const float mu = warp_sum(s) * inv_n;
     float q = 0.f;
 #pragma unroll
@@ -135,14 +139,12 @@ __global__ void __launch_bounds__(32 * kNgWarps) norm_gate_fwd_kernel(
     for (int c = 0; c < CH; ++c) {
       const int col = (c * 32 + lane) * 8;
       if (col < n) {
-        float g[8];
-        if (u != nullptr) load8(u + r * ld_u + col, g);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           float z = (v[c][e] - mu) * rs;
           if (gamma != nullptr) z = z * __ldg(gamma + col + e);
           if (beta != nullptr) z += __ldg(beta + col + e);
-          v[c][e] = u != nullptr ? z * g[e] : z;
+          v[c][e] = u != nullptr ? z * gt[c][e] : z;
         }
         store8(y + r * ld_y + col, v[c]);
       }
@@ -247,9 +249,9 @@ __global__ void colsum_kernel(const float* __restrict__ partials, int blocks, in
   }
 }
 
-static int ng_blocks(int64_t rows) {
+static int ng_blocks(int64_t rows, int per_sm = 4) {
   const int64_t want = (rows + kNgWarps - 1) / kNgWarps;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count_layer() * 4));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count_layer() * per_sm));
 }
 
 template <int CH>
@@ -326,7 +328,7 @@ int jh_norm_gate_fwd(const void* x, int64_t ld_x, const void* u, int64_t ld_u, c
   if (int r = ng_check(rows, n, {{x, ld_x}, {u, ld_u}, {y, ld_y}})) return r;
   if (!x || !y) return set_error(JH_ERR_INVALID, "norm_gate: x / y is NULL");
   if (rows == 0) return JH_OK;
-  const int blocks = ng_blocks(rows);
+  const int blocks = ng_blocks(rows, 8);
   const int ch = (n + 255) / 256;
   cudaStream_t s = (cudaStream_t)stream;
   auto X = (const __nv_bfloat16*)x;

@@ -251,7 +251,8 @@ def test_compute_bias_and_dbias_scatter():
                             16).cpu().numpy()
     idx = oracle.bucketize_array(tq[:, None] - tk[None, :], 16)
     ref = np.bincount(idx.ravel(), weights=db.astype(np.float64).ravel(), minlength=16)
-    assert np.allclose(dw, ref, rtol=1e-9, atol=1e-9)
+    # fp32 per-thread partials for the non-last buckets, fp64 for the last and across threads
+    assert np.allclose(dw, ref, rtol=1e-6, atol=1e-6 * np.abs(ref).max())
 
 
 def test_row_moves_and_padding_are_bitwise():
