@@ -460,77 +460,19 @@ def stack_bench(dev, steps: int, flush):
             "jh_launches_per_step": (kernels.launch_count() - n0) / steps}
 
 
-def cp_sweep(dev, cap_gb: float, ks=(1, 2, 4, 8), layers: int = C4_LAYERS, budget_s: float = 150.0):
-    """Max supported single-sequence length per CP size under a fixed per-GPU
-    memory cap, MEASURED: one rank's share of one sequence of length L (its two
-    balanced mini-chunks, resident rows through the whole 8-layer stack, K/V of
-    the full sequence gathered per layer and re-gathered in the backward) runs
-    fwd+bwd on this GPU under torch.cuda.set_per_process_memory_fraction.
-    Communication is excluded (cp_layer.LoopbackComm: the peers' K/V are
-    replicas of this rank's).  The measured analogue of the reference's modeled
-    per-rank footprint (harness.py:308-374); the paper's claim is 5.3x at CP=8."""
-    import torch
-    from paper_2508_04711_b200.cp_layer import CPAttention, LoopbackComm
-    from paper_2508_04711_b200.hstu_layer import HSTUStack
-    total = torch.cuda.get_device_properties(dev).total_memory
-    torch.cuda.empty_cache()
-    torch.cuda.set_per_process_memory_fraction(min(1.0, cap_gb * 1e9 / total), dev)
-    t0 = time.time()
-    rows = []
-    gran = 2048  # multiple of 2 * cp * 128 for every cp <= 8
-
-    def runs(k, L):
-        try:
-            comm = LoopbackComm(k, 0, peer_lengths=lambda r: [])
-            cp = CPAttention(None, H, NB, comm=comm)
-            st = HSTUStack(layers, C4_E, H, D, NB, seed=SEED, cp=cp).to(dev)
-            plan = cp.plan_for([L], dev)
-            n = plan[0].n_res
-            gen = torch.Generator(device=dev).manual_seed(L)
-            x = torch.randn(n, C4_E, device=dev, generator=gen).bfloat16().requires_grad_(True)
-            ts = torch.cumsum(torch.randint(1, 10**6, (n,), device=dev, generator=gen), 0)
-            y = x
-            for layer in st.layers:
-                y = layer(y, ts, cp=(cp, plan))
-            y.float().sum().backward()
-            torch.cuda.synchronize()
-            peak = torch.cuda.max_memory_allocated(dev)
-            del st, x, y
-            ok = True
-        except torch.OutOfMemoryError:
-            ok, peak = False, None
-        except RuntimeError as e:
-            if "out of memory" not in str(e).lower():
-                raise
-            ok, peak = False, None
-        torch.cuda.empty_cache()
-        torch.cuda.reset_peak_memory_stats(dev)
-        return ok, peak
-
-    for k in ks:
-        lo, hi, peak_lo, L = 0, None, None, 8 * gran
-        while hi is None and time.time() - t0 < budget_s:
-            ok, pk = runs(k, L)
-            if ok:
-                lo, peak_lo, L = L, pk, 2 * L
-            else:
-                hi = L
-        while hi is not None and hi - lo > gran and time.time() - t0 < budget_s:
-            mid = (lo + hi) // 2 // gran * gran
-            ok, pk = runs(k, mid)
-            if ok:
-                lo, peak_lo = mid, pk
-            else:
-                hi = mid
-        rows.append({"cp_size": k, "max_supported_length": lo, "first_failure": hi,
-                     "peak_gb_at_max": None if peak_lo is None else round(peak_lo / 1e9, 2)})
-    torch.cuda.set_per_process_memory_fraction(1.0, dev)
-    base = rows[0]["max_supported_length"] if rows and rows[0]["max_supported_length"] else None
-    for r in rows:
-        r["vs_cp1"] = None if not base else round(r["max_supported_length"] / base, 2)
-    return {"cap_gb": cap_gb, "layers": layers, "embed_dim": C4_E, "heads": H, "head_dim": D, "granularity": gran,
-            "communication": "excluded (LoopbackComm: one rank's memory and kernel work)", "rows": rows,
-            "probe_s": round(time.time() - t0, 1)}
+def cp_sweep(dev, cap_gb: float):
+    """Measured max supported single-sequence length per CP size under a
+    fixed per-GPU memory cap (harness.sweep_max_tokens_measured: one rank's
+    share through the 8-layer stack, communication excluded) -- the measured
+    analogue of the reference's modeled sweep (harness.py:308-374); the
+    paper's claim is 5.3x at CP=8."""
+    from paper_2508_04711_b200.harness import sweep_max_tokens_measured
+    rep = sweep_max_tokens_measured(int(cap_gb * 1e9), (1, 2, 4, 8), embed_dim=C4_E, num_heads=H,
+                                    num_layers=C4_LAYERS, num_buckets=NB, seed=SEED, device=dev)
+    rows = [dict(r, vs_cp1=r.pop("vs_first")) for r in rep.rows]
+    return {"cap_gb": cap_gb, "layers": C4_LAYERS, "embed_dim": C4_E, "heads": H, "head_dim": D,
+            "granularity": 2048, "communication": "excluded (LoopbackComm: one rank's memory and kernel work)",
+            "rows": rows, "model": rep.model}
 
 
 def max_seq_len_probe(dev, w):

@@ -256,8 +256,13 @@ def run_experiment(cfg: ExperimentConfig, scheduling: str = "sequential", device
     a2a = redistribution_peaks(batches, cfg.cp_size, cfg.balance_mode, "alltoall")
     reduction = 1.0 - (max(a2a) / max(ag)) if max(ag) else 0.0
     torch.cuda.synchronize()
-    gpu = {"pipeline_ms": float(ev[0].elapsed_time(ev[1])), "device": torch.cuda.get_device_name(),
-           "note": "global-view pipeline on one device (simulated collectives, fused sm_100a kernels)"}
+    ms = float(ev[0].elapsed_time(ev[1]))
+    # attention work of the forward pipeline: 2 GEMMs x 2 d flops per visible (causal) pair per head
+    fwd_flops = 4.0 * (cfg.embed_dim // cfg.num_heads) * cfg.num_heads * float(result.flops.total)
+    gpu = {"pipeline_ms": ms, "device": torch.cuda.get_device_name(),
+           "attention_flops": fwd_flops, "attention_tflops": fwd_flops / max(ms, 1e-9) / 1e9,
+           "note": "global-view pipeline (simulated collectives, fused sm_100a kernels); the time includes the "
+                   "redistribution / restore row moves and the host-side plan"}
     return ExperimentReport(cfg, max_abs, max_rel, result.redistribute_stats, result.ring_stats,
                             result.restore_stats, list(result.flops.per_rank), result.flops.total,
                             result.flops.max_mean_ratio, list(result.resident_tokens),
@@ -285,12 +290,12 @@ class SweepReport:
     dtype: str
     seed: int
     rows: list
+    model: str = ("per-rank token slabs (q/k/v/ts + output) plus largest score block; "
+                  "balanced mini-chunk shard of a single sequence")
 
     def to_json_dict(self) -> dict:
         return {"budget_bytes": self.budget_bytes, "embed_dim": self.embed_dim, "dtype": self.dtype,
-                "seed": self.seed, "rows": self.rows,
-                "metadata": {"model": "per-rank token slabs (q/k/v/ts + output) plus largest score block; "
-                             "balanced mini-chunk shard of a single sequence"}}
+                "seed": self.seed, "rows": self.rows, "metadata": {"model": self.model}}
 
 
 def sweep_max_tokens(budget_bytes: int, cp_sizes, embed_dim: int = 8, dtype: str = "f32", seed: int = 0) -> SweepReport:
@@ -320,3 +325,93 @@ def sweep_max_tokens(budget_bytes: int, cp_sizes, embed_dim: int = 8, dtype: str
                 hi = mid
         rows.append({"cp_size": int(cp), "max_supported_length": int(lo)})
     return SweepReport(int(budget_bytes), embed_dim, dtype, seed, rows)
+
+
+def sweep_max_tokens_measured(budget_bytes: int, cp_sizes=(1, 2, 4, 8), embed_dim: int = 512, num_heads: int = 4,
+                              num_layers: int = 8, num_buckets: int = 16, seed: int = 7, granularity: int = 2048,
+                              time_budget_s: float = 150.0, device=None) -> SweepReport:
+    """The MEASURED counterpart of ``sweep_max_tokens`` (harness.py:369-394) on
+    the GPU: for each CP size, the longest single sequence whose per-rank share
+    -- its two balanced mini-chunks through ``num_layers`` HSTU layers, K/V of
+    the whole sequence gathered per layer and re-gathered in the backward --
+    runs forward + backward under a per-process memory cap of ``budget_bytes``
+    (torch.cuda.set_per_process_memory_fraction).  Communication is excluded
+    (cp_layer.LoopbackComm: one rank's memory and kernel work, the peers' K/V
+    replaced by replicas).  Doubling from 8 * granularity, then bisection to
+    ``granularity`` tokens (a multiple of 2 * cp * 128 for every cp <= 8).
+    Rows carry ``max_supported_length`` (the reference's key), the first
+    failing length, the peak allocated bytes at the maximum and the ratio to
+    the first CP size."""
+    import time
+
+    from .cp_layer import CPAttention, LoopbackComm
+    from .hstu_layer import HSTUStack
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if embed_dim % num_heads:
+        raise ValueError("embed_dim must be divisible by num_heads")
+    head_dim = embed_dim // num_heads
+    total = torch.cuda.get_device_properties(dev).total_memory
+    if budget_bytes <= 0 or budget_bytes > total:
+        raise ValueError(f"budget {budget_bytes} must be in (0, {total}] bytes")
+    torch.cuda.empty_cache()
+    torch.cuda.set_per_process_memory_fraction(budget_bytes / total, dev)
+    t0 = time.time()
+
+    def runs(k: int, L: int):
+        try:
+            comm = LoopbackComm(k, 0, peer_lengths=lambda r: [])
+            cp = CPAttention(None, num_heads, num_buckets, comm=comm)
+            st = HSTUStack(num_layers, embed_dim, num_heads, head_dim, num_buckets, seed=seed, cp=cp).to(dev)
+            plan = cp.plan_for([L], dev)
+            n = plan[0].n_res
+            gen = torch.Generator(device=dev).manual_seed(L)
+            x = torch.randn(n, embed_dim, device=dev, generator=gen).bfloat16().requires_grad_(True)
+            ts = torch.cumsum(torch.randint(1, 10**6, (n,), device=dev, generator=gen), 0)
+            y = x
+            for layer in st.layers:
+                y = layer(y, ts, cp=(cp, plan))
+            y.float().sum().backward()
+            torch.cuda.synchronize()
+            peak = torch.cuda.max_memory_allocated(dev)
+            del st, x, y
+            ok = True
+        except torch.OutOfMemoryError:
+            ok, peak = False, None
+        except RuntimeError as e:
+            if "out of memory" not in str(e).lower():
+                raise
+            ok, peak = False, None
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats(dev)
+        return ok, peak
+
+    rows = []
+    try:
+        for k in cp_sizes:
+            if k < 1:
+                raise ValueError("cp sizes must be >= 1")
+            lo, hi, peak_lo, L = 0, None, None, 8 * granularity
+            while hi is None and time.time() - t0 < time_budget_s:
+                ok, pk = runs(k, L)
+                if ok:
+                    lo, peak_lo, L = L, pk, 2 * L
+                else:
+                    hi = L
+            while hi is not None and hi - lo > granularity and time.time() - t0 < time_budget_s:
+                mid = (lo + hi) // 2 // granularity * granularity
+                ok, pk = runs(k, mid)
+                if ok:
+                    lo, peak_lo = mid, pk
+                else:
+                    hi = mid
+            rows.append({"cp_size": int(k), "max_supported_length": int(lo), "first_failure": hi,
+                         "peak_gb_at_max": None if peak_lo is None else round(peak_lo / 1e9, 2)})
+    finally:
+        torch.cuda.set_per_process_memory_fraction(1.0, dev)
+    base = rows[0]["max_supported_length"] if rows and rows[0]["max_supported_length"] else None
+    for r in rows:
+        r["vs_first"] = None if not base else round(r["max_supported_length"] / base, 2)
+    model = (f"measured on {torch.cuda.get_device_name(dev)}: one rank's share of one sequence through "
+             f"{num_layers} HSTU layers (E={embed_dim}, H={num_heads}), fwd+bwd under a per-process memory cap; "
+             f"communication excluded (LoopbackComm); granularity {granularity}; {round(time.time() - t0, 1)} s")
+    return SweepReport(int(budget_bytes), embed_dim, "bf16", seed, rows, model)

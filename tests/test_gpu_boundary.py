@@ -130,3 +130,44 @@ def test_run_experiment_checked_against_oracle(cp, mode, sched):
     rep = harness.run_experiment(cfg, scheduling=sched, reference=_oracle_reference)
     print(f"run_experiment cp={cp}: max_abs={rep.max_abs_error:.3e} row_rel={rep.max_rel_error:.3e}")
     assert rep.max_rel_error <= ROW_TOL
+
+
+# -------------------------------------------- reorder_balanced / inverse_reorder
+
+@pytest.mark.parametrize("lens,cp,mode", [([4], 2, "balanced_minichunk"), ([300, 0, 17, 129], 3, "balanced_minichunk"),
+                                          ([8, 5], 2, "naive_contiguous")])
+def test_reorder_balanced_and_inverse_are_bitwise(lens, cp, mode):
+    # jagged.py:232-258: rows in rank-major order (perm bit-exact with the
+    # reference's _rank_major_row_order), values moved bitwise, exact inverse
+    import oracle
+    from paper_2508_04711_b200.jagged import (inverse_reorder, make_contiguous_chunks, make_minichunks,
+                                              new_jagged, reorder_balanced)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    T = int(offs[-1])
+    vals = torch.randn(T, 64, device="cuda").bfloat16()
+    jt = new_jagged(vals, offs, max(lens))
+    layout = make_minichunks(lens, cp) if mode == "balanced_minichunk" else make_contiguous_chunks(lens, cp)
+    out, perm = reorder_balanced(jt, layout)
+    from oracle.jagged import make_contiguous_chunks as o_contig, make_minichunks as o_mini
+    olayout = o_mini(lens, cp) if mode == "balanced_minichunk" else o_contig(lens, cp)
+    want_perm, _ = oracle.rank_major_row_order(offs, olayout)
+    assert np.array_equal(perm.cpu().numpy(), np.asarray(want_perm))
+    assert torch.equal(out.values, vals[perm])
+    back = inverse_reorder(out, perm)
+    assert torch.equal(back.values, vals)
+    if lens == [4]:
+        assert perm.cpu().tolist() == [0, 3, 1, 2]  # rank 0 owns chunks (0, 3), rank 1 (1, 2)
+    with pytest.raises(ValueError, match="bijection"):
+        inverse_reorder(out, torch.zeros(T, dtype=torch.int64))
+
+
+def test_measured_sweep_small_budget():
+    # harness.sweep_max_tokens_measured: the reference's SweepReport schema, lengths
+    # non-decreasing in CP (one rank's share shrinks), a 2-layer stack under a 2 GB cap
+    from paper_2508_04711_b200.harness import sweep_max_tokens_measured
+    rep = sweep_max_tokens_measured(int(2e9), (1, 2), embed_dim=256, num_heads=2, num_layers=2,
+                                    time_budget_s=60)
+    d = rep.to_json_dict()
+    assert [r["cp_size"] for r in d["rows"]] == [1, 2]
+    a, b = (r["max_supported_length"] for r in d["rows"])
+    assert a > 0 and b >= a and "measured" in d["metadata"]["model"]
