@@ -352,6 +352,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     if (has_pos) cb += p.pos_weights[P - 1];
     cb *= c1;
     double acc_w = 0.0, acc_p = 0.0;  // saturated-chunk partials of the last buckets
+    float it_w = 0.f, it_p = 0.f;     // ... of the current item
     uint32_t hc = 0, tcnt = 0;
     const bool tr = (tid == 128 || tid == 256);
     const int trole = tid == 128 ? 2 : 3;
@@ -380,11 +381,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const Seg sg = load_seg(p.seg, it.x);
       int h0, nh;
       dkv_halves(sg, it.y, h0, nh);
-      // publish the previous item's dS blocks to the dQ kernel
+      // publish the previous item's dS blocks to the dQ kernel: the barrier orders
+      // every compute thread's scratch stores before thread 0's gpu-scope fence
+      // (cumulative) and counter increment -- one fence per item, not one per thread
+      acc_w += (double)it_w;
+      acc_p += (double)it_p;
+      it_w = it_p = 0.f;
       if (dep_item != nullptr) {
-        __threadfence();
         named_bar_sync(2, 32 * kCompWarps);
-        if (et == 0) atomicAdd(dep_item, 1);
+        if (et == 0) {
+          __threadfence();
+          atomicAdd(dep_item, 1);
+        }
       }
       dep_item = p.wl.dep + kDepBase + (int64_t)it.x * H + h;
       if (h0 >= nh) continue;
@@ -701,8 +709,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             }
           }
         }
-        acc_w += (double)sat_w;
-        acc_p += (double)sat_p;
+        it_w += sat_w;  // fp32 within an item (<= 16 halves), fp64 across items
+        it_p += sat_p;
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -713,10 +721,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (tr) trace_ev(p, trole, tcnt, 25, t);
       }
     }
+    acc_w += (double)it_w;
+    acc_p += (double)it_p;
     if (dep_item != nullptr) {
-      __threadfence();
       named_bar_sync(2, 32 * kCompWarps);
-      if (et == 0) atomicAdd(dep_item, 1);
+      if (et == 0) {
+        __threadfence();
+        atomicAdd(dep_item, 1);
+      }
     }
     // ---- d_ts_weights / d_pos: last buckets as fp64 partials, the rest from smem bins
 #pragma unroll
