@@ -336,18 +336,23 @@ DETERMINISTIC_DEFAULT = {"value": None}
 _BWD_STATE: dict = {}
 
 
+_TOTAL_MEM: dict = {}
+
+
 def ds_scratch_budget(device) -> int:
     """Bytes the auto policy lets the dS scratch take: JH_DS_SCRATCH_BUDGET, or
-    min(1/8 of the device, 1/4 of what this process may still allocate under
-    its per-process memory fraction)."""
+    1/8 of what this process may allocate under its per-process memory
+    fraction.  (Host-cheap on purpose: torch.cuda.memory_allocated builds the
+    allocator's whole statistics dict, ~150 us per call.)"""
     import os
     env = os.environ.get("JH_DS_SCRATCH_BUDGET")
     if env:
         return int(float(env))
-    total = torch.cuda.get_device_properties(device).total_memory
-    allowed = total * torch.cuda.get_per_process_memory_fraction(device)
-    avail = max(allowed - torch.cuda.memory_allocated(device), 0)
-    return int(min(total // 8, avail // 4))
+    dev = torch.device(device)
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    if key not in _TOTAL_MEM:
+        _TOTAL_MEM[key] = torch.cuda.get_device_properties(key).total_memory
+    return int(_TOTAL_MEM[key] * torch.cuda.get_per_process_memory_fraction(key) // 8)
 
 
 def ds_scratch_bytes(num_heads: int, q_offsets_host, q_pos0_host=None, kv_len_host=None) -> int:

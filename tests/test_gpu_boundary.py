@@ -171,3 +171,28 @@ def test_measured_sweep_small_budget():
     assert [r["cp_size"] for r in d["rows"]] == [1, 2]
     a, b = (r["max_supported_length"] for r in d["rows"])
     assert a > 0 and b >= a and "measured" in d["metadata"]["model"]
+
+
+@pytest.mark.parametrize("groups", [1, 3, 8])
+def test_host_streaming_fwd_bwd_matches_device_call(groups):
+    # attention.hstu_attention_fwd_bwd_host: host buffers in, host results out,
+    # sequence runs pipelined over copy / compute streams -- per-row results are
+    # the device kernels' bitwise (sequences are independent), d_w to fp64 rounding
+    from paper_2508_04711_b200 import kernels
+    from paper_2508_04711_b200.attention import hstu_attention_fwd_bwd_host
+    lens = [300, 0, 17, 129, 1, 64, 700, 5]
+    H, d = 2, 128
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    T = int(offs[-1])
+    rng = np.random.default_rng(9)
+    q, k, v, g = (torch.from_numpy(rng.standard_normal((T, H * d)).astype(np.float32)).bfloat16() for _ in range(4))
+    ts = torch.from_numpy(np.cumsum(rng.integers(1, 10**6, T)).astype(np.int64))
+    w = oracle.normal_init_ts_weights(16, 4)
+    out, dq, dk, dv, dw = hstu_attention_fwd_bwd_host(q, k, v, ts, offs, g, w, H, 16, groups=groups)
+    c = lambda x: x.cuda()  # noqa: E731
+    wd = torch.from_numpy(w.astype(np.float32)).cuda()
+    o2 = kernels.attn_fwd(c(q), c(k), c(v), c(ts), c(ts), c(torch.from_numpy(offs)), H, wd, 16)
+    q2, k2, v2, w2, _ = kernels.attn_bwd(c(q), c(k), c(v), c(ts), c(ts), c(torch.from_numpy(offs)), c(g), H, wd, 16)
+    for a, b in ((out, o2), (dq, q2), (dk, k2), (dv, v2)):
+        assert torch.equal(a, b.cpu())
+    np.testing.assert_allclose(dw.numpy(), w2.cpu().numpy(), rtol=1e-6, atol=1e-9)
