@@ -7,6 +7,8 @@ and max|d_w - ref| / max|ref| <= 1e-3 for d_ts_weights.  The oracle is fed
 the identical bf16-rounded inputs (f32 arithmetic).
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -170,3 +172,28 @@ def test_long_sequences_c3_lengths():
     assert row_rel(got, want)[1] <= ROW_TOL_LONG
     _check_bwd(case, H, _bwd(case, H), tol=ROW_TOL_LONG)
     _check_bwd(case, H, _bwd(case, H, det=True), tol=ROW_TOL_LONG)
+
+
+def test_two_tile_forward_variant_matches_oracle():
+    # attn_fwd2.cu (two q tiles per K/V load, JH_FWD2=1; the library reads the
+    # switch once per process, so the check runs in a child process)
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, oracle
+from _cases import make_case, row_rel, to_cuda
+from paper_2508_04711_b200 import kernels
+for lens, H, d in (([300, 1, 0, 129, 64, 257], 2, 128), ([700, 33], 1, 64)):
+    case = make_case(lens, H * d, seed=len(lens))
+    c = to_cuda(case)
+    out = kernels.attn_fwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], H, c["w"], 16)
+    torch.cuda.synchronize()
+    want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], case["offsets"], case["w"], 16, H)
+    err = row_rel(out.float().cpu().numpy(), want)[1]
+    assert err <= 1e-2, err
+print("ok")
+"""
+    env = dict(os.environ, JH_FWD2="1", PYTHONPATH=os.pathsep.join([os.path.dirname(__file__),
+                                                                      os.path.dirname(os.path.dirname(__file__))]))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
