@@ -71,6 +71,39 @@ def norm_gate(x, u, gamma, beta, eps: float = 1e-6):
     return _NormGateFn.apply(x, u, gamma, beta, eps)
 
 
+class _AttnGateFn(torch.autograd.Function):
+    """uvqk -> y = (LN(attention(q, k, v)) * g + b) * u as ONE autograd node: its
+    backward writes du, dq, dk, dv straight into the column slices of a single
+    d(uvqk) buffer (the kernels take any row stride), instead of four tensors
+    that autograd's split-backward concatenates (r2 C4 stack profile: 55 us of
+    copy per layer)."""
+
+    @staticmethod
+    def forward(ctx, uvqk, ts, offsets, w, gamma, beta, num_heads, num_buckets, max_len, eps):
+        n = uvqk.shape[1] // 4
+        u, v, q, k = uvqk.split(n, dim=1)
+        band = kernels.new_band_table(q.shape[0], offsets.numel() - 1, q.device)
+        a = kernels.attn_fwd(q, k, v, ts, ts, offsets, num_heads, w, num_buckets, band_table=band)
+        y, mean, rstd = kernels.norm_gate_fwd(a, u, gamma, beta, eps)
+        ctx.save_for_backward(uvqk, ts, offsets, w, gamma, beta, a, mean, rstd)
+        ctx.band, ctx.cfg = band, (num_heads, num_buckets, max_len)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        uvqk, ts, offsets, w, gamma, beta, a, mean, rstd = ctx.saved_tensors
+        H, nb, max_len = ctx.cfg
+        n = uvqk.shape[1] // 4
+        u, v, q, k = uvqk.split(n, dim=1)
+        g = torch.empty_like(uvqk)
+        gu, gv, gq, gk = g.split(n, dim=1)
+        da, _, dgam, dbet = kernels.norm_gate_bwd(dy.to(torch.bfloat16).contiguous(), a, u, gamma, beta, mean, rstd,
+                                                  du_out=gu)
+        _, _, _, dw, _ = kernels.attn_bwd(q, k, v, ts, ts, offsets, da, H, w, nb, max_kv_len=max_len,
+                                          band_table=ctx.band, out=(gq, gk, gv))
+        return g, None, None, dw.to(w.dtype), dgam, dbet, None, None, None, None
+
+
 class KernelOps:
     """The layer's row-wise ops on the sm_100a kernels (the product path; tests
     inject a CPU double the same way cp_layer takes a compute backend)."""
@@ -81,6 +114,10 @@ class KernelOps:
     @staticmethod
     def attention(q, k, v, ts, offsets, w, H, nb, max_len):
         return hstu_attention(q, k, v, ts, offsets, w, H, nb, max_len=max_len)
+
+    @staticmethod
+    def attention_gate(uvqk, ts, offsets, w, gamma, beta, H, nb, max_len, eps):
+        return _AttnGateFn.apply(uvqk, ts, offsets, w, gamma, beta, H, nb, max_len, eps)
 
 
 class HSTULayer(torch.nn.Module):
@@ -117,6 +154,10 @@ class HSTULayer(torch.nn.Module):
         dt, ops = x.dtype, self.ops
         xn = ops.norm_gate(x, None, self.in_gamma, self.in_beta, self.eps)
         uvqk = ops.silu(torch.addmm(self.b_uvqk.to(dt), xn, self.w_uvqk.to(dt)))
+        if cp is None and hasattr(ops, "attention_gate") and max_len is not None and self.head_dim in (64, 128):
+            y = ops.attention_gate(uvqk, ts, offsets, self.ts_weights, self.out_gamma, self.out_beta,
+                                   self.num_heads, self.num_buckets, max_len, self.eps)
+            return x + torch.addmm(self.b_o.to(dt), y, self.w_o.to(dt))
         u, v, q, k = uvqk.split(n, dim=1)
         if cp is None:
             a = ops.attention(q, k, v, ts, offsets, self.ts_weights, self.num_heads, self.num_buckets, max_len)

@@ -379,7 +379,7 @@ def bwd_state(q_rows: int, num_segments: int, H: int, dp: int, device) -> torch.
 def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_buckets=16, pos_weights=None,
              q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, accumulate_dkv=False, prof=None,
              max_kv_len=None, dq_accum=None, band_table=None, deterministic=None, dbg_count_buckets=False,
-             seg_host=None):
+             seg_host=None, out=None):
     """Fused jagged HSTU backward (jh_attn_bwd).
 
     Returns (dq bf16, dk, dv, d_ts_weights f64, d_pos f64 or None); dk/dv are
@@ -394,7 +394,10 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
     (q_offsets, q_pos0 or None, kv_len or None) as host arrays sizes the
     scratch exactly; without it ``max_kv_len`` (>= every segment's q and kv
     length) gives a bound, and without either the lengths are read back from
-    the device (one synchronisation)."""
+    the device (one synchronisation).  ``out`` = (dq, dk, dv) bf16 tensors shaped
+    like q (any 16-byte row stride, e.g. column views of one gradient buffer)
+    to write into instead of allocating (not with dq_accum / accumulate_dkv or
+    padded head dims)."""
     if deterministic is None:
         deterministic = DETERMINISTIC_DEFAULT["value"]
     w = ts_weights.to(device=q.device, dtype=torch.float32).contiguous()
@@ -416,6 +419,16 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
         dq = dq_accum
         dqk = _pad_heads(dq_accum, H, d, dp)
         a.dq_accum, a.ld_dq = dqk.data_ptr(), dqk.stride(0)
+    elif out is not None:
+        if dp != d or accumulate_dkv:
+            raise ValueError("out= needs head_dim 64 or 128 and no accumulate_dkv")
+        for name, t in zip(("dq", "dk", "dv"), out):
+            _require_cuda(name, t, torch.bfloat16)
+            _rowmajor(name, t)
+            if t.shape != q.shape or (t.stride(0) * 2) % 16 or t.data_ptr() % 16:
+                raise ValueError(f"{name} out must be shaped like q with 16-byte aligned rows")
+        dq = dqk = out[0]
+        a.dq, a.ld_dq = dqk.data_ptr(), dqk.stride(0)
     else:
         dq = torch.empty_like(q)
         dqk = dq if dp == d else torch.empty_like(qq)
@@ -426,7 +439,7 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
         a.dk_accum, a.dv_accum = dk.data_ptr(), dv.data_ptr()
         a.ld_dk = a.ld_dv = kk.shape[1]
     else:
-        dk, dv = torch.empty_like(kk), torch.empty_like(vv)
+        dk, dv = (out[1], out[2]) if out is not None else (torch.empty_like(kk), torch.empty_like(vv))
         a.dk, a.dv = dk.data_ptr(), dv.data_ptr()
         a.ld_dk, a.ld_dv = dk.stride(0), dv.stride(0)
     d_w = torch.zeros(num_buckets, dtype=torch.float64, device=q.device)
@@ -538,15 +551,18 @@ def norm_gate_fwd(x, u=None, gamma=None, beta=None, eps: float = 1e-6):
     return y, mean, rstd
 
 
-def norm_gate_bwd(dy, x, u, gamma, beta, mean, rstd, need_affine: bool = True):
-    """Gradients of norm_gate_fwd: (dx, du or None, dgamma or None, dbeta or None)."""
+def norm_gate_bwd(dy, x, u, gamma, beta, mean, rstd, need_affine: bool = True, du_out=None):
+    """Gradients of norm_gate_fwd: (dx, du or None, dgamma or None, dbeta or None);
+    ``du_out`` (bf16 [rows, n], any 16-byte row stride) receives du in place."""
     _require_cuda("dy", dy, torch.bfloat16)
     rows, n = x.shape
     dy = dy.contiguous()
     ldx = _ld("x", x, n)
     ldu = 0 if u is None else _ld("u", u, n)
     dx = torch.empty((rows, n), dtype=torch.bfloat16, device=x.device)
-    du = None if u is None else torch.empty((rows, n), dtype=torch.bfloat16, device=x.device)
+    du = None if u is None else (du_out if du_out is not None else
+                                 torch.empty((rows, n), dtype=torch.bfloat16, device=x.device))
+    lddu = n if du is None else _ld("du", du, n)
     g = None if gamma is None else gamma.to(device=x.device, dtype=torch.float32).contiguous()
     b = None if beta is None else beta.to(device=x.device, dtype=torch.float32).contiguous()
     dg = torch.zeros(n, dtype=torch.float32, device=x.device) if (need_affine and gamma is not None) else None
@@ -556,7 +572,7 @@ def norm_gate_bwd(dy, x, u, gamma, beta, mean, rstd, need_affine: bool = True):
         wsb = int(_lib.lib().jh_norm_gate_bwd_workspace_bytes(rows, n))
         ws = torch.empty(wsb, dtype=torch.uint8, device=x.device)
     check(_lib.lib().jh_norm_gate_bwd(_ptr(dy), n, _ptr(x), ldx, _ptr(u), ldu, _ptr(g), _ptr(b), _ptr(mean),
-                                      _ptr(rstd), rows, n, _ptr(dx), n, _ptr(du), n, _ptr(dg), _ptr(db), _ptr(ws), wsb,
-                                      _stream(x)), "norm_gate_bwd")
+                                      _ptr(rstd), rows, n, _ptr(dx), n, _ptr(du), lddu, _ptr(dg), _ptr(db), _ptr(ws),
+                                      wsb, _stream(x)), "norm_gate_bwd")
     _bump(2 if ws is not None else 1)
     return dx, du, dg, db
