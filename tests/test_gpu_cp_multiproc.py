@@ -102,3 +102,74 @@ def test_cuda_cp_layer_matches_oracle(tmp_path, world, dist_kind, B, mode, overl
         print(f"world={world} rank={r} d_w rel-to-max={err:.3e}")
         assert err <= 1e-3
         row += n
+
+
+# ------------------------------------- CP-sharded HSTU stack on the CUDA kernels
+
+def _stack_inputs(rank, lens, E):
+    rng = np.random.default_rng([41, rank])
+    T = int(sum(lens))
+    x = rng.standard_normal((T, E)).astype(np.float32)
+    ts = np.zeros(T, dtype=np.int64)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    for b, L in enumerate(lens):
+        ts[offs[b]:offs[b] + L] = int(rng.integers(0, 10**9)) + np.cumsum(rng.integers(1, 10**6, size=L))
+    gy = rng.standard_normal((T, E)).astype(np.float32)
+    return x, ts, gy
+
+
+def _stack_worker(rank, world, port, lens, out_dir):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2508_04711_b200.cp_layer import CPAttention, HostStagedComm
+    from paper_2508_04711_b200.hstu_layer import HSTUStack
+    E, Hh, dh = 256, 2, 128
+    cp = CPAttention(dist.group.WORLD, Hh, 16, comm=HostStagedComm(dist.group.WORLD))
+    st = HSTUStack(2, E, Hh, dh, 16, seed=3, cp=cp).cuda()
+    x, ts, gy = _stack_inputs(rank, lens[rank], E)
+    xt = torch.from_numpy(x).cuda().bfloat16().requires_grad_(True)
+    out = st(xt, torch.from_numpy(ts).cuda(), local_lengths=lens[rank])
+    out.backward(torch.from_numpy(gy).cuda().bfloat16())
+    st.cp_grad_sync()
+    torch.cuda.synchronize()
+    res = {"out": out.detach().float().cpu().numpy(), "dx": xt.grad.float().cpu().numpy()}
+    for name, p in st.named_parameters():
+        res["g_" + name] = p.grad.float().cpu().numpy()
+    np.savez(os.path.join(out_dir, f"s{rank}.npz"), **res)
+    dist.destroy_process_group()
+
+
+def test_cuda_cp_stack_world2_matches_single_process(tmp_path):
+    # activations CP-sharded across 2 layers, K/V exchanged per layer, the
+    # CP x DP gradient rule (cp_grad_sync): equal to the plain stack on the
+    # concatenated batch up to bf16 rounding
+    from paper_2508_04711_b200.hstu_layer import HSTUStack
+    world, E = 2, 256
+    lens = [[700, 1, 300], [129, 900]]
+    mp.spawn(_stack_worker, args=(world, _free_port(), lens, str(tmp_path)), nprocs=world, join=True)
+    parts = [_stack_inputs(r, lens[r], E) for r in range(world)]
+    x = np.concatenate([p[0] for p in parts])
+    ts = np.concatenate([p[1] for p in parts])
+    gy = np.concatenate([p[2] for p in parts])
+    flat = [L for r in lens for L in r]
+    offs = np.concatenate([[0], np.cumsum(flat)]).astype(np.int64)
+    st = HSTUStack(2, E, 2, 128, 16, seed=3).cuda()
+    xt = torch.from_numpy(x).cuda().bfloat16().requires_grad_(True)
+    out = st(xt, torch.from_numpy(ts).cuda(), torch.from_numpy(offs).cuda(), max(flat))
+    out.backward(torch.from_numpy(gy).cuda().bfloat16())
+    torch.cuda.synchronize()
+    row = 0
+    for r in range(world):
+        res = np.load(os.path.join(tmp_path, f"s{r}.npz"))
+        n = parts[r][0].shape[0]
+        e_out = row_rel(res["out"], out.detach().float().cpu().numpy()[row:row + n])[1]
+        e_dx = row_rel(res["dx"], xt.grad.float().cpu().numpy()[row:row + n])[1]
+        print(f"rank {r}: out {e_out:.2e} dx {e_dx:.2e}")
+        assert e_out <= 2e-2 and e_dx <= 2e-2
+        for name, p in st.named_parameters():
+            ref = p.grad.float().cpu().numpy()
+            e = np.abs(res["g_" + name] - ref).max() / max(np.abs(ref).max(), 1e-6)
+            assert e <= 3e-2, (r, name, e)
+        row += n
