@@ -385,12 +385,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         // band chunks of this tile (window and not entirely masked): prefetch the
         // byte rows of the two right-most ones (the diagonal-most) before any wait
         uint32_t cand = 0;
-        if (use_band && 32 * aq < sg.lq) {  // (a warp past the segment's rows has no q group)
+        // (a warp past the segment's rows has no q group; tiles whose 4 kv groups
+        // [4j, 4j+3] miss the window [bd-3, bd+1] entirely skip the per-chunk test)
+        if (use_band && 32 * aq < sg.lq && 4 * (int64_t)j + 3 >= bd - 3 && 4 * (int64_t)j <= bd + 1) {
+          const int wi0 = (int)(4 * (int64_t)j - bd + 3);
+          const int64_t lim = min(row_hi + 1, kv_lim);  // kv positions 32 b must stay below
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const int64_t b = 4 * (int64_t)j + c;
-            const int64_t wi = b - bd + 3;
-            if (wi >= 0 && wi < kBandNW && 32 * b <= row_hi && 32 * b < kv_lim) cand |= 1u << c;
+            const int wi = wi0 + c;
+            if (wi >= 0 && wi < kBandNW && 32 * (4 * (int64_t)j + c) < lim) cand |= 1u << c;
           }
         }
         const int c_hi = cand ? 31 - __clz(cand) : -1;
