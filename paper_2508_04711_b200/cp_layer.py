@@ -62,11 +62,15 @@ class CPPlan:
     kv_start: np.ndarray
     kv_len: np.ndarray
     group_rows: int
-    local_kv_start: np.ndarray   # overlap split: chunk vs itself (resident rows, q_pos0 = 0)
+    local_kv_start: np.ndarray   # overlap split: the rank's own rows (resident)
     local_kv_len: np.ndarray
-    remote_kv_len: np.ndarray    # ... and vs its sequence prefix [0, start) in the gathered rows
+    remote_kv_len: np.ndarray    # ... remote call A: [0, start of the rank's first chunk) in the gathered rows
     max_local: int = 0           # allgather_split: padded local rows per rank in the gathered batch
     split_perm: np.ndarray = None  # allgather_split: resident row -> index in the padded gathered batch
+    local_q_pos0: np.ndarray = None  # overlap split: local segment q positions (later chunk: len of chunk r)
+    remote2_kv_start: np.ndarray = None  # ... remote call B: the gap between the rank's two chunks
+    remote2_kv_len: np.ndarray = None
+    remote2_q_pos0: np.ndarray = None
 
 
 def build_cp_plan(lengths_per_rank, cp: int, rank: int, balance_mode: str = "balanced_minichunk") -> CPPlan:
@@ -101,16 +105,46 @@ def build_cp_plan(lengths_per_rank, cp: int, rank: int, balance_mode: str = "bal
             g0 = int(goff[e.seq_id])
             seq_perm[g0 + e.start:g0 + e.end] = np.arange(row, row + e.count, dtype=np.int64)
             row += e.count
-    # (4) one attention segment per resident chunk: causal prefix [0, end) of its sequence
-    qo, qp, ks, kl, lks, lkl = [0], [], [], [], [], []
+    # (4) one attention segment per resident chunk: causal prefix [0, end) of its
+    # sequence (non-overlapped form), and the overlapped split of the same work
+    # (SURVEY §8(e)): LOCAL = what the rank's own rows cover -- chunk r against
+    # itself, and chunk 2cp-1-r against [chunk r | itself], which are adjacent
+    # resident rows (positions: chunk r at 0.., the later chunk at len_r..: the
+    # causal mask is exact and the bias depends on timestamps only) -- and
+    # REMOTE = the rest of the prefix in the gathered rows: [0, start of the
+    # rank's first chunk) (call A) and, for a later chunk, the gap between the
+    # rank's two chunks (call B; its own segment, all pairs visible, relative
+    # positions exact by translation)
+    qo, qp, ks, kl, lks, lkl, lqp = [0], [], [], [], [], [], []
+    ra_len, rb_start, rb_len, rb_qp = [], [], [], []
+    prev = None  # (seq_id, resident offset, entry) of the previous non-empty entry
     for e in plan.rank_entries[rank]:
         if e.count == 0:
             continue
-        lks.append(qo[-1])
-        lkl.append(e.count)
-        qo.append(qo[-1] + e.count)
+        off = qo[-1]
+        g0 = int(goff[e.seq_id])
+        pair = prev is not None and prev[0] == e.seq_id
+        if pair:
+            _, poff, pe = prev
+            lks.append(poff)
+            lkl.append(pe.count + e.count)
+            lqp.append(pe.count)
+            ra_len.append(pe.start)
+            rb_start.append(g0 + pe.end)
+            rb_len.append(e.start - pe.end)
+            rb_qp.append(e.start - pe.end)
+        else:
+            lks.append(off)
+            lkl.append(e.count)
+            lqp.append(0)
+            ra_len.append(e.start)
+            rb_start.append(g0)
+            rb_len.append(0)
+            rb_qp.append(0)
+        prev = (e.seq_id, off, e)
+        qo.append(off + e.count)
         qp.append(e.start)
-        ks.append(int(goff[e.seq_id]))
+        ks.append(g0)
         kl.append(e.end)
     # (5) allgather_split (cp_engine.py:246-283): every rank gathers all local
     # batches (rank-major, each padded to max_local rows) and keeps its plan rows
@@ -126,8 +160,8 @@ def build_cp_plan(lengths_per_rank, cp: int, rank: int, balance_mode: str = "bal
     split_perm = np.concatenate(split_rows) if split_rows else np.zeros(0, np.int64)
     a64 = lambda x: np.asarray(x, np.int64)  # noqa: E731
     return CPPlan(cp, rank, plan, send_perm, send_counts, recv_counts, n_res, max_res, res_counts, seq_perm,
-                  a64(qo), a64(qp), a64(ks), a64(kl), int(goff[-1]), a64(lks), a64(lkl), a64(qp), max_local,
-                  split_perm)
+                  a64(qo), a64(qp), a64(ks), a64(kl), int(goff[-1]), a64(lks), a64(lkl), a64(ra_len), max_local,
+                  split_perm, a64(lqp), a64(rb_start), a64(rb_len), a64(rb_qp))
 
 
 class TorchComm:
@@ -381,12 +415,16 @@ class CPAttention:
                # (q_offsets, q_pos0, kv_start, kv_len, kv total, max kv, host (q_offsets, q_pos0, kv_len))
                "segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.kv_len), int(p.kv_len.sum()),
                         int(p.kv_len.max(initial=0)), (p.q_offsets, p.q_pos0, p.kv_len)),
-               "local_segs": (t(p.q_offsets), t(np.zeros_like(p.q_pos0)), t(p.local_kv_start),
+               "local_segs": (t(p.q_offsets), t(p.local_q_pos0), t(p.local_kv_start),
                               t(p.local_kv_len), int(p.local_kv_len.sum()), int(p.local_kv_len.max(initial=0)),
-                              (p.q_offsets, np.zeros_like(p.q_pos0), p.local_kv_len)),
+                              (p.q_offsets, p.local_q_pos0, p.local_kv_len)),
                "remote_segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.remote_kv_len),
                                int(p.remote_kv_len.sum()), int(p.remote_kv_len.max(initial=0)),
                                (p.q_offsets, p.q_pos0, p.remote_kv_len))}
+        if int(p.remote2_kv_len.sum()) > 0:  # remote call B (balanced mode: later chunks' gaps)
+            dev["remote2_segs"] = (t(p.q_offsets), t(p.remote2_q_pos0), t(p.remote2_kv_start), t(p.remote2_kv_len),
+                                   int(p.remote2_kv_len.sum()), int(p.remote2_kv_len.max(initial=0)),
+                                   (p.q_offsets, p.remote2_q_pos0, p.remote2_kv_len))
         self._plans[key] = (p, dev)
         while len(self._plans) > self.max_plans:
             self._plans.popitem(last=False)
@@ -517,6 +555,8 @@ class CPAttention:
         self.be.fwd_partial(q_r, k_r, v_r, ts_r, ts_r, dev["local_segs"], self.H, w, self.nb, acc, False)
         self._join(main, comm, (k_s, v_s, ts_s))
         self.be.fwd_partial(q_r, k_s, v_s, ts_r, ts_s, dev["remote_segs"], self.H, w, self.nb, acc, True)
+        if "remote2_segs" in dev:
+            self.be.fwd_partial(q_r, k_s, v_s, ts_r, ts_s, dev["remote2_segs"], self.H, w, self.nb, acc, True)
         return k_s, v_s, ts_s, acc.to(q_r.dtype)
 
     def _gather_kv_async(self, k_r, v_r, ts_r, p, dev, main, comm):
@@ -571,6 +611,16 @@ class CPAttention:
         self._timed("d_w_all_reduce", dw.numel() * dw.element_size(), lambda: self.comm.all_reduce(dw))
         return dq_r, dk_r, dv_r, dw
 
+    def _remote_bwd(self, q_r, k_s, v_s, ts_r, ts_s, g_r, dev, w, dq_acc):
+        """Remote calls A (and B): dK/dV partials over the gathered rows, dq added."""
+        dk_s, dv_s, dw = self.be.bwd_partial(q_r, k_s, v_s, ts_r, ts_s, dev["remote_segs"], g_r, self.H, w, self.nb,
+                                             dq_acc)
+        if "remote2_segs" in dev:
+            dk2, dv2, dw2 = self.be.bwd_partial(q_r, k_s, v_s, ts_r, ts_s, dev["remote2_segs"], g_r, self.H, w,
+                                                self.nb, dq_acc)
+            dk_s, dv_s, dw = dk_s + dk2, dv_s + dv2, dw + dw2
+        return dk_s, dv_s, dw
+
     def _backward_regather(self, q_r, k_r, v_r, ts_r, g_r, p, dev, w):
         """K/V were not kept: re-gather them on the communication stream while
         the local part (chunk vs itself) computes, then the remote part; its
@@ -583,8 +633,7 @@ class CPAttention:
         dk_l, dv_l, dw_l = self.be.bwd_partial(q_r, k_r, v_r, ts_r, ts_r, dev["local_segs"], g_r, self.H, w, self.nb,
                                                dq_acc)
         self._join(main, comm, (k_s, v_s, ts_s))
-        dk_s, dv_s, dw = self.be.bwd_partial(q_r, k_s, v_s, ts_r, ts_s, dev["remote_segs"], g_r, self.H, w, self.nb,
-                                             dq_acc)
+        dk_s, dv_s, dw = self._remote_bwd(q_r, k_s, v_s, ts_r, ts_s, g_r, dev, w, dq_acc)
         dk_red, dv_red = self._reduce_to_owner(dk_s, p, dev), self._reduce_to_owner(dv_s, p, dev)
         return dq_acc.to(q_r.dtype), (dk_red + dk_l).to(q_r.dtype), (dv_red + dv_l).to(q_r.dtype), dw + dw_l
 
@@ -593,8 +642,7 @@ class CPAttention:
         communication stream while the local (chunk vs itself) part computes."""
         acc_dt = torch.float32 if q_r.dtype in (torch.bfloat16, torch.float16) else q_r.dtype
         dq_acc = torch.zeros(q_r.shape, dtype=acc_dt, device=q_r.device)
-        dk_s, dv_s, dw = self.be.bwd_partial(q_r, k_s, v_s, ts_r, ts_s, dev["remote_segs"], g_r, self.H, w, self.nb,
-                                             dq_acc)
+        dk_s, dv_s, dw = self._remote_bwd(q_r, k_s, v_s, ts_r, ts_s, g_r, dev, w, dq_acc)
         main = torch.cuda.current_stream(q_r.device) if q_r.is_cuda else None
         comm = self.be.comm_stream(q_r.device) if hasattr(self.be, "comm_stream") else None
         if comm is not None:
