@@ -174,14 +174,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       uint32_t it_cnt = 0, tcnt = 0;
       uint32_t rk = 0;
       const uint64_t pol_once = l2_policy_evict_first();  // operands nothing re-reads
-      for (int g; (g = ring_produce(ring, rk, &p.wl.hdr->next_item[1], total)) >= 0;) {
+      for (;;) {
+        // take the next item only once the current one's K/V are released (its last
+        // S^T / dP^T issued, ~2 halves before it ends): enough lead to load the next
+        // K/V, and no CTA sits on an item it will not start for a whole item's time
+        // while others run dry at the end of the list (JH_EAGER_ITEMS: grab first)
+#ifndef JH_EAGER_ITEMS
+        mbar_wait_idle(kv_empty, (it_cnt & 1) ^ 1);
+#endif
+        const int g = ring_produce(ring, rk, &p.wl.hdr->next_item[1], total);
+        if (g < 0) break;
         const int2 it = p.wl.bwd[g / H];
         const int h = g % H;
         const Seg sg = load_seg(p.seg, it.x);
         int h0, nh;
         dkv_halves(sg, it.y, h0, nh);
         if (h0 >= nh) continue;
+#ifdef JH_EAGER_ITEMS
         mbar_wait_idle(kv_empty, (it_cnt & 1) ^ 1);  // last S^T / dP^T of the previous item done
+#endif
         trace_ev(p, 0, tcnt, 1, g);
         mbar_expect_tx(kv_full, 2 * C::TILE);
         const int32_t krow = (int32_t)(sg.kv_row0 + (int64_t)it.y * kBN);
