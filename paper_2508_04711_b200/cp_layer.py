@@ -309,11 +309,11 @@ class GpuBackend:
                                             kv_len=kl, kv_len_total=kvt, accumulate_dkv=True, seg_host=segs[6])
         return dq, dk, dv, dw
 
-    def bwd_partial(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb, dq_acc):
+    def bwd_partial(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb, dq_acc, dkv=None):
         qo, qp, ks, kl, kvt = segs[:5]
         _, dk, dv, dw, _ = self.k.attn_bwd(q, k, v, ts_q, ts_k, qo, g, H, w, nb, q_pos0=qp, kv_start=ks, kv_len=kl,
                                            kv_len_total=kvt, accumulate_dkv=True, seg_host=segs[6],
-                                           dq_accum=dq_acc)
+                                           dq_accum=dq_acc, dkv_accum=dkv)
         return dk, dv, dw
 
 
@@ -615,10 +615,10 @@ class CPAttention:
         """Remote calls A (and B): dK/dV partials over the gathered rows, dq added."""
         dk_s, dv_s, dw = self.be.bwd_partial(q_r, k_s, v_s, ts_r, ts_s, dev["remote_segs"], g_r, self.H, w, self.nb,
                                              dq_acc)
-        if "remote2_segs" in dev:
-            dk2, dv2, dw2 = self.be.bwd_partial(q_r, k_s, v_s, ts_r, ts_s, dev["remote2_segs"], g_r, self.H, w,
-                                                self.nb, dq_acc)
-            dk_s, dv_s, dw = dk_s + dk2, dv_s + dv2, dw + dw2
+        if "remote2_segs" in dev:  # call B adds into call A's group-size fp32 partials (no third buffer)
+            _, _, dw2 = self.be.bwd_partial(q_r, k_s, v_s, ts_r, ts_s, dev["remote2_segs"], g_r, self.H, w,
+                                            self.nb, dq_acc, dkv=(dk_s, dv_s))
+            dw = dw + dw2
         return dk_s, dv_s, dw
 
     def _backward_regather(self, q_r, k_r, v_r, ts_r, g_r, p, dev, w):

@@ -379,7 +379,7 @@ def bwd_state(q_rows: int, num_segments: int, H: int, dp: int, device) -> torch.
 def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_buckets=16, pos_weights=None,
              q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, accumulate_dkv=False, prof=None,
              max_kv_len=None, dq_accum=None, band_table=None, deterministic=None, dbg_count_buckets=False,
-             seg_host=None, out=None):
+             seg_host=None, out=None, dkv_accum=None):
     """Fused jagged HSTU backward (jh_attn_bwd).
 
     Returns (dq bf16, dk, dv, d_ts_weights f64, d_pos f64 or None); dk/dv are
@@ -397,7 +397,8 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
     the device (one synchronisation).  ``out`` = (dq, dk, dv) bf16 tensors shaped
     like q (any 16-byte row stride, e.g. column views of one gradient buffer)
     to write into instead of allocating (not with dq_accum / accumulate_dkv or
-    padded head dims)."""
+    padded head dims).  ``dkv_accum`` = (dk, dv) fp32 tensors shaped like k (with
+    ``accumulate_dkv``) to add the partials into instead of fresh zero buffers."""
     if deterministic is None:
         deterministic = DETERMINISTIC_DEFAULT["value"]
     w = ts_weights.to(device=q.device, dtype=torch.float32).contiguous()
@@ -433,7 +434,14 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
         dq = torch.empty_like(q)
         dqk = dq if dp == d else torch.empty_like(qq)
         a.dq, a.ld_dq = dqk.data_ptr(), dqk.stride(0)
-    if accumulate_dkv:
+    if accumulate_dkv and dkv_accum is not None:
+        dk, dv = dkv_accum
+        for name, t in (("dk", dk), ("dv", dv)):
+            if t.dtype != torch.float32 or tuple(t.shape) != tuple(kk.shape) or not t.is_contiguous():
+                raise ValueError(f"dkv_accum {name} must be a contiguous float32 tensor shaped like k")
+        a.dk_accum, a.dv_accum = dk.data_ptr(), dv.data_ptr()
+        a.ld_dk = a.ld_dv = kk.shape[1]
+    elif accumulate_dkv:
         dk = torch.zeros(kk.shape, dtype=torch.float32, device=k.device)
         dv = torch.zeros(vv.shape, dtype=torch.float32, device=v.device)
         a.dk_accum, a.dv_accum = dk.data_ptr(), dv.data_ptr()

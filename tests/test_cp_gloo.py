@@ -67,9 +67,13 @@ class NumpyBackend:
         else:
             acc.copy_(out)
 
-    def bwd_partial(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb, dq_acc):
+    def bwd_partial(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb, dq_acc, dkv=None):
         dq, dk, dv, dw = self.bwd(q, k, v, ts_q, ts_k, segs, g, H, w, nb)
         dq_acc += dq
+        if dkv is not None:
+            dkv[0].add_(dk)
+            dkv[1].add_(dv)
+            return dkv[0], dkv[1], dw
         return dk, dv, dw
 
     def bwd(self, q, k, v, ts_q, ts_k, segs, g, H, w, nb):
