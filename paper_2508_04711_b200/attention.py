@@ -387,14 +387,23 @@ def hstu_attention_fwd_bwd_host(q, k, v, ts, offsets, upstream, ts_weights, num_
     s_in.wait_stream(main)  # (the outputs / weights above were produced on the caller's stream)
     with torch.cuda.stream(s_in):
         # every run's inputs are enqueued first, so the host's launch overhead of the
-        # runs below overlaps the copies instead of delaying them
+        # runs below overlaps the copies instead of delaying them; the device inputs
+        # are allocated once and filled run by run (slice copies into one buffer run
+        # at the full PCIe rate; per-slice .to() allocations measured ~25 % slower)
+        dev_in = [torch.empty(x.shape, dtype=x.dtype, device=dev) for x in (qh, kh, vh, gh)]
+        for x in dev_in:
+            x.record_stream(main)
         for gi in range(G):
             b0, b1 = cuts[gi], cuts[gi + 1]
             r0, r1 = int(offs[b0]), int(offs[b1])
             if r1 == r0:
                 continue
             sub = offs[b0:b1 + 1] - r0
-            ins = [x[r0:r1].to(dev, non_blocking=True) for x in (qh, kh, vh, gh, tsh)]
+            ins = []
+            for dst, src in zip(dev_in, (qh, kh, vh, gh)):
+                dst[r0:r1].copy_(src[r0:r1], non_blocking=True)
+                ins.append(dst[r0:r1])
+            ins.append(tsh[r0:r1].to(dev, non_blocking=True))  # (its own buffer: 16-byte aligned)
             ins.append(torch.from_numpy(sub).pin_memory().to(dev, non_blocking=True))
             ev = torch.cuda.Event()
             ev.record(s_in)
