@@ -506,9 +506,9 @@ def max_seq_len_probe(dev, w):
     """Longest single sequence (B=1, H=4, d=128, bf16) whose fwd+bwd runs on
     this GPU (the metric's "max supported seq len" at CP=1): lengths double
     from 16K until the first out-of-memory, then a bisection to 4K granularity.
-    Each probe is a real fwd+bwd through the kernels on synthetic data (the
-    backward's auto policy takes the fused O(L)-memory kernel once the
-    two-kernel path's dS scratch would exceed its budget)."""
+    Each probe is a real fwd+bwd through the kernels on synthetic data (once
+    the whole-sequence dS scratch would exceed its budget, the backward's auto
+    policy runs kv windows with a bounded scratch, kernels._attn_bwd_windowed)."""
     import torch
     from paper_2508_04711_b200 import kernels
 
@@ -545,11 +545,13 @@ def max_seq_len_probe(dev, w):
                 lo = mid
             else:
                 hi = mid
+    kernels.release_caches()
+    torch.cuda.empty_cache()
     free, total = torch.cuda.mem_get_info(dev)
     return {"value": lo, "unit": "tokens", "cp": 1, "batch": 1, "heads": H, "head_dim": D,
             "first_failure": hi, "gpu_memory_gb": round(total / 1e9, 1), "granularity": 4096,
-            "binding_term": ("none reached: every buffer is O(L) (beyond the dS-scratch budget the backward is "
-                             "the fused kernel); probe capped at 2^21 tokens / 90 s"),
+            "binding_term": ("none reached: every buffer is O(L) plus a bounded dS scratch (beyond its "
+                             "budget the backward runs kv windows); probe capped at 2^21 tokens / 90 s"),
             "probe_s": round(time.time() - t0, 1)}
 
 

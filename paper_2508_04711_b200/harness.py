@@ -353,6 +353,8 @@ def sweep_max_tokens_measured(budget_bytes: int, cp_sizes=(1, 2, 4, 8), embed_di
     total = torch.cuda.get_device_properties(dev).total_memory
     if budget_bytes <= 0 or budget_bytes > total:
         raise ValueError(f"budget {budget_bytes} must be in (0, {total}] bytes")
+    from . import kernels
+    kernels.release_caches()
     torch.cuda.empty_cache()
     torch.cuda.set_per_process_memory_fraction(budget_bytes / total, dev)
     t0 = time.time()
@@ -381,6 +383,7 @@ def sweep_max_tokens_measured(budget_bytes: int, cp_sizes=(1, 2, 4, 8), embed_di
             if "out of memory" not in str(e).lower():
                 raise
             ok, peak = False, None
+        kernels.release_caches()
         torch.cuda.empty_cache()
         torch.cuda.reset_peak_memory_stats(dev)
         return ok, peak

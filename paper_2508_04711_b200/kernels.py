@@ -364,6 +364,12 @@ def ds_scratch_bytes(num_heads: int, q_offsets_host, q_pos0_host=None, kv_len_ho
     return int(_lib.lib().jh_attn_ds_scratch_bytes_segs(vp(qo), vp(qp), vp(kl), int(qo.size - 1), int(num_heads)))
 
 
+def release_caches() -> None:
+    """Drop the persistent per-device buffers (the fused backward's state) so a
+    memory-capped measurement starts from what it allocates itself."""
+    _BWD_STATE.clear()
+
+
 def bwd_state(q_rows: int, num_segments: int, H: int, dp: int, device) -> torch.Tensor:
     """Persistent zero-initialised state of the fused backward (one per device
     and stream; every call leaves it zero again)."""
@@ -476,7 +482,21 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
                     max_kv_len = max(ql, int(kv_len.max().item())) if kv_len is not None else ql
             ds_bytes = int(_lib.lib().jh_attn_ds_scratch_bytes(kvt, a.num_segments, H, int(max_kv_len)))
         if deterministic is None:
-            deterministic = ds_bytes <= ds_scratch_budget(q.device)
+            budget = ds_scratch_budget(q.device)
+            deterministic = ds_bytes <= budget
+            plain = (q_pos0 is None and kv_start is None and kv_len is None and dq_accum is None
+                     and not accumulate_dkv and pw is None and dp == d and WINDOWED_BWD["enabled"])
+            if not deterministic and plain:
+                qo_host = (np.asarray(seg_host[0], dtype=np.int64) if seg_host is not None
+                           else q_offsets.cpu().numpy().astype(np.int64))
+                if seg_host is None:  # the bound was loose: size the scratch exactly
+                    ds_bytes = ds_scratch_bytes(H, qo_host)
+                    deterministic = ds_bytes <= budget
+                if not deterministic:
+                    win = _windowed_plan(qo_host, H, budget, q.device, 4 * q.numel())
+                    if win is not None:
+                        return _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, qo_host, win,
+                                                  out, prof)
     a.deterministic = int(bool(deterministic))
     a.dbg_count_buckets = int(bool(dbg_count_buckets))
     if deterministic:
@@ -499,6 +519,91 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
             dq.copy_(_unpad_heads(dqk, H, d, dp))
         dk, dv = _unpad_heads(dk, H, d, dp), _unpad_heads(dv, H, d, dp)
     return dq, dk, dv, d_w, d_pos
+
+
+# Long-sequence backward when the whole-sequence dS scratch exceeds the budget:
+# the two-kernel path over kv WINDOWS of width W (multiple of 128).  Call w
+# covers kv rows [wW, (w+1)W) of every sequence against the q rows [wW, L) that
+# see them, split into chunks of WINDOW_Q_CHUNK rows so the dK/dV kernel has
+# enough items: segment-form calls (q_pos0 / kv_start / kv_len, the mode of the
+# CP remote calls) over a compact copy of the window's K / V / timestamps, dq
+# accumulated in fp32 across calls, dK / dV complete within their call (every q
+# row that sees a window is in that call) and scattered back as bf16.  Extra
+# memory: dq in fp32 (as the fused kernel's state) + the window's scratch
+# (~2 H W sum(L) bytes, within the budget) + O(W B) for the window copies.  The
+# tiles run at the two-kernel rate (~750 TF/s at long L vs ~520 for the fused
+# kernel, profiles/r2_ncu_summary.md).
+WINDOWED_BWD = {"enabled": True}
+WINDOW_Q_CHUNK = 16384
+
+
+def _windowed_plan(qo_host, H: int, budget: int, device, dq_bytes: int = 0):
+    """Window width W for _attn_bwd_windowed, or None (no width >= 128 fits)."""
+    lens = np.diff(qo_host)
+    total = int(lens.sum())
+    if total == 0:
+        return None
+    # headroom: at most a quarter of what the process may still allocate (this
+    # branch runs only for long sequences, where the allocator query is cheap
+    # next to the backward itself)
+    dev = torch.device(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    cap = _TOTAL_MEM.get(idx) or torch.cuda.get_device_properties(idx).total_memory
+    avail = cap * torch.cuda.get_per_process_memory_fraction(idx) - torch.cuda.memory_allocated(idx)
+    budget = min(budget, int(avail - dq_bytes) // 4)
+    # scratch of one call <= (rows + 64 per segment) * W * H * 2 bytes (64 x 128 bf16 blocks)
+    nseg_bound = int(sum((int(L) + WINDOW_Q_CHUNK - 1) // WINDOW_Q_CHUNK + 1 for L in lens))
+    W = budget // (2 * H * (total + 64 * nseg_bound)) // 128 * 128
+    W = min(W, 1 << 16)
+    return W if W >= 128 else None
+
+
+def _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, qo_host, W, out, prof):
+    dev = q.device
+    lens = np.diff(qo_host)
+    dq32 = torch.zeros(q.shape, dtype=torch.float32, device=dev)
+    if out is not None:
+        dk, dv = out[1], out[2]
+    else:
+        dk, dv = torch.empty_like(k), torch.empty_like(v)
+    d_w = torch.zeros(num_buckets, dtype=torch.float64, device=dev)
+    nwin = int((int(lens.max()) + W - 1) // W)
+    for wi in range(nwin):
+        w0 = wi * W
+        qo, qp, ks, kl, rows = [0], [], [], [], []
+        c = 0  # compact row of this sequence's window
+        for s, L in enumerate(lens):
+            base, L = int(qo_host[s]), int(L)
+            if L <= w0:  # no q row of this sequence sees the window: one empty segment
+                qo.append(base + L); qp.append(0); ks.append(0); kl.append(0)
+                continue
+            if w0 > 0:  # rows before the window: empty segment
+                qo.append(base + w0); qp.append(0); ks.append(0); kl.append(0)
+            wl = min(W, L - w0)
+            for c0 in range(w0, L, WINDOW_Q_CHUNK):
+                qo.append(base + min(L, c0 + WINDOW_Q_CHUNK)); qp.append(c0 - w0); ks.append(c); kl.append(wl)
+            rows.append(np.arange(base + w0, base + w0 + wl, dtype=np.int64))
+            c += wl
+        qo_a, qp_a, kl_a = (np.asarray(x, dtype=np.int64) for x in (qo, qp, kl))
+        n = qp_a.size
+        t = torch.from_numpy(np.concatenate([qo_a, qp_a, np.asarray(ks, dtype=np.int64), kl_a]
+                                            + rows)).to(dev)
+        idx = t[4 * n + 1:]
+        k_w, v_w, ts_w = k.index_select(0, idx), v.index_select(0, idx), ts_k.index_select(0, idx)
+        dk_w = torch.zeros(k_w.shape, dtype=torch.float32, device=dev)
+        dv_w = torch.zeros(v_w.shape, dtype=torch.float32, device=dev)
+        _, _, _, dwi, _ = attn_bwd(q, k_w, v_w, ts_q, ts_w, t[:n + 1], dout, H, w, num_buckets,
+                                   q_pos0=t[n + 1:2 * n + 1], kv_start=t[2 * n + 1:3 * n + 1],
+                                   kv_len=t[3 * n + 1:4 * n + 1], kv_len_total=c, accumulate_dkv=True,
+                                   dkv_accum=(dk_w, dv_w), dq_accum=dq32, deterministic=True,
+                                   seg_host=(qo_a, qp_a, kl_a), prof=prof)
+        dk.index_copy_(0, idx, dk_w.to(dk.dtype))
+        dv.index_copy_(0, idx, dv_w.to(dv.dtype))
+        d_w += dwi
+    if out is not None:
+        out[0].copy_(dq32)
+        return out[0], dk, dv, d_w, None
+    return dq32.to(torch.bfloat16), dk, dv, d_w, None
 
 
 def debug_umma(a: torch.Tensor, b: torch.Tensor, a_mode: int, b_mode: int) -> torch.Tensor:

@@ -1,6 +1,8 @@
 """Long-sequence backward: the fused one-kernel path (O(L) memory) against the
-two-kernel path (bf16 dS scratch) where the scratch still fits.  Prints time,
-TF/s and the scratch each would need.  --once: one fused call (ncu capture)."""
+two-kernel path (bf16 dS scratch) where the scratch still fits, and the
+windowed two-kernel path (auto mode: JH_WIN_BUDGET bytes of dS scratch, default the
+kernels.ds_scratch_budget, 1/8 of the GPU).  Prints time, TF/s and the extra peak memory of each.
+--once: one fused call (ncu capture)."""
 import os
 import sys
 
@@ -31,15 +33,29 @@ if "--once" in sys.argv:
         kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, 16, deterministic=False)
     torch.cuda.synchronize()
     sys.exit(0)
-for L, B in ((4096, 16), (16384, 4), (65536, 1)):
+win_budget = os.environ.get("JH_WIN_BUDGET")
+if os.environ.get("JH_WIN_CHUNK"):
+    kernels.WINDOW_Q_CHUNK = int(os.environ["JH_WIN_CHUNK"])
+only = os.environ.get("JH_ONLY")  # e.g. "windowed"
+sizes = ((4096, 16), (16384, 4), (65536, 1), (262144, 1), (1 << 20, 1))
+if len(sys.argv) > 1 and sys.argv[1].isdigit():
+    sizes = sizes[:int(sys.argv[1])]
+if len(sys.argv) > 2 and sys.argv[2].isdigit():
+    sizes = sizes[int(sys.argv[2]):]
+for L, B in sizes:
     q, k, v, g, ts, offs, offs_h = case(L, B)
     F = 5.0 * D * H * B * L * (L + 1)
     scratch = kernels.ds_scratch_bytes(H, offs_h)
     res = []
-    for det in (False, True):
+    reps = 3 if L <= 65536 else 1
+    for name, det in (("fused", False), ("two-kernel", True), ("windowed", None)):
+        if only and name not in only.split(","):
+            continue
         if det and scratch > 24e9:
             res.append(f"two-kernel: scratch {scratch / 1e9:.1f} GB (skipped)")
             continue
+        if det is None and win_budget:
+            os.environ["JH_DS_SCRATCH_BUDGET"] = win_budget
         fn = lambda: kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, 16, deterministic=det,  # noqa: E731
                                       seg_host=(offs_h, None, None))
         fn()
@@ -48,12 +64,12 @@ for L, B in ((4096, 16), (16384, 4), (65536, 1)):
         base = torch.cuda.memory_allocated()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(3):
+        for _ in range(reps):
             fn()
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / 3
+        os.environ.pop("JH_DS_SCRATCH_BUDGET", None)
+        ms = e0.elapsed_time(e1) / reps
         peak = (torch.cuda.max_memory_allocated() - base) / 1e9
-        res.append(f"{'two-kernel' if det else 'fused'}: {ms * 1e3:.0f} us {F / ms / 1e9:.0f} TF/s "
-                   f"(extra peak {peak:.2f} GB)")
+        res.append(f"{name}: {ms * 1e3:.0f} us {F / ms / 1e9:.0f} TF/s (extra peak {peak:.2f} GB)")
     print(f"L={L} B={B}: " + " | ".join(res), flush=True)

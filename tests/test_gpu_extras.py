@@ -305,3 +305,43 @@ def test_bwd_remote_segment_long_q_both_paths(split):
         assert np.isfinite(a).all() and np.isfinite(b).all(), name
         assert row_rel(a, b)[1] <= 5e-3, name
     assert np.abs(res[True][3] - res[False][3]).max() / np.abs(res[False][3]).max() <= DW_TOL
+
+
+# ------------------------------------ windowed two-kernel backward (long L)
+
+_WIN_ORACLE: dict = {}
+
+
+@pytest.mark.parametrize("chunk", [16384, 1024])
+def test_bwd_windowed_matches_full(monkeypatch, chunk):
+    # a dS budget far below the whole-sequence scratch: auto mode runs the
+    # two-kernel path over kv windows (segment-form calls accumulating in fp32)
+    lens, H = [3000, 1, 700, 5000, 129], 2
+    case = make_case(lens, H * 128, seed=11)
+    c = to_cuda(case)
+    from paper_2508_04711_b200 import kernels
+    offs_h = np.asarray(case["offsets"], dtype=np.int64)
+    full = kernels.attn_bwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], c["g"], H, c["w"], 16,
+                            deterministic=True, seg_host=(offs_h, None, None))
+    calls = []
+    orig = kernels._attn_bwd_windowed
+    monkeypatch.setattr(kernels, "_attn_bwd_windowed", lambda *a: calls.append(a[-3]) or orig(*a))
+    monkeypatch.setattr(kernels, "WINDOW_Q_CHUNK", chunk)
+    monkeypatch.setenv("JH_DS_SCRATCH_BUDGET", str(16 << 20))
+    win = kernels.attn_bwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], c["g"], H, c["w"], 16,
+                           seg_host=(offs_h, None, None))
+    torch.cuda.synchronize()
+    assert calls and 128 <= calls[0] < max(lens), calls
+    if "want" not in _WIN_ORACLE:  # ~8 s of numpy: shared by both parametrisations
+        _WIN_ORACLE["want"] = oracle.hstu_backward(case["q"], case["k"], case["v"], case["ts"], case["offsets"],
+                                                   case["g"], case["w"], 16, H)
+    want = _WIN_ORACLE["want"]
+    for name, a, b, o in zip(("dq", "dk", "dv"), win[:3], full[:3], want[:3]):
+        a, b = a.float().cpu().numpy(), b.float().cpu().numpy()
+        assert np.isfinite(a).all(), name
+        e_full, e_win, e_ab = row_rel(b, o)[1], row_rel(a, o)[1], row_rel(a, b)[1]
+        print(f"windowed W={calls[0]} chunk={chunk} {name}: row err vs oracle {e_win:.2e} "
+              f"(full two-kernel {e_full:.2e}), vs full {e_ab:.2e}")
+        assert e_win <= ROW_TOL and e_ab <= 1e-2, name
+    a, b = win[3].cpu().numpy(), want[3]
+    assert np.abs(a - b).max() / np.abs(b).max() <= DW_TOL
