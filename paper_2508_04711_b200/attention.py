@@ -333,6 +333,18 @@ def _as_pinned(x, dtype):
 _STREAMS: dict = {}
 
 
+def _stream_cuts(offs: np.ndarray, G: int) -> list:
+    """Sequence-boundary cut points of G runs with ~T/G tokens each (unequal
+    first / last runs were measured: no gain, the PCIe rates bind)."""
+    B, T = offs.size - 1, int(offs[-1])
+    cuts = [0]
+    for gi in range(1, G):
+        b = int(np.searchsorted(offs, gi * T / G))
+        cuts.append(min(max(b, cuts[-1] + 1), B - (G - gi)))
+    cuts.append(B)
+    return cuts
+
+
 def hstu_attention_fwd_bwd_host(q, k, v, ts, offsets, upstream, ts_weights, num_heads: int = 1,
                                 num_buckets: int = 16, groups: int = 4, device=None, out=None):
     """Forward + backward of attention.py:125-148 / 187-234 for inputs that live in
@@ -347,7 +359,7 @@ def hstu_attention_fwd_bwd_host(q, k, v, ts, offsets, upstream, ts_weights, num_
     back on a second copy stream while later runs still copy in, so the two
     PCIe directions overlap each other and the kernels (C2 on one B200: 2.46
     ms vs 2.82 ms for copy-in / compute / copy-out in sequence; PCIe 5 x16,
-    ~35 GB/s per direction while both run).  q, k, v, upstream: (T, H*d) host arrays / tensors (bf16, or anything
+    ~42 GB/s per direction while both run, 55 alone).  q, k, v, upstream: (T, H*d) host arrays / tensors (bf16, or anything
     castable; pinned tensors are used in place); ts: (T,) int64; offsets:
     (B+1,) int64 host.  ``out`` = four pinned bf16 host tensors shaped like q to
     write (out, dq, dk, dv) into (reused across calls; otherwise allocated)."""
@@ -363,22 +375,15 @@ def hstu_attention_fwd_bwd_host(q, k, v, ts, offsets, upstream, ts_weights, num_
             raise ValueError(f"{name} must be (T, H*d) with T = offsets[-1] = {T} rows like q")
     if tsh.shape != (T,):
         raise ValueError("ts must have one timestamp per row")
-    w = torch.as_tensor(np.asarray(ts_weights, dtype=np.float32)).to(dev)
     B = offs.size - 1
     G = max(1, min(int(groups), B))
-    # cut points on sequence boundaries with ~T/G tokens each
-    cuts = [0]
-    for gi in range(1, G):
-        b = int(np.searchsorted(offs, gi * T / G))
-        cuts.append(min(max(b, cuts[-1] + 1), B - (G - gi)))
-    cuts.append(B)
+    cuts = _stream_cuts(offs, G)
     if out is not None:
         outs = list(out)
         if len(outs) != 4 or any(o.shape != qh.shape or o.dtype != torch.bfloat16 or not o.is_pinned() for o in outs):
             raise ValueError("out must be four pinned bf16 host tensors shaped like q")
     else:
         outs = [torch.empty(qh.shape, dtype=torch.bfloat16, pin_memory=True) for _ in range(4)]
-    d_w = torch.zeros(num_buckets, dtype=torch.float64, device=dev)
     if dev not in _STREAMS:
         _STREAMS[dev] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
     s_in, s_out = _STREAMS[dev]
@@ -408,6 +413,9 @@ def hstu_attention_fwd_bwd_host(q, k, v, ts, offsets, upstream, ts_weights, num_
             ev = torch.cuda.Event()
             ev.record(s_in)
             runs.append((b0, b1, r0, r1, sub, ins, ev))
+    # (after the copies are queued: nothing on the host delays the first one)
+    w = torch.as_tensor(np.asarray(ts_weights, dtype=np.float32)).pin_memory().to(dev, non_blocking=True)
+    d_w = torch.zeros(num_buckets, dtype=torch.float64, device=dev)
     keep = []
     for b0, b1, r0, r1, sub, ins, ev in runs:
         main.wait_event(ev)
