@@ -232,6 +232,19 @@ JH_API int jh_padded_to_jagged(const void* padded, const int64_t* offsets, int64
  *              of jh_norm_gate_bwd_workspace_bytes) and writes dx, du. */
 JH_API int jh_silu_fwd(const void* x, void* y, int64_t n, void* stream);
 JH_API int jh_silu_bwd(const void* x, const void* dy, void* dx, int64_t n, void* stream);
+/* SiLU backward fused with the bias gradient of the GEMM that produced x:
+ * dx = silu'(x) * dy over a contiguous [rows, n] matrix and dbias[n] (fp32) +=
+ * column sums of dx (as rounded to bf16).  Deterministic (per-block partial
+ * rows in `workspace`, >= jh_colsum_workspace_bytes(rows, n), added in block
+ * order).  n: multiple of 8 in [8, 8192].  Replaces autograd's separate
+ * reduction for the bias of uvqk = SiLU(x W + b) (layer, not in the reference). */
+JH_API int jh_silu_bwd_colsum(const void* x, const void* dy, void* dx, int64_t rows, int32_t n, float* dbias,
+                              void* workspace, size_t workspace_bytes, void* stream);
+/* out[n] (fp32) += column sums of x ([rows, n] bf16, row stride ld elements):
+ * the bias gradient of out = y W + b.  Deterministic, as above. */
+JH_API int jh_colsum(const void* x, int64_t ld, int64_t rows, int32_t n, float* out, void* workspace,
+                     size_t workspace_bytes, void* stream);
+JH_API size_t jh_colsum_workspace_bytes(int64_t rows, int32_t n);
 JH_API int jh_norm_gate_fwd(const void* x, int64_t ld_x, const void* u, int64_t ld_u, const float* gamma,
                             const float* beta, float eps, int64_t rows, int32_t n, void* y, int64_t ld_y, float* mean,
                             float* rstd, void* stream);

@@ -69,6 +69,11 @@ SIGNATURES = {
     "jh_attn_bwd_state_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]),
     "jh_silu_fwd": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, c_vp]),
     "jh_silu_bwd": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int64, c_vp]),
+    "jh_silu_bwd_colsum": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int64, ctypes.c_int32, c_vp, c_vp,
+                                          ctypes.c_size_t, c_vp]),
+    "jh_colsum": (ctypes.c_int, [c_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, c_vp, c_vp, ctypes.c_size_t,
+                                 c_vp]),
+    "jh_colsum_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32]),
     "jh_norm_gate_fwd": (ctypes.c_int, [c_vp, ctypes.c_int64, c_vp, ctypes.c_int64, c_vp, c_vp, ctypes.c_float,
                                         ctypes.c_int64, ctypes.c_int32, c_vp, ctypes.c_int64, c_vp, c_vp, c_vp]),
     "jh_norm_gate_bwd_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32]),

@@ -160,7 +160,10 @@ JH_DEV T block_exclusive_scan(T v, T* warp_sum, T* total) {
 
 // One block of 1024 threads.  fwd items (s, q_tile) ordered by #kv tiles
 // descending; bwd items (s, kv_tile) ordered by #q tiles descending (counting
-// sort over a 1024-level histogram).  q tiles that see no kv at all (a
+// sort over a 1024-level histogram).  A group of G lanes (G = the largest power
+// of two <= 32 with num_segments * G <= 1024) shares a segment and strides over
+// its tiles, so a few long sequences do not serialise on one thread each (C4:
+// 64 q tiles + 64 kv tiles per sequence, 42 us with one thread per segment).  q tiles that see no kv at all (a
 // segment with kv_len 0) are not items: a run of such items could otherwise
 // stall the persistent kernels' 2-deep item ring (their output rows are zeroed
 // by the host in the segment form, the only form where they occur).  The segment each thread owns first is
@@ -179,26 +182,30 @@ static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, 
   const int tid = threadIdx.x;
   hist_f[tid] = 0;
   hist_b[tid] = 0;
-  const bool own = tid < sa.num_segments;
+  int G = 1;
+  while (G < 32 && sa.num_segments * (int64_t)(2 * G) <= (int64_t)blockDim.x) G <<= 1;
+  const int sub = tid & (G - 1);
+  const int64_t s0 = tid / G, sstride = blockDim.x / G;
+  const bool own = s0 < sa.num_segments;
   Seg g0{};
-  if (own) g0 = load_seg(sa, tid);
+  if (own) g0 = load_seg(sa, s0);
   __syncthreads();
-  auto seg = [&](int64_t s) { return s == tid ? g0 : load_seg(sa, s); };
+  auto seg = [&](int64_t s) { return s == s0 ? g0 : load_seg(sa, s); };
   auto bwd_w = [](const Seg& g, int j) {
     int64_t first = (int64_t)j * kBN - g.qp0;
     first = first < 0 ? 0 : first;
     return (int)((g.lq - first + kBM - 1) / kBM);
   };
   const int fstep = wl.fwd_pairs ? 2 : 1;
-  for (int64_t s = tid; s < sa.num_segments; s += blockDim.x) {
+  for (int64_t s = s0; s < sa.num_segments; s += sstride) {
     const Seg g = seg(s);
     const int nt = (int)((g.lq + kBM - 1) / kBM);
-    for (int t = 0; t < nt; t += fstep) {
+    for (int t = sub * fstep; t < nt; t += G * fstep) {
       const int w = (int)((fwd_kv_lim(g, min(t + fstep - 1, nt - 1)) + kBN - 1) / kBN);
       if (w > 0) atomicAdd(&hist_f[min(w, kLevels - 1)], 1);  // (tiles that see no kv are not items)
     }
     const int nj = (int)((seg_kv_vis(g) + kBN - 1) / kBN);
-    for (int j = 0; j < nj; ++j) atomicAdd(&hist_b[min(bwd_w(g, j), kLevels - 1)], 1);
+    for (int j = sub; j < nj; j += G) atomicAdd(&hist_b[min(bwd_w(g, j), kLevels - 1)], 1);
   }
   __syncthreads();
   // descending starts: level L starts after all items of levels > L
@@ -217,15 +224,15 @@ static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, 
     }
   }
   __syncthreads();
-  for (int64_t s = tid; s < sa.num_segments; s += blockDim.x) {
+  for (int64_t s = s0; s < sa.num_segments; s += sstride) {
     const Seg g = seg(s);
     const int nt = (int)((g.lq + kBM - 1) / kBM);
-    for (int t = 0; t < nt; t += fstep) {
+    for (int t = sub * fstep; t < nt; t += G * fstep) {
       const int w = (int)((fwd_kv_lim(g, min(t + fstep - 1, nt - 1)) + kBN - 1) / kBN);
       if (w > 0) wl.fwd[atomicAdd(&hist_f[min(w, kLevels - 1)], 1)] = make_int2((int)s, t / fstep);
     }
     const int nj = (int)((seg_kv_vis(g) + kBN - 1) / kBN);
-    for (int j = 0; j < nj; ++j) wl.bwd[atomicAdd(&hist_b[min(bwd_w(g, j), kLevels - 1)], 1)] = make_int2((int)s, j);
+    for (int j = sub; j < nj; j += G) wl.bwd[atomicAdd(&hist_b[min(bwd_w(g, j), kLevels - 1)], 1)] = make_int2((int)s, j);
   }
   // dS scratch: exclusive scan of the per-segment block counts (chunks of 1024)
   if (wl.ds_base != nullptr) {
@@ -234,7 +241,7 @@ static __global__ void __launch_bounds__(1024, 1) build_work_kernel(SegArgs sa, 
       const int64_t s = base + tid;
       long long v = 0;
       if (s < sa.num_segments) {
-        const Seg g = seg(s);
+        const Seg g = load_seg(sa, s);
         v = (long long)ds_cnt(g);
       }
       long long tot;

@@ -65,7 +65,7 @@ JH_DEV float warp_sum(float v) {
   return v;
 }
 
-JH_DEV float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
+JH_DEV float sigmoidf_(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }  // (0 for x < -87)
 
 }  // namespace
 
@@ -93,6 +93,102 @@ __global__ void silu_bwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_
       g[e] *= s * (1.f + f[e] * (1.f - s));
     }
     store8(dx + 8 * i, g);
+  }
+}
+
+// SiLU backward fused with the bias gradient of the GEMM that produced x
+// (uvqk = SiLU(xn W1 + b1): db1 = column sums of dx), and the plain column sum
+// (db2 = column sums of d out).  A [rows, n] row-major matrix, n = 8 V: thread
+// t of a 256-thread block owns the 16-byte column vectors c = t mod V + 256 k
+// (VPT = ceil(V / 256) of them) of rows t / V, t / V + R, ... (R = 256 / V
+// rows per block step when V < 256), keeps 8 VPT fp32 sums in registers, and
+// the R threads of one column fold theirs in fixed order through shared
+// memory into one [n] fp32 partial row per block; colsum_kernel adds the
+// partial rows in block order.  Deterministic; one pass over the matrix.
+template <int VPT, bool SILU>
+__global__ void __launch_bounds__(256) silu_colsum_kernel(const __nv_bfloat16* __restrict__ x,
+                                                          const __nv_bfloat16* __restrict__ dy, int64_t ld,
+                                                          __nv_bfloat16* __restrict__ dx, int64_t rows, int n,
+                                                          float* __restrict__ partials) {
+  extern __shared__ float s_red[];  // [R][n] when R > 1
+  const int V = n / 8;
+  const int R = V >= 256 ? 1 : 256 / V;
+  const int t = threadIdx.x;
+  const int cv = V >= 256 ? t : t % V;
+  const int roff = V >= 256 ? 0 : t / V;
+  const bool active = roff < R;
+  float acc[VPT][8];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[k][e] = 0.f;
+  // U rows per trip with every load issued before any use
+  constexpr int U = VPT >= 2 ? 1 : 2;
+  if (active) {
+    const int64_t step = (int64_t)gridDim.x * R;
+    for (int64_t r0 = (int64_t)blockIdx.x * R + roff; r0 < rows; r0 += step * U) {
+      uint4 gv[U][VPT], xv[U][VPT];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+          const int64_t r = r0 + u * step;
+          const int c = cv + 256 * k;
+          if (r < rows && c < V) {
+            gv[u][k] = __ldg(reinterpret_cast<const uint4*>(dy + r * ld + 8 * c));
+            if constexpr (SILU) xv[u][k] = __ldg(reinterpret_cast<const uint4*>(x + r * ld + 8 * c));
+          }
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+          const int64_t r = r0 + u * step;
+          const int c = cv + 256 * k;
+          if (r >= rows || c >= V) continue;
+          float g[8];
+          load8(reinterpret_cast<const __nv_bfloat16*>(&gv[u][k]), g);
+          if constexpr (SILU) {
+            float f[8];
+            load8(reinterpret_cast<const __nv_bfloat16*>(&xv[u][k]), f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float sg = sigmoidf_(f[e]);
+              g[e] *= sg * (1.f + f[e] * (1.f - sg));
+            }
+            uint4 p;
+            p.x = pack_bf16(g[0], g[1]);
+            p.y = pack_bf16(g[2], g[3]);
+            p.z = pack_bf16(g[4], g[5]);
+            p.w = pack_bf16(g[6], g[7]);
+            *reinterpret_cast<uint4*>(dx + r * ld + 8 * c) = p;
+            // the bias gradient sums what the GEMM backward sees: dx as rounded to bf16
+            load8(reinterpret_cast<const __nv_bfloat16*>(&p), g);
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[k][e] += g[e];
+        }
+    }
+  }
+  float* dst = partials + (size_t)blockIdx.x * n;
+  if (R == 1) {
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int c = cv + 256 * k;
+      if (c < V)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dst[8 * c + e] = acc[k][e];
+    }
+    return;
+  }
+  if (active)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s_red[roff * n + 8 * cv + e] = acc[0][e];
+  __syncthreads();
+  for (int i = t; i < n; i += blockDim.x) {
+    float v = 0.f;
+    for (int q = 0; q < R; ++q) v += s_red[q * n + i];
+    dst[i] = v;
   }
 }
 
@@ -262,23 +358,25 @@ __global__ void __launch_bounds__(32 * kNgWarps) norm_gate_bwd_kernel(
 }
 
 // Column sums of the per-block partials [blocks][2n]: a block takes 32 columns,
-// its 8 warps stride over the partial rows (coalesced 128-byte rows), and the
-// 8 per-warp sums are added in warp order -- deterministic, and 8x the
-// parallelism of one thread per column (r2: 27 us per call with 592 blocks).
-__global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ partials, int blocks, int n,
-                                                     float* __restrict__ dgamma, float* __restrict__ dbeta) {
-  __shared__ float red[8][32];
+// its 32 warps stride over the partial rows (coalesced 128-byte rows), and the
+// 32 per-warp sums are added in warp order -- deterministic (r2: 27 us per
+// call with one thread per column, 11.6 us with 8 warps, C4 stack profile).
+constexpr int kColsumWarps = 32;
+__global__ void __launch_bounds__(32 * kColsumWarps) colsum_kernel(const float* __restrict__ partials, int blocks,
+                                                                   int n, float* __restrict__ dgamma,
+                                                                   float* __restrict__ dbeta) {
+  __shared__ float red[kColsumWarps][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + lane;
   float s = 0.f;
   if (i < 2 * n)
-    for (int b = w; b < blocks; b += 8) s += partials[(size_t)b * 2 * n + i];
+    for (int b = w; b < blocks; b += kColsumWarps) s += partials[(size_t)b * 2 * n + i];
   red[w][lane] = s;
   __syncthreads();
   if (w == 0 && i < 2 * n) {
     float t = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t += red[k][lane];
+    for (int k = 0; k < kColsumWarps; ++k) t += red[k][lane];
     if (i < n) {
       if (dgamma) dgamma[i] += t;
     } else if (dbeta) {
@@ -343,6 +441,56 @@ int jh_silu_bwd(const void* x, const void* dy, void* dx, int64_t n, void* stream
                                                             (__nv_bfloat16*)dx, n8);
   cudaError_t e = cudaGetLastError();
   return e ? set_error(JH_ERR_CUDA, "silu_bwd: %s", cudaGetErrorString(e)) : JH_OK;
+}
+
+static int cs_blocks(int64_t rows) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)sm_count_layer() * 4));
+}
+
+size_t jh_colsum_workspace_bytes(int64_t rows, int32_t n) {
+  return (size_t)cs_blocks(std::max<int64_t>(rows, 1)) * std::max(n, 1) * sizeof(float);
+}
+
+// x == nullptr: out += column sums of dy; else dx = silu'(x) dy and out += column sums of dx
+static int silu_colsum(const void* x, const void* dy, int64_t ld, void* dx, int64_t rows, int32_t n, float* out,
+                       void* workspace, size_t workspace_bytes, void* stream, const char* what) {
+  if (rows < 0 || n < 8 || n % 8 || n > 8 * 1024)
+    return set_error(JH_ERR_UNSUPPORTED, "%s: n must be a multiple of 8 in [8, 8192] (got %d)", what, n);
+  if (!dy || !out || (x && !dx)) return set_error(JH_ERR_INVALID, "%s: NULL buffer", what);
+  if (!al16(dy) || (x && (!al16(x) || !al16(dx))) || ld < n || (ld * 2) % 16)
+    return set_error(JH_ERR_INVALID, "%s: buffers must be 16-byte aligned with row stride >= n", what);
+  if (rows == 0) return JH_OK;
+  if (!workspace || workspace_bytes < jh_colsum_workspace_bytes(rows, n))
+    return set_error(JH_ERR_INVALID, "%s: workspace too small", what);
+  const int V = n / 8, vpt = (V + 255) / 256, R = V >= 256 ? 1 : 256 / V;
+  const int blocks = cs_blocks(rows);
+  const size_t smem = R > 1 ? (size_t)R * n * sizeof(float) : 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  auto X = (const __nv_bfloat16*)x;
+  auto DY = (const __nv_bfloat16*)dy;
+  auto DX = (__nv_bfloat16*)dx;
+  float* part = (float*)workspace;
+  switch (vpt * 2 + (x ? 1 : 0)) {
+#define CS(VP, SI) \
+  case VP * 2 + SI: silu_colsum_kernel<VP, SI><<<blocks, 256, smem, s>>>(X, DY, ld, DX, rows, n, part); break;
+    CS(1, 0) CS(1, 1) CS(2, 0) CS(2, 1) CS(3, 0) CS(3, 1) CS(4, 0) CS(4, 1)
+#undef CS
+  }
+  // [blocks][n] partial rows = [blocks][2 (n/2)]: colsum_kernel's two halves land in out[0, n/2), out[n/2, n)
+  colsum_kernel<<<(n + 31) / 32, 32 * kColsumWarps, 0, s>>>(part, blocks, n / 2, out, out + n / 2);
+  cudaError_t e = cudaGetLastError();
+  return e ? set_error(JH_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e)) : JH_OK;
+}
+
+int jh_silu_bwd_colsum(const void* x, const void* dy, void* dx, int64_t rows, int32_t n, float* dbias,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  if (!x) return set_error(JH_ERR_INVALID, "silu_bwd_colsum: x is NULL");
+  return silu_colsum(x, dy, n, dx, rows, n, dbias, workspace, workspace_bytes, stream, "silu_bwd_colsum");
+}
+
+int jh_colsum(const void* x, int64_t ld, int64_t rows, int32_t n, float* out, void* workspace, size_t workspace_bytes,
+              void* stream) {
+  return silu_colsum(nullptr, x, ld, nullptr, rows, n, out, workspace, workspace_bytes, stream, "colsum");
 }
 
 static int ng_check(int64_t rows, int32_t n, std::initializer_list<std::pair<const void*, int64_t>> bufs) {
@@ -411,7 +559,7 @@ int jh_norm_gate_bwd(const void* dy, int64_t ld_dy, const void* x, int64_t ld_x,
     NG_B(1) NG_B(2) NG_B(3) NG_B(4) NG_B(5) NG_B(6) NG_B(7) NG_B(8)
 #undef NG_B
   }
-  if (affine_grads) colsum_kernel<<<(2 * n + 31) / 32, 256, 0, s>>>(part, blocks, n, dgamma, dbeta);
+  if (affine_grads) colsum_kernel<<<(2 * n + 31) / 32, 32 * kColsumWarps, 0, s>>>(part, blocks, n, dgamma, dbeta);
   cudaError_t e = cudaGetLastError();
   return e ? set_error(JH_ERR_CUDA, "norm_gate_bwd: %s", cudaGetErrorString(e)) : JH_OK;
 }

@@ -62,6 +62,47 @@ class _NormGateFn(torch.autograd.Function):
         return dx, du, dg, db, None
 
 
+class _LinearSiluFn(torch.autograd.Function):
+    """uvqk = SiLU(xn W + b) as one node: the backward computes d(pre-activation)
+    and the bias gradient in one pass (jh_silu_bwd_colsum) instead of a SiLU
+    node + autograd's addmm backward re-reading the [rows, 4 H d] gradient for
+    the bias sum (r2 C4 stack profile: 8 x 56 us of torch reductions)."""
+
+    @staticmethod
+    def forward(ctx, xn, w, b):
+        wb = w.to(xn.dtype)
+        h = torch.addmm(b.to(xn.dtype), xn, wb)
+        ctx.save_for_backward(xn, wb, h)
+        return kernels.silu(h)
+
+    @staticmethod
+    def backward(ctx, dy):
+        xn, wb, h = ctx.saved_tensors
+        dh, db = kernels.silu_bwd_colsum(h, dy.to(torch.bfloat16).contiguous())
+        dxn = dh @ wb.t() if ctx.needs_input_grad[0] else None
+        dw = (xn.t() @ dh).float() if ctx.needs_input_grad[1] else None
+        return dxn, dw, db
+
+
+class _LinearResidualFn(torch.autograd.Function):
+    """out = x + y W + b; the bias gradient is a jh_colsum of d out."""
+
+    @staticmethod
+    def forward(ctx, y, w, b, x):
+        wb = w.to(y.dtype)
+        ctx.save_for_backward(y, wb)
+        return x + torch.addmm(b.to(y.dtype), y, wb)
+
+    @staticmethod
+    def backward(ctx, dout):
+        y, wb = ctx.saved_tensors
+        dout = dout.to(torch.bfloat16).contiguous()
+        dy = dout @ wb.t() if ctx.needs_input_grad[0] else None
+        dw = (y.t() @ dout).float() if ctx.needs_input_grad[1] else None
+        db = kernels.colsum(dout) if ctx.needs_input_grad[2] else None
+        return dy, dw, db, dout
+
+
 def silu(x):
     return _SiluFn.apply(x)
 
@@ -112,6 +153,14 @@ class KernelOps:
     norm_gate = staticmethod(norm_gate)
 
     @staticmethod
+    def linear_silu(xn, w, b):
+        return _LinearSiluFn.apply(xn, w, b)
+
+    @staticmethod
+    def linear_residual(y, w, b, x):
+        return _LinearResidualFn.apply(y, w, b, x)
+
+    @staticmethod
     def attention(q, k, v, ts, offsets, w, H, nb, max_len):
         return hstu_attention(q, k, v, ts, offsets, w, H, nb, max_len=max_len)
 
@@ -153,11 +202,16 @@ class HSTULayer(torch.nn.Module):
         n = self.num_heads * self.head_dim
         dt, ops = x.dtype, self.ops
         xn = ops.norm_gate(x, None, self.in_gamma, self.in_beta, self.eps)
-        uvqk = ops.silu(torch.addmm(self.b_uvqk.to(dt), xn, self.w_uvqk.to(dt)))
+        if hasattr(ops, "linear_silu"):
+            uvqk = ops.linear_silu(xn, self.w_uvqk, self.b_uvqk)
+            out_proj = lambda y: ops.linear_residual(y, self.w_o, self.b_o, x)  # noqa: E731
+        else:
+            uvqk = ops.silu(torch.addmm(self.b_uvqk.to(dt), xn, self.w_uvqk.to(dt)))
+            out_proj = lambda y: x + torch.addmm(self.b_o.to(dt), y, self.w_o.to(dt))  # noqa: E731
         if cp is None and hasattr(ops, "attention_gate") and max_len is not None and self.head_dim in (64, 128):
             y = ops.attention_gate(uvqk, ts, offsets, self.ts_weights, self.out_gamma, self.out_beta,
                                    self.num_heads, self.num_buckets, max_len, self.eps)
-            return x + torch.addmm(self.b_o.to(dt), y, self.w_o.to(dt))
+            return out_proj(y)
         u, v, q, k = uvqk.split(n, dim=1)
         if cp is None:
             a = ops.attention(q, k, v, ts, offsets, self.ts_weights, self.num_heads, self.num_buckets, max_len)
@@ -166,7 +220,7 @@ class HSTULayer(torch.nn.Module):
             layer, plan = cp
             a = cp_resident_attention(layer, plan, q, k, v, ts, self.ts_weights)
         y = ops.norm_gate(a, u, self.out_gamma, self.out_beta, self.eps)
-        return x + torch.addmm(self.b_o.to(dt), y, self.w_o.to(dt))
+        return out_proj(y)
 
 
 class HSTUStack(torch.nn.Module):

@@ -642,6 +642,42 @@ def silu_bwd(x: torch.Tensor, dy: torch.Tensor) -> torch.Tensor:
     return dx
 
 
+def _colsum_ws(rows: int, n: int, device):
+    nb = int(_lib.lib().jh_colsum_workspace_bytes(rows, n))
+    return torch.empty(nb, dtype=torch.uint8, device=device), nb
+
+
+def silu_bwd_colsum(x: torch.Tensor, dy: torch.Tensor, dbias: torch.Tensor | None = None):
+    """(dx, dbias): dx = silu'(x) dy and dbias (fp32 [n], added into when given)
+    = column sums of dx -- the bias gradient of uvqk = SiLU(xn W + b) in the
+    same pass (jh_silu_bwd_colsum)."""
+    _require_cuda("x", x, torch.bfloat16)
+    _require_cuda("dy", dy, torch.bfloat16)
+    x, dy = x.contiguous(), dy.contiguous()
+    rows, n = x.shape
+    dx = torch.empty_like(x)
+    if dbias is None:
+        dbias = torch.zeros(n, dtype=torch.float32, device=x.device)
+    ws, nb = _colsum_ws(rows, n, x.device)
+    check(_lib.lib().jh_silu_bwd_colsum(_ptr(x), _ptr(dy), _ptr(dx), rows, n, _ptr(dbias), _ptr(ws), nb, _stream(x)),
+          "silu_bwd_colsum")
+    _bump(2)
+    return dx, dbias
+
+
+def colsum(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """fp32 column sums of a bf16 [rows, n] matrix (jh_colsum; added into ``out``)."""
+    _require_cuda("x", x, torch.bfloat16)
+    rows, n = x.shape
+    ld = _ld("x", x, n)
+    if out is None:
+        out = torch.zeros(n, dtype=torch.float32, device=x.device)
+    ws, nb = _colsum_ws(rows, n, x.device)
+    check(_lib.lib().jh_colsum(_ptr(x), ld, rows, n, _ptr(out), _ptr(ws), nb, _stream(x)), "colsum")
+    _bump(2)
+    return out
+
+
 def norm_gate_fwd(x, u=None, gamma=None, beta=None, eps: float = 1e-6):
     """y = (LayerNorm(x) * gamma + beta) * u per row (jh_norm_gate_fwd).
     x: [rows, n] bf16; u: [rows, n] bf16 view (any 16-B row stride) or None;

@@ -45,6 +45,32 @@ def test_silu_fwd_bwd():
     assert _rel(k.silu_bwd(x, dy), xr.grad) <= 1e-2
 
 
+@pytest.mark.parametrize("rows,n", [(1, 8), (1000, 64), (333, 136), (45105, 2048), (700, 4096), (257, 8192)])
+def test_silu_bwd_colsum_and_colsum(rows, n):
+    # dx bitwise equal to the plain SiLU backward; the fused bias gradient and
+    # jh_colsum against fp64 column sums of the same bf16 values (fp32
+    # accumulation: 1e-5 of the column's absolute sum)
+    g = torch.Generator(device="cuda").manual_seed(rows + n)
+    x = (3 * torch.randn(rows, n, device="cuda", generator=g)).bfloat16()
+    dy = torch.randn(rows, n, device="cuda", generator=g).bfloat16()
+    k = _k()
+    dx, db = k.silu_bwd_colsum(x, dy)
+    assert torch.equal(dx, k.silu_bwd(x, dy))
+    want = dx.double().sum(0)
+    scale = dx.double().abs().sum(0) + 1e-30
+    assert float(((db.double() - want).abs() / scale).max()) <= 1e-5
+    # plain column sums of a strided view, added into an existing vector
+    wide = torch.randn(rows, n + 24, device="cuda", generator=g).bfloat16()
+    view = wide[:, 8:8 + n]
+    out = torch.ones(n, device="cuda")
+    k.colsum(view, out)
+    want = view.double().sum(0) + 1
+    scale = view.double().abs().sum(0) + 1
+    assert float(((out.double() - want).abs() / scale).max()) <= 1e-5
+    # deterministic
+    assert torch.equal(k.silu_bwd_colsum(x, dy)[1], db)
+
+
 @pytest.mark.parametrize("n,gate,affine", [(512, True, True), (512, False, True), (136, True, False),
                                            (2048, True, True)])
 def test_norm_gate_fwd_bwd(n, gate, affine):
