@@ -271,8 +271,8 @@ __global__ void __launch_bounds__(32 * kNgWarps) norm_gate_bwd_kernel(
     const __nv_bfloat16* __restrict__ u, int64_t ld_u, const float* __restrict__ gamma,
     const float* __restrict__ beta, const float* __restrict__ mean, const float* __restrict__ rstd, int64_t rows,
     int n, __nv_bfloat16* __restrict__ dx, int64_t ld_dx, __nv_bfloat16* __restrict__ du, int64_t ld_du,
-    float* __restrict__ partials) {
-  extern __shared__ float s_acc[];  // [2][n]
+    float* __restrict__ partials, int par_epi) {
+  extern __shared__ float s_acc[];  // [2][n], or [kNgWarps][2][n] with par_epi
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const int64_t warps = (int64_t)gridDim.x * kNgWarps;
@@ -338,6 +338,32 @@ __global__ void __launch_bounds__(32 * kNgWarps) norm_gate_bwd_kernel(
   // per-block gamma / beta partials, warps added in a fixed order (the staged
   // gamma / beta rows are overwritten: every warp is past its last row first)
   __syncthreads();
+  if (par_epi) {
+    // every warp stores its sums into its own [2n] slice, then each column is
+    // added over the warps in warp order: one barrier instead of kNgWarps
+    // (r2 ncu: the serial form was 19 % of the warp-stall samples)
+    float* mine = s_acc + (size_t)wid * 2 * n;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int col = (c * 32 + lane) * 8;
+      if (col < n)
+#pragma unroll
+        for (int e = 0; e < 8; e += 4) {
+          *reinterpret_cast<float4*>(mine + col + e) = make_float4(ag[c][e], ag[c][e + 1], ag[c][e + 2], ag[c][e + 3]);
+          *reinterpret_cast<float4*>(mine + n + col + e) =
+              make_float4(ab[c][e], ab[c][e + 1], ab[c][e + 2], ab[c][e + 3]);
+        }
+    }
+    __syncthreads();
+    float* dst = partials + (size_t)blockIdx.x * 2 * n;
+    for (int i = threadIdx.x; i < 2 * n; i += blockDim.x) {
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < kNgWarps; ++w) v += s_acc[(size_t)w * 2 * n + i];
+      dst[i] = v;
+    }
+    return;
+  }
   for (int w = 0; w < kNgWarps; ++w) {
     if (wid == w) {
 #pragma unroll
@@ -385,7 +411,10 @@ __global__ void __launch_bounds__(32 * kColsumWarps) colsum_kernel(const float* 
   }
 }
 
-static int ng_blocks(int64_t rows, int per_sm = 4) {
+#ifndef JH_NG_BWD_PER_SM
+#define JH_NG_BWD_PER_SM 2  // the backward's register-limited residency: one wave of blocks
+#endif
+static int ng_blocks(int64_t rows, int per_sm = JH_NG_BWD_PER_SM) {
   const int64_t want = (rows + kNgWarps - 1) / kNgWarps;
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count_layer() * per_sm));
 }
@@ -403,11 +432,13 @@ static int ng_bwd_launch(int blocks, cudaStream_t s, const __nv_bfloat16* dy, in
                          int64_t ld_x, const __nv_bfloat16* u, int64_t ld_u, const float* g, const float* b,
                          const float* mean, const float* rstd, int64_t rows, int n, __nv_bfloat16* dx, int64_t ld_dx,
                          __nv_bfloat16* du, int64_t ld_du, float* partials) {
-  const size_t smem = (size_t)2 * n * sizeof(float);  // gamma / beta staging, then the partial sums
+  // gamma / beta staging, then the partial sums (one [2n] slice per warp when it fits in 64 KB)
+  const int par_epi = partials != nullptr && (size_t)kNgWarps * 2 * n * sizeof(float) <= 64 * 1024;
+  const size_t smem = (size_t)(par_epi ? kNgWarps : 1) * 2 * n * sizeof(float);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(norm_gate_bwd_kernel<CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   norm_gate_bwd_kernel<CH><<<blocks, 32 * kNgWarps, smem, s>>>(dy, ld_dy, x, ld_x, u, ld_u, g, b, mean, rstd, rows, n,
-                                                               dx, ld_dx, du, ld_du, partials);
+                                                               dx, ld_dx, du, ld_du, partials, par_epi);
   return 0;
 }
 
