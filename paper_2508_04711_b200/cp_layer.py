@@ -412,19 +412,20 @@ class CPAttention:
         p = build_cp_plan([list(x) for x in key], self.cp, self.rank, self.mode)
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
         dev = {"send_perm": t(p.send_perm), "seq_perm": t(p.seq_perm), "split_perm": t(p.split_perm),
-               # (q_offsets, q_pos0, kv_start, kv_len, kv total, max kv, host (q_offsets, q_pos0, kv_len))
+               # (q_offsets, q_pos0, kv_start, kv_len, kv total, max kv,
+               #  host (q_offsets, q_pos0, kv_len, kv_start): exact dS sizing + the windowed long-L backward)
                "segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.kv_len), int(p.kv_len.sum()),
-                        int(p.kv_len.max(initial=0)), (p.q_offsets, p.q_pos0, p.kv_len)),
+                        int(p.kv_len.max(initial=0)), (p.q_offsets, p.q_pos0, p.kv_len, p.kv_start)),
                "local_segs": (t(p.q_offsets), t(p.local_q_pos0), t(p.local_kv_start),
                               t(p.local_kv_len), int(p.local_kv_len.sum()), int(p.local_kv_len.max(initial=0)),
-                              (p.q_offsets, p.local_q_pos0, p.local_kv_len)),
+                              (p.q_offsets, p.local_q_pos0, p.local_kv_len, p.local_kv_start)),
                "remote_segs": (t(p.q_offsets), t(p.q_pos0), t(p.kv_start), t(p.remote_kv_len),
                                int(p.remote_kv_len.sum()), int(p.remote_kv_len.max(initial=0)),
-                               (p.q_offsets, p.q_pos0, p.remote_kv_len))}
+                               (p.q_offsets, p.q_pos0, p.remote_kv_len, p.kv_start))}
         if int(p.remote2_kv_len.sum()) > 0:  # remote call B (balanced mode: later chunks' gaps)
             dev["remote2_segs"] = (t(p.q_offsets), t(p.remote2_q_pos0), t(p.remote2_kv_start), t(p.remote2_kv_len),
                                    int(p.remote2_kv_len.sum()), int(p.remote2_kv_len.max(initial=0)),
-                                   (p.q_offsets, p.remote2_q_pos0, p.remote2_kv_len))
+                                   (p.q_offsets, p.remote2_q_pos0, p.remote2_kv_len, p.remote2_kv_start))
         self._plans[key] = (p, dev)
         while len(self._plans) > self.max_plans:
             self._plans.popitem(last=False)

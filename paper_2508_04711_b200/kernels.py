@@ -355,8 +355,9 @@ def ds_scratch_budget(device) -> int:
     return int(_TOTAL_MEM[key] * torch.cuda.get_per_process_memory_fraction(key) // 8)
 
 
-def ds_scratch_bytes(num_heads: int, q_offsets_host, q_pos0_host=None, kv_len_host=None) -> int:
-    """Exact dS scratch of the deterministic backward for host segment arrays."""
+def ds_scratch_bytes(num_heads: int, q_offsets_host, q_pos0_host=None, kv_len_host=None, kv_start_host=None) -> int:
+    """Exact dS scratch of the deterministic backward for host segment arrays
+    (kv_start does not change it; accepted so seg_host tuples pass through)."""
     qo = np.ascontiguousarray(q_offsets_host, dtype=np.int64)
     qp = None if q_pos0_host is None else np.ascontiguousarray(q_pos0_host, dtype=np.int64)
     kl = None if kv_len_host is None else np.ascontiguousarray(kv_len_host, dtype=np.int64)
@@ -484,19 +485,27 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
         if deterministic is None:
             budget = ds_scratch_budget(q.device)
             deterministic = ds_bytes <= budget
-            plain = (q_pos0 is None and kv_start is None and kv_len is None and dq_accum is None
-                     and not accumulate_dkv and pw is None and dp == d and WINDOWED_BWD["enabled"])
-            if not deterministic and plain:
-                qo_host = (np.asarray(seg_host[0], dtype=np.int64) if seg_host is not None
-                           else q_offsets.cpu().numpy().astype(np.int64))
-                if seg_host is None:  # the bound was loose: size the scratch exactly
-                    ds_bytes = ds_scratch_bytes(H, qo_host)
-                    deterministic = ds_bytes <= budget
+            plain = q_pos0 is None and kv_start is None and kv_len is None
+            segform_host = seg_host is not None and len(seg_host) >= 4 and all(x is not None for x in seg_host[:4])
+            if (not deterministic and pw is None and dp == d and WINDOWED_BWD["enabled"]
+                    and (plain or segform_host) and not (out is not None and not plain)):
+                if plain:
+                    qo_host = (np.asarray(seg_host[0], dtype=np.int64) if seg_host is not None
+                               else q_offsets.cpu().numpy().astype(np.int64))
+                    lens = np.diff(qo_host)
+                    segs = (qo_host, np.zeros_like(lens), lens, qo_host[:-1].copy())
+                    if seg_host is None:  # the bound was loose: size the scratch exactly
+                        ds_bytes = ds_scratch_bytes(H, qo_host)
+                        deterministic = ds_bytes <= budget
+                else:
+                    segs = tuple(np.asarray(x, dtype=np.int64) for x in (seg_host[0], seg_host[1], seg_host[2],
+                                                                          seg_host[3]))
                 if not deterministic:
-                    win = _windowed_plan(qo_host, H, budget, q.device, 4 * q.numel())
+                    extra = 0 if dq_accum is not None else 4 * q.numel()
+                    win = _windowed_plan(segs, H, budget, q.device, extra)
                     if win is not None:
-                        return _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, qo_host, win,
-                                                  out, prof)
+                        return _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, segs, win, out,
+                                                  prof, dq_accum, accumulate_dkv, dkv_accum, unique_kv=plain)
     a.deterministic = int(bool(deterministic))
     a.dbg_count_buckets = int(bool(dbg_count_buckets))
     if deterministic:
@@ -537,11 +546,12 @@ WINDOWED_BWD = {"enabled": True}
 WINDOW_Q_CHUNK = 16384
 
 
-def _windowed_plan(qo_host, H: int, budget: int, device, dq_bytes: int = 0):
-    """Window width W for _attn_bwd_windowed, or None (no width >= 128 fits)."""
-    lens = np.diff(qo_host)
-    total = int(lens.sum())
-    if total == 0:
+def _windowed_plan(segs, H: int, budget: int, device, dq_bytes: int = 0):
+    """Window width W for _attn_bwd_windowed, or None (no width >= 128 fits).
+    ``segs`` = host (q_offsets, q_pos0, kv_len, kv_start)."""
+    qo = segs[0]
+    rows = int(qo[-1] - qo[0])
+    if rows == 0:
         return None
     # headroom: at most a quarter of what the process may still allocate (this
     # branch runs only for long sequences, where the allocator query is cheap
@@ -552,54 +562,85 @@ def _windowed_plan(qo_host, H: int, budget: int, device, dq_bytes: int = 0):
     avail = cap * torch.cuda.get_per_process_memory_fraction(idx) - torch.cuda.memory_allocated(idx)
     budget = min(budget, int(avail - dq_bytes) // 4)
     # scratch of one call <= (rows + 64 per segment) * W * H * 2 bytes (64 x 128 bf16 blocks)
-    nseg_bound = int(sum((int(L) + WINDOW_Q_CHUNK - 1) // WINDOW_Q_CHUNK + 1 for L in lens))
-    W = budget // (2 * H * (total + 64 * nseg_bound)) // 128 * 128
+    nseg_bound = int(sum((int(n) + WINDOW_Q_CHUNK - 1) // WINDOW_Q_CHUNK + 1 for n in np.diff(qo)))
+    W = budget // (2 * H * (rows + 64 * nseg_bound)) // 128 * 128
     W = min(W, 1 << 16)
     return W if W >= 128 else None
 
 
-def _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, qo_host, W, out, prof):
+def _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, segs, W, out, prof, dq_accum=None,
+                       accumulate_dkv=False, dkv_accum=None, unique_kv=False):
+    """Segment s: q rows [qo[s], qo[s+1]) at positions qp[s] + i against kv rows
+    ks[s] + j, j < kl[s] (kernels.attn_bwd's segment form; plain self-attention
+    is qp = 0, ks = qo, kl = lengths).  Window w = kv positions [wW, (w+1)W): the
+    q rows with position >= wW see it, in chunks of WINDOW_Q_CHUNK rows."""
     dev = q.device
-    lens = np.diff(qo_host)
-    dq32 = torch.zeros(q.shape, dtype=torch.float32, device=dev)
-    if out is not None:
-        dk, dv = out[1], out[2]
-    else:
-        dk, dv = torch.empty_like(k), torch.empty_like(v)
+    qo, qp, kl, ks = segs
+    dq32 = dq_accum if dq_accum is not None else torch.zeros(q.shape, dtype=torch.float32, device=dev)
+    if accumulate_dkv or not unique_kv:
+        if dkv_accum is not None:
+            dk32, dv32 = dkv_accum
+        else:
+            dk32 = torch.zeros(k.shape, dtype=torch.float32, device=dev)
+            dv32 = torch.zeros(v.shape, dtype=torch.float32, device=dev)
+        dk = dv = None
+    else:  # every kv row belongs to one (segment, window): written once, as bf16
+        dk32 = dv32 = None
+        if out is not None:
+            dk, dv = out[1], out[2]
+        else:
+            dk, dv = torch.empty_like(k), torch.empty_like(v)
     d_w = torch.zeros(num_buckets, dtype=torch.float64, device=dev)
-    nwin = int((int(lens.max()) + W - 1) // W)
+    nwin = int((int(kl.max(initial=0)) + W - 1) // W)
     for wi in range(nwin):
         w0 = wi * W
-        qo, qp, ks, kl, rows = [0], [], [], [], []
-        c = 0  # compact row of this sequence's window
-        for s, L in enumerate(lens):
-            base, L = int(qo_host[s]), int(L)
-            if L <= w0:  # no q row of this sequence sees the window: one empty segment
-                qo.append(base + L); qp.append(0); ks.append(0); kl.append(0)
+        o, qpn, ksn, kln, rows = [int(qo[0])], [], [], [], []
+        c = 0  # compact kv row of the next window copy
+        for s in range(qp.size):
+            a, b, p0, n = int(qo[s]), int(qo[s + 1]), int(qp[s]), int(kl[s])
+            i0 = max(0, w0 - p0)  # first q row whose position reaches the window
+            if n <= w0 or a + i0 >= b:  # this segment has nothing in the window: one empty segment
+                o.append(b); qpn.append(0); ksn.append(0); kln.append(0)
                 continue
-            if w0 > 0:  # rows before the window: empty segment
-                qo.append(base + w0); qp.append(0); ks.append(0); kl.append(0)
-            wl = min(W, L - w0)
-            for c0 in range(w0, L, WINDOW_Q_CHUNK):
-                qo.append(base + min(L, c0 + WINDOW_Q_CHUNK)); qp.append(c0 - w0); ks.append(c); kl.append(wl)
-            rows.append(np.arange(base + w0, base + w0 + wl, dtype=np.int64))
+            if i0 > 0:  # rows before the window: empty segment
+                o.append(a + i0); qpn.append(0); ksn.append(0); kln.append(0)
+            wl = min(W, n - w0)
+            for c0 in range(a + i0, b, WINDOW_Q_CHUNK):
+                o.append(min(b, c0 + WINDOW_Q_CHUNK)); qpn.append(p0 + (c0 - a) - w0); ksn.append(c); kln.append(wl)
+            rows.append(np.arange(int(ks[s]) + w0, int(ks[s]) + w0 + wl, dtype=np.int64))
             c += wl
-        qo_a, qp_a, kl_a = (np.asarray(x, dtype=np.int64) for x in (qo, qp, kl))
-        n = qp_a.size
-        t = torch.from_numpy(np.concatenate([qo_a, qp_a, np.asarray(ks, dtype=np.int64), kl_a]
-                                            + rows)).to(dev)
-        idx = t[4 * n + 1:]
+        if c == 0:
+            continue
+        o_a, qp_a, kl_a = (np.asarray(x, dtype=np.int64) for x in (o, qpn, kln))
+        m = qp_a.size
+        t = torch.from_numpy(np.concatenate([o_a, qp_a, np.asarray(ksn, dtype=np.int64), kl_a] + rows)).to(dev)
+        idx = t[4 * m + 1:]
         k_w, v_w, ts_w = k.index_select(0, idx), v.index_select(0, idx), ts_k.index_select(0, idx)
         dk_w = torch.zeros(k_w.shape, dtype=torch.float32, device=dev)
         dv_w = torch.zeros(v_w.shape, dtype=torch.float32, device=dev)
-        _, _, _, dwi, _ = attn_bwd(q, k_w, v_w, ts_q, ts_w, t[:n + 1], dout, H, w, num_buckets,
-                                   q_pos0=t[n + 1:2 * n + 1], kv_start=t[2 * n + 1:3 * n + 1],
-                                   kv_len=t[3 * n + 1:4 * n + 1], kv_len_total=c, accumulate_dkv=True,
+        # (q rows outside [o[0], o[-1]) belong to no segment of this call: the kernels never touch them)
+        _, _, _, dwi, _ = attn_bwd(q, k_w, v_w, ts_q, ts_w, t[:m + 1], dout, H, w, num_buckets,
+                                   q_pos0=t[m + 1:2 * m + 1], kv_start=t[2 * m + 1:3 * m + 1],
+                                   kv_len=t[3 * m + 1:4 * m + 1], kv_len_total=c, accumulate_dkv=True,
                                    dkv_accum=(dk_w, dv_w), dq_accum=dq32, deterministic=True,
-                                   seg_host=(qo_a, qp_a, kl_a), prof=prof)
-        dk.index_copy_(0, idx, dk_w.to(dk.dtype))
-        dv.index_copy_(0, idx, dv_w.to(dv.dtype))
+                                   seg_host=(o_a, qp_a, kl_a), prof=prof)
+        if dk32 is not None:
+            dk32.index_add_(0, idx, dk_w)
+            dv32.index_add_(0, idx, dv_w)
+        else:
+            dk.index_copy_(0, idx, dk_w.to(dk.dtype))
+            dv.index_copy_(0, idx, dv_w.to(dv.dtype))
         d_w += dwi
+    if dk32 is not None and not accumulate_dkv:
+        dk, dv = dk32.to(torch.bfloat16), dv32.to(torch.bfloat16)
+        if out is not None:
+            out[1].copy_(dk)
+            out[2].copy_(dv)
+            dk, dv = out[1], out[2]
+    elif dk32 is not None:
+        dk, dv = dk32, dv32
+    if dq_accum is not None:
+        return dq_accum, dk, dv, d_w, None
     if out is not None:
         out[0].copy_(dq32)
         return out[0], dk, dv, d_w, None

@@ -325,7 +325,7 @@ def test_bwd_windowed_matches_full(monkeypatch, chunk):
                             deterministic=True, seg_host=(offs_h, None, None))
     calls = []
     orig = kernels._attn_bwd_windowed
-    monkeypatch.setattr(kernels, "_attn_bwd_windowed", lambda *a: calls.append(a[-3]) or orig(*a))
+    monkeypatch.setattr(kernels, "_attn_bwd_windowed", lambda *a, **kw: calls.append(a[10]) or orig(*a, **kw))
     monkeypatch.setattr(kernels, "WINDOW_Q_CHUNK", chunk)
     monkeypatch.setenv("JH_DS_SCRATCH_BUDGET", str(16 << 20))
     win = kernels.attn_bwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], c["g"], H, c["w"], 16,
@@ -345,3 +345,48 @@ def test_bwd_windowed_matches_full(monkeypatch, chunk):
         assert e_win <= ROW_TOL and e_ab <= 1e-2, name
     a, b = win[3].cpu().numpy(), want[3]
     assert np.abs(a - b).max() / np.abs(b).max() <= DW_TOL
+
+
+def test_bwd_windowed_segment_form_matches_full(monkeypatch):
+    # the CP calls' segment form (q_pos0 / kv_start / kv_len, fp32 dq / dK / dV
+    # accumulators): windowed under a small budget vs the whole-segment path
+    from paper_2508_04711_b200 import kernels
+    H, Dh = 2, 128
+    rng = np.random.default_rng(21)
+    qo = np.array([0, 700, 1100, 1100, 2100, 2600], dtype=np.int64)
+    qp = np.array([1500, 0, 0, 300, 5000], dtype=np.int64)
+    ks = np.array([0, 2200, 0, 1000, 500], dtype=np.int64)
+    kl = np.array([2200, 400, 0, 0, 2500], dtype=np.int64)
+    Tq, Tk = int(qo[-1]), 3000
+    mk = lambda n: torch.from_numpy(rng.standard_normal((n, H * Dh)).astype(np.float32)).cuda().bfloat16()  # noqa: E731
+    q, g, k, v = mk(Tq), mk(Tq), mk(Tk), mk(Tk)
+    ts_q = torch.from_numpy(np.sort(rng.integers(0, 10**6, Tq))).cuda()
+    ts_k = torch.from_numpy(np.sort(rng.integers(0, 10**6, Tk))).cuda()
+    w = torch.from_numpy(rng.standard_normal(16).astype(np.float32) * 0.1).cuda()
+    t = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+    seg_host = (qo, qp, kl, ks)
+
+    def run(det):
+        dq = torch.full((Tq, H * Dh), 0.5, dtype=torch.float32, device="cuda")  # accumulated into
+        dk = torch.full((Tk, H * Dh), 0.25, dtype=torch.float32, device="cuda")
+        dv = torch.zeros((Tk, H * Dh), dtype=torch.float32, device="cuda")
+        _, _, _, dw, _ = kernels.attn_bwd(q, k, v, ts_q, ts_k, t(qo), g, H, w, 16, q_pos0=t(qp), kv_start=t(ks),
+                                          kv_len=t(kl), kv_len_total=Tk, accumulate_dkv=True, dq_accum=dq,
+                                          dkv_accum=(dk, dv), deterministic=det, seg_host=seg_host)
+        torch.cuda.synchronize()
+        return [x.cpu().numpy() for x in (dq, dk, dv, dw)]
+
+    full = run(True)
+    calls = []
+    orig = kernels._attn_bwd_windowed
+    monkeypatch.setattr(kernels, "_attn_bwd_windowed", lambda *a, **kw: calls.append(a[10]) or orig(*a, **kw))
+    monkeypatch.setattr(kernels, "WINDOW_Q_CHUNK", 256)
+    monkeypatch.setenv("JH_DS_SCRATCH_BUDGET", str(4 << 20))
+    win = run(None)
+    assert calls and 128 <= calls[0] < 2500, calls
+    for name, a, b in zip(("dq", "dk", "dv"), win[:3], full[:3]):
+        assert np.isfinite(a).all(), name
+        err = row_rel(a, b)[1]
+        print(f"segment-form windowed W={calls[0]} {name}: row err vs whole-segment path {err:.2e}")
+        assert err <= 5e-3, name
+    assert np.abs(win[3] - full[3]).max() / np.abs(full[3]).max() <= DW_TOL
