@@ -27,6 +27,10 @@
 // accumulates in TMEM across kv tiles (no rescale).
 #include "attn_common.cuh"
 
+#ifndef JH_TRACE_CHUNKS
+#define JH_TRACE_CHUNKS 0
+#endif
+
 namespace jh {
 
 constexpr int kEpiWarps = 8;
@@ -565,6 +569,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               tmem_st4(tS + c0 + (g8 >> 1), pk);  // S columns c0 .. c0+g8+7 were already read
             }
           }
+#if JH_TRACE_CHUNKS
+          if (tr) trace_ev(p, trole, tcnt, 50 + cls, c0);
+#endif
         }
         tmem_st_wait();
         tc_fence_before();
