@@ -411,6 +411,9 @@ __global__ void __launch_bounds__(32 * kColsumWarps) colsum_kernel(const float* 
   }
 }
 
+#ifndef JH_NG_FWD_PER_SM
+#define JH_NG_FWD_PER_SM 8
+#endif
 #ifndef JH_NG_BWD_PER_SM
 #define JH_NG_BWD_PER_SM 2  // the backward's register-limited residency: one wave of blocks
 #endif
@@ -545,7 +548,7 @@ int jh_norm_gate_fwd(const void* x, int64_t ld_x, const void* u, int64_t ld_u, c
   if (int r = ng_check(rows, n, {{x, ld_x}, {u, ld_u}, {y, ld_y}})) return r;
   if (!x || !y) return set_error(JH_ERR_INVALID, "norm_gate: x / y is NULL");
   if (rows == 0) return JH_OK;
-  const int blocks = ng_blocks(rows, 8);
+  const int blocks = ng_blocks(rows, JH_NG_FWD_PER_SM);
   const int ch = (n + 255) / 256;
   cudaStream_t s = (cudaStream_t)stream;
   auto X = (const __nv_bfloat16*)x;
