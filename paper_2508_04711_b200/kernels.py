@@ -272,6 +272,25 @@ def _prof(a, prof):
         a.trace, a.trace_cta = _TRACE["buf"].data_ptr(), _TRACE["cta"]
 
 
+# The fused kernels take deltas in 32 bits: num_buckets <= 23 (cap e^22 - 1 <
+# 2^32).  A larger num_buckets only differs from 23 for pairs whose delta
+# reaches bucket 23 (delta >= e^23 - 1 ~ 9.7e9); when the batch's timestamp span
+# stays below that, every bucket index is the same under both and the call runs
+# with the first 23 weights (d_ts_weights of the higher buckets are 0).
+FUSED_NB_MAX = 23
+
+
+def _effective_buckets(num_buckets: int, ts_q, ts_k) -> int:
+    nb = int(num_buckets)
+    if nb <= FUSED_NB_MAX or ts_q.numel() == 0 or ts_k.numel() == 0:
+        return min(nb, FUSED_NB_MAX) if nb > FUSED_NB_MAX else nb
+    span = int((ts_q.max() - ts_k.min()).item())  # >= every pair's delta (one synchronisation)
+    if span < bias_table(FUSED_NB_MAX + 1)[2]:  # first delta of bucket 23
+        return FUSED_NB_MAX
+    raise NotImplementedError(f"fused attention supports num_buckets <= {FUSED_NB_MAX} when a timestamp delta "
+                              f"reaches bucket {FUSED_NB_MAX} (num_buckets={nb}, span {span})")
+
+
 def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=16, pos_weights=None,
              q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, out=None, prof=None, out_accum=None,
              accumulate=False, band_table=None, dbg_buckets=None):
@@ -286,6 +305,10 @@ def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=
     stays 1/sqrt(head_dim).  ``dbg_buckets`` (uint8 [q_rows, max_kv], tests):
     the bucket the kernel applied to each visible pair of head 0."""
     w = ts_weights.to(device=q.device, dtype=torch.float32).contiguous()
+    if int(num_buckets) > FUSED_NB_MAX:
+        _check_weights(w, num_buckets)
+        num_buckets = _effective_buckets(num_buckets, ts_q, ts_k)
+        w = w[:num_buckets].contiguous()
     pw = None if pos_weights is None else pos_weights.to(device=q.device, dtype=torch.float32).contiguous()
     H = int(num_heads)
     if q.dim() != 2 or q.shape[1] % H:
@@ -409,6 +432,15 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
     if deterministic is None:
         deterministic = DETERMINISTIC_DEFAULT["value"]
     w = ts_weights.to(device=q.device, dtype=torch.float32).contiguous()
+    if int(num_buckets) > FUSED_NB_MAX:  # (see _effective_buckets) d_ts_weights padded back to num_buckets
+        _check_weights(w, num_buckets)
+        nb_eff = _effective_buckets(num_buckets, ts_q, ts_k)
+        res = attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, w[:nb_eff].contiguous(), nb_eff,
+                       pos_weights, q_pos0, kv_start, kv_len, kv_len_total, accumulate_dkv, prof, max_kv_len,
+                       dq_accum, band_table, deterministic, dbg_count_buckets, seg_host, out, dkv_accum)
+        d_w = torch.zeros(int(num_buckets), dtype=torch.float64, device=q.device)
+        d_w[:nb_eff] = res[3]
+        return res[0], res[1], res[2], d_w, res[4]
     pw = None if pos_weights is None else pos_weights.to(device=q.device, dtype=torch.float32).contiguous()
     H = int(num_heads)
     if q.dim() != 2 or q.shape[1] % H:

@@ -48,11 +48,36 @@ def test_fwd_bwd_num_buckets(nb):
     assert np.abs(dw - ww).max() / max(np.abs(ww).max(), 1e-30) <= DW_TOL
 
 
-def test_num_buckets_beyond_fused_limit_is_unsupported():
+@pytest.mark.parametrize("nb", [24, 32, 64])
+def test_num_buckets_beyond_fused_limit(nb):
+    # above 23 buckets the kernels run with the first 23 weights when no delta
+    # reaches bucket 23 (timestamp span < e^23 - 1): identical bucket indices,
+    # d_ts_weights zero above bucket 22
+    lens = [200, 1, 130]
+    case = make_case(lens, 2 * 64, seed=nb, nb=nb)
+    c = to_cuda(case)
+    k = _k()
+    out = k.attn_fwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], 2, c["w"], nb)
+    dq, dk, dv, dw, _ = k.attn_bwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], c["g"], 2, c["w"], nb)
+    torch.cuda.synchronize()
+    want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], case["offsets"], case["w"], nb, 2)
+    assert row_rel(out.float().cpu().numpy(), want)[1] <= ROW_TOL
+    wq, wk, wv, ww, _ = oracle.hstu_backward(case["q"], case["k"], case["v"], case["ts"], case["offsets"],
+                                              case["g"], case["w"], nb, 2)
+    for a, b in ((dq, wq), (dk, wk), (dv, wv)):
+        assert row_rel(a.float().cpu().numpy(), b)[1] <= ROW_TOL
+    dw = dw.cpu().numpy()
+    assert dw.shape == (nb,) and np.all(dw[23:] == 0) and np.all(ww[23:] == 0)
+    assert np.abs(dw - ww).max() / max(np.abs(ww).max(), 1e-30) <= DW_TOL
+
+
+def test_num_buckets_beyond_fused_limit_huge_span_is_unsupported():
     case = make_case([16], 64, seed=1, nb=24)
     c = to_cuda(case)
+    ts = c["ts"].clone()
+    ts[8:] += 10**10  # a delta in bucket 23
     with pytest.raises(NotImplementedError):
-        _k().attn_fwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], 1, c["w"], 24)
+        _k().attn_fwd(c["q"], c["k"], c["v"], ts, ts, c["offsets"], 1, c["w"], 24)
 
 
 # --------------------------------------------------------- positional bias
