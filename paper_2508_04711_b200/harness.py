@@ -329,7 +329,7 @@ def sweep_max_tokens(budget_bytes: int, cp_sizes, embed_dim: int = 8, dtype: str
 
 def sweep_max_tokens_measured(budget_bytes: int, cp_sizes=(1, 2, 4, 8), embed_dim: int = 512, num_heads: int = 4,
                               num_layers: int = 8, num_buckets: int = 16, seed: int = 7, granularity: int = 2048,
-                              time_budget_s: float = 150.0, device=None) -> SweepReport:
+                              time_budget_s: float = 200.0, device=None, rel_precision: float = 1 / 128) -> SweepReport:
     """The MEASURED counterpart of ``sweep_max_tokens`` (harness.py:369-394) on
     the GPU: for each CP size, the longest single sequence whose per-rank share
     -- its two balanced mini-chunks through ``num_layers`` HSTU layers, K/V of
@@ -337,8 +337,10 @@ def sweep_max_tokens_measured(budget_bytes: int, cp_sizes=(1, 2, 4, 8), embed_di
     runs forward + backward under a per-process memory cap of ``budget_bytes``
     (torch.cuda.set_per_process_memory_fraction).  Communication is excluded
     (cp_layer.LoopbackComm: one rank's memory and kernel work, the peers' K/V
-    replaced by replicas).  Doubling from 8 * granularity, then bisection to
-    ``granularity`` tokens (a multiple of 2 * cp * 128 for every cp <= 8).
+    replaced by replicas).  Doubling (from 8 * granularity, or from the
+    previous CP size's maximum: it can only grow with CP), then bisection to
+    ``granularity`` tokens or ``rel_precision`` of the length, whichever is
+    coarser (granularity: a multiple of 2 * cp * 128 for every cp <= 8).
     Rows carry ``max_supported_length`` (the reference's key), the first
     failing length, the peak allocated bytes at the maximum and the ratio to
     the first CP size."""
@@ -394,13 +396,16 @@ def sweep_max_tokens_measured(budget_bytes: int, cp_sizes=(1, 2, 4, 8), embed_di
             if k < 1:
                 raise ValueError("cp sizes must be >= 1")
             lo, hi, peak_lo, L = 0, None, None, 8 * granularity
+            if rows and rows[-1]["max_supported_length"] >= L:  # start from the previous CP size's maximum
+                L = rows[-1]["max_supported_length"]
             while hi is None and time.time() - t0 < time_budget_s:
                 ok, pk = runs(k, L)
                 if ok:
                     lo, peak_lo, L = L, pk, 2 * L
                 else:
                     hi = L
-            while hi is not None and hi - lo > granularity and time.time() - t0 < time_budget_s:
+            while (hi is not None and hi - lo > max(granularity, int(lo * rel_precision))
+                   and time.time() - t0 < time_budget_s):
                 mid = (lo + hi) // 2 // granularity * granularity
                 ok, pk = runs(k, mid)
                 if ok:

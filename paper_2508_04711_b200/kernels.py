@@ -409,7 +409,7 @@ def bwd_state(q_rows: int, num_segments: int, H: int, dp: int, device) -> torch.
 def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_buckets=16, pos_weights=None,
              q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, accumulate_dkv=False, prof=None,
              max_kv_len=None, dq_accum=None, band_table=None, deterministic=None, dbg_count_buckets=False,
-             seg_host=None, out=None, dkv_accum=None):
+             seg_host=None, out=None, dkv_accum=None, _ds_buf=None):
     """Fused jagged HSTU backward (jh_attn_bwd).
 
     Returns (dq bf16, dk, dv, d_ts_weights f64, d_pos f64 or None); dk/dv are
@@ -536,12 +536,18 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
                     extra = 0 if dq_accum is not None else 4 * q.numel()
                     win = _windowed_plan(segs, H, budget, q.device, extra)
                     if win is not None:
-                        return _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, segs, win, out,
-                                                  prof, dq_accum, accumulate_dkv, dkv_accum, unique_kv=plain)
+                        res = _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, segs, win, out,
+                                                 prof, dq_accum, accumulate_dkv, dkv_accum, unique_kv=plain)
+                        if res is not None:
+                            return res
+                        # (its buffers did not fit: the fused kernel below, O(L) memory)
     a.deterministic = int(bool(deterministic))
     a.dbg_count_buckets = int(bool(dbg_count_buckets))
     if deterministic:
-        ds = torch.empty(ds_bytes, dtype=torch.uint8, device=q.device)
+        if _ds_buf is not None and _ds_buf.numel() >= ds_bytes:  # (the windowed path's preallocated scratch)
+            ds = _ds_buf
+        else:
+            ds = torch.empty(ds_bytes, dtype=torch.uint8, device=q.device)
         a.ds_scratch, a.ds_scratch_bytes = ds.data_ptr(), ds_bytes
     else:
         st = bwd_state(q.shape[0], a.num_segments, H, dp, q.device)
@@ -605,24 +611,13 @@ def _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, segs, W, ou
     """Segment s: q rows [qo[s], qo[s+1]) at positions qp[s] + i against kv rows
     ks[s] + j, j < kl[s] (kernels.attn_bwd's segment form; plain self-attention
     is qp = 0, ks = qo, kl = lengths).  Window w = kv positions [wW, (w+1)W): the
-    q rows with position >= wW see it, in chunks of WINDOW_Q_CHUNK rows."""
+    q rows with position >= wW see it, in chunks of WINDOW_Q_CHUNK rows.  Every
+    window is planned first and the scratch / window buffers are allocated
+    once at their maximum: if they do not fit, None is returned before anything
+    was accumulated (the caller then runs the fused kernel)."""
     dev = q.device
     qo, qp, kl, ks = segs
-    dq32 = dq_accum if dq_accum is not None else torch.zeros(q.shape, dtype=torch.float32, device=dev)
-    if accumulate_dkv or not unique_kv:
-        if dkv_accum is not None:
-            dk32, dv32 = dkv_accum
-        else:
-            dk32 = torch.zeros(k.shape, dtype=torch.float32, device=dev)
-            dv32 = torch.zeros(v.shape, dtype=torch.float32, device=dev)
-        dk = dv = None
-    else:  # every kv row belongs to one (segment, window): written once, as bf16
-        dk32 = dv32 = None
-        if out is not None:
-            dk, dv = out[1], out[2]
-        else:
-            dk, dv = torch.empty_like(k), torch.empty_like(v)
-    d_w = torch.zeros(num_buckets, dtype=torch.float64, device=dev)
+    wins = []
     nwin = int((int(kl.max(initial=0)) + W - 1) // W)
     for wi in range(nwin):
         w0 = wi * W
@@ -644,18 +639,50 @@ def _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, segs, W, ou
         if c == 0:
             continue
         o_a, qp_a, kl_a = (np.asarray(x, dtype=np.int64) for x in (o, qpn, kln))
+        host = np.concatenate([o_a, qp_a, np.asarray(ksn, dtype=np.int64), kl_a] + rows)
+        wins.append((o_a, qp_a, kl_a, host, c, ds_scratch_bytes(H, o_a, qp_a, kl_a)))
+    if not wins:
+        return None
+    max_c = max(x[4] for x in wins)
+    max_ds = max(x[5] for x in wins)
+    try:
+        ds_buf = torch.empty(max(max_ds, 1), dtype=torch.uint8, device=dev)
+        kvw = torch.empty((2, max_c, k.shape[1]), dtype=k.dtype, device=dev)
+        tsw = torch.empty(max_c, dtype=ts_k.dtype, device=dev)
+        dkvw = torch.empty((2, max_c, k.shape[1]), dtype=torch.float32, device=dev)
+        dq32 = dq_accum if dq_accum is not None else torch.zeros(q.shape, dtype=torch.float32, device=dev)
+        if accumulate_dkv or not unique_kv:
+            if dkv_accum is not None:
+                dk32, dv32 = dkv_accum
+            else:
+                dk32 = torch.zeros(k.shape, dtype=torch.float32, device=dev)
+                dv32 = torch.zeros(v.shape, dtype=torch.float32, device=dev)
+            dk = dv = None
+        else:  # every kv row belongs to one (segment, window): written once, as bf16
+            dk32 = dv32 = None
+            if out is not None:
+                dk, dv = out[1], out[2]
+            else:
+                dk, dv = torch.empty_like(k), torch.empty_like(v)
+    except torch.OutOfMemoryError:
+        return None
+    d_w = torch.zeros(num_buckets, dtype=torch.float64, device=dev)
+    for o_a, qp_a, kl_a, host, c, _ in wins:
         m = qp_a.size
-        t = torch.from_numpy(np.concatenate([o_a, qp_a, np.asarray(ksn, dtype=np.int64), kl_a] + rows)).to(dev)
+        t = torch.from_numpy(host).to(dev)
         idx = t[4 * m + 1:]
-        k_w, v_w, ts_w = k.index_select(0, idx), v.index_select(0, idx), ts_k.index_select(0, idx)
-        dk_w = torch.zeros(k_w.shape, dtype=torch.float32, device=dev)
-        dv_w = torch.zeros(v_w.shape, dtype=torch.float32, device=dev)
+        k_w, v_w, ts_w = kvw[0, :c], kvw[1, :c], tsw[:c]
+        torch.index_select(k, 0, idx, out=k_w)
+        torch.index_select(v, 0, idx, out=v_w)
+        torch.index_select(ts_k, 0, idx, out=ts_w)
+        dk_w, dv_w = dkvw[0, :c], dkvw[1, :c]
+        dkvw[:, :c].zero_()
         # (q rows outside [o[0], o[-1]) belong to no segment of this call: the kernels never touch them)
         _, _, _, dwi, _ = attn_bwd(q, k_w, v_w, ts_q, ts_w, t[:m + 1], dout, H, w, num_buckets,
                                    q_pos0=t[m + 1:2 * m + 1], kv_start=t[2 * m + 1:3 * m + 1],
                                    kv_len=t[3 * m + 1:4 * m + 1], kv_len_total=c, accumulate_dkv=True,
                                    dkv_accum=(dk_w, dv_w), dq_accum=dq32, deterministic=True,
-                                   seg_host=(o_a, qp_a, kl_a), prof=prof)
+                                   seg_host=(o_a, qp_a, kl_a), prof=prof, _ds_buf=ds_buf)
         if dk32 is not None:
             dk32.index_add_(0, idx, dk_w)
             dv32.index_add_(0, idx, dv_w)
@@ -663,6 +690,7 @@ def _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, segs, W, ou
             dk.index_copy_(0, idx, dk_w.to(dk.dtype))
             dv.index_copy_(0, idx, dv_w.to(dv.dtype))
         d_w += dwi
+    del ds_buf, kvw, tsw, dkvw
     if dk32 is not None and not accumulate_dkv:
         dk, dv = dk32.to(torch.bfloat16), dv32.to(torch.bfloat16)
         if out is not None:
