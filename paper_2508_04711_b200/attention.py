@@ -345,24 +345,29 @@ def _stream_cuts(offs: np.ndarray, G: int) -> list:
     return cuts
 
 
-def hstu_attention_fwd_bwd_host(q, k, v, ts, offsets, upstream, ts_weights, num_heads: int = 1,
-                                num_buckets: int = 16, groups: int = 4, device=None, out=None):
-    """Forward + backward of attention.py:125-148 / 187-234 for inputs that live in
-    HOST memory (the reference's numpy calling convention), returning host
-    results: (out, dq, dk, dv) as bf16 host tensors shaped like q and
-    d_ts_weights (float64, host).
+class HostStreamResult:
+    """Handle of an enqueued host-streaming call: ``wait()`` blocks until every
+    result reached the host and returns (out, dq, dk, dv, d_ts_weights)."""
 
-    The batch is cut into ``groups`` runs of whole sequences with about equal
-    token counts (sequences never interact, so each run is an independent
-    problem); every run's host->device copy is enqueued first on a copy
-    stream, each run's kernels start when its inputs land, and its results go
-    back on a second copy stream while later runs still copy in, so the two
-    PCIe directions overlap each other and the kernels (C2 on one B200: 2.46
-    ms vs 2.82 ms for copy-in / compute / copy-out in sequence; PCIe 5 x16,
-    ~42 GB/s per direction while both run, 55 alone).  q, k, v, upstream: (T, H*d) host arrays / tensors (bf16, or anything
-    castable; pinned tensors are used in place); ts: (T,) int64; offsets:
-    (B+1,) int64 host.  ``out`` = four pinned bf16 host tensors shaped like q to
-    write (out, dq, dk, dv) into (reused across calls; otherwise allocated)."""
+    def __init__(self, event, results, keep):
+        self._event, self._results, self._keep = event, results, keep
+
+    def done(self) -> bool:
+        return self._event.query()
+
+    def wait(self):
+        self._event.synchronize()
+        self._keep = None
+        return self._results
+
+
+def hstu_attention_fwd_bwd_host_async(q, k, v, ts, offsets, upstream, ts_weights, num_heads: int = 1,
+                                      num_buckets: int = 16, groups: int = 4, device=None, out=None):
+    """Enqueue hstu_attention_fwd_bwd_host without waiting: returns a
+    HostStreamResult.  Consecutive calls overlap -- one call's results copy
+    back while the next call's inputs copy in (PCIe is full duplex) -- as long
+    as calls in flight write different ``out`` buffers (a caller double-
+    buffers them, and waits for call i before reusing call i's buffers)."""
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     offs = np.asarray(offsets.cpu() if isinstance(offsets, torch.Tensor) else offsets, dtype=np.int64)
     if offs.ndim != 1 or offs.size < 1 or offs[0] != 0 or np.any(np.diff(offs) < 0):
@@ -389,7 +394,8 @@ def hstu_attention_fwd_bwd_host(q, k, v, ts, offsets, upstream, ts_weights, num_
     s_in, s_out = _STREAMS[dev]
     main = torch.cuda.current_stream(dev)
     runs = []
-    s_in.wait_stream(main)  # (the outputs / weights above were produced on the caller's stream)
+    # (no wait on the caller's stream: the copies read host memory into fresh
+    # buffers, so the next call's inputs can copy in while this one still runs)
     with torch.cuda.stream(s_in):
         # every run's inputs are enqueued first, so the host's launch overhead of the
         # runs below overlaps the copies instead of delaying them; the device inputs
@@ -433,6 +439,33 @@ def hstu_attention_fwd_bwd_host(q, k, v, ts, offsets, upstream, ts_weights, num_
                 src.record_stream(s_out)
                 dst[r0:r1].copy_(src, non_blocking=True)
         keep.append((o, gq, gk, gv))
-    main.wait_stream(s_out)
-    dwh = d_w.to("cpu")  # synchronises: every group's results are on the host
-    return outs[0], outs[1], outs[2], outs[3], dwh
+    dwh = torch.empty(num_buckets, dtype=torch.float64, pin_memory=True)
+    s_out.wait_stream(main)
+    with torch.cuda.stream(s_out):
+        d_w.record_stream(s_out)
+        dwh.copy_(d_w, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(s_out)
+    return HostStreamResult(done, (outs[0], outs[1], outs[2], outs[3], dwh), keep)
+
+
+def hstu_attention_fwd_bwd_host(q, k, v, ts, offsets, upstream, ts_weights, num_heads: int = 1,
+                                num_buckets: int = 16, groups: int = 4, device=None, out=None):
+    """Forward + backward of attention.py:125-148 / 187-234 for inputs that live in
+    HOST memory (the reference's numpy calling convention), returning host
+    results: (out, dq, dk, dv) as bf16 host tensors shaped like q and
+    d_ts_weights (float64, host).
+
+    The batch is cut into ``groups`` runs of whole sequences with about equal
+    token counts (sequences never interact, so each run is an independent
+    problem); every run's host->device copy is enqueued first on a copy
+    stream, each run's kernels start when its inputs land, and its results go
+    back on a second copy stream while later runs still copy in, so the two
+    PCIe directions overlap each other and the kernels (C2 on one B200: 2.46
+    ms vs 2.82 ms for copy-in / compute / copy-out in sequence; PCIe 5 x16,
+    ~42 GB/s per direction while both run, 55 alone).  q, k, v, upstream: (T, H*d) host arrays / tensors (bf16, or anything
+    castable; pinned tensors are used in place); ts: (T,) int64; offsets:
+    (B+1,) int64 host.  ``out`` = four pinned bf16 host tensors shaped like q to
+    write (out, dq, dk, dv) into (reused across calls; otherwise allocated)."""
+    return hstu_attention_fwd_bwd_host_async(q, k, v, ts, offsets, upstream, ts_weights, num_heads, num_buckets,
+                                             groups, device, out).wait()

@@ -33,3 +33,24 @@ for rep in range(2):
                 attention.hstu_attention_fwd_bwd_host(q, k, v, ts, h["offsets"], g, w, 4, 16, groups=G, out=outs)
             row.append(f"G={G} {(time.perf_counter() - t0) / 20 * 1e3:.3f}")
         print(f"edge {e}: " + "  ".join(row), flush=True)
+
+# back-to-back async calls (two output buffer sets), per G
+outs2 = [torch.empty(q.shape, dtype=torch.bfloat16, pin_memory=True) for _ in range(4)]
+row = []
+for G in (1, 2, 3, 4):
+    sets = (outs, outs2)
+    for i in range(4):
+        attention.hstu_attention_fwd_bwd_host_async(q, k, v, ts, h["offsets"], g, w, 4, 16, groups=G,
+                                                    out=sets[i % 2]).wait()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    prev = None
+    for i in range(20):
+        cur = attention.hstu_attention_fwd_bwd_host_async(q, k, v, ts, h["offsets"], g, w, 4, 16, groups=G,
+                                                          out=sets[i % 2])
+        if prev is not None:
+            prev.wait()
+        prev = cur
+    prev.wait()
+    row.append(f"G={G} {(time.perf_counter() - t0) / 20 * 1e3:.3f}")
+print("pipelined: " + "  ".join(row), flush=True)
