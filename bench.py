@@ -404,7 +404,7 @@ def run_gpu(args):
             tot += e0.elapsed_time(e1)
         return tot / K
 
-    if world == 1:
+    if world == 1 and not args.no_e2e:
         e2e_ms = pipe_time()
         call_ms = stream_time()
         api_ms = e2e_time(True)
@@ -722,6 +722,7 @@ def main():
                     help="batch -> sequence redistribution protocol for N > 1")
     ap.add_argument("--e2e-groups", type=int, default=2, help="sequence runs of the host-streaming e2e call")
     ap.add_argument("--no-stack", action="store_true", help="skip the 8-layer HSTU stack (C4 batch) measurement")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e legs (profiling runs)")
     ap.add_argument("--cp-sweep-gb", type=float, default=24.0,
                     help="per-GPU memory cap of the CP max-length sweep (0 = skip)")
     args = ap.parse_args()

@@ -82,6 +82,11 @@ def main():
     rec("silu_fwd", timed(lambda: kernels.silu(uvqk), flush), 2 * R * 4 * N * 2, [R, 4 * N])
     dyu = torch.randn(R, 4 * N, device=dev).bfloat16()
     rec("silu_bwd", timed(lambda: kernels.silu_bwd(uvqk, dyu), flush), 3 * R * 4 * N * 2, [R, 4 * N])
+    # + the uvqk bias gradient in the same pass (partial rows + column sweep included)
+    rec("silu_bwd_colsum", timed(lambda: kernels.silu_bwd_colsum(uvqk, dyu), flush), 3 * R * 4 * N * 2,
+        [R, 4 * N])
+    dyn = dyu[:, :N].contiguous()
+    rec("colsum", timed(lambda: kernels.colsum(dyn), flush), R * N * 2, [R, N])
     xa = torch.randn(R, N, device=dev).bfloat16()
     u = uvqk[:, :N]
     g_, b_ = torch.ones(N, device=dev), torch.zeros(N, device=dev)
