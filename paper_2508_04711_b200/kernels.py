@@ -580,7 +580,7 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
 # (~2 H W sum(L) bytes, within the budget) + O(W B) for the window copies.  The
 # tiles run at the two-kernel rate (~750 TF/s at long L vs ~520 for the fused
 # kernel, profiles/r2_ncu_summary.md).
-WINDOWED_BWD = {"enabled": True}
+WINDOWED_BWD = {"enabled": True, "calls": 0}  # calls: completed windowed backward calls
 WINDOW_Q_CHUNK = 16384
 
 
@@ -691,6 +691,7 @@ def _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, segs, W, ou
             dv.index_copy_(0, idx, dv_w.to(dv.dtype))
         d_w += dwi
     del ds_buf, kvw, tsw, dkvw
+    WINDOWED_BWD["calls"] += 1
     if dk32 is not None and not accumulate_dkv:
         dk, dv = dk32.to(torch.bfloat16), dv32.to(torch.bfloat16)
         if out is not None:

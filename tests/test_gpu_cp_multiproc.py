@@ -51,9 +51,12 @@ def _batch(seed, rank, dist_kind, B):
     return dict(q=q, k=k, v=v, g=g, ts=ts, offsets=offs)
 
 
-def _worker(rank, world, port, dist_kind, B, mode, overlap, out_dir, protocol="alltoall", retain=False):
+def _worker(rank, world, port, dist_kind, B, mode, overlap, out_dir, protocol="alltoall", retain=False,
+            budget=None):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if budget:  # a dS budget below the calls' whole-segment scratch: the windowed backward
+        os.environ["JH_DS_SCRATCH_BUDGET"] = budget
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2508_04711_b200.cp_layer import CPAttention, HostStagedComm
@@ -68,21 +71,27 @@ def _worker(rank, world, port, dist_kind, B, mode, overlap, out_dir, protocol="a
         out, ctx = layer.forward(t["q"], t["k"], t["v"], ts, lens, w)
         dq, dk, dv, dw = layer.backward(ctx, t["g"], w)
     torch.cuda.synchronize()
+    if budget:
+        from paper_2508_04711_b200 import kernels
+        assert kernels.WINDOWED_BWD["calls"] > 0, "the windowed backward did not run"
     f = lambda x: x.float().cpu().numpy()  # noqa: E731
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), out=f(out), dq=f(dq), dk=f(dk), dv=f(dv),
              dw=dw.double().cpu().numpy())
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,dist_kind,B,mode,overlap,protocol,retain", [
-    (2, "uniform", 3, "balanced_minichunk", True, "alltoall", False),
-    (2, "uniform", 3, "naive_contiguous", False, "alltoall", False),
-    (2, "uniform", 3, "balanced_minichunk", True, "allgather_split", True),
-    (4, "lognormal", 3, "balanced_minichunk", True, "alltoall", False),
-    (4, "lognormal", 2, "naive_contiguous", True, "allgather_split", False),
+@pytest.mark.parametrize("world,dist_kind,B,mode,overlap,protocol,retain,budget", [
+    (2, "uniform", 3, "balanced_minichunk", True, "alltoall", False, None),
+    (2, "uniform", 3, "naive_contiguous", False, "alltoall", False, None),
+    (2, "uniform", 3, "balanced_minichunk", True, "allgather_split", True, None),
+    (4, "lognormal", 3, "balanced_minichunk", True, "alltoall", False, None),
+    (4, "lognormal", 2, "naive_contiguous", True, "allgather_split", False, None),
+    (2, "uniform", 3, "balanced_minichunk", True, "alltoall", False, "2e6"),
+    (2, "uniform", 3, "naive_contiguous", True, "alltoall", True, "2e6"),
 ])
-def test_cuda_cp_layer_matches_oracle(tmp_path, world, dist_kind, B, mode, overlap, protocol, retain):
-    mp.spawn(_worker, args=(world, _free_port(), dist_kind, B, mode, overlap, str(tmp_path), protocol, retain),
+def test_cuda_cp_layer_matches_oracle(tmp_path, world, dist_kind, B, mode, overlap, protocol, retain, budget):
+    mp.spawn(_worker, args=(world, _free_port(), dist_kind, B, mode, overlap, str(tmp_path), protocol, retain,
+                            budget),
              nprocs=world, join=True)
     batches = [_batch(17, r, dist_kind, B) for r in range(world)]
     cat = oracle.concat_batches(batches)
