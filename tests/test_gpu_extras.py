@@ -415,3 +415,30 @@ def test_bwd_windowed_segment_form_matches_full(monkeypatch):
         print(f"segment-form windowed W={calls[0]} {name}: row err vs whole-segment path {err:.2e}")
         assert err <= 5e-3, name
     assert np.abs(win[3] - full[3]).max() / np.abs(full[3]).max() <= DW_TOL
+
+
+def test_bwd_windowed_into_strided_out(monkeypatch):
+    # the HSTU layer's call shape: dq / dk / dv written into column views of one
+    # d(uvqk) buffer (row stride 4 H d) -- windowed under a small budget equals
+    # the whole-sequence two-kernel path bit for bit on dk / dv rows
+    from paper_2508_04711_b200 import kernels
+    lens, H = [2500, 3, 900], 2
+    case = make_case(lens, H * 128, seed=12)
+    c = to_cuda(case)
+    offs_h = np.asarray(case["offsets"], dtype=np.int64)
+    T, n = int(offs_h[-1]), H * 128
+    full = kernels.attn_bwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], c["g"], H, c["w"], 16,
+                            deterministic=True, seg_host=(offs_h, None, None))
+    buf = torch.full((T, 4 * n), 7.0, dtype=torch.bfloat16, device="cuda")
+    views = (buf[:, n:2 * n], buf[:, 2 * n:3 * n], buf[:, 3 * n:])
+    monkeypatch.setenv("JH_DS_SCRATCH_BUDGET", str(8 << 20))
+    calls0 = kernels.WINDOWED_BWD["calls"]
+    res = kernels.attn_bwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], c["g"], H, c["w"], 16,
+                           seg_host=(offs_h, None, None), out=views)
+    torch.cuda.synchronize()
+    assert kernels.WINDOWED_BWD["calls"] == calls0 + 1
+    assert torch.equal(buf[:, :n], torch.full_like(buf[:, :n], 7.0))  # columns outside the views untouched
+    for name, a, b in zip(("dq", "dk", "dv"), views, full[:3]):
+        err = row_rel(a.float().cpu().numpy(), b.float().cpu().numpy())[1]
+        assert err <= 1e-2, (name, err)
+    assert np.abs(res[3].cpu().numpy() - full[3].cpu().numpy()).max() / np.abs(full[3].cpu().numpy()).max() <= DW_TOL
