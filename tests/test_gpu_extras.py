@@ -419,8 +419,8 @@ def test_bwd_windowed_segment_form_matches_full(monkeypatch):
 
 def test_bwd_windowed_into_strided_out(monkeypatch):
     # the HSTU layer's call shape: dq / dk / dv written into column views of one
-    # d(uvqk) buffer (row stride 4 H d) -- windowed under a small budget equals
-    # the whole-sequence two-kernel path bit for bit on dk / dv rows
+    # d(uvqk) buffer (row stride 4 H d) -- windowed under a small budget matches
+    # the whole-sequence two-kernel path and leaves the other columns untouched
     from paper_2508_04711_b200 import kernels
     lens, H = [2500, 3, 900], 2
     case = make_case(lens, H * 128, seed=12)
