@@ -207,9 +207,12 @@ def run_gpu(args):
         bwd_two_kernel = kernels.ds_scratch_bytes(H, h["offsets"]) <= kernels.ds_scratch_budget(dev)
 
         def step_fn(prof=None):
-            kernels.attn_fwd(q, k, v, ts, ts, offs, H, w, NB, prof=None if prof is None else prof[0], band_table=band)
-            return kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, NB, prof=None if prof is None else prof[1],
-                                    seg_host=seg_host, band_table=band)
+            if prof is None:  # forward and backward concurrently on two streams (kernels.attn_fwd_bwd)
+                return kernels.attn_fwd_bwd(q, k, v, ts, offs, g, H, w, NB, seg_host=seg_host, band_table=band)[1:]
+            # the per-kernel (roofline) pass: the two calls in sequence, CUDA events around each kernel
+            kernels.attn_fwd(q, k, v, ts, ts, offs, H, w, NB, prof=prof[0], band_table=band)
+            return kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, NB, prof=prof[1], seg_host=seg_host,
+                                    band_table=band)
         tokens_total = T
         flat_lens = [int(x) for x in lens]
 
@@ -292,7 +295,9 @@ def run_gpu(args):
                                                                 else f"cp{cp_size}xdp{world // cp_size}"),
                    "cp_protocol": None if world == 1 else args.protocol,
                    "l2": "flushed between timed steps (512 MiB write, outside the timed events)",
-                   "cuda_graph": graph is not None},
+                   "cuda_graph": graph is not None,
+                   "schedule": ("band table, then forward || backward on two streams (kernels.attn_fwd_bwd; the HSTU "
+                                "backward recomputes from q, k, v)") if world == 1 else "CP layer forward, backward"},
         "tflops": F / (ms_per_step / 1e3) / 1e12,
         "tensor_frac_step": F / (ms_per_step / 1e3) / (world * peak * 1e12),
         "gpu_launches": int(launches),

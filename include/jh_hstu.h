@@ -202,6 +202,13 @@ JH_API size_t jh_attn_ds_scratch_bytes_segs(const int64_t* q_offsets, const int6
                                             int64_t num_segments, int32_t num_heads);
 
 /* Forward: attention.py:125 hstu_attention_reference / :151 blockwise_partial. */
+/* The band table alone (exact bucket bytes of the near-diagonal pairs) into
+ * a->band_table, from q_offsets / q_pos0 / kv_start / kv_len, ts_q, ts_k and
+ * num_buckets (other fields ignored).  A forward / backward call then takes it
+ * with band_table_ready = 1, so the two can run concurrently on two streams
+ * (the HSTU backward recomputes from q, k, v and never reads the forward's
+ * output: attention.py:187-234). */
+JH_API int jh_attn_band(const jh_attn_args* a, void* stream);
 JH_API int jh_attn_fwd(const jh_attn_args* a, void* stream);
 /* Backward: attention.py:187 hstu_attention_backward (dq, dk, dv, d_ts_weights). */
 JH_API int jh_attn_bwd(const jh_attn_args* a, void* stream);

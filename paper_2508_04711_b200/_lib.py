@@ -81,6 +81,7 @@ SIGNATURES = {
                                         c_vp, c_vp, ctypes.c_int64, ctypes.c_int32, c_vp, ctypes.c_int64, c_vp,
                                         ctypes.c_int64, c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp]),
     "jh_attn_fwd": (ctypes.c_int, [ctypes.POINTER(JhAttnArgs), c_vp]),
+    "jh_attn_band": (ctypes.c_int, [ctypes.POINTER(JhAttnArgs), c_vp]),
     "jh_attn_bwd": (ctypes.c_int, [ctypes.POINTER(JhAttnArgs), c_vp]),
     "jh_gather_rows": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int64, ctypes.c_int64, c_vp]),
     "jh_scatter_rows": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int64, ctypes.c_int64, c_vp]),

@@ -357,6 +357,36 @@ size_t jh_attn_workspace_bytes(int64_t q_rows, int64_t kv_len_total, int64_t num
   return std::max(a.total, b.total) + 256;
 }
 
+int jh_attn_band(const jh_attn_args* a, void* stream) {
+  // the band table alone (exact near-diagonal buckets): reads q_offsets /
+  // q_pos0 / kv_start / kv_len, ts_q, ts_k, num_buckets; writes a->band_table
+  if (!a) return set_error(JH_ERR_INVALID, "args is NULL");
+  if (a->num_segments < 0 || a->q_rows < 0) return set_error(JH_ERR_INVALID, "negative size");
+  if (a->num_buckets < 1 || a->num_buckets > 256) return set_error(JH_ERR_INVALID, "num_buckets must be in [1, 256]");
+  if (a->q_rows == 0 || a->num_segments == 0 || a->num_pos > 0) return JH_OK;  // (no band with a positional bias)
+  if (!a->q_offsets || !a->ts_q || !a->ts_k) return set_error(JH_ERR_INVALID, "NULL q_offsets / ts_q / ts_k");
+  if (!a->band_table || (uintptr_t)a->band_table % 16 ||
+      a->band_table_bytes < band_bytes(a->q_rows, a->num_segments))
+    return set_error(JH_ERR_INVALID, "band_table missing, smaller than jh_attn_band_table_bytes() or misaligned");
+  const BiasTable* bt = bias_table_cached(a->num_buckets);
+  if (!bt) return set_error(JH_ERR_INVALID, "num_buckets must be >= 1");
+  if (bt->cap >= 0xFFFFFFFFll)
+    return set_error(JH_ERR_UNSUPPORTED, "fused attention supports num_buckets <= 23 (got %d)", a->num_buckets);
+  DevBiasTable bias;
+  for (int i = 0; i < 64; ++i) {
+    bias.thr[i] = bt->thr[i];
+    bias.base[i] = bt->base[i];
+  }
+  bias.cap = bt->cap;
+  bias.nb = a->num_buckets;
+  const SegArgs seg{a->q_offsets, a->q_pos0, a->kv_start, a->kv_len, a->num_segments};
+  const size_t warps = (band_groups_bound(a->q_rows, a->num_segments) + 1) * kBandNW;
+  band_table_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, (cudaStream_t)stream>>>(seg, a->ts_q, a->ts_k, bias,
+                                                                                   (uint8_t*)a->band_table);
+  cudaError_t e = cudaGetLastError();
+  return e ? set_error(JH_ERR_CUDA, "band_table: %s", cudaGetErrorString(e)) : JH_OK;
+}
+
 int jh_attn_fwd(const jh_attn_args* a, void* stream) {
   int rc = validate(a, false);
   if (rc) return rc;

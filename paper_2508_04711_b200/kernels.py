@@ -293,14 +293,15 @@ def _effective_buckets(num_buckets: int, ts_q, ts_k) -> int:
 
 def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=16, pos_weights=None,
              q_pos0=None, kv_start=None, kv_len=None, kv_len_total=None, out=None, prof=None, out_accum=None,
-             accumulate=False, band_table=None, dbg_buckets=None):
+             accumulate=False, band_table=None, dbg_buckets=None, band_ready=False):
     """Fused jagged HSTU forward (jh_attn_fwd).  bf16 in/out, fp32 weights.
 
     ``out_accum`` (fp32, q's shape): write the fp32 result there instead of a
     bf16 ``out`` (``accumulate=True``: add it; rows that see no kv are left
     untouched) -- the additive partials of the CP pipeline (cp_engine.py:441-450).
     ``band_table`` (uint8, ``band_table_bytes``): the near-diagonal bucket table
-    is computed into it, for a backward call on the same inputs to reuse.
+    is computed into it, for a backward call on the same inputs to reuse
+    (``band_ready=True``: it already holds the table, see ``compute_band``).
     Head dims below 64 (or between 64 and 128) are zero-padded; the score scale
     stays 1/sqrt(head_dim).  ``dbg_buckets`` (uint8 [q_rows, max_kv], tests):
     the bucket the kernel applied to each visible pair of head 0."""
@@ -337,7 +338,7 @@ def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=
     ws, nbytes = _workspace(q.shape[0], q.shape[0] if kv_len_total is None else kv_len_total, a.num_segments,
                             H, dp, q.device)
     a.workspace, a.workspace_bytes = ws.data_ptr(), nbytes
-    _band(a, band_table, ready=False)
+    _band(a, band_table, ready=band_ready)
     if dbg_buckets is not None:
         if dbg_buckets.dtype != torch.uint8 or dbg_buckets.dim() != 2 or dbg_buckets.shape[0] < q.shape[0] \
                 or dbg_buckets.stride(1) != 1:
@@ -345,10 +346,73 @@ def attn_fwd(q, k, v, ts_q, ts_k, q_offsets, num_heads, ts_weights, num_buckets=
         a.dbg_buckets, a.dbg_ld = dbg_buckets.data_ptr(), dbg_buckets.stride(0)
     _prof(a, prof)
     check(_lib.lib().jh_attn_fwd(ctypes.byref(a), _stream(q)), "hstu_attention forward")
-    _bump(2 if pw is not None else 3)  # (band table) + work-list build + fused forward
+    _bump(2 if (pw is not None or band_ready) else 3)  # (band table) + work-list build + fused forward
     if dp != d:
         ret.copy_(_unpad_heads(acc, H, d, dp))
     return ret
+
+
+def compute_band(q, ts_q, ts_k, q_offsets, num_heads, num_buckets, band_table, q_pos0=None, kv_start=None,
+                 kv_len=None):
+    """The near-diagonal bucket table alone (jh_attn_band) into ``band_table``,
+    for forward / backward calls with ``band_ready`` / ``band_table``."""
+    _require_cuda("band_table", band_table, torch.uint8)
+    a = JhAttnArgs()
+    for name, t in (("ts_q", ts_q), ("ts_k", ts_k), ("q_offsets", q_offsets)):
+        _require_cuda(name, t, torch.int64)
+    a.q_offsets, a.ts_q, a.ts_k = q_offsets.data_ptr(), ts_q.data_ptr(), ts_k.data_ptr()
+    a.q_pos0 = None if q_pos0 is None else q_pos0.data_ptr()
+    a.kv_start = None if kv_start is None else kv_start.data_ptr()
+    a.kv_len = None if kv_len is None else kv_len.data_ptr()
+    a.num_segments, a.q_rows, a.num_heads = q_offsets.numel() - 1, q.shape[0], int(num_heads)
+    a.num_buckets = int(num_buckets)
+    a.band_table, a.band_table_bytes = band_table.data_ptr(), band_table.numel()
+    check(_lib.lib().jh_attn_band(ctypes.byref(a), _stream(q)), "band table")
+    _bump()
+
+
+_FB_STREAMS: dict = {}
+
+
+def attn_fwd_bwd(q, k, v, ts, q_offsets, dout, num_heads, ts_weights, num_buckets=16, seg_host=None,
+                 band_table=None, out=None, grads_out=None):
+    """Forward AND backward of the same jagged batch (self-attention), the two
+    running concurrently on two side streams after one band-table launch: the
+    HSTU backward recomputes S and P from q, k, v (attention.py:187-234) and
+    never reads the forward's output, so the forward's tail and the
+    backward's head share the GPU (C2: ~2 % of the step).  Returns (out, dq,
+    dk, dv, d_ts_weights); ``out`` / ``grads_out`` = preallocated bf16 tensors
+    as in attn_fwd / attn_bwd(out=)."""
+    dev = q.device
+    nb = int(num_buckets)
+    if nb > FUSED_NB_MAX:  # (the effective-bucket path syncs anyway: keep it simple)
+        o = attn_fwd(q, k, v, ts, ts, q_offsets, num_heads, ts_weights, nb, out=out)
+        g = attn_bwd(q, k, v, ts, ts, q_offsets, dout, num_heads, ts_weights, nb, seg_host=seg_host, out=grads_out)
+        return (o,) + tuple(g[:4])
+    if band_table is None:
+        band_table = new_band_table(q.shape[0], q_offsets.numel() - 1, dev)
+    main = torch.cuda.current_stream(dev)
+    compute_band(q, ts, ts, q_offsets, num_heads, nb, band_table)
+    key = (dev.index, main.cuda_stream)
+    if key not in _FB_STREAMS:
+        _FB_STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    s_f, s_b = _FB_STREAMS[key]
+    s_f.wait_stream(main)
+    s_b.wait_stream(main)
+    for t in (q, k, v, ts, q_offsets, dout, band_table):
+        t.record_stream(s_f)
+        t.record_stream(s_b)
+    with torch.cuda.stream(s_f):
+        o = attn_fwd(q, k, v, ts, ts, q_offsets, num_heads, ts_weights, nb, out=out, band_table=band_table,
+                     band_ready=True)
+    with torch.cuda.stream(s_b):
+        dq, dk, dv, dw, _ = attn_bwd(q, k, v, ts, ts, q_offsets, dout, num_heads, ts_weights, nb, seg_host=seg_host,
+                                     band_table=band_table, out=grads_out)
+    main.wait_stream(s_f)
+    main.wait_stream(s_b)
+    for t in (o, dq, dk, dv, dw):
+        t.record_stream(main)
+    return o, dq, dk, dv, dw
 
 
 # Backward variant.  None = auto: the two-kernel path (dK/dV kernel writes bf16

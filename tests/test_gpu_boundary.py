@@ -223,3 +223,28 @@ def test_host_streaming_async_back_to_back():
         for a, b in zip(got[:4], ref[:4]):
             assert torch.equal(a, b)
         np.testing.assert_allclose(got[4].numpy(), ref[4].numpy(), rtol=1e-6, atol=1e-9)
+
+
+def test_attn_fwd_bwd_concurrent_equals_sequential():
+    # kernels.attn_fwd_bwd (band table once, forward || backward on two streams)
+    # gives exactly the results of the two calls in sequence
+    from paper_2508_04711_b200 import kernels
+    lens = [300, 0, 17, 129, 1, 700]
+    H, d = 2, 128
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    T = int(offs[-1])
+    rng = np.random.default_rng(31)
+    q, k, v, g = (torch.from_numpy(rng.standard_normal((T, H * d)).astype(np.float32)).bfloat16().cuda()
+                  for _ in range(4))
+    ts = torch.from_numpy(np.cumsum(rng.integers(1, 10**6, T)).astype(np.int64)).cuda()
+    o_ = torch.from_numpy(offs).cuda()
+    w = torch.from_numpy(oracle.normal_init_ts_weights(16, 4).astype(np.float32)).cuda()
+    want_o = kernels.attn_fwd(q, k, v, ts, ts, o_, H, w, 16)
+    want = kernels.attn_bwd(q, k, v, ts, ts, o_, g, H, w, 16, seg_host=(offs, None, None))
+    for _ in range(2):
+        got = kernels.attn_fwd_bwd(q, k, v, ts, o_, g, H, w, 16, seg_host=(offs, None, None))
+        torch.cuda.synchronize()
+        assert torch.equal(got[0], want_o)
+        for a, b in zip(got[1:4], want[:3]):
+            assert torch.equal(a, b)
+        np.testing.assert_allclose(got[4].cpu().numpy(), want[3].cpu().numpy(), rtol=1e-6, atol=1e-9)
