@@ -395,19 +395,22 @@ def attn_fwd_bwd(q, k, v, ts, q_offsets, dout, num_heads, ts_weights, num_bucket
     compute_band(q, ts, ts, q_offsets, num_heads, nb, band_table)
     key = (dev.index, main.cuda_stream)
     if key not in _FB_STREAMS:
-        _FB_STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+        # the backward (the longer one) on a higher-priority stream and enqueued
+        # first: its CTAs take the SMs, the forward's fill the backward's tail
+        lo, hi = torch.cuda.Stream.priority_range()
+        _FB_STREAMS[key] = (torch.cuda.Stream(dev, priority=lo), torch.cuda.Stream(dev, priority=hi))
     s_f, s_b = _FB_STREAMS[key]
     s_f.wait_stream(main)
     s_b.wait_stream(main)
     for t in (q, k, v, ts, q_offsets, dout, band_table):
         t.record_stream(s_f)
         t.record_stream(s_b)
-    with torch.cuda.stream(s_f):
-        o = attn_fwd(q, k, v, ts, ts, q_offsets, num_heads, ts_weights, nb, out=out, band_table=band_table,
-                     band_ready=True)
     with torch.cuda.stream(s_b):
         dq, dk, dv, dw, _ = attn_bwd(q, k, v, ts, ts, q_offsets, dout, num_heads, ts_weights, nb, seg_host=seg_host,
                                      band_table=band_table, out=grads_out)
+    with torch.cuda.stream(s_f):
+        o = attn_fwd(q, k, v, ts, ts, q_offsets, num_heads, ts_weights, nb, out=out, band_table=band_table,
+                     band_ready=True)
     main.wait_stream(s_f)
     main.wait_stream(s_b)
     for t in (o, dq, dk, dv, dw):

@@ -25,7 +25,8 @@ band_f = kernels.new_band_table(q.shape[0], offs.numel() - 1, dev)
 band_b = kernels.new_band_table(q.shape[0], offs.numel() - 1, dev)
 kernels.attn_fwd(q, k, v, ts, ts, offs, H, w, 16, band_table=band_b)  # band_b computed once, reused ready
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-sf, sb = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+PRI = os.environ.get("PRI", "0,0").split(",")  # stream priorities (fwd, bwd): lower = higher priority
+sf, sb = torch.cuda.Stream(dev, priority=int(PRI[0])), torch.cuda.Stream(dev, priority=int(PRI[1]))
 
 
 def serial():
@@ -72,5 +73,5 @@ def graph_time(fn, n=30):
 
 
 for rep in range(2):
-    print(f"serial {graph_time(serial):.1f} us | fwd || bwd (fwd first) {graph_time(two_streams):.1f} us | "
+    print(f"[prio fwd,bwd = {PRI}] serial {graph_time(serial):.1f} us | fwd || bwd (fwd first) {graph_time(two_streams):.1f} us | "
           f"(bwd first) {graph_time(lambda: two_streams(True)):.1f} us", flush=True)
