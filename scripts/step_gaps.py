@@ -25,8 +25,11 @@ band = kernels.new_band_table(q.shape[0], offs.numel() - 1, q.device)
 
 
 def step():
-    kernels.attn_fwd(q, k, v, ts, ts, offs, H, w, 16, band_table=band)
-    kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, 16, seg_host=seg, band_table=band)
+    if os.environ.get("SERIAL"):
+        kernels.attn_fwd(q, k, v, ts, ts, offs, H, w, 16, band_table=band)
+        kernels.attn_bwd(q, k, v, ts, ts, offs, g, H, w, 16, seg_host=seg, band_table=band)
+    else:  # the bench's step: band table, then forward || backward on two streams
+        kernels.attn_fwd_bwd(q, k, v, ts, offs, g, H, w, 16, seg_host=seg, band_table=band)
 
 
 for _ in range(3):
