@@ -736,7 +736,9 @@ def _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, segs, W, ou
     d_w = torch.zeros(num_buckets, dtype=torch.float64, device=dev)
     for o_a, qp_a, kl_a, host, c, _ in wins:
         m = qp_a.size
-        t = torch.from_numpy(host).to(dev)
+        # (pinned + non-blocking: a pageable copy would make the host wait for the
+        # previous window's kernels before it can queue this one's)
+        t = torch.from_numpy(host).pin_memory().to(dev, non_blocking=True)
         idx = t[4 * m + 1:]
         k_w, v_w, ts_w = kvw[0, :c], kvw[1, :c], tsw[:c]
         torch.index_select(k, 0, idx, out=k_w)
