@@ -58,7 +58,10 @@ class BiasParams:
         object.__setattr__(self, "ts_weights", w)
 
     def device_weights(self, device) -> torch.Tensor:
-        return torch.from_numpy(np.ascontiguousarray(self.ts_weights, dtype=np.float32)).to(device, non_blocking=True)
+        t = torch.from_numpy(np.ascontiguousarray(self.ts_weights, dtype=np.float32))
+        if torch.device(device).type == "cuda":  # (pinned: a pageable copy would wait for the stream)
+            t = t.pin_memory()
+        return t.to(device, non_blocking=True)
 
 
 def silu(x):

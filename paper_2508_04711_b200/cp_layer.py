@@ -198,7 +198,9 @@ class TorchComm:
         row = np.zeros(self.MAX_SEQS + 1, dtype=np.int64)
         row[0] = loc.size
         row[1:1 + loc.size] = loc
-        send = torch.from_numpy(row).to(dev, non_blocking=dev.type == "cuda")
+        t_row = torch.from_numpy(row)
+        # (pinned: a pageable host->device copy makes the host wait for the stream first)
+        send = t_row.pin_memory().to(dev, non_blocking=True) if dev.type == "cuda" else t_row
         full = torch.empty((self.size, self.MAX_SEQS + 1), dtype=torch.int64, device=dev)
         self._all_gather(list(full.unbind(0)), send)
         if dev.type == "cuda":

@@ -121,8 +121,17 @@ def new_jagged(values, offsets, max_length: int, device=None, dtype=DEFAULT_DTYP
     v = vals.to(device=dev, dtype=dtype, non_blocking=True).contiguous()
     if copy and v.data_ptr() == getattr(values, "data_ptr", lambda: None)():
         v = v.clone()  # the container owns its storage (jagged.py:95)
-    o = torch.from_numpy(offs).to(dev, non_blocking=True)
+    o = _h2d(offs, dev)
     return JaggedTensor(v, o, int(max_length), offs)
+
+
+def _h2d(a: np.ndarray, dev) -> torch.Tensor:
+    """Host int64 array -> device without stalling the host (a pageable
+    host->device copy first waits for the stream to drain)."""
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if torch.device(dev).type == "cuda":
+        t = t.pin_memory()
+    return t.to(dev, non_blocking=True)
 
 
 def new_int_series(values, offsets, device=None) -> JaggedIntSeries:
@@ -135,7 +144,7 @@ def new_int_series(values, offsets, device=None) -> JaggedIntSeries:
     offs = _host_offsets(offsets)
     _check_offsets(offs, vals.shape[0])
     v = vals.to(device=dev, dtype=torch.int64, non_blocking=True).contiguous()
-    return JaggedIntSeries(v, torch.from_numpy(offs).to(dev, non_blocking=True), offs)
+    return JaggedIntSeries(v, _h2d(offs, dev), offs)
 
 
 def lengths(jt) -> np.ndarray:
@@ -261,7 +270,7 @@ def reorder_balanced(jt: JaggedTensor, layout: MiniChunkLayout):
     if tuple(int(x) for x in lengths(jt)) != layout.seq_lengths():
         raise ValueError("layout chunk lengths do not sum to the tensor's sequence lengths")
     perm_h, _ = rank_major_perm(jt.host_offsets, layout.cp_size, _mode_of(layout))
-    perm = torch.from_numpy(perm_h).to(jt.values.device, non_blocking=True)
+    perm = _h2d(perm_h, jt.values.device)
     vals = kernels.gather_rows(jt.values, perm)
     return JaggedTensor(vals, jt.offsets, jt.max_length, jt.host_offsets), perm
 
@@ -290,6 +299,6 @@ def padded_to_jagged(padded: torch.Tensor, offsets, max_length: int | None = Non
     """(new) inverse of jagged_to_padded."""
     offs = _host_offsets(offsets)
     dev = padded.device
-    o = torch.from_numpy(offs).to(dev)
+    o = _h2d(offs, dev)
     vals = kernels.padded_to_jagged(padded, o, int(offs[-1]))
     return JaggedTensor(vals, o, int(padded.shape[1] if max_length is None else max_length), offs)
