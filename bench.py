@@ -383,7 +383,10 @@ def run_gpu(args):
                 prev = cur
             prev.wait()
 
-        run(max(args.warmup, 3) + 2)  # (warm-up in the same two-in-flight pattern: every buffer exists)
+        # warm-up in the same two-in-flight pattern, long enough for the caching
+        # allocators to hold every buffer of two calls in flight (the first ~8
+        # calls of a process allocate: scripts/e2e_pipe_probe.py)
+        run(max(args.warmup, 3) + 9)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)

@@ -334,6 +334,36 @@ def _as_pinned(x, dtype):
 
 
 _STREAMS: dict = {}
+_PIN_RING: dict = {}
+_PIN_SLOTS = 8
+
+
+class _PinSlot:
+    """Page-locked staging buffers of one in-flight host-streaming call
+    (segment offsets, ts_weights, d_ts_weights).  Allocating page-locked memory
+    per call stalled the host for tens of ms in the first calls of a process
+    (scripts/e2e_pipe_probe.py); a ring of slots reuses them once the call that
+    last used the slot has finished."""
+
+    def __init__(self):
+        self.event = None
+        self.bufs = {}
+
+    def get(self, name, n, dtype):
+        b = self.bufs.get(name)
+        if b is None or b.numel() < n or b.dtype != dtype:
+            b = torch.empty(max(n, 64), dtype=dtype, pin_memory=True)
+            self.bufs[name] = b
+        return b[:n]
+
+
+def _pin_slot(dev) -> _PinSlot:
+    ring = _PIN_RING.setdefault(dev, {"slots": [_PinSlot() for _ in range(_PIN_SLOTS)], "k": 0})
+    slot = ring["slots"][ring["k"] % _PIN_SLOTS]
+    ring["k"] += 1
+    if slot.event is not None:
+        slot.event.synchronize()  # (normally long done: _PIN_SLOTS calls ago)
+    return slot
 
 
 def _stream_cuts(offs: np.ndarray, G: int) -> list:
@@ -361,7 +391,8 @@ class HostStreamResult:
     def wait(self):
         self._event.synchronize()
         self._keep = None
-        return self._results
+        r = self._results
+        return r[0], r[1], r[2], r[3], r[4].clone()  # (d_ts_weights: out of the reused staging slot)
 
 
 def hstu_attention_fwd_bwd_host_async(q, k, v, ts, offsets, upstream, ts_weights, num_heads: int = 1,
@@ -397,9 +428,19 @@ def hstu_attention_fwd_bwd_host_async(q, k, v, ts, offsets, upstream, ts_weights
     s_in, s_out = _STREAMS[dev]
     main = torch.cuda.current_stream(dev)
     runs = []
+    slot = _pin_slot(dev)
+    subs = [offs[cuts[gi]:cuts[gi + 1] + 1] - offs[cuts[gi]] for gi in range(G)]
+    pos = [0]
+    for x in subs:  # each run's offsets at a 64-byte aligned position
+        pos.append(pos[-1] + (x.size + 7) // 8 * 8)
+    offs_pin = slot.get("offs", pos[-1], torch.int64)
+    for x, p0 in zip(subs, pos):
+        offs_pin.numpy()[p0:p0 + x.size] = x
     # (no wait on the caller's stream: the copies read host memory into fresh
     # buffers, so the next call's inputs can copy in while this one still runs)
     with torch.cuda.stream(s_in):
+        offs_dev = offs_pin.to(dev, non_blocking=True)
+        offs_dev.record_stream(main)
         # every run's inputs are enqueued first, so the host's launch overhead of the
         # runs below overlaps the copies instead of delaying them; the device inputs
         # are allocated once and filled run by run (slice copies into one buffer run
@@ -412,18 +453,21 @@ def hstu_attention_fwd_bwd_host_async(q, k, v, ts, offsets, upstream, ts_weights
             r0, r1 = int(offs[b0]), int(offs[b1])
             if r1 == r0:
                 continue
-            sub = offs[b0:b1 + 1] - r0
+            sub = subs[gi]
             ins = []
             for dst, src in zip(dev_in, (qh, kh, vh, gh)):
                 dst[r0:r1].copy_(src[r0:r1], non_blocking=True)
                 ins.append(dst[r0:r1])
             ins.append(tsh[r0:r1].to(dev, non_blocking=True))  # (its own buffer: 16-byte aligned)
-            ins.append(torch.from_numpy(sub).pin_memory().to(dev, non_blocking=True))
+            ins.append(offs_dev[pos[gi]:pos[gi] + sub.size])
             ev = torch.cuda.Event()
             ev.record(s_in)
             runs.append((b0, b1, r0, r1, sub, ins, ev))
     # (after the copies are queued: nothing on the host delays the first one)
-    w = torch.as_tensor(np.asarray(ts_weights, dtype=np.float32)).pin_memory().to(dev, non_blocking=True)
+    w_np = np.asarray(ts_weights, dtype=np.float32).reshape(-1)
+    w_pin = slot.get("w", w_np.size, torch.float32)
+    w_pin.numpy()[:] = w_np
+    w = w_pin.to(dev, non_blocking=True)
     d_w = torch.zeros(num_buckets, dtype=torch.float64, device=dev)
     keep = []
     for b0, b1, r0, r1, sub, ins, ev in runs:
@@ -442,13 +486,14 @@ def hstu_attention_fwd_bwd_host_async(q, k, v, ts, offsets, upstream, ts_weights
                 src.record_stream(s_out)
                 dst[r0:r1].copy_(src, non_blocking=True)
         keep.append((o, gq, gk, gv))
-    dwh = torch.empty(num_buckets, dtype=torch.float64, pin_memory=True)
+    dwh = slot.get("dw", num_buckets, torch.float64)
     s_out.wait_stream(main)
     with torch.cuda.stream(s_out):
         d_w.record_stream(s_out)
         dwh.copy_(d_w, non_blocking=True)
         done = torch.cuda.Event()
         done.record(s_out)
+    slot.event = done
     return HostStreamResult(done, (outs[0], outs[1], outs[2], outs[3], dwh), keep)
 
 

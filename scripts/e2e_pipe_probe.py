@@ -28,10 +28,12 @@ for i in range(3):
 torch.cuda.synchronize()
 prev = None
 t_last = time.perf_counter()
-times = []
+times, submit = [], []
 for i in range(K):
+    t_s = time.perf_counter()
     cur = attention.hstu_attention_fwd_bwd_host_async(q, k, v, ts, h["offsets"], g, w, 4, 16, groups=2,
                                                       out=sets[i % 2])
+    submit.append((time.perf_counter() - t_s) * 1e3)
     if prev is not None:
         prev.wait()
     prev = cur
@@ -40,6 +42,7 @@ for i in range(K):
     t_last = t
 prev.wait()
 print("per-step ms:", " ".join(f"{x:.2f}" for x in times))
+print(f"host submit ms: mean {np.mean(submit):.3f} max {np.max(submit):.3f}")
 print("reserved GB", torch.cuda.memory_reserved() / 1e9, "num_alloc_retries",
       torch.cuda.memory_stats().get("num_alloc_retries"))
 try:
