@@ -75,3 +75,37 @@ def graph_time(fn, n=30):
 for rep in range(2):
     print(f"[prio fwd,bwd = {PRI}] serial {graph_time(serial):.1f} us | fwd || bwd (fwd first) {graph_time(two_streams):.1f} us | "
           f"(bwd first) {graph_time(lambda: two_streams(True)):.1f} us", flush=True)
+
+# the batch split into two halves of whole sequences, each half's fwd || bwd on its own stream pair
+import numpy as np  # noqa: E402
+offs_h = h["offsets"]
+B = offs_h.size - 1
+cut = int(np.searchsorted(offs_h, offs_h[-1] / 2))
+halves = []
+for b0, b1 in ((0, cut), (cut, B)):
+    r0, r1 = int(offs_h[b0]), int(offs_h[b1])
+    sub = offs_h[b0:b1 + 1] - r0
+    halves.append(dict(q=q[r0:r1], k=k[r0:r1], v=v[r0:r1], g=g[r0:r1], ts=ts[r0:r1].clone(),
+                       o=torch.from_numpy(sub).to(dev), seg=(sub, None, None),
+                       band=kernels.new_band_table(r1 - r0, b1 - b0, dev)))
+side = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+
+
+def split_step():
+    main = torch.cuda.current_stream(dev)
+    for s_, hh in zip(side, halves):
+        s_.wait_stream(main)
+        with torch.cuda.stream(s_):
+            kernels.attn_fwd_bwd(hh["q"], hh["k"], hh["v"], hh["ts"], hh["o"], hh["g"], H, w, 16, seg_host=hh["seg"],
+                                 band_table=hh["band"])
+    for s_ in side:
+        main.wait_stream(s_)
+
+
+def full_step():
+    kernels.attn_fwd_bwd(q, k, v, ts, offs, g, H, w, 16, seg_host=seg, band_table=band_f)
+
+
+for rep in range(2):
+    print(f"attn_fwd_bwd full batch {graph_time(full_step):.1f} us | two halves on two stream pairs "
+          f"{graph_time(split_step):.1f} us", flush=True)
