@@ -460,6 +460,14 @@ def run_gpu(args):
         del flush
         torch.cuda.empty_cache()
         result["max_seq_len"] = max_seq_len_probe(dev, w)
+    if world == 1:
+        from paper_2508_04711_b200.harness import protocol_memory_measured
+        lens4, _ = _c4_batch()
+        result["protocol_memory"] = {
+            "workload": "C4 per-rank batch (rank 0's 4 sequences, lognormal(ln 1024, 1.0), E=512) on every rank: "
+                        "per-rank transient bytes of redistributing q, k, v, ts (communication excluded, "
+                        "LoopbackComm)",
+            "rows": protocol_memory_measured(lens4[:4], (2, 4, 8), embed_dim=C4_E, num_heads=H, device=dev)}
     if world == 1 and args.cp_sweep_gb > 0:
         result["cp_sweep"] = cp_sweep(dev, args.cp_sweep_gb)
     if world > 1:

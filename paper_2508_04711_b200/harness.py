@@ -327,6 +327,43 @@ def sweep_max_tokens(budget_bytes: int, cp_sizes, embed_dim: int = 8, dtype: str
     return SweepReport(int(budget_bytes), embed_dim, dtype, seed, rows)
 
 
+def protocol_memory_measured(lengths, cp_sizes=(2, 4, 8), embed_dim: int = 512, num_heads: int = 4,
+                             num_buckets: int = 16, device=None) -> list:
+    """MEASURED per-rank transient memory of the batch -> sequence
+    redistribution of q, k, v, ts (CPAttention.redistribute) under the two
+    protocols -- the measured counterpart of ``redistribution_peaks``
+    (harness.py:256-267; the paper's -60 % for all-to-all).
+    Every rank holds ``lengths`` (cp_layer.LoopbackComm: one rank's buffers,
+    communication excluded).  Rows: cp, peak bytes above the inputs for
+    "alltoall" and "allgather_split", and their ratio."""
+    from .cp_layer import CPAttention, LoopbackComm
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    lens = np.asarray(lengths, dtype=np.int64)
+    T = int(lens.sum())
+    gen = torch.Generator(device=dev).manual_seed(3)
+    q, k, v = (torch.randn(T, embed_dim, device=dev, generator=gen).bfloat16() for _ in range(3))
+    ts = torch.cumsum(torch.randint(1, 10**6, (T,), device=dev, generator=gen), 0)
+    rows = []
+    for cp_size in cp_sizes:
+        row = {"cp_size": int(cp_size)}
+        for protocol in ("alltoall", "allgather_split"):
+            cp = CPAttention(None, num_heads, num_buckets, comm=LoopbackComm(cp_size, 0), protocol=protocol)
+            plan = cp.plan_for(lens, dev)
+            torch.cuda.synchronize(dev)
+            torch.cuda.empty_cache()
+            torch.cuda.reset_peak_memory_stats(dev)
+            base = torch.cuda.memory_allocated(dev)
+            res = [cp.redistribute(x, *plan) for x in (q, k, v)] + [cp.redistribute(ts.view(-1, 1), *plan)]
+            torch.cuda.synchronize(dev)
+            row[f"{protocol}_peak_bytes"] = int(torch.cuda.max_memory_allocated(dev) - base)
+            row[f"{protocol}_resident_rows"] = int(res[0].shape[0])
+            del res, cp, plan
+        row["allgather_split_over_alltoall"] = round(row["allgather_split_peak_bytes"] /
+                                                     max(row["alltoall_peak_bytes"], 1), 2)
+        rows.append(row)
+    return rows
+
+
 def sweep_max_tokens_measured(budget_bytes: int, cp_sizes=(1, 2, 4, 8), embed_dim: int = 512, num_heads: int = 4,
                               num_layers: int = 8, num_buckets: int = 16, seed: int = 7, granularity: int = 2048,
                               time_budget_s: float = 200.0, device=None, rel_precision: float = 1 / 128) -> SweepReport:

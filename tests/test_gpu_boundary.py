@@ -248,3 +248,15 @@ def test_attn_fwd_bwd_concurrent_equals_sequential():
         for a, b in zip(got[1:4], want[:3]):
             assert torch.equal(a, b)
         np.testing.assert_allclose(got[4].cpu().numpy(), want[3].cpu().numpy(), rtol=1e-6, atol=1e-9)
+
+
+def test_protocol_memory_measured():
+    # all-to-all moves each rank's own share; allgather_split materialises the
+    # whole group batch on every rank: its transient is larger, growing with cp
+    from paper_2508_04711_b200.harness import protocol_memory_measured
+    rows = protocol_memory_measured([700, 33, 1200, 5], (2, 4), embed_dim=256, num_heads=2)
+    assert [r["cp_size"] for r in rows] == [2, 4]
+    for r in rows:
+        assert r["alltoall_peak_bytes"] > 0 and r["allgather_split_peak_bytes"] > r["alltoall_peak_bytes"]
+        assert r["alltoall_resident_rows"] == r["allgather_split_resident_rows"]
+    assert rows[1]["allgather_split_over_alltoall"] > rows[0]["allgather_split_over_alltoall"]
