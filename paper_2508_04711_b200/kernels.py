@@ -673,18 +673,16 @@ def _windowed_plan(segs, H: int, budget: int, device, dq_bytes: int = 0):
     return W if W >= 128 else None
 
 
-def _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, segs, W, out, prof, dq_accum=None,
-                       accumulate_dkv=False, dkv_accum=None, unique_kv=False):
-    """Segment s: q rows [qo[s], qo[s+1]) at positions qp[s] + i against kv rows
-    ks[s] + j, j < kl[s] (kernels.attn_bwd's segment form; plain self-attention
-    is qp = 0, ks = qo, kl = lengths).  Window w = kv positions [wW, (w+1)W): the
-    q rows with position >= wW see it, in chunks of WINDOW_Q_CHUNK rows.  Every
-    window is planned first and the scratch / window buffers are allocated
-    once at their maximum: if they do not fit, None is returned before anything
-    was accumulated (the caller then runs the fused kernel)."""
-    dev = q.device
+def window_segments(segs, W: int, q_chunk: int) -> list:
+    """The windowed backward's decomposition (host, no GPU): for each kv window
+    w = positions [wW, (w+1)W) of every segment, the segment arrays of one
+    segment-form call -- (q_offsets, q_pos0, kv_len, host block, compact kv
+    rows) where the host block is [q_offsets, q_pos0, kv_start, kv_len, kv row
+    indices of the compact window copy].  ``segs`` = host (q_offsets, q_pos0,
+    kv_len, kv_start) of the original call.  Every visible (q, kv) pair of the
+    original call appears in exactly one window call (tests/test_windows.py)."""
     qo, qp, kl, ks = segs
-    wins = []
+    out = []
     nwin = int((int(kl.max(initial=0)) + W - 1) // W)
     for wi in range(nwin):
         w0 = wi * W
@@ -699,15 +697,29 @@ def _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, segs, W, ou
             if i0 > 0:  # rows before the window: empty segment
                 o.append(a + i0); qpn.append(0); ksn.append(0); kln.append(0)
             wl = min(W, n - w0)
-            for c0 in range(a + i0, b, WINDOW_Q_CHUNK):
-                o.append(min(b, c0 + WINDOW_Q_CHUNK)); qpn.append(p0 + (c0 - a) - w0); ksn.append(c); kln.append(wl)
+            for c0 in range(a + i0, b, q_chunk):
+                o.append(min(b, c0 + q_chunk)); qpn.append(p0 + (c0 - a) - w0); ksn.append(c); kln.append(wl)
             rows.append(np.arange(int(ks[s]) + w0, int(ks[s]) + w0 + wl, dtype=np.int64))
             c += wl
         if c == 0:
             continue
         o_a, qp_a, kl_a = (np.asarray(x, dtype=np.int64) for x in (o, qpn, kln))
         host = np.concatenate([o_a, qp_a, np.asarray(ksn, dtype=np.int64), kl_a] + rows)
-        wins.append((o_a, qp_a, kl_a, host, c, ds_scratch_bytes(H, o_a, qp_a, kl_a)))
+        out.append((o_a, qp_a, kl_a, host, c))
+    return out
+
+
+def _attn_bwd_windowed(q, k, v, ts_q, ts_k, dout, H, w, num_buckets, segs, W, out, prof, dq_accum=None,
+                       accumulate_dkv=False, dkv_accum=None, unique_kv=False):
+    """Segment s: q rows [qo[s], qo[s+1]) at positions qp[s] + i against kv rows
+    ks[s] + j, j < kl[s] (kernels.attn_bwd's segment form; plain self-attention
+    is qp = 0, ks = qo, kl = lengths).  Window w = kv positions [wW, (w+1)W): the
+    q rows with position >= wW see it, in chunks of WINDOW_Q_CHUNK rows.  Every
+    window is planned first and the scratch / window buffers are allocated
+    once at their maximum: if they do not fit, None is returned before anything
+    was accumulated (the caller then runs the fused kernel)."""
+    dev = q.device
+    wins = [w_ + (ds_scratch_bytes(H, w_[0], w_[1], w_[2]),) for w_ in window_segments(segs, W, WINDOW_Q_CHUNK)]
     if not wins:
         return None
     max_c = max(x[4] for x in wins)
