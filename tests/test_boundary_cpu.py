@@ -125,3 +125,21 @@ def test_generator_matches_reference_integer_stream():
         assert h["offsets"].tolist() == c["offsets"], c["cfg"]
         assert h["ts"].tolist() == c["ts"], c["cfg"]
         assert abs(float(np.asarray(h["q"], np.float64).sum()) - c["q_sum"]) <= 1e-9 * max(1.0, abs(c["q_sum"]))
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 8, 40])
+def test_host_streaming_cut_points(G):
+    # the host-streaming call's runs: whole sequences, every sequence in exactly
+    # one run, G clamped to the sequence count, ~T/G tokens per run
+    from paper_2508_04711_b200.attention import _stream_cuts
+    rng = np.random.default_rng(G)
+    lens = rng.integers(0, 1025, 32)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    g = max(1, min(G, lens.size))
+    cuts = _stream_cuts(offs, g)
+    assert cuts[0] == 0 and cuts[-1] == lens.size and len(cuts) == g + 1
+    assert all(b > a for a, b in zip(cuts, cuts[1:]))  # no empty run of sequences
+    sizes = [int(offs[b] - offs[a]) for a, b in zip(cuts, cuts[1:])]
+    assert sum(sizes) == int(offs[-1])
+    if g > 1:
+        assert max(sizes) <= int(offs[-1]) / g + int(lens.max())  # within one sequence of the even share
