@@ -442,3 +442,35 @@ def test_bwd_windowed_into_strided_out(monkeypatch):
         err = row_rel(a.float().cpu().numpy(), b.float().cpu().numpy())[1]
         assert err <= 1e-2, (name, err)
     assert np.abs(res[3].cpu().numpy() - full[3].cpu().numpy()).max() / np.abs(full[3].cpu().numpy()).max() <= DW_TOL
+
+
+@pytest.mark.parametrize("d,H", [(64, 4), (32, 2), (128, 1)])
+def test_new_paths_head_dims(monkeypatch, d, H):
+    # this round's paths at other head dims (64 native, 32 padded to 64, one
+    # 128-wide head): the two-stream fwd || bwd step equals the sequential
+    # calls bitwise; the windowed backward matches the whole-sequence one
+    from paper_2508_04711_b200 import kernels
+    lens = [900, 1, 333, 0, 1500]
+    case = make_case(lens, H * d, seed=d + H)
+    c = to_cuda(case)
+    offs_h = np.asarray(case["offsets"], dtype=np.int64)
+    seg = (offs_h, None, None)
+    o = kernels.attn_fwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], H, c["w"], 16)
+    full = kernels.attn_bwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], c["g"], H, c["w"], 16,
+                            seg_host=seg)
+    both = kernels.attn_fwd_bwd(c["q"], c["k"], c["v"], c["ts"], c["offsets"], c["g"], H, c["w"], 16, seg_host=seg)
+    torch.cuda.synchronize()
+    for a, b in zip(both[:4], (o,) + tuple(full[:3])):
+        assert torch.equal(a, b)
+    want = oracle.hstu_forward(case["q"], case["k"], case["v"], case["ts"], case["offsets"], case["w"], 16, H)
+    assert row_rel(o.float().cpu().numpy(), want)[1] <= ROW_TOL
+    if d == kernels.padded_head_dim(d):  # (the windowed path is for unpadded head dims)
+        # below the whole-sequence scratch (~H * sum L^2 bytes), above one 128-wide window
+        monkeypatch.setenv("JH_DS_SCRATCH_BUDGET", str(H * (2 << 20)))
+        n0 = kernels.WINDOWED_BWD["calls"]
+        win = kernels.attn_bwd(c["q"], c["k"], c["v"], c["ts"], c["ts"], c["offsets"], c["g"], H, c["w"], 16,
+                               seg_host=seg)
+        torch.cuda.synchronize()
+        assert kernels.WINDOWED_BWD["calls"] == n0 + 1
+        for a, b in zip(win[:3], full[:3]):
+            assert row_rel(a.float().cpu().numpy(), b.float().cpu().numpy())[1] <= 1e-2
