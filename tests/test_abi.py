@@ -151,3 +151,27 @@ def test_ds_scratch_exact_and_bound(L, seed):
     one = kernels.ds_scratch_bytes(4, np.array([0, 2048]), np.array([2048]), np.array([2048]))
     assert one == 4 * 16 * 32 * 16384
     assert L.jh_attn_ds_scratch_bytes(2048, 1, 4, 2048) >= one
+
+
+def test_attn_entry_points_validate_before_touching_the_gpu(L):
+    # argument errors are reported through the status code / jh_last_error
+    # before any CUDA call (runs without a GPU)
+    from paper_2508_04711_b200._lib import JH_ERR_INVALID, JhAttnArgs
+    a = JhAttnArgs()
+    assert L.jh_attn_band(None, None) == JH_ERR_INVALID
+    assert b"NULL" in L.jh_last_error()
+    buf = (ctypes.c_int64 * 8)()
+    a.q_offsets = a.ts_q = a.ts_k = ctypes.cast(buf, ctypes.c_void_p).value
+    a.num_segments, a.q_rows, a.num_heads, a.num_buckets = 1, 64, 1, 16
+    assert L.jh_attn_band(ctypes.byref(a), None) == JH_ERR_INVALID  # no band table
+    assert b"band_table" in L.jh_last_error()
+    a.num_buckets = 0
+    assert L.jh_attn_band(ctypes.byref(a), None) == JH_ERR_INVALID
+    a.num_buckets, a.num_pos = 16, 3  # a positional bias has no band table: nothing to do
+    assert L.jh_attn_band(ctypes.byref(a), None) == 0
+    a.num_pos, a.q_rows = 0, 0  # empty: nothing to do
+    assert L.jh_attn_band(ctypes.byref(a), None) == 0
+    # the layer's column sums: shape and workspace checks
+    assert L.jh_colsum(None, 8, 4, 8, None, None, 0, None) == JH_ERR_INVALID
+    assert L.jh_silu_bwd_colsum(None, None, None, 4, 8, None, None, 0, None) == JH_ERR_INVALID
+    assert L.jh_colsum_workspace_bytes(1000, 512) >= 512 * 4
