@@ -156,10 +156,24 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # JH_BENCH_TEST_GLOO=1 (tests only): N > 1 ranks on ONE GPU, exchanging over gloo
+    # through host memory (cp_layer.HostStagedComm) -- exercises this script's
+    # multi-rank logic where only one GPU exists; never a measurement
+    test_gloo = world > 1 and os.environ.get("JH_BENCH_TEST_GLOO") == "1"
+    if test_gloo:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if test_gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def allreduce_max(x: float) -> float:
+        t = torch.tensor([x], device="cpu" if test_gloo else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     from paper_2508_04711_b200 import kernels
     from paper_2508_04711_b200.attention import (AttentionInputs, BiasConfig, BiasParams,
@@ -188,13 +202,22 @@ def run_gpu(args):
             cp_group, dp_group = dist.group.WORLD, None
         else:  # hybrid CP x DP (config C5): CP groups of consecutive ranks, DP across them
             cp_group, dp_group, _, _ = make_cp_dp_groups(cp_size)
-        cp = CPAttention(cp_group, H, NB, protocol=args.protocol)
+        if test_gloo:
+            from paper_2508_04711_b200.cp_layer import HostStagedComm
+            cp = CPAttention(cp_group, H, NB, protocol=args.protocol, comm=HostStagedComm(cp_group))
+        else:
+            cp = CPAttention(cp_group, H, NB, protocol=args.protocol)
         cp_step = cp.bench_step(q, k, v, ts, h["offsets"], g, w)
 
         def step_fn(prof=None):
             dq_, dk_, dv_, dw_ = cp_step()
             if dp_group is not None:  # DDP rule: summed over CP (inside), averaged over DP
-                dist.all_reduce(dw_, group=dp_group)
+                if test_gloo:
+                    h_ = dw_.cpu()
+                    dist.all_reduce(h_, group=dp_group)
+                    dw_.copy_(h_)
+                else:
+                    dist.all_reduce(dw_, group=dp_group)
                 dw_ /= world // cp_size
             return dq_, dk_, dv_, dw_
         all_lens = [None] * world
@@ -276,9 +299,7 @@ def run_gpu(args):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = float(sum(step_ms))
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = allreduce_max(total_ms)
     ms_per_step = total_ms / K
     value = tokens_total / (ms_per_step / 1e3)
 
@@ -318,6 +339,8 @@ def run_gpu(args):
                     "algorithmic_flops_per_launch": Ff, "ms_per_launch": fwd_ms, "traffic": _traffic("fwd")},
         }
     result["clocks"] = clk.summary()
+    if test_gloo:
+        result["test_mode"] = "JH_BENCH_TEST_GLOO: all ranks on cuda:0, gloo host-staged exchange -- not a measurement"
 
     # ---------------- e2e through the public API with host buffers
     import torch as _t
@@ -448,9 +471,7 @@ def run_gpu(args):
         cp.meter = {"coll": [], "join": []}
         step_fn()
         rep = cp.exchange_report()
-        t = torch.tensor([rep.get("exposed_ms", 0.0)], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        rep["exposed_ms_max_over_ranks"] = float(t.item())
+        rep["exposed_ms_max_over_ranks"] = allreduce_max(rep.get("exposed_ms", 0.0))
         result["cp_exchange"] = rep
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(h, g_host, w_host)
