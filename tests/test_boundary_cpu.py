@@ -143,3 +143,28 @@ def test_host_streaming_cut_points(G):
     assert sum(sizes) == int(offs[-1])
     if g > 1:
         assert max(sizes) <= int(offs[-1]) / g + int(lens.max())  # within one sequence of the even share
+
+
+def test_bench_reference_arm_under_torchrun():
+    # the driver launches --impl reference like the GPU arm (torchrun for N > 1):
+    # rank 0 alone runs the reference's CPU path and prints the one JSON line
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", f"--master-port={port}", os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+           "--steps", "1", "--warmup", "1"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    j = json.loads(lines[0])
+    assert j["impl"] == "reference" and j["n_gpus"] == 2 and j["value"] > 0
+    assert j["e2e"]["value"] == j["value"] and j["cpu_baseline"]["kind"] in ("reference", "port")
