@@ -483,7 +483,8 @@ class CPAttention:
         rank's whole local batch, keep the plan rows (cp_engine.py:246-283;
         peak = the full group batch on every rank)."""
         if self.protocol == "allgather_split":
-            pad = x.new_zeros((p.max_local,) + tuple(x.shape[1:]))
+            # (padding rows are gathered but never selected by split_perm: left uninitialised)
+            pad = x.new_empty((p.max_local,) + tuple(x.shape[1:]))
             pad[: x.shape[0]] = x
             full = x.new_empty((self.cp * p.max_local,) + tuple(x.shape[1:]))
             self._timed("allgather_split", full.numel() * full.element_size(),
@@ -499,7 +500,7 @@ class CPAttention:
 
     def _gather_seq(self, x_res, p, dev):
         """resident slabs of all ranks -> group rows in sequence order."""
-        pad = x_res.new_zeros((p.max_res,) + tuple(x_res.shape[1:]))
+        pad = x_res.new_empty((p.max_res,) + tuple(x_res.shape[1:]))  # (padding never selected by seq_perm)
         pad[: p.n_res] = x_res
         full = x_res.new_empty((self.cp * p.max_res,) + tuple(x_res.shape[1:]))
         self._timed("kv_all_gather", full.numel() * full.element_size(), lambda: self.comm.all_gather_into(full, pad))
@@ -507,7 +508,9 @@ class CPAttention:
 
     def _reduce_to_owner(self, x_seq, p, dev):
         """sum of per-rank partials over group rows (sequence order) -> my resident rows."""
-        full = x_seq.new_zeros((self.cp * p.max_res,) + tuple(x_seq.shape[1:]))
+        # every owner's real rows are written by the scatter; the padding rows of
+        # each owner's slice are reduced too but sliced off below: no zero fill
+        full = x_seq.new_empty((self.cp * p.max_res,) + tuple(x_seq.shape[1:]))
         self.be.scatter(x_seq, dev["seq_perm"], full)
         mine = x_seq.new_empty((p.max_res,) + tuple(x_seq.shape[1:]))
         self._timed("dkv_reduce_scatter", full.numel() * full.element_size(),
