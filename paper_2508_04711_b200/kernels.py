@@ -420,8 +420,10 @@ def attn_fwd_bwd(q, k, v, ts, q_offsets, dout, num_heads, ts_weights, num_bucket
 
 # Backward variant.  None = auto: the two-kernel path (dK/dV kernel writes bf16
 # dS tiles, the dQ GEMM reads them; fastest at C2) whenever its exact dS
-# scratch fits DS_SCRATCH_BUDGET, else the fused one-kernel path (dq reduced
-# in fp32, O(L) memory: the long-sequence regime).  True / False force one.
+# scratch fits the budget (ds_scratch_budget), else the same two kernels over
+# kv windows with a bounded scratch (_attn_bwd_windowed), else -- no 128-wide
+# window fits, or a positional bias -- the fused one-kernel path (dq reduced in
+# fp32, O(L) memory).  True / False force the two-kernel / fused path.
 DETERMINISTIC_DEFAULT = {"value": None}
 _BWD_STATE: dict = {}
 
@@ -487,7 +489,8 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
     ``deterministic``: True = the two-kernel path over a bf16 dS scratch
     (bitwise reproducible dq; scratch ~H L^2 bytes per sequence), False = the
     fused kernel (dq reduced in fp32, O(L) memory), None = auto (the two-kernel
-    path when its scratch fits ``ds_scratch_budget``).  ``seg_host`` =
+    path when its scratch fits ``ds_scratch_budget``, else kv windows of it,
+    else the fused kernel).  ``seg_host`` =
     (q_offsets, q_pos0 or None, kv_len or None) as host arrays sizes the
     scratch exactly; without it ``max_kv_len`` (>= every segment's q and kv
     length) gives a bound, and without either the lengths are read back from
