@@ -491,8 +491,9 @@ def attn_bwd(q, k, v, ts_q, ts_k, q_offsets, dout, num_heads, ts_weights, num_bu
     fused kernel (dq reduced in fp32, O(L) memory), None = auto (the two-kernel
     path when its scratch fits ``ds_scratch_budget``, else kv windows of it,
     else the fused kernel).  ``seg_host`` =
-    (q_offsets, q_pos0 or None, kv_len or None) as host arrays sizes the
-    scratch exactly; without it ``max_kv_len`` (>= every segment's q and kv
+    (q_offsets, q_pos0 or None, kv_len or None[, kv_start]) as host arrays sizes
+    the scratch exactly (a segment-form call also needs kv_start there to be
+    windowed); without it ``max_kv_len`` (>= every segment's q and kv
     length) gives a bound, and without either the lengths are read back from
     the device (one synchronisation).  ``out`` = (dq, dk, dv) bf16 tensors shaped
     like q (any 16-byte row stride, e.g. column views of one gradient buffer)
