@@ -671,6 +671,9 @@ class CPAttention:
 
         def step(prof=None):
             _, ctx = self.forward(q, k, v, ts, lengths, w)
+            # the next step's length exchange starts now (a training loop would
+            # pass its next batch's lengths), so plan_for never waits for it
+            self.prefetch_plan(lengths)
             return self.backward(ctx, g, w)
 
         return step
